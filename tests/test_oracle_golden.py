@@ -1,0 +1,141 @@
+"""The CPU oracle (oracle/levsketch_oracle.py) pinned to golden vectors made by
+importing the reference (oracle/gen_golden.py).  CPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import levsketch_oracle as O
+
+
+def test_hash_kats(golden, golden_meta):
+    for ci, m in enumerate(golden_meta["hash"]):
+        hp = O.HashParams(m["family"], m["seed"], m["k"], m["s"])
+        keys = golden[f"hash{ci}_keys"]
+        assert [int(v) for v in keys[0]] == hp.a
+        assert [int(v) for v in keys[1]] == hp.b
+        assert [int(v) for v in keys[2]] == hp.sign_keys
+        assert list(golden[f"hash{ci}_sizes"]) == hp.sizes
+        assert list(golden[f"hash{ci}_offsets"]) == hp.offsets
+        idx = golden[f"hash{ci}_idx"]
+        for j in range(m["s"]):
+            assert np.array_equal(O.block_buckets(hp, idx, j), golden[f"hash{ci}_buckets"][j])
+            assert np.array_equal(O.sign_of(idx, hp.sign_keys[j]), golden[f"hash{ci}_signs"][j])
+
+
+def test_survey_kats():
+    # SURVEY.md §8c excerpts (countsketch seed 0, k 4096)
+    hp = O.HashParams("countsketch", 0, 4096, 1)
+    assert hp.a[0] == 0xD855BAC60E2F2043 and hp.b[0] == 0xA6CFAE49D58DFD30
+    idx = np.arange(8, dtype=np.uint64)
+    assert O.block_buckets(hp, idx, 0).tolist() == [2668, 2034, 1399, 765, 130, 3591, 2957, 2322]
+    assert O.sign_of(idx, hp.sign_keys[0]).tolist() == [-1, -1, -1, 1, 1, -1, -1, 1]
+
+
+def test_hashed_sketch_bit_exact(golden, golden_meta):
+    for ci, m in enumerate(golden_meta["sketch"]):
+        x = golden[f"sk{ci}_x"]
+        hi, lo = O.hashed_sketch(x, m["family"], m["k"], m["seed"], m["s"])
+        assert np.array_equal(hi, golden[f"sk{ci}_hi"])
+        assert np.array_equal(lo, golden[f"sk{ci}_lo"])
+        assert np.array_equal(hi + lo, golden[f"sk{ci}_data"])
+        cut = m["cut"]
+        hp = O.HashParams(m["family"], m["seed"], m["k"], m["s"])
+        h1 = np.zeros_like(hi); l1 = np.zeros_like(hi)
+        O.hashed_consume(h1, l1, hp, x[:cut], 0)
+        assert np.array_equal(h1, golden[f"sk{ci}_part1_hi"]) and np.array_equal(l1, golden[f"sk{ci}_part1_lo"])
+        h2 = np.zeros_like(hi); l2 = np.zeros_like(hi)
+        O.hashed_consume(h2, l2, hp, x[cut:], cut)
+        mh, ml = O.merge_hashed(h1, l1, h2, l2)
+        assert np.array_equal(mh + ml, golden[f"sk{ci}_merged"])
+
+
+def test_fp32_sketch_bit_exact(golden, golden_meta):
+    for ci, m in enumerate(golden_meta["fp32_sketch"]):
+        hi, lo = O.hashed_sketch(golden[f"f32sk{ci}_x"], m["family"], m["k"], m["seed"], m["s"])
+        assert np.array_equal(hi + lo, golden[f"f32sk{ci}_data"])
+
+
+def test_srht(golden, golden_meta):
+    for ci, m in enumerate(golden_meta["srht"]):
+        signs, sample = O.srht_signs_sample(m["seed"], O.next_pow2(m["n"]), m["k"])
+        assert np.array_equal(signs, golden[f"srht{ci}_signs"])
+        assert np.array_equal(sample, golden[f"srht{ci}_sample"])
+        sx = O.srht_sketch(golden[f"srht{ci}_x"], m["k"], m["seed"])
+        assert np.array_equal(sx, golden[f"srht{ci}_data"])
+        S = O.explicit_srht_matrix(m["k"], m["seed"], m["n"])
+        assert np.allclose(S @ golden[f"srht{ci}_x"], sx, atol=1e-10)
+
+
+def test_srht_c3_sample(golden):
+    import hashlib
+
+    signs, sample = O.srht_signs_sample(0, 2**21, 4096)
+    assert np.array_equal(sample, golden["srht_c3_sample"])
+    assert np.array_equal(signs[:4096], golden["srht_c3_signs_head"])
+    dig = hashlib.sha256(np.packbits(signs > 0).tobytes()).digest()
+    assert np.array_equal(np.frombuffer(dig, dtype=np.uint8), golden["srht_c3_signs_sha256"])
+    # SURVEY §8c excerpts
+    assert signs[:8].tolist() == [1, -1, -1, -1, 1, -1, 1, -1]
+    assert sample[:8].tolist() == [1167, 1188, 1610, 2434, 2767, 2990, 3174, 3195] and sample[-1] == 2096942
+
+
+def test_fwht(golden):
+    assert np.array_equal(O.walsh_hadamard(golden["fwht_x"]), golden["fwht_y"])
+    assert np.array_equal(O.walsh_hadamard([1.0, 0, 0, 0]), golden["fwht_imp"])
+
+
+def test_leverage(golden, golden_meta):
+    for ci, m in enumerate(golden_meta["leverage"]):
+        x = golden[f"lev{ci}_x"]
+        sk = m["spec"]
+        fam = sk["family"]
+        k = O.sketch_rows(fam, sk["eps"], sk["d"], sk.get("osnap_s"), sk.get("rows_override"), sk.get("sizing_c"))
+        if fam == "srht":
+            sx = O.srht_sketch(x, k, sk["seed"])
+        else:
+            hi, lo = O.hashed_sketch(x, fam, k, sk["seed"], O.osnap_nnz(fam, sk["d"], sk.get("osnap_s")))
+            sx = hi + lo
+        tol = 0.0 if m["sv_tol"] is None else m["sv_tol"]
+        scores, r, _ = O.leverage_from_sketch(x, sx, tol)
+        assert r == m["rank"]
+        ref = golden[f"lev{ci}_scores"]
+        np.testing.assert_allclose(scores, ref, rtol=1e-9, atol=1e-12 * ref.max())
+
+
+def test_distributed(golden):
+    x = golden["lev3_x"]
+    k = O.sketch_rows("osnap", 0.5, 16)
+    scores, r, sx = O.pipeline_hashed(x, "osnap", k, 4, O.osnap_nnz("osnap", 16, None), 1e-3, workers=3)
+    assert np.array_equal(sx, golden["dist_w3_merged"])
+    np.testing.assert_allclose(scores, golden["dist_w3_scores"], rtol=1e-9)
+
+
+def test_order(golden):
+    p = golden["ord_p"]
+    assert np.array_equal(O.distribution(golden["ord_scores"]), p)
+    assert np.array_equal(O.order(p, "dec"), golden["ord_dec"])
+    assert np.array_equal(O.order(p, "dec_swor", 3, 2), golden["ord_swor_s3_e2"])
+    assert np.array_equal(O.order(p, "shuffle", 3, 2), golden["ord_shuffle_s3_e2"])
+    assert np.array_equal(O.order(p, "dec_swr", 3, 2), golden["ord_swr_s3_e2"])
+
+
+def test_sizing(golden_meta):
+    sz = golden_meta["sizing"]
+    assert O.sketch_rows("countsketch", 0.5, 16, sizing_c=1.0) == sz["countsketch_eps.5_d16"]
+    assert O.sketch_rows("osnap", 0.5, 16, sizing_c=1.0) == sz["osnap_eps.5_d16_c1"]
+    assert O.sketch_rows("srht", 0.5, 16, sizing_c=1.0) == sz["srht_eps.5_d16"]
+    assert O.sketch_rows("osnap", 0.5, 100) == sz["osnap_eps.5_d100"]
+
+
+def test_gaussian_generator_properties():
+    z = O.gaussian_z(0, 64, 0, 4096)
+    assert z.dtype == np.float32 and z.shape == (64, 4096)
+    # bf16-representable
+    assert not (z.view(np.uint32) & 0xFFFF).any()
+    assert abs(float(z.mean())) < 0.01 and abs(float(z.std()) - 1.0) < 0.01
+    # counter-based: a row window equals the slice of a larger draw
+    assert np.array_equal(O.gaussian_z(0, 64, 100, 50), z[:, 100:150])
+    # different seeds differ
+    assert not np.array_equal(O.gaussian_z(1, 64, 0, 16), z[:, :16])

@@ -1,0 +1,477 @@
+"""Benchmark: leverage-score rows/s on B200 (BASELINE.json metric).
+
+Workload at N=1 = BASELINE configs[1] ("C2"): CountSketch, X fp32
+1,000,000 x 512 (rank-50 + 0.01 noise, singular values 10 -> 1), k = 4096,
+JL r = 64, sv_tol 1e-6, curriculum order "dec".  One step = one full pass of
+the hot path over device-resident X:
+    K1 sketch -> fp64 factorisation -> fold M -> K5 leverage pass
+    -> normalise -> K7 argsort.
+N > 1 (torchrun, NCCL): weak scaling, 1e6 rows per rank with global row
+indices; the compensated sketch partials are all-gathered and folded in rank
+order, rank 0 factorises and broadcasts M, scores stay rank-local, and the
+global "dec" order is formed on rank 0 from the gathered probabilities.
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy port in oracle/, all host threads, bounded row sample per step).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "leverage-score rows/s"
+UNIT = "rows/s"
+
+CONFIGS = {
+    # name: family, n (per rank), d, k, r, s, dtype, sv_tol
+    "c2": dict(family="countsketch", n=1_000_000, d=512, k=4096, r=64, s=None, dtype="f32", sv_tol=1e-6,
+               desc="configs[1]: CountSketch dense fp32 1e6x512, k=4096, r=64"),
+    "c1": dict(family="gaussian", n=20_000, d=256, k=1024, r=64, s=None, dtype="f32", sv_tol=1e-6,
+               desc="configs[0]: Gaussian sketch fp32 20000x256, k=1024, r=64"),
+    "c3": dict(family="srht", n=2**21, d=256, k=4096, r=64, s=None, dtype="f32", sv_tol=1e-6,
+               desc="configs[2]: SRHT fp32 2^21x256, k=4096, r=64"),
+}
+
+
+def gen_x(cfg, rank: int, device):
+    """Seeded synthetic X with the config's structure, generated on the device."""
+    import torch
+
+    n, d = cfg["n"], cfg["d"]
+    g = torch.Generator(device=device).manual_seed(1000 + rank)
+    if cfg["family"] == "countsketch":
+        # rank-50, singular values linear 10 -> 1, plus 0.01 N(0,1)
+        u = torch.randn(n, 50, generator=g, device=device, dtype=torch.float32) / math.sqrt(n)
+        v, _ = torch.linalg.qr(torch.randn(d, 50, generator=g, device=device, dtype=torch.float32))
+        s = torch.linspace(10.0, 1.0, 50, device=device)
+        x = (u * s) @ v.T + 0.01 * torch.randn(n, d, generator=g, device=device, dtype=torch.float32)
+    elif cfg["family"] == "srht":
+        x = torch.randn(n, d, generator=g, device=device) / torch.sqrt(torch.arange(1, d + 1, device=device, dtype=torch.float32))
+    else:
+        u, _ = torch.linalg.qr(torch.randn(n, d, generator=g, device=device))
+        v, _ = torch.linalg.qr(torch.randn(d, d, generator=g, device=device))
+        s = 0.9 ** torch.arange(d, device=device, dtype=torch.float32)
+        x = (u * s) @ v.T + 0.01 * torch.randn(n, d, generator=g, device=device)
+    return x.contiguous()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy burst)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port of the reference algorithm)
+
+
+def cpu_leg(cfg, rows: int, threads: int):
+    """Time the reference algorithm (numpy port, oracle/) on `rows` rows of the
+    workload: sketch (threads = row partitions merged in order, dist.py style)
+    -> SVD -> fold -> scores -> dec argsort.  Returns (rows/s, seconds)."""
+    import numpy as np
+
+    from oracle import levsketch_oracle as O
+
+    rng = np.random.default_rng(7)
+    d = cfg["d"]
+    x = (rng.standard_normal((rows, 50)) @ (np.linspace(10, 1, 50)[:, None] * rng.standard_normal((50, d)))
+         + 0.01 * rng.standard_normal((rows, d))).astype(np.float32).astype(np.float64)
+    pi = O.jl_matrix(0, d, cfg["r"])
+    t0 = time.perf_counter()
+    if cfg["family"] == "countsketch":
+        scores, _, _ = O.pipeline_hashed(x, "countsketch", cfg["k"], 0, 1, cfg["sv_tol"], pi, workers=threads)
+    elif cfg["family"] == "srht":
+        sx = O.srht_sketch(x, cfg["k"], 0)
+        scores, _, _ = O.leverage_from_sketch(x, sx, cfg["sv_tol"], pi)
+    else:
+        sx = O.gaussian_sketch(x, cfg["k"], 0)
+        scores, _, _ = O.leverage_from_sketch(x, sx, cfg["sv_tol"], pi)
+    O.order(O.distribution(scores), "dec")
+    dt = time.perf_counter() - t0
+    return rows / dt, dt
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, rank: int):
+    if rank != 0:
+        return
+    threads = host_threads()
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(threads)
+    except ImportError:
+        pass
+    sample = args.ref_rows
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_leg(cfg, min(sample, 20_000), threads)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_leg(cfg, sample, threads)
+        times.append(dt)
+    total = sum(times)
+    value = sample * args.steps / total
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000 * total / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg["desc"], "rows_per_step": sample, "note": "bounded row sample per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} rows x {cfg['d']} of the {args.config} workload per step "
+                                   "(oracle/levsketch_oracle.py numpy port of the reference path, "
+                                   "row partitions in threads + BLAS threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def run_ours(args, cfg, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1812_07903_b200 as P
+    from paper_1812_07903_b200 import _native as N
+    from paper_1812_07903_b200.leverage import factor_device, fold_device, jl_device, split_m
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
+    n, d, k, r = cfg["n"], cfg["d"], cfg["k"], cfg["r"]
+    spec = P.SketchSpec(cfg["family"], eps=0.5, d=d, seed=0, rows_override=k, osnap_s=cfg["s"])
+    X = gen_x(cfg, rank, dev).to(dtype)
+    torch.cuda.synchronize()
+    row0 = rank * n
+    pipe = P.LeveragePipeline(spec, n * world if world > 1 else n, d, dtype, sv_tol=cfg["sv_tol"], jl_dim=r,
+                              order=(world == 1), row0=row0)
+    if world > 1:
+        pipe.n = n  # local rows; the state covers n*world global rows
+        pipe.scores = torch.empty(n, dtype=torch.float64, device=dev)
+    gather_p = torch.empty(n * world, dtype=torch.float64, device=dev) if world > 1 else None
+    order_all = torch.empty(n * world, dtype=torch.int64, device=dev) if world > 1 else None
+    ws_sort = torch.empty(max(N.lib().lvsk_argsort_workspace_bytes(n * world), 256), dtype=torch.uint8, device=dev)
+    pi = jl_device(0, d, r)
+
+    def step(timing=False):
+        if world == 1:
+            pipe.run(X, timing=timing, check=False)
+            return
+        # multi-rank: local sketch -> all_gather (hi, lo) -> rank-ordered fold -> factor on 0 -> bcast M
+        ev = pipe.events
+        if timing:
+            ev["sketch"][0].record()
+        pipe._sketch(X)
+        if timing:
+            ev["sketch"][1].record()
+        s = pipe.state
+        his = [torch.empty_like(s._hi) for _ in range(world)]
+        los = [torch.empty_like(s._lo) for _ in range(world)]
+        dist.all_gather(his, s._hi)
+        dist.all_gather(los, s._lo)
+        hi, lo = his[0], los[0]
+        for q in range(1, world):
+            N.check(N.lib().lvsk_merge_compensated(hi.data_ptr(), lo.data_ptr(), his[q].data_ptr(), los[q].data_ptr(),
+                                                   hi.data_ptr(), lo.data_ptr(), hi.numel(), N.stream_ptr()))
+        N.check(N.lib().lvsk_fold_compensated(hi.data_ptr(), lo.data_ptr(), pipe.sx.data_ptr(), pipe.sx.numel(),
+                                              N.stream_ptr()))
+        if timing:
+            ev["factor"][0].record()
+        M = torch.empty((d, r), dtype=torch.float64, device=dev)
+        if rank == 0:
+            sigma, vt, s_host = factor_device(pipe.sx, cfg["sv_tol"], None)
+            M.copy_(fold_device(sigma, vt, s_host, pi))
+        dist.broadcast(M, 0)
+        pipe.m_hi, pipe.m_lo = split_m(M, dtype)
+        pipe.r = r
+        if timing:
+            ev["factor"][1].record()
+            ev["leverage"][0].record()
+        pipe._leverage(X)
+        if timing:
+            ev["leverage"][1].record()
+            ev["order"][0].record()
+        # global dec order: p = s / global sum, gathered on every rank, sorted on rank 0
+        local_sum = pipe.scores.sum().reshape(1)
+        dist.all_reduce(local_sum)
+        p_local = pipe.scores / local_sum
+        dist.all_gather_into_tensor(gather_p, p_local)
+        if rank == 0:
+            N.check(N.lib().lvsk_argsort_f64(gather_p.data_ptr(), n * world, 1, order_all.data_ptr(),
+                                             ws_sort.data_ptr(), ws_sort.numel(), N.stream_ptr()))
+        if timing:
+            ev["order"][1].record()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    pipe.check()
+    barrier()
+
+    # ---- timed region (device events; inputs 2 GB >> 126 MB L2) ----
+    stage_sum = {"sketch": 0.0, "factor": 0.0, "leverage": 0.0, "order": 0.0}
+    gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0]) if os.environ.get(
+        "CUDA_VISIBLE_DEVICES", "").strip().isdigit() else local_rank
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_index) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            step(timing=True)
+            for name, ms in pipe.stage_ms().items() if args.stage_sync else ():
+                stage_sum[name] += ms
+        stop.record()
+        torch.cuda.synchronize()
+        barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    if not args.stage_sync:
+        # stage events of the last step only (no extra syncs inside the timed loop)
+        for name, ms in pipe.stage_ms().items():
+            stage_sum[name] = ms * args.steps
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    pipe.check()
+    ms_per_step = elapsed_ms / args.steps
+    rows_total = n * world
+    value = rows_total / (ms_per_step / 1000.0)
+
+    # ---- per-kernel roofline (algorithmic bytes / event-timed duration) ----
+    peak, peak_src = measured_peaks()
+    elt = X.element_size()
+    stage_ms = {k_: v / args.steps for k_, v in stage_sum.items()}
+    lev_bytes = n * d * elt + 8 * n  # X once + float64 scores
+    sk_bytes = n * d * elt + 2 * 8 * k * d  # X once + compensated state write
+    lev_gbs = lev_bytes / (stage_ms["leverage"] / 1000) / 1e9 if stage_ms.get("leverage") else None
+    sk_gbs = sk_bytes / (stage_ms["sketch"] / 1000) / 1e9 if stage_ms.get("sketch") else None
+    dominant = "sketch" if stage_ms.get("sketch", 0) >= stage_ms.get("leverage", 0) else "leverage"
+    dom_gbs = sk_gbs if dominant == "sketch" else lev_gbs
+    dom_bytes = sk_bytes if dominant == "sketch" else lev_bytes
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"{args.config}:{dominant}")
+        except (ValueError, OSError):
+            traffic = None
+    roofline = {
+        "bound": "hbm",
+        "kernel": {"sketch": "hashed_gather_kernel (K1, with keygen+radix grouping)",
+                   "leverage": "rowsumsq kernel (K5)"}[dominant],
+        "achieved": dom_gbs,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": (dom_gbs / peak) if dom_gbs else None,
+        "traffic": traffic,
+        "algorithmic_bytes_per_launch": dom_bytes,
+        "peak_source": peak_src,
+    }
+    other = {
+        "sketch": {"ms": stage_ms.get("sketch"), "GB/s": sk_gbs, "frac": sk_gbs / peak if sk_gbs else None},
+        "leverage": {"ms": stage_ms.get("leverage"), "GB/s": lev_gbs, "frac": lev_gbs / peak if lev_gbs else None},
+        "factor_ms": stage_ms.get("factor"),
+        "order_ms": stage_ms.get("order"),
+    }
+
+    # ---- e2e through the public API with host buffers (rank 0 view) ----
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty((n, d), dtype=dtype, pin_memory=True)
+        Xh.copy_(X)
+        e2e_steps = max(2, min(args.steps, args.e2e_steps))
+
+        def e2e_step():
+            if world == 1:
+                res = P.leverage_sketched_trunc(Xh, spec, cfg["sv_tol"], jl_dim=r)
+                plan = P.make_plan(P.scores_to_distribution(res.scores), P.OrderingPolicy("dec"))
+                return plan.indices
+            local, *_ = P.run_sharded(Xh, row0, n * world, spec, cfg["sv_tol"], jl_dim=r)
+            return local.cpu()
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        h2d = n * d * elt + (2 * 8 * n if world == 1 else 0)
+        d2h = (3 * 8 * n) if world == 1 else 8 * n
+        e2e = {"value": rows_total / float(e2e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+               "api": "leverage_sketched_trunc(pinned host X) -> scores_to_distribution -> make_plan('dec')"
+               if world == 1 else "run_sharded(pinned host shard)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = host_threads()
+        rows = args.cpu_rows
+        v, dt = cpu_leg(cfg, rows, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{rows} rows of the {args.config} workload ({dt:.1f} s), oracle numpy port of the reference "
+                         "path incl. SVD and dec argsort, sketch partitions in threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {"f32": "f32", "bf16": "bf16"}[cfg["dtype"]],
+            "data": "synthetic (seeded, generated on device; random-init, no dataset)",
+            "config": {"workload": cfg["desc"], "rows_per_gpu": n, "d": d, "k": k, "jl_r": r,
+                       "sv_tol": cfg["sv_tol"], "parallelism": f"row-partition x{world}",
+                       "l2": f"inputs larger than L2 (X = {n * d * elt / 1e9:.2f} GB per GPU)"},
+            "stages_ms": other,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": pipe.launches_per_run() * args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-rows", type=int, default=200_000)
+    ap.add_argument("--ref-rows", type=int, default=100_000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--stage-sync", action="store_true", help="sync after every step to sum stage times")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

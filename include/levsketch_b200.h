@@ -1,0 +1,164 @@
+/*
+ * levsketch_b200 — C ABI of the B200 (sm_100a) sketched leverage-score path.
+ *
+ * The reference (levsketch, arXiv 1812.07903; pure Python/numpy) has no native
+ * boundary: its hot path is the Python call chain
+ *     leverage_sketched_trunc -> apply_sketch/consume_rows -> thin_svd/truncate
+ *     -> _approx_basis -> _block_scores -> scores_to_distribution -> make_plan
+ * (reference pkg/src/levsketch/leverage.py:115-132, sketch.py:289-319,
+ *  svd.py:30-54, order.py:51-100).  Each entry point below replaces one of the
+ * numpy kernels of that chain; the Python package paper_1812_07903_b200 binds
+ * them with ctypes and keeps the reference API above them.
+ *
+ * Conventions
+ *  - extern "C", plain pointers and sizes, no torch types.
+ *  - All array pointers are DEVICE pointers owned by the caller unless noted
+ *    "host".  Matrices are row-major with an explicit leading dimension (in
+ *    elements).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - No allocation inside: every entry that needs scratch has a
+ *    *_workspace_bytes query; the caller passes `ws`/`ws_bytes`.
+ *  - Return value: LVSK_OK or an error code mapping 1:1 onto the reference's
+ *    exception classes (errors.py:4-41); lvsk_last_error() returns a
+ *    thread-local message.  Device-side data errors (non-finite input) are
+ *    reported through a caller-provided device flag, checked by the host
+ *    after synchronisation.
+ *  - Reentrant; no global mutable state except the thread-local message.
+ */
+#ifndef LEVSKETCH_B200_H
+#define LEVSKETCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LVSK_API __attribute__((visibility("default")))
+#else
+#define LVSK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes ↔ reference errors.py classes. */
+enum {
+  LVSK_OK = 0,
+  LVSK_ERR_CONFIGURATION = 1, /* ConfigurationError      errors.py:38-39 */
+  LVSK_ERR_DIMENSION = 2,     /* DimensionMismatchError  errors.py:18-19 */
+  LVSK_ERR_FORMAT = 3,        /* FormatError             errors.py:6-7   */
+  LVSK_ERR_CAPACITY = 4,      /* CapacityError           errors.py:14-15 */
+  LVSK_ERR_UNSUPPORTED = 5,   /* UnsupportedFamilyError  errors.py:34-35 */
+  LVSK_ERR_DEGENERATE = 6,    /* DegenerateInputError    errors.py:26-27 */
+  LVSK_ERR_INCOMPATIBLE = 7,  /* IncompatibleSketchError errors.py:22-23 */
+  LVSK_ERR_CUDA = 8           /* CUDA runtime failure (no reference class) */
+};
+
+/* Element type of the input matrix X. */
+enum { LVSK_F32 = 0, LVSK_F64 = 1, LVSK_BF16 = 2 };
+
+/* Device-flag bits written by kernels (OR-ed into *flags). */
+enum { LVSK_FLAG_NONFINITE = 1, LVSK_FLAG_NEGATIVE = 2, LVSK_FLAG_BADINDEX = 4 };
+
+/* One OSNAP block (CountSketch: s = 1 block covering all k rows).
+ * Mirrors SketchState.__init__ (reference sketch.py:232-239). */
+typedef struct {
+  uint64_t a;        /* multiply-shift multiplier (odd) */
+  uint64_t b;        /* multiply-shift offset */
+  uint64_t sign_key; /* splitmix sign key */
+  int64_t offset;    /* first sketch row of the block */
+  int64_t size;      /* rows in the block */
+} lvsk_hash_block;
+
+LVSK_API const char* lvsk_last_error(void);
+LVSK_API int32_t lvsk_abi_version(void);
+
+/* ---- K1: CountSketch / OSNAP on dense rows ------------------------------
+ * Replaces SketchState._update_hashed + _scatter_add + _two_sum
+ * (reference sketch.py:260-266, 173-191, 166-170) as driven by consume_rows
+ * (sketch.py:289-312).  Rows X[0..n) carry GLOBAL indices row0..row0+n-1.
+ * The compensated state (hi, lo), k x d float64 row-major, is read from
+ * (hi_in, lo_in) and written to (hi_out, lo_out) (may alias).  Contributions to
+ * one bucket are applied in ascending row index, each as a TwoSum, which is
+ * the reference's exact operation sequence: the result is bit-identical.
+ * blocks: HOST array of s blocks.  scale = 1/sqrt(s) (float64). */
+LVSK_API size_t lvsk_hashed_workspace_bytes(int64_t n, int32_t s, int64_t k);
+LVSK_API int32_t lvsk_hashed_sketch(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx,
+                           uint64_t row0, const lvsk_hash_block* blocks, int32_t s, double scale,
+                           const double* hi_in, const double* lo_in, double* hi_out, double* lo_out,
+                           int64_t k, void* ws, size_t ws_bytes, int32_t* flags, void* stream);
+
+/* Bucket / sign of arbitrary global indices (KAT parity of the hash family;
+ * reference sketch.py:151-159).  buckets_out, signs_out: s x n. */
+LVSK_API int32_t lvsk_hash_rows(const uint64_t* idx, int64_t n, const lvsk_hash_block* blocks, int32_t s,
+                       int64_t* buckets_out, double* signs_out, void* stream);
+
+/* merge(): hi_out, lo_out = TwoSum(hi1, hi2), lo1 + lo2 + err
+ * (reference sketch.py:352-355); count elements; may alias the inputs. */
+LVSK_API int32_t lvsk_merge_compensated(const double* hi1, const double* lo1, const double* hi2,
+                               const double* lo2, double* hi_out, double* lo_out, int64_t count,
+                               void* stream);
+
+/* SketchState.data for the hashed families: out = hi + lo
+ * (reference sketch.py:258); may alias. */
+LVSK_API int32_t lvsk_fold_compensated(const double* hi, const double* lo, double* out, int64_t count,
+                                       void* stream);
+
+/* ---- K3: SRHT ------------------------------------------------------------
+ * Replaces SketchState.data's SRHT branch + fwht (reference sketch.py:248-257,
+ * 364-385): SX[t,:] = (H_m D X)[sample[t], :] / divisor, H_m unnormalised
+ * Walsh-Hadamard of order m = 2^L >= n (rows >= n are the zero padding).
+ * signs: m int8 (+1/-1) or NULL for all +1; sample: k int64, each in [0, m).
+ * SX: k x d float64 (overwritten).  divisor = sqrt(k) for SRHT, 1 for fwht(). */
+LVSK_API size_t lvsk_srht_workspace_bytes(int64_t m, int64_t d, int32_t dtype, int64_t k);
+LVSK_API int32_t lvsk_srht(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx, int64_t m,
+                  const int8_t* signs, const int64_t* sample, int64_t k, double divisor, double* SX,
+                  void* ws, size_t ws_bytes, int32_t* flags, void* stream);
+
+/* ---- K4: Gaussian sketch (extension: the reference rejects "gaussian",
+ * sketch.py:74-75) ----------------------------------------------------------
+ * SX (+)= Z X / sqrt(k), Z[j,i] = bf16-rounded standard normal from
+ * Philox4x32-10(counter=(i_lo,i_hi,j>>2,0), key=(seed_lo, seed_hi^0x47415553)),
+ * Box-Muller with IEEE-only fp32 transcendentals (oracle/levsketch_oracle.py
+ * gaussian_z).  Rows carry global indices row0..  SX: k x d float64;
+ * accumulate != 0 adds to SX instead of overwriting. */
+LVSK_API size_t lvsk_gaussian_workspace_bytes(int64_t n, int64_t d, int64_t k, int32_t dtype);
+LVSK_API int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx,
+                             uint64_t row0, uint64_t seed, int64_t k, double* SX, int32_t accumulate,
+                             void* ws, size_t ws_bytes, int32_t* flags, void* stream);
+/* Materialise Z (k x n float32, row-major) for KAT parity. */
+LVSK_API int32_t lvsk_gaussian_entries(uint64_t seed, int64_t k, uint64_t row0, int64_t n, float* Z,
+                              void* stream);
+
+/* ---- K5: leverage pass --------------------------------------------------
+ * Replaces _block_scores (reference leverage.py:88-95):
+ *     scores[i] = sum_c (X[i,:] . M[:,c])^2,  i < n.
+ * M is d x r row-major, float32 for F32/BF16 inputs (M_lo optional: the
+ * low-order part of a float64 M split hi+lo, may be NULL) and float64 for F64
+ * inputs.  scores: n float64.  Non-finite X sets LVSK_FLAG_NONFINITE. */
+LVSK_API int32_t lvsk_rowsumsq_gemm(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx,
+                           const void* M, const void* M_lo, int64_t r, double* scores,
+                           int32_t* flags, void* stream);
+
+/* ---- ordering -------------------------------------------------------------
+ * scores_to_distribution (order.py:51-63): p = scores / sum(scores), with
+ * the sum a deterministic two-level float64 reduction.  Sets
+ * LVSK_FLAG_NONFINITE / LVSK_FLAG_NEGATIVE in *flags; *total receives the sum. */
+LVSK_API size_t lvsk_normalize_workspace_bytes(int64_t n);
+LVSK_API int32_t lvsk_normalize_scores(const double* scores, int64_t n, double* p_out, double* total,
+                              void* ws, size_t ws_bytes, int32_t* flags, void* stream);
+/* Deterministic float64 sum of x[0..n) into *out (device). */
+LVSK_API int32_t lvsk_sum_f64(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* K7: stable argsort of float64 keys.  descending != 0 reproduces
+ * np.argsort(-p, kind="stable") (make_plan "dec", order.py:89-90); descending
+ * == 0 reproduces np.argsort(keys, kind="stable") ("dec_swor", order.py:95-99).
+ * NaNs sort last; -0.0 == +0.0.  idx_out: n int64. */
+LVSK_API size_t lvsk_argsort_workspace_bytes(int64_t n);
+LVSK_API int32_t lvsk_argsort_f64(const double* keys, int64_t n, int32_t descending, int64_t* idx_out,
+                         void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEVSKETCH_B200_H */

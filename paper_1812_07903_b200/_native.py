@@ -1,0 +1,162 @@
+"""ctypes binding of liblevsketch_b200.so (the C ABI in include/levsketch_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is visible, every compute entry point raises.  ``build()`` in
+``__graft_entry__`` (or ``make -C paper_1812_07903_b200/csrc``) produces the
+library in-tree.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import torch
+
+from . import errors
+
+LIB_PATH = Path(__file__).resolve().parent / "liblevsketch_b200.so"
+
+LVSK_F32, LVSK_F64, LVSK_BF16 = 0, 1, 2
+FLAG_NONFINITE, FLAG_NEGATIVE, FLAG_BADINDEX = 1, 2, 4
+
+_ERRORS = {
+    1: errors.ConfigurationError,
+    2: errors.DimensionMismatchError,
+    3: errors.FormatError,
+    4: errors.CapacityError,
+    5: errors.UnsupportedFamilyError,
+    6: errors.DegenerateInputError,
+    7: errors.IncompatibleSketchError,
+    8: RuntimeError,
+}
+
+_DTYPE = {torch.float32: LVSK_F32, torch.float64: LVSK_F64, torch.bfloat16: LVSK_BF16}
+
+
+class HashBlock(C.Structure):
+    _fields_ = [("a", C.c_uint64), ("b", C.c_uint64), ("sign_key", C.c_uint64), ("offset", C.c_int64), ("size", C.c_int64)]
+
+
+_P, _I64, _I32, _U64, _D, _SZ = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.c_size_t
+
+_SIGS = {
+    "lvsk_last_error": (C.c_char_p, []),
+    "lvsk_abi_version": (_I32, []),
+    "lvsk_hashed_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
+    "lvsk_hashed_sketch": (
+        _I32,
+        [_P, _I32, _I64, _I64, _I64, _U64, C.POINTER(HashBlock), _I32, _D, _P, _P, _P, _P, _I64, _P, _SZ, _P, _P],
+    ),
+    "lvsk_hash_rows": (_I32, [_P, _I64, C.POINTER(HashBlock), _I32, _P, _P, _P]),
+    "lvsk_merge_compensated": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _P]),
+    "lvsk_fold_compensated": (_I32, [_P, _P, _P, _I64, _P]),
+    "lvsk_srht_workspace_bytes": (_SZ, [_I64, _I64, _I32, _I64]),
+    "lvsk_srht": (_I32, [_P, _I32, _I64, _I64, _I64, _I64, _P, _P, _I64, _D, _P, _P, _SZ, _P, _P]),
+    "lvsk_gaussian_workspace_bytes": (_SZ, [_I64, _I64, _I64, _I32]),
+    "lvsk_gaussian_sketch": (_I32, [_P, _I32, _I64, _I64, _I64, _U64, _U64, _I64, _P, _I32, _P, _SZ, _P, _P]),
+    "lvsk_gaussian_entries": (_I32, [_U64, _I64, _U64, _I64, _P, _P]),
+    "lvsk_rowsumsq_gemm": (_I32, [_P, _I32, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P]),
+    "lvsk_normalize_workspace_bytes": (_SZ, [_I64]),
+    "lvsk_normalize_scores": (_I32, [_P, _I64, _P, _P, _P, _SZ, _P, _P]),
+    "lvsk_sum_f64": (_I32, [_P, _I64, _P, _P, _SZ, _P]),
+    "lvsk_argsort_workspace_bytes": (_SZ, [_I64]),
+    "lvsk_argsort_f64": (_I32, [_P, _I64, _I32, _P, _P, _SZ, _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """The loaded library (raises ImportError loudly if it was never built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} not found: build the sm_100a kernels first "
+                "(python -c 'import __graft_entry__ as g; g.build()' or make -C paper_1812_07903_b200/csrc)"
+            )
+        handle = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = lib().lvsk_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(f"{what}: {msg}" if what else msg)
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("levsketch_b200 needs a CUDA device (B200 / sm_100a); no CPU fallback exists")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DTYPE[t.dtype]
+    except KeyError:
+        raise errors.FormatError(f"unsupported element type {t.dtype}") from None
+
+
+class Workspace:
+    """Grow-only device scratch buffer reused across calls (no allocation in the C ABI)."""
+
+    def __init__(self):
+        self._buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self._buf is None or self._buf.numel() < nbytes or self._buf.device != device():
+            self._buf = torch.empty(nbytes, dtype=torch.uint8, device=device())
+        return self._buf
+
+
+_ws = Workspace()
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    return _ws.get(nbytes)
+
+
+class Flags:
+    """One device int32 for kernel-side data errors (non-finite, negative...)."""
+
+    def __init__(self):
+        self.t = torch.zeros(1, dtype=torch.int32, device=device())
+
+    @property
+    def p(self) -> int:
+        return self.t.data_ptr()
+
+    def read(self) -> int:
+        return int(self.t.item())
+
+
+def hash_blocks(blocks) -> C.Array:
+    arr = (HashBlock * len(blocks))()
+    for i, (a, b, key, off, size) in enumerate(blocks):
+        arr[i] = HashBlock(a, b, key, off, size)
+    return arr
+
+
+if os.environ.get("LVSK_EAGER_LOAD"):
+    lib()

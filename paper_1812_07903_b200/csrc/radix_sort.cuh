@@ -1,0 +1,202 @@
+// Stable LSD radix sort of (key, value) pairs — the building block of the
+// bucket grouping in K1 (hashed sketch) and of K7 (argsort for make_plan).
+//
+// Per pass (<= 8 key bits): tile histogram -> exclusive scan over
+// (digit, tile) -> stable tile-local ranking with __match_any_sync and a
+// per-warp digit counter -> scatter.  Items inside a tile are visited in
+// (warp, step, lane) order, which is index order, so every pass is stable.
+#pragma once
+
+#include "common.cuh"
+
+namespace lvsk {
+namespace radix {
+
+constexpr int THREADS = 256;
+constexpr int ITEMS = 16;
+constexpr int TILE = THREADS * ITEMS;  // 4096 keys per tile
+constexpr int WARPS = THREADS / 32;
+constexpr int WARP_ITEMS = TILE / WARPS;  // 512 contiguous keys per warp
+constexpr int RADIX = 256;
+constexpr int SCAN_THREADS = 1024;
+
+inline int64_t num_tiles(int64_t n) { return (n + TILE - 1) / TILE; }
+
+template <typename K>
+__global__ void __launch_bounds__(THREADS) hist_kernel(const K* __restrict__ keys, int64_t n, int shift,
+                                                       uint32_t mask, uint32_t* __restrict__ hist,
+                                                       int64_t ntiles) {
+  __shared__ uint32_t h[RADIX];
+  for (int i = threadIdx.x; i < RADIX; i += THREADS) h[i] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * TILE;
+#pragma unroll 4
+  for (int j = 0; j < ITEMS; ++j) {
+    int64_t i = base + j * THREADS + threadIdx.x;
+    if (i < n) atomicAdd(&h[static_cast<uint32_t>(keys[i] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  for (int dg = threadIdx.x; dg < RADIX; dg += THREADS) hist[dg * ntiles + blockIdx.x] = h[dg];
+}
+
+// Exclusive scan of `total` uint32 counts in one block (digit-major layout).
+static __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(uint32_t* __restrict__ data, int64_t total) {
+  __shared__ uint32_t sums[SCAN_THREADS];
+  const int64_t per = (total + SCAN_THREADS - 1) / SCAN_THREADS;
+  const int64_t lo = threadIdx.x * per;
+  const int64_t hi = min(total, lo + per);
+  uint32_t s = 0;
+  for (int64_t i = lo; i < hi; ++i) s += data[i];
+  sums[threadIdx.x] = s;
+  __syncthreads();
+  // Hillis-Steele inclusive scan of the per-thread sums
+  for (int off = 1; off < SCAN_THREADS; off <<= 1) {
+    uint32_t v = threadIdx.x >= off ? sums[threadIdx.x - off] : 0u;
+    __syncthreads();
+    sums[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = threadIdx.x ? sums[threadIdx.x - 1] : 0u;
+  for (int64_t i = lo; i < hi; ++i) {
+    uint32_t v = data[i];
+    data[i] = run;
+    run += v;
+  }
+}
+
+// vals_in == nullptr means "value = item index" (argsort identity).
+template <typename K, typename VIn, typename VOut>
+__global__ void __launch_bounds__(THREADS) scatter_kernel(const K* __restrict__ keys_in,
+                                                          const VIn* __restrict__ vals_in,
+                                                          K* __restrict__ keys_out, VOut* __restrict__ vals_out,
+                                                          int64_t n, int shift, uint32_t mask,
+                                                          const uint32_t* __restrict__ offsets,
+                                                          int64_t ntiles) {
+  __shared__ uint32_t cnt[WARPS][RADIX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < WARPS * RADIX; i += THREADS) (&cnt[0][0])[i] = 0u;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * TILE + warp * WARP_ITEMS;
+  const uint32_t lt = lanemask_lt();
+  K k[ITEMS];
+  VOut v[ITEMS];
+  uint32_t rank[ITEMS];
+  uint32_t dg[ITEMS];
+#pragma unroll
+  for (int t = 0; t < ITEMS; ++t) {
+    const int64_t i = base + t * 32 + lane;
+    const bool valid = i < n;
+    uint32_t d = 0xFFFFFFFFu;
+    if (valid) {
+      k[t] = keys_in[i];
+      v[t] = vals_in ? static_cast<VOut>(vals_in[i]) : static_cast<VOut>(i);
+      d = static_cast<uint32_t>(k[t] >> shift) & mask;
+    }
+    dg[t] = d;
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+    const uint32_t before = valid ? cnt[warp][d] : 0u;
+    __syncwarp();
+    if (valid) {
+      rank[t] = before + __popc(peers & lt);
+      if (lane == __ffs(peers) - 1) cnt[warp][d] = before + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < RADIX; d += THREADS) {
+    uint32_t run = offsets[d * ntiles + blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      uint32_t c = cnt[w][d];
+      cnt[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < ITEMS; ++t) {
+    if (dg[t] != 0xFFFFFFFFu) {
+      const uint32_t pos = cnt[warp][dg[t]] + rank[t];
+      if (keys_out) keys_out[pos] = k[t];
+      vals_out[pos] = v[t];
+    }
+  }
+}
+
+// start[b] = first position of bucket b in the sorted key array, start[k] = N.
+template <typename I>
+__global__ void bucket_bounds_kernel(const I* __restrict__ sorted, int64_t N, int64_t k, uint32_t* __restrict__ start) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i <= N;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t prev = i == 0 ? -1 : static_cast<int64_t>(sorted[i - 1]);
+    const int64_t cur = i == N ? k : static_cast<int64_t>(sorted[i]);
+    for (int64_t b = prev + 1; b <= cur && b <= k; ++b) start[b] = static_cast<uint32_t>(i);
+  }
+}
+
+template <typename K>
+struct Buffers {
+  K* keys[2];
+  uint32_t* vals[2];
+  uint32_t* hist;
+};
+
+template <typename K>
+inline void measure(Measure& m, int64_t n) {
+  m.take<K>(n);
+  m.take<K>(n);
+  m.take<uint32_t>(n);
+  m.take<uint32_t>(n);
+  m.take<uint32_t>(static_cast<size_t>(RADIX) * num_tiles(n));
+}
+
+template <typename K>
+inline Buffers<K> carve(Carve& c, int64_t n) {
+  Buffers<K> b;
+  b.keys[0] = c.take<K>(n);
+  b.keys[1] = c.take<K>(n);
+  b.vals[0] = c.take<uint32_t>(n);
+  b.vals[1] = c.take<uint32_t>(n);
+  b.hist = c.take<uint32_t>(static_cast<size_t>(RADIX) * num_tiles(n));
+  return b;
+}
+
+// Sort `n` pairs on key bits [0, nbits).  vals == nullptr: value = index.
+// Final keys land in *keys_final (may be nullptr), final values in vals_final.
+template <typename K, typename VOut>
+int32_t sort_pairs(const K* keys, const uint32_t* vals, int64_t n, int nbits, Buffers<K>& b,
+                   K* keys_final, VOut* vals_final, cudaStream_t st) {
+  if (n <= 0) return LVSK_OK;
+  if (n > 0xFFFFFFFFll) {
+    set_error("radix sort supports at most 2^32-1 items, got %lld", (long long)n);
+    return LVSK_ERR_CAPACITY;
+  }
+  const int64_t ntiles = num_tiles(n);
+  const int passes = nbits <= 0 ? 1 : (nbits + 7) / 8;
+  const K* kin = keys;
+  const uint32_t* vin = vals;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    const int bits = nbits <= 0 ? 1 : min(8, nbits - shift);
+    const uint32_t mask = (1u << bits) - 1u;
+    const bool last = p == passes - 1;
+    hist_kernel<K><<<static_cast<unsigned>(ntiles), THREADS, 0, st>>>(kin, n, shift, mask, b.hist, ntiles);
+    scan_kernel<<<1, SCAN_THREADS, 0, st>>>(b.hist, RADIX * ntiles);
+    if (last) {
+      scatter_kernel<K, uint32_t, VOut><<<static_cast<unsigned>(ntiles), THREADS, 0, st>>>(
+          kin, vin, keys_final, vals_final, n, shift, mask, b.hist, ntiles);
+    } else {
+      K* ko = b.keys[p & 1];
+      uint32_t* vo = b.vals[p & 1];
+      scatter_kernel<K, uint32_t, uint32_t><<<static_cast<unsigned>(ntiles), THREADS, 0, st>>>(
+          kin, vin, ko, vo, n, shift, mask, b.hist, ntiles);
+      kin = ko;
+      vin = vo;
+    }
+    LVSK_CHECK_LAUNCH("radix sort pass");
+  }
+  return LVSK_OK;
+}
+
+}  // namespace radix
+}  // namespace lvsk

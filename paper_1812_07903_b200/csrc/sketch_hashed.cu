@@ -1,0 +1,327 @@
+// K1 — CountSketch / OSNAP on dense rows, as an owner-computes gather.
+//
+// Reference: SketchState._update_hashed -> _scatter_add -> _two_sum
+// (pkg/src/levsketch/sketch.py:260-266, 173-191, 166-170), driven by
+// consume_rows (sketch.py:289-312).
+//
+// B200 design: instead of scattering rows into buckets (atomics, order-
+// dependent), the row -> bucket map (pure integer hash of the GLOBAL row
+// index) is inverted with a stable radix sort, and one warp owns one
+// (bucket, 32*VEC-column chunk).  The warp walks its bucket's rows in
+// ascending global index and applies each contribution as a TwoSum into
+// float64 (hi, lo) registers — exactly the reference's per-bucket operation
+// sequence — so SX is bit-identical to the reference, with no atomics.  X is
+// read once per block j (s times for OSNAP), in 512-byte warp-contiguous
+// row segments; the accumulator never round-trips HBM.
+#include "radix_sort.cuh"
+
+namespace lvsk {
+
+constexpr int KEYGEN_MAX_BLOCKS = 64;
+
+struct KeygenBlocks {
+  uint64_t a[KEYGEN_MAX_BLOCKS];
+  uint64_t b[KEYGEN_MAX_BLOCKS];
+  uint64_t key[KEYGEN_MAX_BLOCKS];
+  uint32_t offset[KEYGEN_MAX_BLOCKS];
+  uint32_t size[KEYGEN_MAX_BLOCKS];
+};
+
+// keys[j*n + r] = global bucket of row r in block j; vals = (r << 1) | negative
+__global__ void hashed_keygen_kernel(int64_t n, uint64_t row0, int j0, int nb, KeygenBlocks P,
+                                     uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t total = n * nb;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int jj = static_cast<int>(t / n);
+    const int64_t r = t - static_cast<int64_t>(jj) * n;
+    const uint64_t g = row0 + static_cast<uint64_t>(r);
+    const uint32_t bk = P.offset[jj] + bucket_hash(g, P.a[jj], P.b[jj], P.size[jj]);
+    const bool neg = sign_negative(g, P.key[jj]);
+    const int64_t o = static_cast<int64_t>(j0 + jj) * n + r;
+    keys[o] = bk;
+    vals[o] = (static_cast<uint32_t>(r) << 1) | (neg ? 1u : 0u);
+  }
+}
+
+template <typename T, int VEC>
+struct VecLoad;
+template <>
+struct VecLoad<float, 4> {
+  using V = float4;
+  __device__ static void load(const float* p, float (&o)[4]) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+};
+template <>
+struct VecLoad<double, 2> {
+  __device__ static void load(const double* p, double (&o)[2]) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = v.x; o[1] = v.y;
+  }
+};
+template <>
+struct VecLoad<__nv_bfloat16, 8> {
+  __device__ static void load(const __nv_bfloat16* p, __nv_bfloat16 (&o)[8]) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = h[i];
+  }
+};
+template <typename T>
+struct VecLoad<T, 1> {
+  __device__ static void load(const T* p, T (&o)[1]) { o[0] = p[0]; }
+};
+
+constexpr int GATHER_UNROLL = 4;
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) hashed_gather_kernel(
+    const T* __restrict__ X, int64_t ldx, int64_t d, int nchunks, const uint32_t* __restrict__ vals,
+    const uint32_t* __restrict__ start, int64_t k, double scale, const double* hi_in, const double* lo_in,
+    double* hi_out, double* lo_out, int32_t* flags) {
+  const int64_t unit = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (unit >= k * nchunks) return;  // warp-uniform
+  const int64_t b = unit / nchunks;
+  const int64_t col0 = (unit - b * nchunks) * (32 * VEC) + lane * VEC;
+  const bool active = col0 < d;
+  double h[VEC], l[VEC];
+  const int64_t so = b * d + col0;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    h[v] = (active && col0 + v < d) ? hi_in[so + v] : 0.0;
+    l[v] = (active && col0 + v < d) ? lo_in[so + v] : 0.0;
+  }
+  const uint32_t p0 = start[b], p1 = start[b + 1];
+  bool bad = false;
+  for (uint32_t base = p0; base < p1; base += 32) {
+    const uint32_t cnt = min(32u, p1 - base);
+    const uint32_t mine = lane < cnt ? vals[base + lane] : 0u;
+    for (uint32_t t = 0; t < cnt; t += GATHER_UNROLL) {
+      T xs[GATHER_UNROLL][VEC];
+#pragma unroll
+      for (int u = 0; u < GATHER_UNROLL; ++u) {
+        const uint32_t vv = __shfl_sync(0xFFFFFFFFu, mine, (t + u) & 31);
+        if (t + u < cnt && active) VecLoad<T, VEC>::load(X + static_cast<int64_t>(vv >> 1) * ldx + col0, xs[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < GATHER_UNROLL; ++u) {
+        const uint32_t vv = __shfl_sync(0xFFFFFFFFu, mine, (t + u) & 31);
+        if (t + u < cnt && active) {
+          const double sg = (vv & 1u) ? -scale : scale;  // (sign * scale), exact
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            const double xv = to_f64<T>(xs[u][v]);
+            bad |= !isfinite(xv);
+            double s, e;
+            two_sum(h[v], __dmul_rn(sg, xv), s, e);
+            h[v] = s;
+            l[v] = __dadd_rn(l[v], e);
+          }
+        }
+      }
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      if (col0 + v < d) {
+        hi_out[so + v] = h[v];
+        lo_out[so + v] = l[v];
+      }
+    }
+  }
+  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
+}
+
+// copies hi/lo rows of buckets that no row touched when in != out
+__global__ void copy_f64_kernel(const double* __restrict__ a, double* __restrict__ b, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    b[i] = a[i];
+}
+
+__global__ void merge_kernel(const double* hi1, const double* lo1, const double* hi2, const double* lo2,
+                             double* hi_out, double* lo_out, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s, e;
+    two_sum(hi1[i], hi2[i], s, e);
+    const double l = __dadd_rn(__dadd_rn(lo1[i], lo2[i]), e);  // (lo1 + lo2) + e, sketch.py:355
+    hi_out[i] = s;
+    lo_out[i] = l;
+  }
+}
+
+__global__ void hash_rows_kernel(const uint64_t* __restrict__ idx, int64_t n, int nb, KeygenBlocks P, int j0,
+                                 int64_t* __restrict__ buckets, double* __restrict__ signs) {
+  const int64_t total = n * nb;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int jj = static_cast<int>(t / n);
+    const int64_t r = t - static_cast<int64_t>(jj) * n;
+    const uint64_t g = idx[r];
+    const int64_t o = static_cast<int64_t>(j0 + jj) * n + r;
+    buckets[o] = static_cast<int64_t>(P.offset[jj]) + bucket_hash(g, P.a[jj], P.b[jj], P.size[jj]);
+    signs[o] = sign_negative(g, P.key[jj]) ? -1.0 : 1.0;
+  }
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  int64_t cap = static_cast<int64_t>(num_sms()) * 32;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+static int ceil_log2(int64_t v) {
+  int b = 0;
+  while ((int64_t{1} << b) < v) ++b;
+  return b;
+}
+
+static void fill_blocks(KeygenBlocks& P, const lvsk_hash_block* blocks, int j0, int nb) {
+  for (int jj = 0; jj < nb; ++jj) {
+    const lvsk_hash_block& B = blocks[j0 + jj];
+    P.a[jj] = B.a;
+    P.b[jj] = B.b;
+    P.key[jj] = B.sign_key;
+    P.offset[jj] = static_cast<uint32_t>(B.offset);
+    P.size[jj] = static_cast<uint32_t>(B.size);
+  }
+}
+
+template <typename T, int VEC>
+static void launch_gather(const void* X, int64_t ldx, int64_t d, const uint32_t* vals, const uint32_t* start,
+                          int64_t k, double scale, const double* hi_in, const double* lo_in, double* hi_out,
+                          double* lo_out, int32_t* flags, cudaStream_t st) {
+  const int nchunks = static_cast<int>((d + 32 * VEC - 1) / (32 * VEC));
+  const int64_t threads = k * nchunks * 32;
+  const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+  hashed_gather_kernel<T, VEC><<<grid, 256, 0, st>>>(static_cast<const T*>(X), ldx, d, nchunks, vals, start, k,
+                                                     scale, hi_in, lo_in, hi_out, lo_out, flags);
+}
+
+}  // namespace lvsk
+
+using namespace lvsk;
+
+extern "C" size_t lvsk_hashed_workspace_bytes(int64_t n, int32_t s, int64_t k) {
+  Measure m;
+  const int64_t N = n * s;
+  m.take<uint32_t>(N);  // keys
+  m.take<uint32_t>(N);  // vals
+  m.take<uint32_t>(N);  // sorted keys
+  m.take<uint32_t>(N);  // sorted vals
+  m.take<uint32_t>(k + 1);
+  radix::measure<uint32_t>(m, N);
+  return m.off;
+}
+
+extern "C" int32_t lvsk_hashed_sketch(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx,
+                                      uint64_t row0, const lvsk_hash_block* blocks, int32_t s, double scale,
+                                      const double* hi_in, const double* lo_in, double* hi_out, double* lo_out,
+                                      int64_t k, void* ws, size_t ws_bytes, int32_t* flags, void* stream) {
+  LVSK_REQUIRE(n >= 0 && d >= 1 && ldx >= d, LVSK_ERR_DIMENSION, "bad shape n=%lld d=%lld ldx=%lld",
+               (long long)n, (long long)d, (long long)ldx);
+  LVSK_REQUIRE(s >= 1 && k >= s, LVSK_ERR_CONFIGURATION, "need 1 <= s <= k (s=%d, k=%lld)", s, (long long)k);
+  LVSK_REQUIRE(k < (int64_t{1} << 31), LVSK_ERR_CAPACITY, "k=%lld too large", (long long)k);
+  LVSK_REQUIRE(n < (int64_t{1} << 31) && n * s < 0xFFFFFFFFll, LVSK_ERR_CAPACITY,
+               "row block of %lld rows x s=%d too large for one call; split it", (long long)n, s);
+  LVSK_REQUIRE(dtype == LVSK_F32 || dtype == LVSK_F64 || dtype == LVSK_BF16, LVSK_ERR_CONFIGURATION,
+               "unknown dtype %d", dtype);
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) {
+    if (hi_in != hi_out) copy_f64_kernel<<<grid_for(k * d, 256), 256, 0, st>>>(hi_in, hi_out, k * d);
+    if (lo_in != lo_out) copy_f64_kernel<<<grid_for(k * d, 256), 256, 0, st>>>(lo_in, lo_out, k * d);
+    LVSK_CHECK_LAUNCH("hashed copy");
+    return LVSK_OK;
+  }
+  const int64_t N = n * s;
+  Carve c(ws, ws_bytes);
+  uint32_t* keys = c.take<uint32_t>(N);
+  uint32_t* vals = c.take<uint32_t>(N);
+  uint32_t* skeys = c.take<uint32_t>(N);
+  uint32_t* svals = c.take<uint32_t>(N);
+  uint32_t* start = c.take<uint32_t>(k + 1);
+  auto rb = radix::carve<uint32_t>(c, N);
+  LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
+
+  for (int j0 = 0; j0 < s; j0 += KEYGEN_MAX_BLOCKS) {
+    const int nb = s - j0 < KEYGEN_MAX_BLOCKS ? s - j0 : KEYGEN_MAX_BLOCKS;
+    KeygenBlocks P;
+    fill_blocks(P, blocks, j0, nb);
+    hashed_keygen_kernel<<<grid_for(n * nb, 256), 256, 0, st>>>(n, row0, j0, nb, P, keys, vals);
+  }
+  LVSK_CHECK_LAUNCH("hashed keygen");
+  int32_t rc = radix::sort_pairs<uint32_t, uint32_t>(keys, vals, N, ceil_log2(k), rb, skeys, svals, st);
+  if (rc != LVSK_OK) return rc;
+  radix::bucket_bounds_kernel<uint32_t><<<grid_for(N + 1, 256), 256, 0, st>>>(skeys, N, k, start);
+  LVSK_CHECK_LAUNCH("bucket bounds");
+
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(X);
+  switch (dtype) {
+    case LVSK_F32:
+      if (xa % 16 == 0 && (ldx * 4) % 16 == 0 && d % 4 == 0)
+        launch_gather<float, 4>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
+      else
+        launch_gather<float, 1>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
+      break;
+    case LVSK_F64:
+      if (xa % 16 == 0 && (ldx * 8) % 16 == 0 && d % 2 == 0)
+        launch_gather<double, 2>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
+      else
+        launch_gather<double, 1>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
+      break;
+    default:
+      if (xa % 16 == 0 && (ldx * 2) % 16 == 0 && d % 8 == 0)
+        launch_gather<__nv_bfloat16, 8>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags,
+                                         st);
+      else
+        launch_gather<__nv_bfloat16, 1>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags,
+                                         st);
+  }
+  LVSK_CHECK_LAUNCH("hashed gather");
+  return LVSK_OK;
+}
+
+extern "C" int32_t lvsk_hash_rows(const uint64_t* idx, int64_t n, const lvsk_hash_block* blocks, int32_t s,
+                                  int64_t* buckets_out, double* signs_out, void* stream) {
+  LVSK_REQUIRE(n >= 0 && s >= 1, LVSK_ERR_CONFIGURATION, "bad arguments");
+  cudaStream_t st = as_stream(stream);
+  for (int j0 = 0; j0 < s; j0 += KEYGEN_MAX_BLOCKS) {
+    const int nb = s - j0 < KEYGEN_MAX_BLOCKS ? s - j0 : KEYGEN_MAX_BLOCKS;
+    KeygenBlocks P;
+    fill_blocks(P, blocks, j0, nb);
+    if (n > 0) hash_rows_kernel<<<grid_for(n * nb, 256), 256, 0, st>>>(idx, n, nb, P, j0, buckets_out, signs_out);
+  }
+  LVSK_CHECK_LAUNCH("hash rows");
+  return LVSK_OK;
+}
+
+extern "C" int32_t lvsk_merge_compensated(const double* hi1, const double* lo1, const double* hi2,
+                                          const double* lo2, double* hi_out, double* lo_out, int64_t count,
+                                          void* stream) {
+  if (count <= 0) return LVSK_OK;
+  merge_kernel<<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(hi1, lo1, hi2, lo2, hi_out, lo_out, count);
+  LVSK_CHECK_LAUNCH("merge");
+  return LVSK_OK;
+}
+
+namespace lvsk {
+__global__ void fold_kernel(const double* hi, const double* lo, double* out, int64_t count) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __dadd_rn(hi[i], lo[i]);
+}
+}  // namespace lvsk
+
+extern "C" int32_t lvsk_fold_compensated(const double* hi, const double* lo, double* out, int64_t count,
+                                         void* stream) {
+  if (count <= 0) return LVSK_OK;
+  fold_kernel<<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(hi, lo, out, count);
+  LVSK_CHECK_LAUNCH("fold");
+  return LVSK_OK;
+}

@@ -1,0 +1,276 @@
+"""Leverage scores: exact, oracle, and the two sketched variants (+ JL fold).
+
+Drop-in for the reference module (pkg/src/levsketch/leverage.py:33-185).
+The sketched methods run entirely on the device:
+
+    X --K1/K3/K4--> SX (k x d, float64) --cuSOLVER fp64--> sigma, V
+      --truncate (strict, relative)--> fold M (d x r) --K5--> ||X M||^2
+
+``jl_dim=r`` (extension, BASELINE configs) replaces the d x r' basis V'/sigma'
+by the basis-free JL fold M = V' diag(1/sigma') V'^T Pi with
+Pi ~ N(0, 1/r) (d x r) drawn from Philox(SeedSequence([0x4A4C, jl_seed]));
+with Pi = I it reduces to the reference scores exactly.  ``rank=`` caps the
+kept components (fixed-rank truncation, BASELINE config 5).
+"""
+
+from __future__ import annotations
+
+import csv
+import json
+import math
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .config import ensure_capacity
+from .errors import CapacityError, DegenerateInputError, FormatError, SingularInversionError
+from .matrix import device_matrix, format_float
+from .sketch import SketchSpec, apply_sketch, sketch_rows
+from .svd import SvdResult, thin_svd, truncate
+
+MACHINE_RANK_TOL = 1e-12
+ORACLE_MAX_ROWS = 5000
+_JL_STREAM = 0x4A4C
+
+
+@dataclass
+class LeverageResult:
+    scores: np.ndarray
+    method: str
+    effective_rank: int
+    eps: float = 0.0
+    spec: SketchSpec | None = None
+    sv_tol: float | None = None
+    wall_time_s: float | None = None
+
+
+# ---------------------------------------------------------------------------
+# device building blocks shared with pipeline.py and dist.py
+
+
+def jl_matrix(seed: int, d: int, r: int) -> np.ndarray:
+    """Pi (d x r) with N(0, 1/r) entries; host-drawn once, identical to the oracle."""
+    g = np.random.Generator(np.random.Philox(np.random.SeedSequence([_JL_STREAM, seed])))
+    return g.standard_normal((d, r)) / math.sqrt(r)
+
+
+_JL_CACHE: dict = {}
+
+
+def jl_device(seed: int, d: int, r: int) -> torch.Tensor:
+    key = (seed, d, r, N.device())
+    if key not in _JL_CACHE:
+        _JL_CACHE[key] = torch.from_numpy(jl_matrix(seed, d, r)).to(N.device())
+    return _JL_CACHE[key]
+
+
+def factor_device(sx: torch.Tensor, sv_tol: float | None, rank: int | None = None, method: str = "auto"):
+    """(sigma, vt) of SX on the device in float64, truncated like svd.truncate
+    (strict relative threshold) and optionally capped at ``rank``.
+
+    method "svd": cuSOLVER gesvd of the k x d sketch.  "gram": eigh of the
+    d x d Gram SX^T SX (k >= d; its small-sigma accuracy is eps*sigma_1^2/
+    sigma_j^2, so "auto" only picks it when the truncation threshold
+    discards every component it could misjudge)."""
+    k, d = sx.shape
+    if method == "auto":
+        method = "gram" if (sv_tol is not None and sv_tol >= 1e-6 and k >= d and d >= 256) else "svd"
+    if method == "gram":
+        g = sx.T @ sx
+        lam, v = torch.linalg.eigh(g)
+        sigma = torch.sqrt(torch.clamp(lam.flip(0), min=0.0))
+        vt = v.flip(1).T
+    else:
+        _, sigma, vt = torch.linalg.svd(sx, full_matrices=False, driver="gesvd")
+    s_host = sigma.cpu().numpy()
+    if sv_tol is not None:
+        if s_host.shape[0] == 0 or s_host[0] <= 0:
+            raise DegenerateInputError("cannot truncate an all-zero matrix (largest singular value is 0)")
+        r = int(np.count_nonzero(s_host > sv_tol * s_host[0]))
+    else:
+        r = s_host.shape[0]
+    if rank is not None:
+        r = min(r, rank)
+    return sigma[:r], vt[:r], s_host[:r]
+
+
+def fold_device(sigma: torch.Tensor, vt: torch.Tensor, s_host: np.ndarray, pi: torch.Tensor | None) -> torch.Tensor:
+    """M = V'/sigma' (d x r', leverage.py:75-85) or the JL fold V' S'^-1 V'^T Pi."""
+    if np.any(s_host == 0.0):
+        raise SingularInversionError("sketch has an exactly-zero singular value; use the truncated method")
+    basis = vt.T / sigma
+    if pi is None:
+        return basis.contiguous()
+    return (basis @ (vt @ pi)).contiguous()
+
+
+def split_m(M: torch.Tensor, x_dtype: torch.dtype):
+    """float64 M -> the K5 operand(s): float64 for float64 X, else fp32 hi + lo."""
+    if x_dtype == torch.float64:
+        return M.contiguous(), None
+    hi = M.to(torch.float32)
+    lo = (M - hi.to(torch.float64)).to(torch.float32)
+    return hi.contiguous(), lo.contiguous()
+
+
+def scores_device(X: torch.Tensor, M: torch.Tensor, out: torch.Tensor | None = None, flags=None) -> torch.Tensor:
+    """K5: ||X[i] M||^2 for every row (float64 scores on the device)."""
+    n, d = X.shape
+    r = M.shape[1]
+    if M.shape[0] != d:
+        from .errors import DimensionMismatchError
+
+        raise DimensionMismatchError(f"basis has {M.shape[0]} rows, expected {d}")
+    m_hi, m_lo = split_m(M, X.dtype)
+    if out is None:
+        out = torch.empty(n, dtype=torch.float64, device=X.device)
+    own = flags is None
+    flags = flags or N.Flags()
+    N.check(
+        N.lib().lvsk_rowsumsq_gemm(
+            X.data_ptr(), N.dtype_code(X), n, d, X.stride(0), m_hi.data_ptr(), N.ptr(m_lo), r,
+            out.data_ptr(), flags.p, N.stream_ptr(),
+        ),
+        "leverage pass",
+    )
+    if own and flags.read() & N.FLAG_NONFINITE:
+        raise FormatError("matrix contains non-finite entries")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference API
+
+
+def leverage_exact(a) -> LeverageResult:
+    """Exact scores from the thin-SVD left factor (reference leverage.py:44-53;
+    a test oracle, computed in float64 on the device)."""
+    X = device_matrix(a).to(torch.float64)
+    u, s, _ = torch.linalg.svd(X, full_matrices=False, driver="gesvd")
+    s_host = s.cpu().numpy()
+    if s_host[0] <= 0:
+        raise DegenerateInputError("leverage scores of an all-zero matrix are undefined")
+    r = int(np.count_nonzero(s_host > MACHINE_RANK_TOL * s_host[0]))
+    ur = u[:, :r]
+    scores = (ur * ur).sum(dim=1)
+    return LeverageResult(scores=scores.cpu().numpy(), method="exact", effective_rank=r)
+
+
+def leverage_oracle(a) -> LeverageResult:
+    """Projector-based scores A (A^T A)^+ A^T (reference leverage.py:56-72)."""
+    X = device_matrix(a).to(torch.float64)
+    n = X.shape[0]
+    if n > ORACLE_MAX_ROWS:
+        raise CapacityError(f"oracle forms an n x n projector; n={n} exceeds {ORACLE_MAX_ROWS}")
+    ensure_capacity(8 * n * n, "projection matrix")
+    if not bool(X.any()):
+        raise DegenerateInputError("leverage scores of an all-zero matrix are undefined")
+    h = X @ torch.linalg.pinv(X.T @ X) @ X.T
+    scores = (h * h).sum(dim=1)
+    rank = int(round(float(torch.trace(h))))
+    return LeverageResult(scores=scores.cpu().numpy(), method="oracle", effective_rank=rank)
+
+
+def _approx_basis(svd: SvdResult) -> np.ndarray:
+    """V / sigma columnwise, refusing an exactly-zero sigma (leverage.py:75-85)."""
+    if np.any(svd.sigma == 0.0):
+        raise SingularInversionError("sketch has an exactly-zero singular value; use the truncated method")
+    return svd.vt.T / svd.sigma
+
+
+def _block_scores(rows, basis) -> np.ndarray:
+    """Squared row norms of rows @ basis through K5 (leverage.py:88-95)."""
+    X = device_matrix(rows)
+    M = basis if isinstance(basis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(basis, dtype=np.float64))
+    M = M.to(X.device, torch.float64)
+    return scores_device(X, M).cpu().numpy()
+
+
+def _sketched(a, spec, sv_tol, mem_cap_bytes, jl_dim, jl_seed, rank, method):
+    X = device_matrix(a)
+    state = apply_sketch(X, spec, mem_cap=mem_cap_bytes)
+    sx = state.data_device
+    sigma, vt, s_host = factor_device(sx, sv_tol, rank)
+    pi = None if jl_dim is None else jl_device(jl_seed, X.shape[1], jl_dim)
+    M = fold_device(sigma, vt, s_host, pi)
+    scores = scores_device(X, M)
+    return LeverageResult(
+        scores=scores.cpu().numpy(),
+        method=method,
+        effective_rank=int(s_host.shape[0]),
+        eps=spec.eps,
+        spec=spec,
+        sv_tol=sv_tol,
+    )
+
+
+def leverage_sketched(a, spec: SketchSpec, mem_cap_bytes: int | None = None, *, jl_dim: int | None = None,
+                      jl_seed: int = 0) -> LeverageResult:
+    """Uncorrected sketched scores (reference leverage.py:98-112)."""
+    return _sketched(a, spec, None, mem_cap_bytes, jl_dim, jl_seed, None, "sketch")
+
+
+def leverage_sketched_trunc(a, spec: SketchSpec, sv_tol: float, mem_cap_bytes: int | None = None, *,
+                            jl_dim: int | None = None, jl_seed: int = 0, rank: int | None = None) -> LeverageResult:
+    """Sketched scores with components sigma_j <= sv_tol * sigma_1 dropped
+    (reference leverage.py:115-132)."""
+    from .errors import ConfigurationError
+
+    if not 0 <= sv_tol < 1:
+        raise ConfigurationError(f"truncation threshold must be in [0, 1), got {sv_tol}")
+    return _sketched(a, spec, sv_tol, mem_cap_bytes, jl_dim, jl_seed, rank, "sketch_trunc")
+
+
+# ---------------------------------------------------------------------------
+# scores CSV + JSON sidecar (reference leverage.py:139-185)
+
+
+def save_scores(result: LeverageResult, csv_path, meta_path=None, extra_meta: dict | None = None) -> None:
+    csv_path = Path(csv_path)
+    meta_path = Path(meta_path) if meta_path is not None else Path(str(csv_path) + ".json")
+    with open(csv_path, "w") as f:
+        for i, v in enumerate(np.asarray(result.scores)):
+            f.write(f"{i},{format_float(v)}\n")
+    meta = {
+        "method": result.method,
+        "eps": result.eps,
+        "sv_tol": result.sv_tol,
+        "effective_rank": result.effective_rank,
+        "seed": result.spec.seed if result.spec is not None else None,
+        "wall_time_s": result.wall_time_s,
+        "n": int(np.asarray(result.scores).shape[0]),
+    }
+    if result.spec is not None:
+        meta["sketch"] = {
+            "family": result.spec.family,
+            "k": sketch_rows(result.spec),
+            "osnap_s": result.spec.osnap_s,
+            "rows_override": result.spec.rows_override,
+            "sizing_c": result.spec.sizing_c,
+        }
+    if extra_meta:
+        meta.update(extra_meta)
+    with open(meta_path, "w") as f:
+        json.dump(meta, f, indent=2, sort_keys=True)
+        f.write("\n")
+
+
+def load_scores(path) -> np.ndarray:
+    path = Path(path)
+    scores = []
+    with open(path) as f:
+        for lineno, row in enumerate(csv.reader(f), start=1):
+            if not row:
+                continue
+            if len(row) != 2:
+                raise FormatError(f"{path}: expected index,score at line {lineno}, got {len(row)} fields")
+            try:
+                scores.append(float(row[1]))
+            except ValueError:
+                raise FormatError(f"{path}: non-numeric score {row[1]!r} at line {lineno}") from None
+    if not scores:
+        raise FormatError(f"{path}: no scores found")
+    return np.asarray(scores, dtype=np.float64)

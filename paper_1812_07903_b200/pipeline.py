@@ -1,0 +1,161 @@
+"""Preallocated device-resident leverage pipeline (the bench / serving path).
+
+One ``run(X)`` is the whole hot path of reference leverage_sketched_trunc +
+scores_to_distribution + make_plan("dec") (leverage.py:115-132,
+order.py:51-100) on a CUDA-resident X:
+
+    sketch (K1 | K3 | K4) -> fold SX -> fp64 factorisation (cuSOLVER)
+    -> truncate + fold M -> K5 leverage pass -> normalise -> K7 argsort
+
+All buffers and workspaces are allocated once in the constructor; the only
+host synchronisations per run are the factorisation's (cuSOLVER returns
+its spectrum to pick the truncation rank) and the final flag check.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import FormatError
+from .leverage import factor_device, fold_device, jl_device, split_m
+from .sketch import GAUSSIAN, SRHT, SketchSpec, SketchState, sketch_rows
+
+STAGES = ("sketch", "factor", "leverage", "order")
+
+
+class LeveragePipeline:
+    def __init__(self, spec: SketchSpec, n: int, d: int, dtype=torch.float32, sv_tol: float = 1e-6,
+                 jl_dim: int | None = None, jl_seed: int = 0, rank: int | None = None, order: bool = True,
+                 row0: int = 0, factor_method: str = "auto"):
+        if d != spec.d:
+            raise ValueError(f"spec.d={spec.d} but d={d}")
+        self.spec, self.n, self.d, self.dtype = spec, n, d, dtype
+        self.sv_tol, self.rank, self.order, self.row0 = sv_tol, rank, order, row0
+        self.factor_method = factor_method
+        self.k = sketch_rows(spec)
+        dev = N.device()
+        self.dev = dev
+        self.state = SketchState(spec, n, mem_cap=1 << 62)
+        self.sx = torch.empty((self.k, d), dtype=torch.float64, device=dev)
+        code = {torch.float32: N.LVSK_F32, torch.float64: N.LVSK_F64, torch.bfloat16: N.LVSK_BF16}[dtype]
+        self.code = code
+        L = N.lib()
+        if spec.family == SRHT:
+            wsb = L.lvsk_srht_workspace_bytes(self.state._m, d, code, self.k)
+        elif spec.family == GAUSSIAN:
+            wsb = L.lvsk_gaussian_workspace_bytes(n, d, self.k, code)
+        else:
+            wsb = L.lvsk_hashed_workspace_bytes(n, spec.s, self.k)
+        self.ws_sketch = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
+        self.scores = torch.empty(n, dtype=torch.float64, device=dev)
+        self.p = torch.empty(n, dtype=torch.float64, device=dev)
+        self.total = torch.empty(1, dtype=torch.float64, device=dev)
+        self.idx = torch.empty(n, dtype=torch.int64, device=dev)
+        self.ws_norm = torch.empty(max(L.lvsk_normalize_workspace_bytes(n), 256), dtype=torch.uint8, device=dev)
+        self.ws_sort = torch.empty(max(L.lvsk_argsort_workspace_bytes(n), 256), dtype=torch.uint8, device=dev)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.pi = None if jl_dim is None else jl_device(jl_seed, d, jl_dim)
+        self.effective_rank = None
+        self.events = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in STAGES}
+
+    # -- stages ------------------------------------------------------------
+    def _sketch(self, X: torch.Tensor) -> None:
+        L, st, s = N.lib(), N.stream_ptr(), self.state
+        fam = self.spec.family
+        ldx = X.stride(0)
+        if fam == SRHT:
+            N.check(L.lvsk_srht(X.data_ptr(), self.code, self.n, self.d, ldx, s._m, s._signs_dev.data_ptr(),
+                                s._sample_dev.data_ptr(), self.k, math.sqrt(self.k), self.sx.data_ptr(),
+                                self.ws_sketch.data_ptr(), self.ws_sketch.numel(), self.flags.data_ptr(), st), "srht")
+        elif fam == GAUSSIAN:
+            N.check(L.lvsk_gaussian_sketch(X.data_ptr(), self.code, self.n, self.d, ldx, self.row0, self.spec.seed,
+                                           self.k, self.sx.data_ptr(), 0, self.ws_sketch.data_ptr(),
+                                           self.ws_sketch.numel(), self.flags.data_ptr(), st), "gaussian")
+        else:
+            s._hi.zero_()
+            s._lo.zero_()
+            N.check(L.lvsk_hashed_sketch(X.data_ptr(), self.code, self.n, self.d, ldx, self.row0, s._blocks,
+                                         self.spec.s, s._scale, s._hi.data_ptr(), s._lo.data_ptr(), s._hi.data_ptr(),
+                                         s._lo.data_ptr(), self.k, self.ws_sketch.data_ptr(), self.ws_sketch.numel(),
+                                         self.flags.data_ptr(), st), "hashed sketch")
+            N.check(L.lvsk_fold_compensated(s._hi.data_ptr(), s._lo.data_ptr(), self.sx.data_ptr(), self.sx.numel(), st),
+                    "fold")
+
+    def _factor(self) -> None:
+        sigma, vt, s_host = factor_device(self.sx, self.sv_tol, self.rank, self.factor_method)
+        self.effective_rank = int(s_host.shape[0])
+        M = fold_device(sigma, vt, s_host, self.pi)
+        self.m_hi, self.m_lo = split_m(M, self.dtype)
+        self.r = M.shape[1]
+
+    def _leverage(self, X: torch.Tensor) -> None:
+        N.check(N.lib().lvsk_rowsumsq_gemm(X.data_ptr(), self.code, self.n, self.d, X.stride(0),
+                                           self.m_hi.data_ptr(), N.ptr(self.m_lo), self.r, self.scores.data_ptr(),
+                                           self.flags.data_ptr(), N.stream_ptr()), "leverage pass")
+
+    def _order(self) -> None:
+        L, st = N.lib(), N.stream_ptr()
+        N.check(L.lvsk_normalize_scores(self.scores.data_ptr(), self.n, self.p.data_ptr(), self.total.data_ptr(),
+                                        self.ws_norm.data_ptr(), self.ws_norm.numel(), self.flags.data_ptr(), st),
+                "normalize")
+        N.check(L.lvsk_argsort_f64(self.p.data_ptr(), self.n, 1, self.idx.data_ptr(), self.ws_sort.data_ptr(),
+                                   self.ws_sort.numel(), st), "argsort")
+
+    # -- public --------------------------------------------------------------
+    def run(self, X: torch.Tensor, timing: bool = False, check: bool = True):
+        """Full pass over device-resident X (n x d, self.dtype).  Returns
+        (scores, order) CUDA tensors (order is None when order=False)."""
+        if X.shape != (self.n, self.d) or X.dtype != self.dtype or X.stride(1) != 1:
+            raise ValueError(f"expected a ({self.n}, {self.d}) {self.dtype} row-major CUDA tensor")
+        self.flags.zero_()
+        ev = self.events
+        steps = [("sketch", lambda: self._sketch(X)), ("factor", self._factor), ("leverage", lambda: self._leverage(X))]
+        if self.order:
+            steps.append(("order", self._order))
+        for name, fn in steps:
+            if timing:
+                ev[name][0].record()
+            fn()
+            if timing:
+                ev[name][1].record()
+        if check:
+            self.check()
+        return self.scores, (self.idx if self.order else None)
+
+    def stage_ms(self) -> dict:
+        torch.cuda.synchronize()
+        out = {}
+        for name in STAGES:
+            a, b = self.events[name]
+            try:
+                out[name] = a.elapsed_time(b)
+            except RuntimeError:
+                pass
+        return out
+
+    def check(self) -> None:
+        f = int(self.flags.item())
+        if f & N.FLAG_NONFINITE:
+            raise FormatError("matrix contains non-finite entries")
+
+    def launches_per_run(self) -> int:
+        """Kernels this library launches per run() (host-side count)."""
+        fam = self.spec.family
+        radix = lambda items, bits: 3 * max(1, (bits + 7) // 8)  # noqa: E731
+        if fam == SRHT:
+            m = self.state._m
+            L = int(math.log2(m))
+            cb = 8 if L <= 8 else min(L, 16)
+            chunks = max(1, -(-self.n // (1 << cb)))
+            sk = 1 + radix(self.k, 8) + 1 + 2 * chunks
+        elif fam == GAUSSIAN:
+            sk = 2
+        else:
+            sk = 1 + radix(self.n * self.spec.s, max(1, (self.k - 1).bit_length())) + 1 + 1 + 1
+        lev = 1
+        order = (3 + 1 + radix(self.n, 64)) if self.order else 0
+        return sk + lev + order

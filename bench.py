@@ -179,9 +179,10 @@ def run_reference(args, cfg, rank: int):
         threadpool_limits(threads)
     except ImportError:
         pass
-    sample = args.ref_rows
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_leg(cfg, min(sample, 20_000), threads)
+    # adaptive sample: the whole --steps K run should take about two minutes
+    rate, _ = cpu_leg(cfg, 20_000, threads)
+    per_step_s = 120.0 / max(1, args.steps)
+    sample = int(min(args.ref_rows, max(10_000, rate * per_step_s)))
     times = []
     for _ in range(args.steps):
         _, dt = cpu_leg(cfg, sample, threads)
@@ -223,7 +224,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
 
     import paper_1812_07903_b200 as P
     from paper_1812_07903_b200 import _native as N
-    from paper_1812_07903_b200.leverage import factor_device, fold_device, jl_device, split_m
+    from paper_1812_07903_b200.leverage import jl_device, sketch_fold
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -269,11 +270,9 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             ev["factor"][0].record()
         M = torch.empty((d, r), dtype=torch.float64, device=dev)
         if rank == 0:
-            sigma, vt, s_host = factor_device(pipe.sx, cfg["sv_tol"], None)
-            M.copy_(fold_device(sigma, vt, s_host, pi))
+            M.copy_(sketch_fold(pipe.sx, cfg["sv_tol"], None, pi)[0])
         dist.broadcast(M, 0)
-        pipe.m_hi, pipe.m_lo = split_m(M, dtype)
-        pipe.r = r
+        pipe.set_fold(M)
         if timing:
             ev["factor"][1].record()
             ev["leverage"][0].record()

@@ -76,10 +76,6 @@ __global__ void __launch_bounds__(256) rowsumsq_simt_kernel(const T* __restrict_
   if (__syncthreads_or(bad) && tid == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
 }
 
-// implemented in leverage_tc.cu; returns false when the shape is not covered
-bool rowsumsq_tc_f32(const float* X, int64_t n, int64_t d, int64_t ldx, const float* M_hi, const float* M_lo,
-                     int64_t r, double* scores, int32_t* flags, cudaStream_t st, int32_t* rc);
-
 }  // namespace lvsk
 
 using namespace lvsk;
@@ -94,10 +90,6 @@ extern "C" int32_t lvsk_rowsumsq_gemm(const void* X, int32_t dtype, int64_t n, i
   const unsigned grid = static_cast<unsigned>((n + L_BM - 1) / L_BM);
   switch (dtype) {
     case LVSK_F32: {
-      int32_t rc = LVSK_OK;
-      if (rowsumsq_tc_f32(static_cast<const float*>(X), n, d, ldx, static_cast<const float*>(M),
-                          static_cast<const float*>(M_lo), r, scores, flags, st, &rc))
-        return rc;
       rowsumsq_simt_kernel<float, float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx,
                                                                static_cast<const float*>(M), r, scores, flags);
       break;

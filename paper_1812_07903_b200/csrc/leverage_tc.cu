@@ -1,9 +1,371 @@
-// K5 tensor-core path (placeholder until the tcgen05 kernel lands).
+// K5 on the 5th-gen tensor cores: scores[i] = || X[i,:] M ||^2, fp32 X,
+// 3xTF32 split for fp32-level accuracy, accumulators in TMEM.
+//
+// Reference: _block_scores (pkg/src/levsketch/leverage.py:88-95).
+//
+// Per CTA (persistent, one per SM): row tiles of 256 rows = two M=128 UMMA
+// sub-tiles; K streamed in 32-float (128 B) chunks through a 4-stage
+// TMA -> smem ring (SWIZZLE_128B, K-major).  Per stage:
+//   warp 0   TMA: X[256 x 32] + Mt_hi[N x 32] + Mt_lo[N x 32]     (full)
+//   warp 1   MMA: acc += x.Mhi + x.Mlo         (tcgen05 kind::tf32) (xdone)
+//   warps 2-5     x -> x_lo = x - tf32(x) in place (+ finiteness)    (loready)
+//   warp 1   MMA: acc += x_lo.Mhi                                    (empty)
+// and at the end of a row tile warps 2-5 drain the TMEM accumulator
+// (tcgen05.ld 32x32b), square and row-reduce in registers and write float64
+// scores.  Accumulators are double-buffered in TMEM so the epilogue of tile
+// t overlaps the MMAs of tile t+1.  X is read from HBM exactly once.
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace lvsk {
-bool rowsumsq_tc_f32(const float*, int64_t, int64_t, int64_t, const float*, const float*, int64_t, double*, int32_t*,
-                     cudaStream_t, int32_t*) {
-  return false;
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int SUB = 2;
+constexpr int TILE_ROWS = BM * SUB;  // 256
+constexpr int BK = 32;               // fp32 per 128-byte swizzle row
+constexpr int THREADS = 192;
+constexpr int EPI_THREADS = 128;
+
+template <int N>
+struct Cfg {
+  static constexpr int STAGES = N <= 64 ? 4 : 3;
+  static constexpr int X_BYTES = TILE_ROWS * BK * 4;  // 32 KB
+  static constexpr int M_BYTES = N * BK * 4;
+  static constexpr int STAGE_BYTES = X_BYTES + 2 * M_BYTES;
+  static constexpr int ACC_COLS = SUB * N;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // instruction descriptor: F32 accum, A/B TF32, K-major both, N>>3, M>>4
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+// K-major, SWIZZLE_128B canonical layout: 8-row x 128 B atoms, SBO = 1024 B.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= uint64_t{1} << 16;             // LBO (ignored for swizzled K-major)
+  d |= uint64_t{1024 >> 4} << 32;     // SBO
+  d |= uint64_t{1} << 46;             // descriptor version (sm100)
+  d |= uint64_t{2} << 61;             // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+template <int N>
+__global__ void __launch_bounds__(THREADS, 1)
+    leverage_tf32x3_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapHi,
+                           const __grid_constant__ CUtensorMap mapLo, int64_t n, int kchunks,
+                           double* __restrict__ scores, int32_t* flags) {
+  using C = Cfg<N>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* xdone = bars + C::STAGES;
+  uint64_t* loready = bars + 2 * C::STAGES;
+  uint64_t* empty = bars + 3 * C::STAGES;
+  uint64_t* accfull = bars + 4 * C::STAGES;
+  uint64_t* accempty = accfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&xdone[s], 1);
+      mbar_init(&loready[s], EPI_THREADS);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accfull[b], 1);
+      mbar_init(&accempty[b], EPI_THREADS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapHi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapLo) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint64_t pol_x = l2_policy_evict_first(), pol_m = l2_policy_evict_last();
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          tma_load_2d(&mapX, &full[s], st, kc * BK, static_cast<int>(t * TILE_ROWS), pol_x);
+          tma_load_2d(&mapHi, &full[s], st + C::X_BYTES, kc * BK, 0, pol_m);
+          tma_load_2d(&mapLo, &full[s], st + C::X_BYTES + C::M_BYTES, kc * BK, 0, pol_m);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread) ----------------
+    if (lane == 0) {
+      uint32_t it = 0, lt = 0;
+      int64_t pend = -1;  // stage iteration whose x_lo MMAs are outstanding
+      uint32_t pend_acc = 0;
+      bool pend_last = false;
+      auto issue_lo = [&](uint32_t pit, uint32_t acc_col, bool last) {
+        const uint32_t ps = pit % C::STAGES, pph = (pit / C::STAGES) & 1u;
+        mbar_wait(&loready[ps], pph);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + ps * C::STAGE_BYTES);
+        const uint64_t bhi = sw128_desc(st + C::X_BYTES);
+#pragma unroll
+        for (int sub = 0; sub < SUB; ++sub) {
+          const uint64_t a = sw128_desc(st + sub * (BM * 128));
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            umma_tf32(tmem_base + acc_col + sub * N, a + 2 * kk, bhi + 2 * kk, C::IDESC, 1u);
+        }
+        umma_commit(&empty[ps]);
+        if (last) umma_commit(&accfull[(acc_col / C::ACC_COLS) & 1u]);
+      };
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        const uint32_t ab = lt & 1u, aph = (lt >> 1) & 1u;
+        const uint32_t acc_col = ab * C::ACC_COLS;
+        mbar_wait(&accempty[ab], aph ^ 1u);
+        tc_fence_after();
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
+          const uint64_t bhi = sw128_desc(st + C::X_BYTES);
+          const uint64_t blo = sw128_desc(st + C::X_BYTES + C::M_BYTES);
+#pragma unroll
+          for (int sub = 0; sub < SUB; ++sub) {
+            const uint64_t a = sw128_desc(st + sub * (BM * 128));
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t d = tmem_base + acc_col + sub * N;
+              umma_tf32(d, a + 2 * kk, bhi + 2 * kk, C::IDESC, (kc | kk) ? 1u : 0u);
+              umma_tf32(d, a + 2 * kk, blo + 2 * kk, C::IDESC, 1u);
+            }
+          }
+          umma_commit(&xdone[s]);
+          if (pend >= 0) issue_lo(static_cast<uint32_t>(pend), pend_acc, pend_last);
+          pend = it;
+          pend_acc = acc_col;
+          pend_last = kc == kchunks - 1;
+        }
+      }
+      if (pend >= 0) issue_lo(static_cast<uint32_t>(pend), pend_acc, pend_last);
+    }
+  } else {
+    // ---------------- transform + epilogue (warps 2..5) ----------------
+    const int et = threadIdx.x - 64;
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    bool bad = false;
+    uint32_t it = 0, lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        mbar_wait(&xdone[s], ph);
+        float4* xs = reinterpret_cast<float4*>(smem + s * C::STAGE_BYTES);
+#pragma unroll 4
+        for (int i = et; i < C::X_BYTES / 16; i += EPI_THREADS) {
+          float4 v = xs[i];
+          bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+          v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          xs[i] = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&loready[s]);
+      }
+      // epilogue for tile t
+      const uint32_t ab = lt & 1u, aph = (lt >> 1) & 1u;
+      mbar_wait(&accfull[ab], aph);
+      tc_fence_after();
+#pragma unroll
+      for (int sub = 0; sub < SUB; ++sub) {
+        float acc = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + ab * C::ACC_COLS + sub * N + c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float u = __uint_as_float(v[j]);
+            acc = fmaf(u, u, acc);
+          }
+        }
+        const int64_t row = t * TILE_ROWS + sub * BM + quarter * 32 + lane;
+        if (row < n) scores[row] = static_cast<double>(acc);
+      }
+      tc_fence_before();
+      mbar_arrive(&accempty[ab]);
+    }
+    if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeFn>(nullptr);
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                     uint32_t box_inner, uint32_t box_outer) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int N>
+static int32_t launch(const float* X, int64_t n, int64_t d, int64_t ldx, const float* Mt_hi, const float* Mt_lo,
+                      int64_t r, double* scores, int32_t* flags, cudaStream_t st) {
+  using C = Cfg<N>;
+  CUtensorMap mx, mh, ml;
+  if (!make_map(&mx, X, d, n, ldx * 4, BK, TILE_ROWS) || !make_map(&mh, Mt_hi, d, r, d * 4, BK, N) ||
+      !make_map(&ml, Mt_lo, d, r, d * 4, BK, N)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return LVSK_ERR_CUDA;
+  }
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(leverage_tf32x3_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "leverage tc smem attribute");
+    attr_done = true;
+  }
+  const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
+  const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
+  const int kchunks = static_cast<int>((d + BK - 1) / BK);
+  leverage_tf32x3_kernel<N><<<grid, THREADS, C::SMEM_BYTES, st>>>(mx, mh, ml, n, kchunks, scores, flags);
+  LVSK_CHECK_LAUNCH("leverage tf32x3");
+  return LVSK_OK;
+}
+
+}  // namespace tc
 }  // namespace lvsk
+
+using namespace lvsk;
+
+extern "C" int32_t lvsk_leverage_tf32x3(const float* X, int64_t n, int64_t d, int64_t ldx, const float* Mt_hi,
+                                        const float* Mt_lo, int64_t r, double* scores, int32_t* flags,
+                                        void* stream) {
+  LVSK_REQUIRE(n >= 0 && d >= 1 && ldx >= d && r >= 1, LVSK_ERR_DIMENSION, "bad shape");
+  LVSK_REQUIRE(r <= 128, LVSK_ERR_UNSUPPORTED, "tensor-core leverage pass supports r <= 128 (got %lld)", (long long)r);
+  LVSK_REQUIRE(reinterpret_cast<uintptr_t>(X) % 16 == 0 && (ldx * 4) % 16 == 0 && (d * 4) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(Mt_hi) % 16 == 0 && reinterpret_cast<uintptr_t>(Mt_lo) % 16 == 0,
+               LVSK_ERR_UNSUPPORTED, "tensor-core leverage pass needs 16-byte aligned rows");
+  LVSK_REQUIRE(n < (int64_t{1} << 31), LVSK_ERR_UNSUPPORTED, "n too large for one launch");
+  if (n == 0) return LVSK_OK;
+  cudaStream_t st = as_stream(stream);
+  if (r <= 64) return tc::launch<64>(X, n, d, ldx, Mt_hi, Mt_lo, r, scores, flags, st);
+  return tc::launch<128>(X, n, d, ldx, Mt_hi, Mt_lo, r, scores, flags, st);
+}

@@ -13,10 +13,10 @@ namespace lvsk {
 namespace radix {
 
 constexpr int THREADS = 256;
-constexpr int ITEMS = 16;
-constexpr int TILE = THREADS * ITEMS;  // 4096 keys per tile
+constexpr int ITEMS = 8;
+constexpr int TILE = THREADS * ITEMS;  // 2048 keys per tile
 constexpr int WARPS = THREADS / 32;
-constexpr int WARP_ITEMS = TILE / WARPS;  // 512 contiguous keys per warp
+constexpr int WARP_ITEMS = TILE / WARPS;  // 256 contiguous keys per warp
 constexpr int RADIX = 256;
 constexpr int SCAN_THREADS = 1024;
 
@@ -39,44 +39,74 @@ __global__ void __launch_bounds__(THREADS) hist_kernel(const K* __restrict__ key
   for (int dg = threadIdx.x; dg < RADIX; dg += THREADS) hist[dg * ntiles + blockIdx.x] = h[dg];
 }
 
-// Exclusive scan of `total` uint32 counts in one block (digit-major layout).
-static __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(uint32_t* __restrict__ data, int64_t total) {
-  __shared__ uint32_t sums[SCAN_THREADS];
-  const int64_t per = (total + SCAN_THREADS - 1) / SCAN_THREADS;
-  const int64_t lo = threadIdx.x * per;
-  const int64_t hi = min(total, lo + per);
-  uint32_t s = 0;
-  for (int64_t i = lo; i < hi; ++i) s += data[i];
-  sums[threadIdx.x] = s;
+// Block-wide exclusive scan of one value per thread (THREADS threads).
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* sh_warp, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) sh_warp[warp] = x;
   __syncthreads();
-  // Hillis-Steele inclusive scan of the per-thread sums
-  for (int off = 1; off < SCAN_THREADS; off <<= 1) {
-    uint32_t v = threadIdx.x >= off ? sums[threadIdx.x - off] : 0u;
-    __syncthreads();
-    sums[threadIdx.x] += v;
-    __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < WARPS ? sh_warp[lane] : 0u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, off);
+      if (lane >= off) w += y;
+    }
+    if (lane < WARPS) sh_warp[lane] = w;  // inclusive warp totals
   }
-  uint32_t run = threadIdx.x ? sums[threadIdx.x - 1] : 0u;
-  for (int64_t i = lo; i < hi; ++i) {
-    uint32_t v = data[i];
-    data[i] = run;
-    run += v;
+  __syncthreads();
+  total = sh_warp[WARPS - 1];
+  const uint32_t base = warp ? sh_warp[warp - 1] : 0u;
+  __syncthreads();
+  return base + x - v;
+}
+
+// Row scan: block d turns hist[d][0..ntiles) into its exclusive prefix and
+// writes the row total to totals[d] (digit-major layout, one block per digit).
+static __global__ void __launch_bounds__(THREADS) scan_rows_kernel(uint32_t* __restrict__ hist, int64_t ntiles,
+                                                                   uint32_t* __restrict__ totals) {
+  __shared__ uint32_t sh[WARPS];
+  uint32_t* row = hist + static_cast<int64_t>(blockIdx.x) * ntiles;
+  uint32_t run = 0;
+  for (int64_t c0 = 0; c0 < ntiles; c0 += THREADS) {
+    const int64_t i = c0 + threadIdx.x;
+    const uint32_t v = i < ntiles ? row[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan(v, sh, tot);
+    if (i < ntiles) row[i] = run + ex;
+    run += tot;
   }
+  if (threadIdx.x == 0) totals[blockIdx.x] = run;
 }
 
 // vals_in == nullptr means "value = item index" (argsort identity).
+// offsets: row-scanned hist (exclusive within each digit row), totals: per-digit
+// counts.  Items are ranked stably inside the tile, staged in shared memory in
+// digit order and written out as contiguous per-digit runs (coalesced).
 template <typename K, typename VIn, typename VOut>
 __global__ void __launch_bounds__(THREADS) scatter_kernel(const K* __restrict__ keys_in,
                                                           const VIn* __restrict__ vals_in,
                                                           K* __restrict__ keys_out, VOut* __restrict__ vals_out,
                                                           int64_t n, int shift, uint32_t mask,
                                                           const uint32_t* __restrict__ offsets,
-                                                          int64_t ntiles) {
+                                                          const uint32_t* __restrict__ totals, int64_t ntiles) {
+  static_assert(THREADS == RADIX, "one thread per digit");
   __shared__ uint32_t cnt[WARPS][RADIX];
+  __shared__ uint32_t loc_start[RADIX];
+  __shared__ uint32_t gbase[RADIX];
+  __shared__ uint32_t sh[WARPS];
+  __shared__ K keys_s[TILE];
+  __shared__ VOut vals_s[TILE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < WARPS * RADIX; i += THREADS) (&cnt[0][0])[i] = 0u;
   __syncthreads();
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * TILE + warp * WARP_ITEMS;
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * TILE;
+  const int64_t base = tile0 + warp * WARP_ITEMS;
   const uint32_t lt = lanemask_lt();
   K k[ITEMS];
   VOut v[ITEMS];
@@ -103,23 +133,39 @@ __global__ void __launch_bounds__(THREADS) scatter_kernel(const K* __restrict__ 
     __syncwarp();
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < RADIX; d += THREADS) {
-    uint32_t run = offsets[d * ntiles + blockIdx.x];
+  // per digit: warp offsets inside the tile, tile count, local and global starts
+  const int dd = threadIdx.x;
+  uint32_t tile_cnt = 0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) {
-      uint32_t c = cnt[w][d];
-      cnt[w][d] = run;
-      run += c;
-    }
+  for (int w = 0; w < WARPS; ++w) {
+    const uint32_t c = cnt[w][dd];
+    cnt[w][dd] = tile_cnt;
+    tile_cnt += c;
   }
+  uint32_t tot_all;
+  const uint32_t ls = block_exclusive_scan(tile_cnt, sh, tot_all);
+  uint32_t dummy;
+  const uint32_t db = block_exclusive_scan(totals[dd], sh, dummy);
+  loc_start[dd] = ls;
+  gbase[dd] = db + offsets[dd * ntiles + blockIdx.x];
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < ITEMS; ++t) {
     if (dg[t] != 0xFFFFFFFFu) {
-      const uint32_t pos = cnt[warp][dg[t]] + rank[t];
-      if (keys_out) keys_out[pos] = k[t];
-      vals_out[pos] = v[t];
+      const uint32_t lp = loc_start[dg[t]] + cnt[warp][dg[t]] + rank[t];
+      keys_s[lp] = k[t];
+      vals_s[lp] = v[t];
     }
+  }
+  __syncthreads();
+  const int64_t rem = n - tile0;
+  const int tile_n = rem < TILE ? static_cast<int>(rem) : TILE;
+  for (int i = threadIdx.x; i < tile_n; i += THREADS) {
+    const K key = keys_s[i];
+    const uint32_t d = static_cast<uint32_t>(key >> shift) & mask;
+    const uint32_t pos = gbase[d] + (i - loc_start[d]);
+    if (keys_out) keys_out[pos] = key;
+    vals_out[pos] = vals_s[i];
   }
 }
 
@@ -139,6 +185,7 @@ struct Buffers {
   K* keys[2];
   uint32_t* vals[2];
   uint32_t* hist;
+  uint32_t* totals;
 };
 
 template <typename K>
@@ -148,6 +195,7 @@ inline void measure(Measure& m, int64_t n) {
   m.take<uint32_t>(n);
   m.take<uint32_t>(n);
   m.take<uint32_t>(static_cast<size_t>(RADIX) * num_tiles(n));
+  m.take<uint32_t>(RADIX);
 }
 
 template <typename K>
@@ -158,6 +206,7 @@ inline Buffers<K> carve(Carve& c, int64_t n) {
   b.vals[0] = c.take<uint32_t>(n);
   b.vals[1] = c.take<uint32_t>(n);
   b.hist = c.take<uint32_t>(static_cast<size_t>(RADIX) * num_tiles(n));
+  b.totals = c.take<uint32_t>(RADIX);
   return b;
 }
 
@@ -181,15 +230,15 @@ int32_t sort_pairs(const K* keys, const uint32_t* vals, int64_t n, int nbits, Bu
     const uint32_t mask = (1u << bits) - 1u;
     const bool last = p == passes - 1;
     hist_kernel<K><<<static_cast<unsigned>(ntiles), THREADS, 0, st>>>(kin, n, shift, mask, b.hist, ntiles);
-    scan_kernel<<<1, SCAN_THREADS, 0, st>>>(b.hist, RADIX * ntiles);
+    scan_rows_kernel<<<RADIX, THREADS, 0, st>>>(b.hist, ntiles, b.totals);
     if (last) {
       scatter_kernel<K, uint32_t, VOut><<<static_cast<unsigned>(ntiles), THREADS, 0, st>>>(
-          kin, vin, keys_final, vals_final, n, shift, mask, b.hist, ntiles);
+          kin, vin, keys_final, vals_final, n, shift, mask, b.hist, b.totals, ntiles);
     } else {
       K* ko = b.keys[p & 1];
       uint32_t* vo = b.vals[p & 1];
       scatter_kernel<K, uint32_t, uint32_t><<<static_cast<unsigned>(ntiles), THREADS, 0, st>>>(
-          kin, vin, ko, vo, n, shift, mask, b.hist, ntiles);
+          kin, vin, ko, vo, n, shift, mask, b.hist, b.totals, ntiles);
       kin = ko;
       vin = vo;
     }

@@ -18,6 +18,7 @@ from __future__ import annotations
 import csv
 import json
 import math
+import os
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -107,8 +108,75 @@ def fold_device(sigma: torch.Tensor, vt: torch.Tensor, s_host: np.ndarray, pi: t
     return (basis @ (vt @ pi)).contiguous()
 
 
+def newton_schulz_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor | None, max_iter: int = 40):
+    """M = (SX^T SX)^(-1/2) [Pi] by the coupled Newton-Schulz iteration
+    (fp64 cuBLAS GEMMs only, no eigensolver).  Equal to the spectral fold
+    V S^-1 V^T [Pi] whenever truncation keeps every component, which is
+    certified here by the rigorous bound
+        lambda_min >= 1/trace(G^-1)  and  lambda_max <= trace(G):
+    trace(G) * trace(G^-1) < 1/sv_tol^2  ==>  every sigma_j > sv_tol*sigma_1.
+    Returns None when convergence or the certificate fails (caller falls
+    back to the eigensolver)."""
+    k, d = sx.shape
+    if k < d:
+        return None
+    G = sx.T @ sx
+    # scale by a Rayleigh-quotient estimate of lambda_max (power iteration on a
+    # 4-vector block); NS converges for eigenvalues of G/c in (0, 2), and the
+    # residual check below rejects any failure.
+    v = torch.ones((d, 4), dtype=G.dtype, device=G.device)
+    v[:, 1:] += torch.linspace(-1.0, 1.0, d, dtype=G.dtype, device=G.device)[:, None] * torch.tensor(
+        [1.0, -0.5, 0.25], dtype=G.dtype, device=G.device)
+    for _ in range(10):
+        v = G @ v
+        v = v / torch.linalg.vector_norm(v, dim=0, keepdim=True)
+    lam = ((v * (G @ v)).sum(0)).max()
+    c = 1.1 * lam
+    Y = G / c
+    eye = torch.eye(d, dtype=G.dtype, device=G.device)
+    Z = eye.clone()
+    it, burst = 0, 8
+    while True:
+        for _ in range(burst):
+            T = torch.addmm(eye, Z, Y, beta=1.5, alpha=-0.5)
+            Y = Y @ T
+            Z = T @ Z
+            it += 1
+        res = float(torch.linalg.matrix_norm(T - eye, ord="fro"))
+        if res < 1e-12 * math.sqrt(d):
+            break
+        if it >= max_iter or not math.isfinite(res):
+            return None
+        burst = 3
+    inv_sqrt = Z / torch.sqrt(c)
+    tr_g = float(torch.trace(G))
+    tr_ginv = float((inv_sqrt * inv_sqrt).sum())  # = trace(G^-1)
+    if not math.isfinite(tr_ginv) or tr_ginv <= 0:
+        return None
+    if sv_tol is not None and sv_tol > 0 and tr_g * tr_ginv >= 1.0 / (sv_tol * sv_tol):
+        return None
+    return (inv_sqrt if pi is None else inv_sqrt @ pi).contiguous()
+
+
+def sketch_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor | None,
+                method: str = "auto"):
+    """SX -> (M, effective_rank).  "auto" uses the eigensolver-free
+    Newton-Schulz fold when it is certified equal to the truncated spectral
+    fold (no rank cap, no component below the threshold), else the spectral
+    path (factor_device + fold_device)."""
+    k, d = sx.shape
+    if method in ("auto", "ns") and rank is None and k >= d and d >= 64:
+        M = newton_schulz_fold(sx, sv_tol, pi)
+        if M is not None:
+            return M, d
+        if method == "ns":
+            raise RuntimeError("Newton-Schulz fold not certified for this sketch")
+    sigma, vt, s_host = factor_device(sx, sv_tol, rank, "svd" if method == "ns" else ("auto" if method == "auto" else method))
+    return fold_device(sigma, vt, s_host, pi), int(s_host.shape[0])
+
+
 def split_m(M: torch.Tensor, x_dtype: torch.dtype):
-    """float64 M -> the K5 operand(s): float64 for float64 X, else fp32 hi + lo."""
+    """float64 M -> the SIMT K5 operand(s): float64 for float64 X, else fp32 hi + lo."""
     if x_dtype == torch.float64:
         return M.contiguous(), None
     hi = M.to(torch.float32)
@@ -116,26 +184,66 @@ def split_m(M: torch.Tensor, x_dtype: torch.dtype):
     return hi.contiguous(), lo.contiguous()
 
 
+def split_m_tf32(M: torch.Tensor):
+    """float64 M -> (Mt_hi, Mt_lo) for the tcgen05 path: M^T with an exactly
+    TF32-representable high part (low 13 mantissa bits cleared) and the
+    float32 remainder, so hi + lo carries ~22 bits and the tensor core's own
+    TF32 reading of each part is exact / harmless."""
+    hi = (M.to(torch.float32).view(torch.int32) & ~0x1FFF).view(torch.float32)
+    lo = (M - hi.to(torch.float64)).to(torch.float32)
+    return hi.T.contiguous(), lo.T.contiguous()
+
+
+def use_tensor_cores(X: torch.Tensor, r: int) -> bool:
+    return (
+        X.dtype == torch.float32
+        and r <= 128
+        and os.environ.get("LVSK_NO_TC", "0") != "1"
+        and X.data_ptr() % 16 == 0
+        and (X.stride(0) * 4) % 16 == 0
+        and (X.shape[1] * 4) % 16 == 0
+    )
+
+
+class KernelOperands:
+    """K5 operands prepared once per fold M (reused across row blocks)."""
+
+    def __init__(self, M: torch.Tensor, X_like: torch.Tensor):
+        self.d, self.r = M.shape
+        self.tc = use_tensor_cores(X_like, self.r)
+        if self.tc:
+            self.a, self.b = split_m_tf32(M)
+        else:
+            self.a, self.b = split_m(M, X_like.dtype)
+
+    def run(self, X: torch.Tensor, out: torch.Tensor, flags_ptr: int) -> None:
+        n, d = X.shape
+        L = N.lib()
+        if self.tc and use_tensor_cores(X, self.r):
+            rc = L.lvsk_leverage_tf32x3(X.data_ptr(), n, d, X.stride(0), self.a.data_ptr(), self.b.data_ptr(), self.r,
+                                        out.data_ptr(), flags_ptr, N.stream_ptr())
+            if rc != 5:  # LVSK_ERR_UNSUPPORTED -> SIMT kernel below
+                N.check(rc, "leverage pass (tcgen05)")
+                return
+            a, b = split_m(self.a.T.double() + self.b.T.double(), X.dtype)
+        else:
+            a, b = self.a, self.b
+        N.check(L.lvsk_rowsumsq_gemm(X.data_ptr(), N.dtype_code(X), n, d, X.stride(0), a.data_ptr(), N.ptr(b),
+                                     self.r, out.data_ptr(), flags_ptr, N.stream_ptr()), "leverage pass")
+
+
 def scores_device(X: torch.Tensor, M: torch.Tensor, out: torch.Tensor | None = None, flags=None) -> torch.Tensor:
     """K5: ||X[i] M||^2 for every row (float64 scores on the device)."""
     n, d = X.shape
-    r = M.shape[1]
     if M.shape[0] != d:
         from .errors import DimensionMismatchError
 
         raise DimensionMismatchError(f"basis has {M.shape[0]} rows, expected {d}")
-    m_hi, m_lo = split_m(M, X.dtype)
     if out is None:
         out = torch.empty(n, dtype=torch.float64, device=X.device)
     own = flags is None
     flags = flags or N.Flags()
-    N.check(
-        N.lib().lvsk_rowsumsq_gemm(
-            X.data_ptr(), N.dtype_code(X), n, d, X.stride(0), m_hi.data_ptr(), N.ptr(m_lo), r,
-            out.data_ptr(), flags.p, N.stream_ptr(),
-        ),
-        "leverage pass",
-    )
+    KernelOperands(M, X).run(X, out, flags.p)
     if own and flags.read() & N.FLAG_NONFINITE:
         raise FormatError("matrix contains non-finite entries")
     return out
@@ -193,14 +301,13 @@ def _sketched(a, spec, sv_tol, mem_cap_bytes, jl_dim, jl_seed, rank, method):
     X = device_matrix(a)
     state = apply_sketch(X, spec, mem_cap=mem_cap_bytes)
     sx = state.data_device
-    sigma, vt, s_host = factor_device(sx, sv_tol, rank)
     pi = None if jl_dim is None else jl_device(jl_seed, X.shape[1], jl_dim)
-    M = fold_device(sigma, vt, s_host, pi)
+    M, eff = sketch_fold(sx, sv_tol, rank, pi)
     scores = scores_device(X, M)
     return LeverageResult(
         scores=scores.cpu().numpy(),
         method=method,
-        effective_rank=int(s_host.shape[0]),
+        effective_rank=eff,
         eps=spec.eps,
         spec=spec,
         sv_tol=sv_tol,

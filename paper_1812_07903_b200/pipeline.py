@@ -21,7 +21,7 @@ import torch
 
 from . import _native as N
 from .errors import FormatError
-from .leverage import factor_device, fold_device, jl_device, split_m
+from .leverage import KernelOperands, jl_device, sketch_fold
 from .sketch import GAUSSIAN, SRHT, SketchSpec, SketchState, sketch_rows
 
 STAGES = ("sketch", "factor", "leverage", "order")
@@ -59,6 +59,8 @@ class LeveragePipeline:
         self.ws_sort = torch.empty(max(L.lvsk_argsort_workspace_bytes(n), 256), dtype=torch.uint8, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.pi = None if jl_dim is None else jl_device(jl_seed, d, jl_dim)
+        # a dtype/alignment witness for choosing the K5 kernel (real X has the same layout)
+        self._x_like = torch.empty((1, d), dtype=dtype, device=dev)
         self.effective_rank = None
         self.events = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in STAGES}
 
@@ -86,16 +88,15 @@ class LeveragePipeline:
                     "fold")
 
     def _factor(self) -> None:
-        sigma, vt, s_host = factor_device(self.sx, self.sv_tol, self.rank, self.factor_method)
-        self.effective_rank = int(s_host.shape[0])
-        M = fold_device(sigma, vt, s_host, self.pi)
-        self.m_hi, self.m_lo = split_m(M, self.dtype)
+        M, self.effective_rank = sketch_fold(self.sx, self.sv_tol, self.rank, self.pi, self.factor_method)
+        self.set_fold(M)
+
+    def set_fold(self, M: torch.Tensor) -> None:
+        self.ops = KernelOperands(M, self._x_like)
         self.r = M.shape[1]
 
     def _leverage(self, X: torch.Tensor) -> None:
-        N.check(N.lib().lvsk_rowsumsq_gemm(X.data_ptr(), self.code, self.n, self.d, X.stride(0),
-                                           self.m_hi.data_ptr(), N.ptr(self.m_lo), self.r, self.scores.data_ptr(),
-                                           self.flags.data_ptr(), N.stream_ptr()), "leverage pass")
+        self.ops.run(X, self.scores, self.flags.data_ptr())
 
     def _order(self) -> None:
         L, st = N.lib(), N.stream_ptr()
@@ -157,5 +158,5 @@ class LeveragePipeline:
         else:
             sk = 1 + radix(self.n * self.spec.s, max(1, (self.k - 1).bit_length())) + 1 + 1 + 1
         lev = 1
-        order = (3 + 1 + radix(self.n, 64)) if self.order else 0
-        return sk + lev + order
+        order_ = (3 + 1 + radix(self.n, 64)) if self.order else 0
+        return sk + lev + order_

@@ -143,12 +143,14 @@ LVSK_API int32_t lvsk_rowsumsq_gemm(const void* X, int32_t dtype, int64_t n, int
 /* K5 on tcgen05 tensor cores (fp32 X, 3xTF32 split, TMEM accumulators):
  * same result as lvsk_rowsumsq_gemm for F32 inputs, with M supplied
  * TRANSPOSED (r x d row-major) as an exact-TF32 high part Mt_hi and the
- * float32 remainder Mt_lo = M^T - Mt_hi.  Returns LVSK_ERR_UNSUPPORTED when
- * the shape is not covered (r > 128, rows not 16-byte aligned); callers then
- * use lvsk_rowsumsq_gemm. */
+ * float32 remainder Mt_lo = M^T - Mt_hi.  Mt_hi_bf16 (optional, r x d
+ * bfloat16 = bf16(Mt_hi)) selects the r <= 64 kernel that runs the x_lo
+ * correction as a BF16 MMA.  Returns LVSK_ERR_UNSUPPORTED when the shape is
+ * not covered (r > 128, rows not 16-byte aligned); callers then use
+ * lvsk_rowsumsq_gemm. */
 LVSK_API int32_t lvsk_leverage_tf32x3(const float* X, int64_t n, int64_t d, int64_t ldx, const float* Mt_hi,
-                                      const float* Mt_lo, int64_t r, double* scores, int32_t* flags,
-                                      void* stream);
+                                      const float* Mt_lo, const void* Mt_hi_bf16, int64_t r, double* scores,
+                                      int32_t* flags, void* stream);
 
 /* ---- ordering -------------------------------------------------------------
  * scores_to_distribution (order.py:51-63): p = scores / sum(scores), with

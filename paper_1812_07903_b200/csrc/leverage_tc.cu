@@ -16,6 +16,8 @@
 // t overlaps the MMAs of tile t+1.  X is read from HBM exactly once.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace lvsk {
@@ -293,6 +295,213 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// v2 (r <= 64): main term x.[M_hi | M_lo] as ONE N=128 TF32 MMA (A read once
+// for both halves), correction x_lo.M_hi as a BF16 MMA (x_lo written by the
+// transform warps as bf16 into its own SW64 tile, M_hi in bf16 by TMA).  The
+// x_lo / M_hi roundings to bf16 perturb a 2^-11-relative term by 2^-8, i.e.
+// ~2^-19 of the result.  Per 256 x 32 stage the tensor core reads 88 KB of
+// smem operands instead of 144 KB in v1.
+
+struct Cfg2 {
+  static constexpr int N = 64;
+  static constexpr int STAGES = 3;
+  static constexpr int X_BYTES = TILE_ROWS * BK * 4;      // 32 KB fp32, SW128
+  static constexpr int B_BYTES = 2 * N * BK * 4;          // 16 KB: Mt_hi rows 0..63, Mt_lo rows 64..127
+  static constexpr int BB_BYTES = N * BK * 2;             // 4 KB: Mt_hi bf16, SW64
+  static constexpr int XL_BYTES = TILE_ROWS * BK * 2;     // 16 KB: x_lo bf16, SW64
+  static constexpr int OFF_B = X_BYTES, OFF_BB = OFF_B + B_BYTES, OFF_XL = OFF_BB + BB_BYTES;
+  static constexpr int STAGE_BYTES = OFF_XL + XL_BYTES;  // 68 KB (all offsets 1024-aligned)
+  static constexpr int TMA_BYTES = X_BYTES + B_BYTES + BB_BYTES;
+  static constexpr int ACC_COLS = SUB * 2 * N;           // 256 per accumulator buffer
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t IDESC_TF32 =
+      (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t((2 * N) >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  static constexpr uint32_t IDESC_BF16 =
+      (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+};
+
+// K-major SWIZZLE_64B: 8-row x 64 B atoms, SBO = 512 B.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= uint64_t{1} << 16;
+  d |= uint64_t{512 >> 4} << 32;
+  d |= uint64_t{1} << 46;
+  d |= uint64_t{4} << 61;  // SWIZZLE_64B
+  return d;
+}
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    leverage_v2_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapHi,
+                       const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ CUtensorMap mapHb,
+                       int64_t n, int kchunks, double* __restrict__ scores, int32_t* flags) {
+  using C = Cfg2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* loready = bars + C::STAGES;
+  uint64_t* empty = bars + 2 * C::STAGES;
+  uint64_t* accfull = bars + 3 * C::STAGES;
+  uint64_t* accempty = accfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&loready[s], EPI_THREADS);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accfull[b], 1);
+      mbar_init(&accempty[b], EPI_THREADS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapHi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapLo) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapHb) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_x = l2_policy_evict_first(), pol_m = l2_policy_evict_last();
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          mbar_expect_tx(&full[s], C::TMA_BYTES);
+          tma_load_2d(&mapX, &full[s], st, kc * BK, static_cast<int>(t * TILE_ROWS), pol_x);
+          tma_load_2d(&mapHi, &full[s], st + C::OFF_B, kc * BK, 0, pol_m);
+          tma_load_2d(&mapLo, &full[s], st + C::OFF_B + C::B_BYTES / 2, kc * BK, 0, pol_m);
+          tma_load_2d(&mapHb, &full[s], st + C::OFF_BB, kc * BK, 0, pol_m);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t it = 0, lt = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        const uint32_t ab = lt & 1u, aph = (lt >> 1) & 1u;
+        const uint32_t acc_col = ab * C::ACC_COLS;
+        mbar_wait(&accempty[ab], aph ^ 1u);
+        tc_fence_after();
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
+          const uint64_t bm = sw128_desc(st + C::OFF_B);
+#pragma unroll
+          for (int sub = 0; sub < SUB; ++sub) {
+            const uint64_t a = sw128_desc(st + sub * (BM * 128));
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk)
+              umma_tf32(tmem_base + acc_col + sub * 2 * C::N, a + 2 * kk, bm + 2 * kk, C::IDESC_TF32,
+                        (kc | kk) ? 1u : 0u);
+          }
+          mbar_wait(&loready[s], ph);
+          tc_fence_after();
+          const uint64_t bb = sw64_desc(st + C::OFF_BB);
+#pragma unroll
+          for (int sub = 0; sub < SUB; ++sub) {
+            const uint64_t a = sw64_desc(st + C::OFF_XL + sub * (BM * 64));
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_f16(tmem_base + acc_col + sub * 2 * C::N, a + 2 * kk, bb + 2 * kk, C::IDESC_BF16, 1u);
+          }
+          umma_commit(&empty[s]);
+          if (kc == kchunks - 1) umma_commit(&accfull[ab]);
+        }
+      }
+    }
+  } else {
+    const int et = threadIdx.x - 64;
+    const int quarter = warp & 3;
+    bool bad = false;
+    uint32_t it = 0, lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      for (int kc = 0; kc < kchunks; ++kc, ++it) {
+        const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+#pragma unroll 4
+        for (int i = et; i < TILE_ROWS * 8; i += EPI_THREADS) {
+          const int row = i >> 3, c = i & 7;
+          const float4 v = *reinterpret_cast<const float4*>(st + row * 128 + ((c ^ (row & 7)) << 4));
+          bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+          const float l0 = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          const float l1 = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          const float l2 = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          const float l3 = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(l0, l1);
+          __nv_bfloat162 p1 = __floats2bfloat162_rn(l2, l3);
+          uint2 packed;
+          packed.x = *reinterpret_cast<uint32_t*>(&p0);
+          packed.y = *reinterpret_cast<uint32_t*>(&p1);
+          *reinterpret_cast<uint2*>(st + C::OFF_XL + row * 64 + ((((c >> 1) ^ ((row >> 1) & 3))) << 4) + ((c & 1) << 3)) =
+              packed;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&loready[s]);
+      }
+      const uint32_t ab = lt & 1u, aph = (lt >> 1) & 1u;
+      mbar_wait(&accfull[ab], aph);
+      tc_fence_after();
+#pragma unroll
+      for (int sub = 0; sub < SUB; ++sub) {
+        float acc = 0.f;
+        const uint32_t base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + ab * C::ACC_COLS + sub * 2 * C::N;
+#pragma unroll
+        for (int c0 = 0; c0 < C::N; c0 += 32) {
+          uint32_t vh[32], vl[32];
+          tmem_ld32(base + c0, vh);
+          tmem_ld32(base + C::N + c0, vl);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float u = __uint_as_float(vh[j]) + __uint_as_float(vl[j]);
+            acc = fmaf(u, u, acc);
+          }
+        }
+        const int64_t row = t * TILE_ROWS + sub * BM + quarter * 32 + lane;
+        if (row < n) scores[row] = static_cast<double>(acc);
+      }
+      tc_fence_before();
+      mbar_arrive(&accempty[ab]);
+    }
+    if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -312,16 +521,17 @@ static EncodeFn encode_fn() {
 }
 
 static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                     uint32_t box_inner, uint32_t box_outer) {
+                     uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -350,14 +560,38 @@ static int32_t launch(const float* X, int64_t n, int64_t d, int64_t ldx, const f
   return LVSK_OK;
 }
 
+static int32_t launch_v2(const float* X, int64_t n, int64_t d, int64_t ldx, const float* Mt_hi, const float* Mt_lo,
+                         const __nv_bfloat16* Mt_hb, int64_t r, double* scores, int32_t* flags, cudaStream_t st) {
+  using C = Cfg2;
+  CUtensorMap mx, mh, ml, mb;
+  if (!make_map(&mx, X, d, n, ldx * 4, BK, TILE_ROWS) || !make_map(&mh, Mt_hi, d, r, d * 4, BK, C::N) ||
+      !make_map(&ml, Mt_lo, d, r, d * 4, BK, C::N) ||
+      !make_map(&mb, Mt_hb, d, r, d * 2, BK, C::N, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_64B)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return LVSK_ERR_CUDA;
+  }
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(leverage_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "leverage v2 smem attribute");
+    attr_done = true;
+  }
+  const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
+  const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
+  const int kchunks = static_cast<int>((d + BK - 1) / BK);
+  leverage_v2_kernel<<<grid, THREADS, C::SMEM_BYTES, st>>>(mx, mh, ml, mb, n, kchunks, scores, flags);
+  LVSK_CHECK_LAUNCH("leverage v2");
+  return LVSK_OK;
+}
+
 }  // namespace tc
 }  // namespace lvsk
 
 using namespace lvsk;
 
 extern "C" int32_t lvsk_leverage_tf32x3(const float* X, int64_t n, int64_t d, int64_t ldx, const float* Mt_hi,
-                                        const float* Mt_lo, int64_t r, double* scores, int32_t* flags,
-                                        void* stream) {
+                                        const float* Mt_lo, const void* Mt_hi_bf16, int64_t r, double* scores,
+                                        int32_t* flags, void* stream) {
   LVSK_REQUIRE(n >= 0 && d >= 1 && ldx >= d && r >= 1, LVSK_ERR_DIMENSION, "bad shape");
   LVSK_REQUIRE(r <= 128, LVSK_ERR_UNSUPPORTED, "tensor-core leverage pass supports r <= 128 (got %lld)", (long long)r);
   LVSK_REQUIRE(reinterpret_cast<uintptr_t>(X) % 16 == 0 && (ldx * 4) % 16 == 0 && (d * 4) % 16 == 0 &&
@@ -366,6 +600,10 @@ extern "C" int32_t lvsk_leverage_tf32x3(const float* X, int64_t n, int64_t d, in
   LVSK_REQUIRE(n < (int64_t{1} << 31), LVSK_ERR_UNSUPPORTED, "n too large for one launch");
   if (n == 0) return LVSK_OK;
   cudaStream_t st = as_stream(stream);
+  if (r <= 64 && Mt_hi_bf16 != nullptr && d % 8 == 0 && reinterpret_cast<uintptr_t>(Mt_hi_bf16) % 16 == 0 &&
+      getenv("LVSK_K5_V1") == nullptr)
+    return tc::launch_v2(X, n, d, ldx, Mt_hi, Mt_lo, static_cast<const __nv_bfloat16*>(Mt_hi_bf16), r, scores, flags,
+                         st);
   if (r <= 64) return tc::launch<64>(X, n, d, ldx, Mt_hi, Mt_lo, r, scores, flags, st);
   return tc::launch<128>(X, n, d, ldx, Mt_hi, Mt_lo, r, scores, flags, st);
 }

@@ -75,10 +75,10 @@ struct VecLoad<T, 1> {
   __device__ static void load(const T* p, T (&o)[1]) { o[0] = p[0]; }
 };
 
-constexpr int GATHER_UNROLL = 4;
+constexpr int GATHER_UNROLL = 8;  // rows in flight per lane (memory-level parallelism)
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(256) hashed_gather_kernel(
+__global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
     const T* __restrict__ X, int64_t ldx, int64_t d, int nchunks, const uint32_t* __restrict__ vals,
     const uint32_t* __restrict__ start, int64_t k, double scale, const double* hi_in, const double* lo_in,
     double* hi_out, double* lo_out, int32_t* flags) {

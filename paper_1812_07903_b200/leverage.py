@@ -108,54 +108,56 @@ def fold_device(sigma: torch.Tensor, vt: torch.Tensor, s_host: np.ndarray, pi: t
     return (basis @ (vt @ pi)).contiguous()
 
 
-def newton_schulz_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor | None, max_iter: int = 40):
+def _ns_body(sx: torch.Tensor, pi: torch.Tensor | None, iters: int, eye: torch.Tensor):
+    """Shape-static part of the Newton-Schulz fold (CUDA-graph capturable).
+    Returns (M, diag) with diag = [residual, trace(G), trace(G^-1)]."""
+    G = sx.T @ sx
+    G2 = G @ G
+    # lambda_max <= ||G^4||_F^(1/4) <= d^(1/8) lambda_max: a safe NS scaling
+    c = torch.linalg.matrix_norm(G2 @ G2, ord="fro").sqrt().sqrt()
+    Y = G / c
+    Z = eye
+    T = eye
+    for _ in range(iters):
+        T = torch.addmm(eye, Z, Y, beta=1.5, alpha=-0.5)
+        Y = Y @ T
+        Z = T @ Z
+    inv_sqrt = Z / torch.sqrt(c)
+    diag = torch.stack([torch.linalg.matrix_norm(T - eye, ord="fro"), torch.trace(G), (inv_sqrt * inv_sqrt).sum()])
+    M = inv_sqrt if pi is None else inv_sqrt @ pi
+    return M, diag
+
+
+def ns_certified(diag, d: int, sv_tol: float | None) -> bool:
+    """Convergence + the no-truncation certificate
+    trace(G) * trace(G^-1) < 1/sv_tol^2  (lambda_min >= 1/trace(G^-1),
+    lambda_max <= trace(G)  ==>  every sigma_j > sv_tol * sigma_1)."""
+    res, tr_g, tr_ginv = (float(v) for v in diag)
+    if not (math.isfinite(res) and math.isfinite(tr_ginv)) or tr_ginv <= 0 or res >= 1e-12 * math.sqrt(d):
+        return False
+    if sv_tol is not None and sv_tol > 0 and tr_g * tr_ginv >= 1.0 / (sv_tol * sv_tol):
+        return False
+    return True
+
+
+def newton_schulz_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor | None, max_iter: int = 30):
     """M = (SX^T SX)^(-1/2) [Pi] by the coupled Newton-Schulz iteration
     (fp64 cuBLAS GEMMs only, no eigensolver).  Equal to the spectral fold
     V S^-1 V^T [Pi] whenever truncation keeps every component, which is
-    certified here by the rigorous bound
-        lambda_min >= 1/trace(G^-1)  and  lambda_max <= trace(G):
-    trace(G) * trace(G^-1) < 1/sv_tol^2  ==>  every sigma_j > sv_tol*sigma_1.
-    Returns None when convergence or the certificate fails (caller falls
-    back to the eigensolver)."""
+    certified by :func:`ns_certified`.  Returns None when convergence or the
+    certificate fails (the caller falls back to the eigensolver)."""
     k, d = sx.shape
     if k < d:
         return None
-    G = sx.T @ sx
-    # scale by a Rayleigh-quotient estimate of lambda_max (power iteration on a
-    # 4-vector block); NS converges for eigenvalues of G/c in (0, 2), and the
-    # residual check below rejects any failure.
-    v = torch.ones((d, 4), dtype=G.dtype, device=G.device)
-    v[:, 1:] += torch.linspace(-1.0, 1.0, d, dtype=G.dtype, device=G.device)[:, None] * torch.tensor(
-        [1.0, -0.5, 0.25], dtype=G.dtype, device=G.device)
-    for _ in range(10):
-        v = G @ v
-        v = v / torch.linalg.vector_norm(v, dim=0, keepdim=True)
-    lam = ((v * (G @ v)).sum(0)).max()
-    c = 1.1 * lam
-    Y = G / c
-    eye = torch.eye(d, dtype=G.dtype, device=G.device)
-    Z = eye.clone()
-    it, burst = 0, 8
-    while True:
-        for _ in range(burst):
-            T = torch.addmm(eye, Z, Y, beta=1.5, alpha=-0.5)
-            Y = Y @ T
-            Z = T @ Z
-            it += 1
-        res = float(torch.linalg.matrix_norm(T - eye, ord="fro"))
-        if res < 1e-12 * math.sqrt(d):
-            break
-        if it >= max_iter or not math.isfinite(res):
-            return None
-        burst = 3
-    inv_sqrt = Z / torch.sqrt(c)
-    tr_g = float(torch.trace(G))
-    tr_ginv = float((inv_sqrt * inv_sqrt).sum())  # = trace(G^-1)
-    if not math.isfinite(tr_ginv) or tr_ginv <= 0:
-        return None
-    if sv_tol is not None and sv_tol > 0 and tr_g * tr_ginv >= 1.0 / (sv_tol * sv_tol):
-        return None
-    return (inv_sqrt if pi is None else inv_sqrt @ pi).contiguous()
+    eye = torch.eye(d, dtype=sx.dtype, device=sx.device)
+    for iters in (10, 20, max_iter):
+        M, diag = _ns_body(sx, pi, iters, eye)
+        vals = diag.tolist()
+        if ns_certified(vals, d, sv_tol):
+            return M.contiguous()
+        if math.isfinite(vals[0]) and vals[0] < 1e-12 * math.sqrt(d):
+            return None  # converged but truncation would bite
+    return None
 
 
 def sketch_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor | None,
@@ -206,30 +208,93 @@ def use_tensor_cores(X: torch.Tensor, r: int) -> bool:
 
 
 class KernelOperands:
-    """K5 operands prepared once per fold M (reused across row blocks)."""
+    """K5 operands for a fold M (d x r): TF32 hi/lo transposes (+ bf16 hi) for
+    the tcgen05 kernels, fp32 hi/lo or fp64 for the SIMT kernel.  Buffers are
+    allocated once; :meth:`set` refills them (CUDA-graph capturable)."""
 
-    def __init__(self, M: torch.Tensor, X_like: torch.Tensor):
-        self.d, self.r = M.shape
+    def __init__(self, M: torch.Tensor | None, X_like: torch.Tensor, shape: tuple[int, int] | None = None):
+        self.d, self.r = M.shape if M is not None else shape
         self.tc = use_tensor_cores(X_like, self.r)
+        dev = X_like.device
+        self.hb = None
         if self.tc:
-            self.a, self.b = split_m_tf32(M)
+            self.a = torch.empty((self.r, self.d), dtype=torch.float32, device=dev)
+            self.b = torch.empty((self.r, self.d), dtype=torch.float32, device=dev)
+            if self.r <= 64:
+                self.hb = torch.empty((self.r, self.d), dtype=torch.bfloat16, device=dev)
+        elif X_like.dtype == torch.float64:
+            self.a = torch.empty((self.d, self.r), dtype=torch.float64, device=dev)
+            self.b = None
         else:
-            self.a, self.b = split_m(M, X_like.dtype)
+            self.a = torch.empty((self.d, self.r), dtype=torch.float32, device=dev)
+            self.b = torch.empty((self.d, self.r), dtype=torch.float32, device=dev)
+        if M is not None:
+            self.set(M)
+
+    def set(self, M: torch.Tensor) -> None:
+        if self.tc:
+            hi, lo = split_m_tf32(M)
+            self.a.copy_(hi)
+            self.b.copy_(lo)
+            if self.hb is not None:
+                self.hb.copy_(hi)
+        else:
+            hi, lo = split_m(M, self.a.dtype)
+            self.a.copy_(hi)
+            if self.b is not None:
+                self.b.copy_(lo)
 
     def run(self, X: torch.Tensor, out: torch.Tensor, flags_ptr: int) -> None:
         n, d = X.shape
         L = N.lib()
         if self.tc and use_tensor_cores(X, self.r):
-            rc = L.lvsk_leverage_tf32x3(X.data_ptr(), n, d, X.stride(0), self.a.data_ptr(), self.b.data_ptr(), self.r,
-                                        out.data_ptr(), flags_ptr, N.stream_ptr())
+            rc = L.lvsk_leverage_tf32x3(X.data_ptr(), n, d, X.stride(0), self.a.data_ptr(), self.b.data_ptr(),
+                                        N.ptr(self.hb), self.r, out.data_ptr(), flags_ptr, N.stream_ptr())
             if rc != 5:  # LVSK_ERR_UNSUPPORTED -> SIMT kernel below
                 N.check(rc, "leverage pass (tcgen05)")
                 return
+            a, b = split_m(self.a.T.double() + self.b.T.double(), X.dtype)
+        elif self.tc:
             a, b = split_m(self.a.T.double() + self.b.T.double(), X.dtype)
         else:
             a, b = self.a, self.b
         N.check(L.lvsk_rowsumsq_gemm(X.data_ptr(), N.dtype_code(X), n, d, X.stride(0), a.data_ptr(), N.ptr(b),
                                      self.r, out.data_ptr(), flags_ptr, N.stream_ptr()), "leverage pass")
+
+
+class FoldGraph:
+    """The certified Newton-Schulz fold + K5 operand split for a fixed
+    (k, d, r) captured once as a CUDA graph; ``run()`` replays it and returns
+    False when the certificate fails (caller then takes the eager path)."""
+
+    def __init__(self, sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor | None, X_like: torch.Tensor,
+                 iters: int = 10):
+        self.sx, self.sv_tol, self.pi = sx, sv_tol, pi
+        k, d = sx.shape
+        r = d if pi is None else pi.shape[1]
+        self.ops = KernelOperands(None, X_like, (d, r))
+        self.eye = torch.eye(d, dtype=torch.float64, device=sx.device)
+        self.diag = torch.zeros(3, dtype=torch.float64, device=sx.device)
+        self.iters = iters
+        self.graph = None
+        # warm up cuBLAS handles / workspaces outside capture
+        M, diag = _ns_body(sx, pi, 1, self.eye)
+        self.ops.set(M)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                M, diag = _ns_body(self.sx, self.pi, iters, self.eye)
+                self.ops.set(M)
+                self.diag.copy_(diag)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+
+    def run(self) -> bool:
+        self.graph.replay()
+        return ns_certified(self.diag.tolist(), self.sx.shape[1], self.sv_tol)
 
 
 def scores_device(X: torch.Tensor, M: torch.Tensor, out: torch.Tensor | None = None, flags=None) -> torch.Tensor:

@@ -15,13 +15,14 @@ its spectrum to pick the truncation rank) and the final flag check.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
 
 from . import _native as N
 from .errors import FormatError
-from .leverage import KernelOperands, jl_device, sketch_fold
+from .leverage import FoldGraph, KernelOperands, jl_device, sketch_fold
 from .sketch import GAUSSIAN, SRHT, SketchSpec, SketchState, sketch_rows
 
 STAGES = ("sketch", "factor", "leverage", "order")
@@ -61,6 +62,7 @@ class LeveragePipeline:
         self.pi = None if jl_dim is None else jl_device(jl_seed, d, jl_dim)
         # a dtype/alignment witness for choosing the K5 kernel (real X has the same layout)
         self._x_like = torch.empty((1, d), dtype=dtype, device=dev)
+        self._fold_graph = None
         self.effective_rank = None
         self.events = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in STAGES}
 
@@ -88,6 +90,16 @@ class LeveragePipeline:
                     "fold")
 
     def _factor(self) -> None:
+        k, d = self.sx.shape
+        if (self.factor_method == "auto" and self.rank is None and k >= d and d >= 64
+                and os.environ.get("LVSK_NO_GRAPH", "0") != "1"):
+            if self._fold_graph is None:
+                self._fold_graph = FoldGraph(self.sx, self.sv_tol, self.pi, self._x_like)
+            if self._fold_graph.run():
+                self.ops = self._fold_graph.ops
+                self.r = self.ops.r
+                self.effective_rank = d
+                return
         M, self.effective_rank = sketch_fold(self.sx, self.sv_tol, self.rank, self.pi, self.factor_method)
         self.set_fold(M)
 

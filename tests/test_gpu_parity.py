@@ -252,14 +252,16 @@ def test_tcgen05_leverage_vs_fp64(n, d, r):
     M = (torch.randn(d, r, generator=g, dtype=torch.float64) / math.sqrt(d)).cuda()
     ref = ((X.double() @ M) ** 2).sum(1)
     mt_hi, mt_lo = P.leverage.split_m_tf32(M)
-    out = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+    hb = mt_hi.to(torch.bfloat16).contiguous()
     flags = N.Flags()
-    rc = N.lib().lvsk_leverage_tf32x3(X.data_ptr(), n, d, X.stride(0), mt_hi.data_ptr(), mt_lo.data_ptr(), r,
-                                      out.data_ptr(), flags.p, N.stream_ptr())
-    N.check(rc)
-    assert flags.read() == 0
-    rel = ((out - ref).abs() / ref).max().item()
-    assert rel < 2e-5, rel
+    for variant in (None, hb):  # v1 (x_lo as TF32) and v2 (x_lo as BF16, r <= 64)
+        out = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+        rc = N.lib().lvsk_leverage_tf32x3(X.data_ptr(), n, d, X.stride(0), mt_hi.data_ptr(), mt_lo.data_ptr(),
+                                          N.ptr(variant), r, out.data_ptr(), flags.p, N.stream_ptr())
+        N.check(rc)
+        assert flags.read() == 0
+        rel = ((out - ref).abs() / ref).max().item()
+        assert rel < 2e-5, (rel, variant is None)
     # the SIMT kernel agrees too
     simt = torch.empty_like(out)
     a, b = P.leverage.split_m(M, torch.float32)

@@ -304,17 +304,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 struct Cfg2 {
   static constexpr int N = 64;
-  static constexpr int STAGES = 3;
-  static constexpr int X_BYTES = TILE_ROWS * BK * 4;      // 32 KB fp32, SW128
-  static constexpr int B_BYTES = 2 * N * BK * 4;          // 16 KB: Mt_hi rows 0..63, Mt_lo rows 64..127
-  static constexpr int BB_BYTES = N * BK * 2;             // 4 KB: Mt_hi bf16, SW64
-  static constexpr int XL_BYTES = TILE_ROWS * BK * 2;     // 16 KB: x_lo bf16, SW64
-  static constexpr int OFF_B = X_BYTES, OFF_BB = OFF_B + B_BYTES, OFF_XL = OFF_BB + BB_BYTES;
-  static constexpr int STAGE_BYTES = OFF_XL + XL_BYTES;  // 68 KB (all offsets 1024-aligned)
-  static constexpr int TMA_BYTES = X_BYTES + B_BYTES + BB_BYTES;
-  static constexpr int ACC_COLS = SUB * 2 * N;           // 256 per accumulator buffer
+  static constexpr int SX = 4;                             // X ring (the HBM stream)
+  static constexpr int SB = 2;                             // M-chunk ring (L2 hits)
+  static constexpr int SL = 2;                             // x_lo ring (produced on chip)
+  static constexpr int X_BYTES = TILE_ROWS * BK * 4;       // 32 KB fp32, SW128
+  static constexpr int B_BYTES = 2 * N * BK * 4;           // 16 KB: Mt_hi rows 0..63, Mt_lo rows 64..127
+  static constexpr int BB_BYTES = N * BK * 2;              // 4 KB: Mt_hi bf16, SW64
+  static constexpr int BSTAGE = B_BYTES + BB_BYTES;        // 20 KB
+  static constexpr int XL_BYTES = TILE_ROWS * BK * 2;      // 16 KB: x_lo bf16, SW64
+  static constexpr int OFF_B = SX * X_BYTES;
+  static constexpr int OFF_XL = OFF_B + SB * BSTAGE;
+  static constexpr int OFF_BAR = OFF_XL + SL * XL_BYTES;   // 200 KB
+  static constexpr int ACC_COLS = SUB * 2 * N;             // 256 per accumulator buffer
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM_BYTES = OFF_BAR + 1024 + 512;
   static constexpr uint32_t IDESC_TF32 =
       (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t((2 * N) >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   static constexpr uint32_t IDESC_BF16 =
@@ -345,22 +348,32 @@ __global__ void __launch_bounds__(THREADS, 1)
   using C = Cfg2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* full = bars;
-  uint64_t* loready = bars + C::STAGES;
-  uint64_t* empty = bars + 2 * C::STAGES;
-  uint64_t* accfull = bars + 3 * C::STAGES;
-  uint64_t* accempty = accfull + 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* xfull = bars;                 // [SX] TMA complete_tx
+  uint64_t* xempty = xfull + C::SX;       // [SX] main-MMA commit (1) + transform threads (128)
+  uint64_t* bfull = xempty + C::SX;       // [SB]
+  uint64_t* bempty = bfull + C::SB;       // [SB] lo-MMA commit
+  uint64_t* xlfull = bempty + C::SB;      // [SL] transform threads
+  uint64_t* xlempty = xlfull + C::SL;     // [SL] lo-MMA commit
+  uint64_t* accfull = xlempty + C::SL;    // [2]
+  uint64_t* accempty = accfull + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&loready[s], EPI_THREADS);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < C::SX; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1 + EPI_THREADS);
+    }
+    for (int s = 0; s < C::SB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    for (int s = 0; s < C::SL; ++s) {
+      mbar_init(&xlfull[s], EPI_THREADS);
+      mbar_init(&xlempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
@@ -383,19 +396,30 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // lane 0 streams X (4 stages ahead), lane 1 streams the M chunks (2 ahead)
     if (lane == 0) {
-      const uint64_t pol_x = l2_policy_evict_first(), pol_m = l2_policy_evict_last();
+      const uint64_t pol = l2_policy_evict_first();
       uint32_t it = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kc = 0; kc < kchunks; ++kc, ++it) {
-          const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);
-          uint8_t* st = smem + s * C::STAGE_BYTES;
-          mbar_expect_tx(&full[s], C::TMA_BYTES);
-          tma_load_2d(&mapX, &full[s], st, kc * BK, static_cast<int>(t * TILE_ROWS), pol_x);
-          tma_load_2d(&mapHi, &full[s], st + C::OFF_B, kc * BK, 0, pol_m);
-          tma_load_2d(&mapLo, &full[s], st + C::OFF_B + C::B_BYTES / 2, kc * BK, 0, pol_m);
-          tma_load_2d(&mapHb, &full[s], st + C::OFF_BB, kc * BK, 0, pol_m);
+          const uint32_t s = it % C::SX, ph = (it / C::SX) & 1u;
+          mbar_wait(&xempty[s], ph ^ 1u);
+          mbar_expect_tx(&xfull[s], C::X_BYTES);
+          tma_load_2d(&mapX, &xfull[s], smem + s * C::X_BYTES, kc * BK, static_cast<int>(t * TILE_ROWS), pol);
+        }
+      }
+    } else if (lane == 1) {
+      const uint64_t pol = l2_policy_evict_last();
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < kchunks; ++kc, ++it) {
+          const uint32_t s = it % C::SB, ph = (it / C::SB) & 1u;
+          mbar_wait(&bempty[s], ph ^ 1u);
+          uint8_t* bs = smem + C::OFF_B + s * C::BSTAGE;
+          mbar_expect_tx(&bfull[s], C::BSTAGE);
+          tma_load_2d(&mapHi, &bfull[s], bs, kc * BK, 0, pol);
+          tma_load_2d(&mapLo, &bfull[s], bs + C::B_BYTES / 2, kc * BK, 0, pol);
+          tma_load_2d(&mapHb, &bfull[s], bs + C::B_BYTES, kc * BK, 0, pol);
         }
       }
     }
@@ -408,30 +432,37 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&accempty[ab], aph ^ 1u);
         tc_fence_after();
         for (int kc = 0; kc < kchunks; ++kc, ++it) {
-          const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
-          mbar_wait(&full[s], ph);
+          const uint32_t sx = it % C::SX, phx = (it / C::SX) & 1u;
+          const uint32_t sb = it % C::SB, phb = (it / C::SB) & 1u;
+          const uint32_t sl = it % C::SL, phl = (it / C::SL) & 1u;
+          mbar_wait(&xfull[sx], phx);
+          mbar_wait(&bfull[sb], phb);
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + s * C::STAGE_BYTES);
-          const uint64_t bm = sw128_desc(st + C::OFF_B);
+          const uint32_t xs = smem_u32(smem + sx * C::X_BYTES);
+          const uint32_t bs = smem_u32(smem + C::OFF_B + sb * C::BSTAGE);
+          const uint64_t bm = sw128_desc(bs);
 #pragma unroll
           for (int sub = 0; sub < SUB; ++sub) {
-            const uint64_t a = sw128_desc(st + sub * (BM * 128));
+            const uint64_t a = sw128_desc(xs + sub * (BM * 128));
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk)
               umma_tf32(tmem_base + acc_col + sub * 2 * C::N, a + 2 * kk, bm + 2 * kk, C::IDESC_TF32,
                         (kc | kk) ? 1u : 0u);
           }
-          mbar_wait(&loready[s], ph);
+          umma_commit(&xempty[sx]);
+          mbar_wait(&xlfull[sl], phl);
           tc_fence_after();
-          const uint64_t bb = sw64_desc(st + C::OFF_BB);
+          const uint64_t bb = sw64_desc(bs + C::B_BYTES);
+          const uint32_t xls = smem_u32(smem + C::OFF_XL + sl * C::XL_BYTES);
 #pragma unroll
           for (int sub = 0; sub < SUB; ++sub) {
-            const uint64_t a = sw64_desc(st + C::OFF_XL + sub * (BM * 64));
+            const uint64_t a = sw64_desc(xls + sub * (BM * 64));
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
               umma_f16(tmem_base + acc_col + sub * 2 * C::N, a + 2 * kk, bb + 2 * kk, C::IDESC_BF16, 1u);
           }
-          umma_commit(&empty[s]);
+          umma_commit(&xlempty[sl]);
+          umma_commit(&bempty[sb]);
           if (kc == kchunks - 1) umma_commit(&accfull[ab]);
         }
       }
@@ -443,13 +474,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t it = 0, lt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
       for (int kc = 0; kc < kchunks; ++kc, ++it) {
-        const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
-        mbar_wait(&full[s], ph);
-        uint8_t* st = smem + s * C::STAGE_BYTES;
+        const uint32_t sx = it % C::SX, phx = (it / C::SX) & 1u;
+        const uint32_t sl = it % C::SL, phl = (it / C::SL) & 1u;
+        mbar_wait(&xfull[sx], phx);
+        mbar_wait(&xlempty[sl], phl ^ 1u);
+        const uint8_t* xsm = smem + sx * C::X_BYTES;
+        uint8_t* xl = smem + C::OFF_XL + sl * C::XL_BYTES;
 #pragma unroll 4
         for (int i = et; i < TILE_ROWS * 8; i += EPI_THREADS) {
           const int row = i >> 3, c = i & 7;
-          const float4 v = *reinterpret_cast<const float4*>(st + row * 128 + ((c ^ (row & 7)) << 4));
+          const float4 v = *reinterpret_cast<const float4*>(xsm + row * 128 + ((c ^ (row & 7)) << 4));
           bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
           const float l0 = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
           const float l1 = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
@@ -460,11 +494,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint2 packed;
           packed.x = *reinterpret_cast<uint32_t*>(&p0);
           packed.y = *reinterpret_cast<uint32_t*>(&p1);
-          *reinterpret_cast<uint2*>(st + C::OFF_XL + row * 64 + ((((c >> 1) ^ ((row >> 1) & 3))) << 4) + ((c & 1) << 3)) =
+          *reinterpret_cast<uint2*>(xl + row * 64 + ((((c >> 1) ^ ((row >> 1) & 3))) << 4) + ((c & 1) << 3)) =
               packed;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&loready[s]);
+        mbar_arrive(&xlfull[sl]);
+        mbar_arrive(&xempty[sx]);
       }
       const uint32_t ab = lt & 1u, aph = (lt >> 1) & 1u;
       mbar_wait(&accfull[ab], aph);

@@ -13,6 +13,8 @@
 // sequence — so SX is bit-identical to the reference, with no atomics.  X is
 // read once per block j (s times for OSNAP), in 512-byte warp-contiguous
 // row segments; the accumulator never round-trips HBM.
+#include <cstdlib>
+
 #include "radix_sort.cuh"
 
 namespace lvsk {
@@ -53,6 +55,10 @@ struct VecLoad<float, 4> {
     float4 v = __ldg(reinterpret_cast<const float4*>(p));
     o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
   }
+  __device__ static void load_smem(const float* p, float (&o)[4]) {
+    float4 v = *reinterpret_cast<const float4*>(p);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
 };
 template <>
 struct VecLoad<double, 2> {
@@ -60,11 +66,21 @@ struct VecLoad<double, 2> {
     double2 v = __ldg(reinterpret_cast<const double2*>(p));
     o[0] = v.x; o[1] = v.y;
   }
+  __device__ static void load_smem(const double* p, double (&o)[2]) {
+    double2 v = *reinterpret_cast<const double2*>(p);
+    o[0] = v.x; o[1] = v.y;
+  }
 };
 template <>
 struct VecLoad<__nv_bfloat16, 8> {
   __device__ static void load(const __nv_bfloat16* p, __nv_bfloat16 (&o)[8]) {
     uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = h[i];
+  }
+  __device__ static void load_smem(const __nv_bfloat16* p, __nv_bfloat16 (&o)[8]) {
+    uint4 v = *reinterpret_cast<const uint4*>(p);
     const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[i] = h[i];
@@ -137,6 +153,119 @@ __global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy gather (default when rows are 16-byte aligned): one CTA owns one
+// (bucket, 2 KB column group).  A producer warp streams the bucket's row
+// segments into a 16-slot shared-memory ring with cp.async.bulk (TMA 1-D,
+// mbarrier complete_tx), so 32 KB per CTA (~200 KB per SM) are in flight;
+// four consumer warps apply the rows in ascending index order, TwoSum into
+// float64 (hi, lo) registers, exactly as the reference does per bucket.
+constexpr int BULK_SLOTS = 16;
+constexpr int BULK_SEG = 2048;  // bytes per row segment
+constexpr int BULK_CONSUMERS = 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(c));
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "BW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni BW_%=;\n}" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_kernel(
+    const T* __restrict__ X, int64_t ldx, int64_t d, int ngroups, const uint32_t* __restrict__ vals,
+    const uint32_t* __restrict__ start, int64_t k, double scale, const double* hi_in, const double* lo_in,
+    double* hi_out, double* lo_out, int32_t* flags) {
+  __shared__ alignas(128) uint8_t ring[BULK_SLOTS][BULK_SEG];
+  __shared__ uint64_t full[BULK_SLOTS], empty[BULK_SLOTS];
+  const int64_t b = blockIdx.x / ngroups;
+  const int g = blockIdx.x - static_cast<int>(b * ngroups);
+  constexpr int SEG_ELEMS = BULK_SEG / static_cast<int>(sizeof(T));
+  const int64_t c0 = static_cast<int64_t>(g) * SEG_ELEMS;
+  const int64_t cols = d - c0 < SEG_ELEMS ? d - c0 : SEG_ELEMS;
+  const uint32_t seg_bytes = static_cast<uint32_t>(cols * sizeof(T));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < BULK_SLOTS; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], BULK_CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t p0 = start[b], p1 = start[b + 1];
+  const uint32_t cnt = p1 - p0;
+  if (warp == BULK_CONSUMERS) {  // producer
+    if (lane == 0) {
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
+        bar_wait(&empty[s], ph ^ 1u);
+        const T* src = X + static_cast<int64_t>(vals[p0 + j] >> 1) * ldx + c0;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[s])),
+                     "r"(seg_bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(ring[s])),
+            "l"(src), "r"(seg_bytes), "r"(smem_addr(&full[s]))
+            : "memory");
+      }
+    }
+    return;
+  }
+  const int64_t col = static_cast<int64_t>(warp * 32 + lane) * VEC;  // within the segment
+  const bool active = col < cols;
+  double h[VEC], l[VEC];
+  const int64_t so = b * d + c0 + col;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    h[v] = active ? hi_in[so + v] : 0.0;
+    l[v] = active ? lo_in[so + v] : 0.0;
+  }
+  bool bad = false;
+  for (uint32_t j = 0; j < cnt; ++j) {
+    const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
+    const uint32_t vv = vals[p0 + j];
+    bar_wait(&full[s], ph);
+    if (active) {
+      T xs[VEC];
+      VecLoad<T, VEC>::load_smem(reinterpret_cast<const T*>(ring[s]) + col, xs);
+      const double sg = (vv & 1u) ? -scale : scale;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const double xv = to_f64<T>(xs[v]);
+        bad |= !isfinite(xv);
+        double sum, e;
+        two_sum(h[v], __dmul_rn(sg, xv), sum, e);
+        h[v] = sum;
+        l[v] = __dadd_rn(l[v], e);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[s]);
+  }
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      hi_out[so + v] = h[v];
+      lo_out[so + v] = l[v];
+    }
+  }
+  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
+}
+
 // copies hi/lo rows of buckets that no row touched when in != out
 __global__ void copy_f64_kernel(const double* __restrict__ a, double* __restrict__ b, int64_t count) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
@@ -191,6 +320,16 @@ static void fill_blocks(KeygenBlocks& P, const lvsk_hash_block* blocks, int j0, 
     P.offset[jj] = static_cast<uint32_t>(B.offset);
     P.size[jj] = static_cast<uint32_t>(B.size);
   }
+}
+
+template <typename T, int VEC>
+static void launch_gather_bulk(const void* X, int64_t ldx, int64_t d, const uint32_t* vals, const uint32_t* start,
+                               int64_t k, double scale, const double* hi_in, const double* lo_in, double* hi_out,
+                               double* lo_out, int32_t* flags, cudaStream_t st) {
+  const int ngroups = static_cast<int>((d * static_cast<int64_t>(sizeof(T)) + BULK_SEG - 1) / BULK_SEG);
+  const unsigned grid = static_cast<unsigned>(k * ngroups);
+  hashed_gather_bulk_kernel<T, VEC><<<grid, 32 * (BULK_CONSUMERS + 1), 0, st>>>(
+      static_cast<const T*>(X), ldx, d, ngroups, vals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags);
 }
 
 template <typename T, int VEC>
@@ -262,21 +401,29 @@ extern "C" int32_t lvsk_hashed_sketch(const void* X, int32_t dtype, int64_t n, i
   LVSK_CHECK_LAUNCH("bucket bounds");
 
   const uintptr_t xa = reinterpret_cast<uintptr_t>(X);
+  const bool bulk = getenv("LVSK_K1_REGS") == nullptr;  // register-path gather kept for A/B checks
   switch (dtype) {
     case LVSK_F32:
-      if (xa % 16 == 0 && (ldx * 4) % 16 == 0 && d % 4 == 0)
+      if (bulk && xa % 16 == 0 && (ldx * 4) % 16 == 0 && d % 4 == 0)
+        launch_gather_bulk<float, 4>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
+      else if (xa % 16 == 0 && (ldx * 4) % 16 == 0 && d % 4 == 0)
         launch_gather<float, 4>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
       else
         launch_gather<float, 1>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
       break;
     case LVSK_F64:
-      if (xa % 16 == 0 && (ldx * 8) % 16 == 0 && d % 2 == 0)
+      if (bulk && xa % 16 == 0 && (ldx * 8) % 16 == 0 && d % 2 == 0)
+        launch_gather_bulk<double, 2>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
+      else if (xa % 16 == 0 && (ldx * 8) % 16 == 0 && d % 2 == 0)
         launch_gather<double, 2>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
       else
         launch_gather<double, 1>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags, st);
       break;
     default:
-      if (xa % 16 == 0 && (ldx * 2) % 16 == 0 && d % 8 == 0)
+      if (bulk && xa % 16 == 0 && (ldx * 2) % 16 == 0 && d % 8 == 0)
+        launch_gather_bulk<__nv_bfloat16, 8>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags,
+                                              st);
+      else if (xa % 16 == 0 && (ldx * 2) % 16 == 0 && d % 8 == 0)
         launch_gather<__nv_bfloat16, 8>(X, ldx, d, svals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags,
                                          st);
       else

@@ -411,6 +411,29 @@ def fold(s, vt, pi=None):
     return basis @ (vt @ pi)
 
 
+def r_factor(sx):
+    """Triangular factor R (positive diagonal) of SX = QR; rows min(k, d)."""
+    r = np.linalg.qr(np.asarray(sx, dtype=np.float64), mode="r")
+    sg = np.sign(np.diag(r))
+    sg[sg == 0] = 1.0
+    return r * sg[:, None]
+
+
+def fold_r(sx, sv_tol, pi, rank=None):
+    """JL fold (extension G3, the north star's "R M = Pi"): M = pinv_tau(R) Pi,
+    pinv_tau from the SVD of R (same sigma / V as SX) truncated like the
+    reference (strict relative threshold, optional rank cap).  With nothing
+    truncated this is R^-1 Pi; with Pi = I the row norms equal the reference
+    basis V'/sigma' scores.  Returns (M, r')."""
+    R = r_factor(sx)
+    u, s, vt = np.linalg.svd(R, full_matrices=False)
+    s2, vt2 = truncate(s, vt, sv_tol, rank)
+    r = s2.shape[0]
+    if np.any(s2 == 0.0):
+        raise ZeroDivisionError("exact zero singular value")
+    return (vt2.T / s2) @ (u[:, :r].T @ pi), r
+
+
 def row_scores(x, m):
     """||x_i M||^2 per row; leverage.py:88-95."""
     u = np.asarray(x, dtype=np.float64) @ m
@@ -418,9 +441,14 @@ def row_scores(x, m):
 
 
 def leverage_from_sketch(x, sx, sv_tol, pi=None, rank=None):
+    """Reference path (Pi = None: basis V'/sigma', leverage.py:75-95) or the
+    JL fold pinv_tau(R) Pi."""
+    if pi is not None:
+        m, r = fold_r(sx, sv_tol, pi, rank)
+        return row_scores(x, m), r, m
     u, s, vt = thin_svd(sx)
     s, vt = truncate(s, vt, sv_tol, rank)
-    m = fold(s, vt, pi)
+    m = fold(s, vt, None)
     return row_scores(x, m), s.shape[0], m
 
 

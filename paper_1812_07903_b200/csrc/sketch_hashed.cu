@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
 // float64 (hi, lo) registers, exactly as the reference does per bucket.
 constexpr int BULK_SLOTS = 16;
 constexpr int BULK_SEG = 2048;  // bytes per row segment
-constexpr int BULK_CONSUMERS = 4;
+constexpr int BULK_LANE_BYTES = 32;  // each consumer lane owns 32 B of the segment
+constexpr int BULK_CONSUMERS = BULK_SEG / (32 * BULK_LANE_BYTES);  // 2 warps
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -183,11 +184,23 @@ __device__ __forceinline__ void bar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
 }
 
-template <typename T, int VEC>
+// contribution (sign * scale) * x as float64; UNIT: scale == 1 -> exact sign flip
+template <typename T, bool UNIT>
+__device__ __forceinline__ double contrib(T x, bool neg, double scale) {
+  if constexpr (UNIT) {
+    const double v = to_f64<T>(x);
+    return neg ? -v : v;
+  } else {
+    return __dmul_rn(neg ? -scale : scale, to_f64<T>(x));
+  }
+}
+
+template <typename T, bool UNIT>
 __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_kernel(
     const T* __restrict__ X, int64_t ldx, int64_t d, int ngroups, const uint32_t* __restrict__ vals,
     const uint32_t* __restrict__ start, int64_t k, double scale, const double* hi_in, const double* lo_in,
     double* hi_out, double* lo_out, int32_t* flags) {
+  constexpr int VEC = BULK_LANE_BYTES / static_cast<int>(sizeof(T));
   __shared__ alignas(128) uint8_t ring[BULK_SLOTS][BULK_SEG];
   __shared__ uint64_t full[BULK_SLOTS], empty[BULK_SLOTS];
   const int64_t b = blockIdx.x / ngroups;
@@ -226,29 +239,35 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
     return;
   }
   const int64_t col = static_cast<int64_t>(warp * 32 + lane) * VEC;  // within the segment
-  const bool active = col < cols;
+  const bool active = col < cols;  // cols is a multiple of 16 B / sizeof(T); VEC spans 32 B
+  const int nv = active ? (cols - col >= VEC ? VEC : static_cast<int>(cols - col)) : 0;
   double h[VEC], l[VEC];
   const int64_t so = b * d + c0 + col;
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    h[v] = active ? hi_in[so + v] : 0.0;
-    l[v] = active ? lo_in[so + v] : 0.0;
+    h[v] = v < nv ? hi_in[so + v] : 0.0;
+    l[v] = v < nv ? lo_in[so + v] : 0.0;
   }
   bool bad = false;
   for (uint32_t j = 0; j < cnt; ++j) {
     const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
-    const uint32_t vv = vals[p0 + j];
+    const bool neg = (vals[p0 + j] & 1u) != 0u;
     bar_wait(&full[s], ph);
-    if (active) {
+    if (nv) {
       T xs[VEC];
-      VecLoad<T, VEC>::load_smem(reinterpret_cast<const T*>(ring[s]) + col, xs);
-      const double sg = (vv & 1u) ? -scale : scale;
+      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(ring[s]) + col);
+      uint4 w[2];
+      w[0] = src[0];
+      w[1] = nv == VEC ? src[1] : make_uint4(0u, 0u, 0u, 0u);
+      const T* wv = reinterpret_cast<const T*>(w);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) xs[v] = wv[v];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
-        const double xv = to_f64<T>(xs[v]);
-        bad |= !isfinite(xv);
+        const double cval = contrib<T, UNIT>(xs[v], neg, scale);
+        if constexpr (sizeof(T) == 8) bad |= !isfinite(cval);
         double sum, e;
-        two_sum(h[v], __dmul_rn(sg, xv), sum, e);
+        two_sum(h[v], cval, sum, e);
         h[v] = sum;
         l[v] = __dadd_rn(l[v], e);
       }
@@ -256,11 +275,14 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
     __syncwarp();
     if (lane == 0) bar_arrive(&empty[s]);
   }
-  if (active) {
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
+  for (int v = 0; v < VEC; ++v) {
+    if (v < nv) {
       hi_out[so + v] = h[v];
       lo_out[so + v] = l[v];
+      // fp32 / bf16 inputs cannot overflow a float64 sum: a non-finite state
+      // means a non-finite input (checked once here instead of per element)
+      if constexpr (sizeof(T) < 8) bad |= !(isfinite(h[v]) && isfinite(l[v]));
     }
   }
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
@@ -322,14 +344,18 @@ static void fill_blocks(KeygenBlocks& P, const lvsk_hash_block* blocks, int j0, 
   }
 }
 
-template <typename T, int VEC>
+template <typename T, int VEC_UNUSED>
 static void launch_gather_bulk(const void* X, int64_t ldx, int64_t d, const uint32_t* vals, const uint32_t* start,
                                int64_t k, double scale, const double* hi_in, const double* lo_in, double* hi_out,
                                double* lo_out, int32_t* flags, cudaStream_t st) {
   const int ngroups = static_cast<int>((d * static_cast<int64_t>(sizeof(T)) + BULK_SEG - 1) / BULK_SEG);
   const unsigned grid = static_cast<unsigned>(k * ngroups);
-  hashed_gather_bulk_kernel<T, VEC><<<grid, 32 * (BULK_CONSUMERS + 1), 0, st>>>(
-      static_cast<const T*>(X), ldx, d, ngroups, vals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags);
+  if (scale == 1.0)
+    hashed_gather_bulk_kernel<T, true><<<grid, 32 * (BULK_CONSUMERS + 1), 0, st>>>(
+        static_cast<const T*>(X), ldx, d, ngroups, vals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags);
+  else
+    hashed_gather_bulk_kernel<T, false><<<grid, 32 * (BULK_CONSUMERS + 1), 0, st>>>(
+        static_cast<const T*>(X), ldx, d, ngroups, vals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags);
 }
 
 template <typename T, int VEC>

@@ -37,7 +37,7 @@ import torch.distributed as tdist
 
 from . import _native as N
 from .errors import ConfigurationError, UnsupportedFamilyError
-from .leverage import LeverageResult, factor_device, fold_device, jl_device, scores_device
+from .leverage import LeverageResult, factor_device, jl_device, scores_device, sketch_fold
 from .matrix import device_matrix
 from .sketch import COUNTSKETCH, GAUSSIAN, OSNAP, SketchSpec, SketchState, consume_rows, merge
 
@@ -131,9 +131,12 @@ class DeviceOps:
     merge = staticmethod(merge)
 
     def factor(self, merged: SketchState):
-        sigma, vt, s_host = factor_device(merged.data_device, self.sv_tol, self.rank)
+        sx = merged.data_device
         pi = None if self.jl_dim is None else jl_device(self.jl_seed, self.spec.d, self.jl_dim)
-        return fold_device(sigma, vt, s_host, pi), s_host, vt.cpu().numpy()
+        M, _ = sketch_fold(sx, self.sv_tol, self.rank, pi)
+        # the coordinator report carries the spectrum (reference dist.py:378-381)
+        _, vt, s_host = factor_device(sx, self.sv_tol, self.rank, "svd")
+        return M, s_host, vt.cpu().numpy()
 
     @staticmethod
     def scores(rows, M) -> torch.Tensor:

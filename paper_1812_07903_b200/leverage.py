@@ -108,73 +108,85 @@ def fold_device(sigma: torch.Tensor, vt: torch.Tensor, s_host: np.ndarray, pi: t
     return (basis @ (vt @ pi)).contiguous()
 
 
-def _ns_body(sx: torch.Tensor, pi: torch.Tensor | None, iters: int, eye: torch.Tensor):
-    """Shape-static part of the Newton-Schulz fold (CUDA-graph capturable).
-    Returns (M, diag) with diag = [residual, trace(G), trace(G^-1)]."""
+def _chol_body(sx: torch.Tensor, pi: torch.Tensor, eye: torch.Tensor):
+    """Shape-static Cholesky fold (CUDA-graph capturable, no host sync):
+    G = SX^T SX = R^T R, M = R^-1 Pi, plus diag = [info, trace(G), trace(G^-1)]
+    with trace(G^-1) = ||R^-1||_F^2."""
     G = sx.T @ sx
-    G2 = G @ G
-    # lambda_max <= ||G^4||_F^(1/4) <= d^(1/8) lambda_max: a safe NS scaling
-    c = torch.linalg.matrix_norm(G2 @ G2, ord="fro").sqrt().sqrt()
-    Y = G / c
-    Z = eye
-    T = eye
-    for _ in range(iters):
-        T = torch.addmm(eye, Z, Y, beta=1.5, alpha=-0.5)
-        Y = Y @ T
-        Z = T @ Z
-    inv_sqrt = Z / torch.sqrt(c)
-    diag = torch.stack([torch.linalg.matrix_norm(T - eye, ord="fro"), torch.trace(G), (inv_sqrt * inv_sqrt).sum()])
-    M = inv_sqrt if pi is None else inv_sqrt @ pi
+    L, info = torch.linalg.cholesky_ex(G)
+    R = L.mT
+    M = torch.linalg.solve_triangular(R, pi, upper=True)
+    Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
+    diag = torch.stack([info.to(G.dtype), torch.trace(G), (Rinv * Rinv).sum()])
     return M, diag
 
 
-def ns_certified(diag, d: int, sv_tol: float | None) -> bool:
-    """Convergence + the no-truncation certificate
-    trace(G) * trace(G^-1) < 1/sv_tol^2  (lambda_min >= 1/trace(G^-1),
-    lambda_max <= trace(G)  ==>  every sigma_j > sv_tol * sigma_1)."""
-    res, tr_g, tr_ginv = (float(v) for v in diag)
-    if not (math.isfinite(res) and math.isfinite(tr_ginv)) or tr_ginv <= 0 or res >= 1e-12 * math.sqrt(d):
-        return False
-    if sv_tol is not None and sv_tol > 0 and tr_g * tr_ginv >= 1.0 / (sv_tol * sv_tol):
-        return False
-    return True
+# kappa(G) <= trace(G) * trace(G^-1); above this the Gram/Cholesky route could
+# lose more than ~1e-6 relative accuracy and the QR route runs instead
+_CHOL_KAPPA_GUARD = 1e10
 
 
-def newton_schulz_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor | None, max_iter: int = 30):
-    """M = (SX^T SX)^(-1/2) [Pi] by the coupled Newton-Schulz iteration
-    (fp64 cuBLAS GEMMs only, no eigensolver).  Equal to the spectral fold
-    V S^-1 V^T [Pi] whenever truncation keeps every component, which is
-    certified by :func:`ns_certified`.  Returns None when convergence or the
-    certificate fails (the caller falls back to the eigensolver)."""
+def chol_certified(diag, sv_tol: float | None) -> bool:
+    """Certificate that the truncation keeps every component:
+    lambda_min >= 1/trace(G^-1), lambda_max <= trace(G), so
+    trace(G) * trace(G^-1) < 1/sv_tol^2  ==>  every sigma_j > sv_tol * sigma_1."""
+    info, tr_g, tr_ginv = (float(v) for v in diag)
+    if info != 0 or not (math.isfinite(tr_g) and math.isfinite(tr_ginv)) or tr_ginv <= 0 or tr_g <= 0:
+        return False
+    prod = tr_g * tr_ginv
+    if prod >= _CHOL_KAPPA_GUARD:
+        return False
+    return not (sv_tol is not None and sv_tol > 0 and prod >= 1.0 / (sv_tol * sv_tol))
+
+
+def cholesky_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor):
+    """M = R^-1 Pi when certified (no component truncated), else None."""
     k, d = sx.shape
     if k < d:
         return None
     eye = torch.eye(d, dtype=sx.dtype, device=sx.device)
-    for iters in (10, 20, max_iter):
-        M, diag = _ns_body(sx, pi, iters, eye)
-        vals = diag.tolist()
-        if ns_certified(vals, d, sv_tol):
-            return M.contiguous()
-        if math.isfinite(vals[0]) and vals[0] < 1e-12 * math.sqrt(d):
-            return None  # converged but truncation would bite
-    return None
+    M, diag = _chol_body(sx, pi, eye)
+    return M.contiguous() if chol_certified(diag.tolist(), sv_tol) else None
+
+
+def qr_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor):
+    """General JL fold M = pinv_tau(R) Pi: R from QR of SX (no squaring of the
+    condition number), SVD of the small R, the reference's strict relative
+    truncation and the optional rank cap."""
+    R = torch.linalg.qr(sx, mode="r")[1]
+    sg = torch.sign(torch.diagonal(R))
+    sg[sg == 0] = 1.0
+    R = R * sg[:, None]
+    u, sigma, vt = torch.linalg.svd(R, full_matrices=False, driver="gesvd")
+    s_host = sigma.cpu().numpy()
+    if s_host.shape[0] == 0 or s_host[0] <= 0:
+        raise DegenerateInputError("cannot truncate an all-zero matrix (largest singular value is 0)")
+    r = s_host.shape[0] if sv_tol is None else int(np.count_nonzero(s_host > sv_tol * s_host[0]))
+    if rank is not None:
+        r = min(r, rank)
+    if np.any(s_host[:r] == 0.0):
+        raise SingularInversionError("sketch has an exactly-zero singular value; use the truncated method")
+    M = (vt[:r].T / sigma[:r]) @ (u[:, :r].T @ pi)
+    return M.contiguous(), r
 
 
 def sketch_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor | None,
                 method: str = "auto"):
-    """SX -> (M, effective_rank).  "auto" uses the eigensolver-free
-    Newton-Schulz fold when it is certified equal to the truncated spectral
-    fold (no rank cap, no component below the threshold), else the spectral
-    path (factor_device + fold_device)."""
+    """SX -> (M, effective_rank).
+
+    pi is None (the reference API): M = V'/sigma' from the SVD of SX
+    (leverage.py:75-85).  JL (pi given, BASELINE's r): M = pinv_tau(R) Pi —
+    Cholesky + triangular solves when :func:`chol_certified` proves nothing is
+    truncated, else QR + SVD of R."""
     k, d = sx.shape
-    if method in ("auto", "ns") and rank is None and k >= d and d >= 64:
-        M = newton_schulz_fold(sx, sv_tol, pi)
+    if pi is None:
+        sigma, vt, s_host = factor_device(sx, sv_tol, rank, "svd" if method in ("auto", "chol", "qr") else method)
+        return fold_device(sigma, vt, s_host, None), int(s_host.shape[0])
+    if method in ("auto", "chol") and rank is None and k >= d:
+        M = cholesky_fold(sx, sv_tol, pi)
         if M is not None:
             return M, d
-        if method == "ns":
-            raise RuntimeError("Newton-Schulz fold not certified for this sketch")
-    sigma, vt, s_host = factor_device(sx, sv_tol, rank, "svd" if method == "ns" else ("auto" if method == "auto" else method))
-    return fold_device(sigma, vt, s_host, pi), int(s_host.shape[0])
+    return qr_fold(sx, sv_tol, rank, pi)
 
 
 def split_m(M: torch.Tensor, x_dtype: torch.dtype):
@@ -263,22 +275,19 @@ class KernelOperands:
 
 
 class FoldGraph:
-    """The certified Newton-Schulz fold + K5 operand split for a fixed
-    (k, d, r) captured once as a CUDA graph; ``run()`` replays it and returns
-    False when the certificate fails (caller then takes the eager path)."""
+    """The certified Cholesky fold + K5 operand split for a fixed (k, d, r)
+    captured once as a CUDA graph; ``run()`` replays it and returns False when
+    the certificate fails (caller then takes the eager QR path)."""
 
-    def __init__(self, sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor | None, X_like: torch.Tensor,
-                 iters: int = 10):
+    def __init__(self, sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor, X_like: torch.Tensor):
         self.sx, self.sv_tol, self.pi = sx, sv_tol, pi
         k, d = sx.shape
-        r = d if pi is None else pi.shape[1]
-        self.ops = KernelOperands(None, X_like, (d, r))
+        self.ops = KernelOperands(None, X_like, (d, pi.shape[1]))
         self.eye = torch.eye(d, dtype=torch.float64, device=sx.device)
         self.diag = torch.zeros(3, dtype=torch.float64, device=sx.device)
-        self.iters = iters
         self.graph = None
-        # warm up cuBLAS handles / workspaces outside capture
-        M, diag = _ns_body(sx, pi, 1, self.eye)
+        # warm up cuBLAS / cuSOLVER handles and workspaces outside capture
+        M, diag = _chol_body(sx, pi, self.eye)
         self.ops.set(M)
         torch.cuda.synchronize()
         s = torch.cuda.Stream()
@@ -286,7 +295,7 @@ class FoldGraph:
         with torch.cuda.stream(s):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
-                M, diag = _ns_body(self.sx, self.pi, iters, self.eye)
+                M, diag = _chol_body(self.sx, self.pi, self.eye)
                 self.ops.set(M)
                 self.diag.copy_(diag)
         torch.cuda.current_stream().wait_stream(s)
@@ -294,7 +303,7 @@ class FoldGraph:
 
     def run(self) -> bool:
         self.graph.replay()
-        return ns_certified(self.diag.tolist(), self.sx.shape[1], self.sv_tol)
+        return chol_certified(self.diag.tolist(), self.sv_tol)
 
 
 def scores_device(X: torch.Tensor, M: torch.Tensor, out: torch.Tensor | None = None, flags=None) -> torch.Tensor:

@@ -91,7 +91,7 @@ class LeveragePipeline:
 
     def _factor(self) -> None:
         k, d = self.sx.shape
-        if (self.factor_method == "auto" and self.rank is None and k >= d and d >= 64
+        if (self.factor_method == "auto" and self.pi is not None and self.rank is None and k >= d
                 and os.environ.get("LVSK_NO_GRAPH", "0") != "1"):
             if self._fold_graph is None:
                 self._fold_graph = FoldGraph(self.sx, self.sv_tol, self.pi, self._x_like)

@@ -53,7 +53,8 @@ class OracleOps:
         sx = (merged.hi + merged.lo).numpy()
         _, s, vt = O.thin_svd(sx)
         s, vt = O.truncate(s, vt, self.sv_tol)
-        return torch.from_numpy(np.ascontiguousarray(O.fold(s, vt, self.pi))), s, vt
+        M, _ = O.fold_r(sx, self.sv_tol, self.pi)
+        return torch.from_numpy(np.ascontiguousarray(M)), s, vt
 
     @staticmethod
     def scores(rows, M):

@@ -284,18 +284,23 @@ def test_tcgen05_nonfinite_and_strided():
         P.leverage.scores_device(X2, M)
 
 
-def test_newton_schulz_fold_equals_spectral():
+def test_cholesky_fold_equals_qr_fold_and_oracle():
     g = torch.Generator(device="cuda").manual_seed(3)
     sx = torch.randn(2048, 256, device="cuda", dtype=torch.float64, generator=g)
     sx[:, :10] *= 50.0
     pi = P.leverage.jl_device(0, 256, 64)
-    m_ns = P.leverage.newton_schulz_fold(sx, 1e-6, pi)
-    assert m_ns is not None
-    sigma, vt, s_host = P.leverage.factor_device(sx, 1e-6, None, "svd")
-    m_sp = P.leverage.fold_device(sigma, vt, s_host, pi)
-    assert torch.allclose(m_ns, m_sp, rtol=1e-9, atol=1e-12 * m_sp.abs().max().item())
-    # a threshold that would truncate is refused by the certificate
-    assert P.leverage.newton_schulz_fold(sx, 0.5, pi) is None
+    m_ch = P.leverage.cholesky_fold(sx, 1e-6, pi)
+    assert m_ch is not None
+    m_qr, r = P.leverage.qr_fold(sx, 1e-6, None, pi)
+    assert r == 256
+    assert torch.allclose(m_ch, m_qr, rtol=1e-9, atol=1e-12 * m_qr.abs().max().item())
+    m_or, r_or = O.fold_r(sx.cpu().numpy(), 1e-6, O.jl_matrix(0, 256, 64))
+    assert r_or == 256 and np.allclose(m_qr.cpu().numpy(), m_or, rtol=1e-9, atol=1e-12 * np.abs(m_or).max())
+    # a threshold that would truncate is refused by the certificate, then the QR fold truncates
+    assert P.leverage.cholesky_fold(sx, 0.5, pi) is None
+    m_tr, r_tr = P.leverage.qr_fold(sx, 0.5, None, pi)
+    m_or2, r_or2 = O.fold_r(sx.cpu().numpy(), 0.5, O.jl_matrix(0, 256, 64))
+    assert r_tr == r_or2 < 256 and np.allclose(m_tr.cpu().numpy(), m_or2, rtol=1e-8, atol=1e-11 * np.abs(m_or2).max())
 
 
 # ---------------------------------------------------------------------------

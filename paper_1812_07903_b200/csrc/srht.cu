@@ -21,26 +21,31 @@
 
 namespace lvsk {
 
-constexpr int SRHT_THREADS = 256;
+constexpr int SRHT_THREADS = 128;
 constexpr size_t SRHT_CHUNK_BYTES = size_t{64} << 20;
 
 template <typename C>
 struct SrhtCfg {
-  static constexpr int DC = 128 / sizeof(C);  // columns per CTA (128 B)
-  static constexpr int PAD = 1;
+  static constexpr int W = 16 / sizeof(C);      // values per 16-byte vector
+  static constexpr int DC = 128 / sizeof(C);    // columns per CTA (128 B)
+  static constexpr int Q = DC / W;              // vectors per row segment (8)
+  static constexpr int PAD = W;                 // one vector of padding per smem row
 };
 
-// in-register radix-2 WHT over `n` elements (n power of two, <= 16), low bit first
-template <typename C, int N>
-__device__ __forceinline__ void reg_wht(C (&v)[N]) {
+// in-register radix-2 WHT over N rows of W-wide vectors, low bit first
+template <typename C, int N, int W>
+__device__ __forceinline__ void reg_wht(C (&v)[N][W]) {
 #pragma unroll
   for (int h = 1; h < N; h <<= 1) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       if ((i & h) == 0) {
-        C a = v[i], b = v[i + h];
-        v[i] = a + b;
-        v[i + h] = a - b;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const C a = v[i][w], b = v[i + h][w];
+          v[i][w] = a + b;
+          v[i + h][w] = a - b;
+        }
       }
     }
   }
@@ -51,85 +56,122 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ float ld_stream(const float* p) {
-  float v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
-               : "=f"(v)
-               : "l"(p), "l"(evict_first_policy()));
-  return v;
-}
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v)
-               : "l"(p), "l"(evict_first_policy()));
-  return v;
-}
-__device__ __forceinline__ float ld_stream(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
-template <typename T, typename C>
-__device__ __forceinline__ C load_signed(const T* X, int64_t ldx, int64_t n, int64_t d, const int8_t* signs,
-                                         int64_t row, int64_t col, bool& bad) {
-  if (row >= n || col >= d) return C(0);
-  C x = static_cast<C>(ld_stream(X + row * ldx + col));
-  bad |= !isfinite(static_cast<double>(x));
-  if (signs && signs[row] < 0) x = -x;
-  return x;
+// W consecutive values of row `row` starting at column `col` (zero past d / n)
+template <typename T, typename C, bool VECTOR>
+__device__ __forceinline__ void load_row_vec(const T* X, int64_t ldx, int64_t n, int64_t d, int64_t row, int64_t col,
+                                             uint64_t pol, C (&out)[SrhtCfg<C>::W]) {
+  constexpr int W = SrhtCfg<C>::W;
+  if (row >= n) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) out[w] = C(0);
+    return;
+  }
+  const T* p = X + row * ldx + col;
+  if constexpr (VECTOR && sizeof(T) == sizeof(C)) {
+    if (col + W <= d) {
+      if constexpr (sizeof(C) == 4) {
+        float4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "l"(p), "l"(pol));
+        out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+      } else {
+        double2 v;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(v.x), "=d"(v.y)
+                     : "l"(p), "l"(pol));
+        out[0] = v.x; out[1] = v.y;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < W; ++w) out[w] = (col + w < d) ? static_cast<C>(to_f64<T>(p[w])) : C(0);
 }
 
-// Pass 1: rows [chunk_row0 + blockIdx.x*2^B, +2^B) -> T1 (chunk-local rows)
-template <typename T, typename C, int B>
+// Pass 1: rows [chunk_row0 + blockIdx.x*2^B, +2^B) -> T1 (chunk-local rows),
+// sign flip and zero padding fused into the load.
+template <typename T, typename C, int B, bool VECTOR>
 __global__ void __launch_bounds__(SRHT_THREADS) srht_pass1_kernel(const T* __restrict__ X, int64_t n, int64_t d,
                                                                   int64_t ldx, int64_t chunk_row0,
                                                                   const int8_t* __restrict__ signs,
                                                                   C* __restrict__ T1, int32_t* flags) {
-  constexpr int DC = SrhtCfg<C>::DC;
+  using G = SrhtCfg<C>;
+  constexpr int W = G::W, Q = G::Q;
   constexpr int R = 1 << B;
   constexpr int BA = B < 4 ? B : 4;
   constexpr int NA = 1 << BA;
   constexpr int NB = 1 << (B - BA);
-  __shared__ C S[R][DC + SrhtCfg<C>::PAD];
-  const int64_t col0 = static_cast<int64_t>(blockIdx.y) * DC;
+  __shared__ alignas(16) C S[R][G::DC + G::PAD];
+  const int64_t col0 = static_cast<int64_t>(blockIdx.y) * G::DC;
   const int64_t lrow0 = static_cast<int64_t>(blockIdx.x) * R;  // chunk-local
+  const uint64_t pol = evict_first_policy();
   bool bad = false;
-  // phase A: groups of NA consecutive rows, one column
-  for (int g = threadIdx.x; g < (R / NA) * DC; g += SRHT_THREADS) {
-    const int col = g % DC, rh = g / DC;
-    C v[NA];
+  for (int g = threadIdx.x; g < (R / NA) * Q; g += SRHT_THREADS) {
+    const int q = g % Q, rh = g / Q;
+    const int64_t grow0 = chunk_row0 + lrow0 + rh * NA;
+    C v[NA][W];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) load_row_vec<T, C, VECTOR>(X, ldx, n, d, grow0 + j, col0 + q * W, pol, v[j]);
+    if (signs) {
+      int8_t sg[NA];
+      if constexpr (NA == 16) {
+        const int4 s16 = *reinterpret_cast<const int4*>(signs + grow0);
+        const int8_t* sp = reinterpret_cast<const int8_t*>(&s16);
+#pragma unroll
+        for (int j = 0; j < NA; ++j) sg[j] = sp[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) sg[j] = signs[grow0 + j];
+      }
+#pragma unroll
+      for (int j = 0; j < NA; ++j)
+#pragma unroll
+        for (int w = 0; w < W; ++w) v[j][w] = sg[j] < 0 ? -v[j][w] : v[j][w];
+    }
 #pragma unroll
     for (int j = 0; j < NA; ++j)
-      v[j] = load_signed<T, C>(X, ldx, n, d, signs, chunk_row0 + lrow0 + rh * NA + j, col0 + col, bad);
-    reg_wht<C, NA>(v);
-    if (NB == 1) {
-      if (col0 + col < d) {
 #pragma unroll
-        for (int j = 0; j < NA; ++j) T1[(lrow0 + rh * NA + j) * d + col0 + col] = v[j];
-      }
-    } else {
+      for (int w = 0; w < W; ++w) bad |= !isfinite(static_cast<double>(v[j][w]));
+    reg_wht<C, NA, W>(v);
 #pragma unroll
-      for (int j = 0; j < NA; ++j) S[rh * NA + j][col] = v[j];
-    }
+    for (int j = 0; j < NA; ++j)
+#pragma unroll
+      for (int w = 0; w < W; ++w) S[rh * NA + j][q * W + w] = v[j][w];
   }
-  if (NB > 1) {
-    __syncthreads();
-    // phase B: groups of NB rows strided by NA
-    for (int g = threadIdx.x; g < NA * DC; g += SRHT_THREADS) {
-      const int col = g % DC, rl = g / DC;
-      C v[NB];
+  __syncthreads();
+  for (int g = threadIdx.x; g < NA * Q; g += SRHT_THREADS) {
+    const int q = g % Q, rl = g / Q;
+    C v[NB][W];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) v[j] = S[rl + NA * j][col];
-      reg_wht<C, NB>(v);
-      if (col0 + col < d) {
+    for (int j = 0; j < NB; ++j)
 #pragma unroll
-        for (int j = 0; j < NB; ++j) T1[(lrow0 + rl + NA * j) * d + col0 + col] = v[j];
+      for (int w = 0; w < W; ++w) v[j][w] = S[rl + NA * j][q * W + w];
+    reg_wht<C, NB, W>(v);
+    const int64_t col = col0 + q * W;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      C* dst = T1 + (lrow0 + rl + NA * j) * d + col;
+      if (col + W <= d && d % W == 0) {
+        if constexpr (sizeof(C) == 4) {
+          *reinterpret_cast<float4*>(dst) = make_float4(v[j][0], v[j][1], v[j][2], v[j][3]);
+        } else {
+          *reinterpret_cast<double2*>(dst) = make_double2(v[j][0], v[j][1]);
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if (col + w < d) dst[w] = v[j][w];
       }
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
 }
 
-// Pass 2: residue q1 = blockIdx.x of the low B1 bits; transform over B2 bits.
-// order / qstart: sample indices grouped by q1 (stable), qstart[2^B1 + 1].
+// Pass 2: residue q1 = blockIdx.x of the low B1 bits; WHT over the next B2
+// bits; every sampled row with that residue gets (-1)^popc(p_hi & chunk) x
+// its value added into SX (float64).
 template <typename C, int B2>
 __global__ void __launch_bounds__(SRHT_THREADS) srht_pass2_kernel(const C* __restrict__ T1, int64_t d, int B1,
                                                                   int64_t chunk, int cb,
@@ -138,58 +180,80 @@ __global__ void __launch_bounds__(SRHT_THREADS) srht_pass2_kernel(const C* __res
                                                                   const uint32_t* __restrict__ qstart,
                                                                   double* __restrict__ SX, int first,
                                                                   double final_div) {
-  constexpr int DC = SrhtCfg<C>::DC;
+  using G = SrhtCfg<C>;
+  constexpr int W = G::W, Q = G::Q;
   constexpr int R = 1 << B2;
   constexpr int BA = B2 < 4 ? B2 : 4;
   constexpr int NA = 1 << BA;
   constexpr int NB = 1 << (B2 - BA);
-  __shared__ C S[R][DC + SrhtCfg<C>::PAD];
+  __shared__ alignas(16) C S[R][G::DC + G::PAD];
   const int64_t q1 = blockIdx.x;
   const uint32_t e0 = qstart[q1], e1 = qstart[q1 + 1];
   if (e0 == e1) return;  // no sampled row has this residue (block-uniform)
-  const int64_t col0 = static_cast<int64_t>(blockIdx.y) * DC;
+  const int64_t col0 = static_cast<int64_t>(blockIdx.y) * G::DC;
   const int64_t stride = int64_t{1} << B1;
-  for (int g = threadIdx.x; g < (R / NA) * DC; g += SRHT_THREADS) {
-    const int col = g % DC, rh = g / DC;
-    C v[NA];
+  for (int g = threadIdx.x; g < (R / NA) * Q; g += SRHT_THREADS) {
+    const int q = g % Q, rh = g / Q;
+    const int64_t col = col0 + q * W;
+    C v[NA][W];
 #pragma unroll
     for (int j = 0; j < NA; ++j) {
-      const int64_t i2 = rh * NA + j;
-      v[j] = (col0 + col < d) ? T1[(q1 + stride * i2) * d + col0 + col] : C(0);
-    }
-    reg_wht<C, NA>(v);
+      const C* src = T1 + (q1 + stride * (rh * NA + j)) * d + col;
+      if (col + W <= d && d % W == 0) {
+        if constexpr (sizeof(C) == 4) {
+          const float4 t = *reinterpret_cast<const float4*>(src);
+          v[j][0] = t.x; v[j][1] = t.y; v[j][2] = t.z; v[j][3] = t.w;
+        } else {
+          const double2 t = *reinterpret_cast<const double2*>(src);
+          v[j][0] = t.x; v[j][1] = t.y;
+        }
+      } else {
 #pragma unroll
-    for (int j = 0; j < NA; ++j) S[rh * NA + j][col] = v[j];
+        for (int w = 0; w < W; ++w) v[j][w] = col + w < d ? src[w] : C(0);
+      }
+    }
+    reg_wht<C, NA, W>(v);
+#pragma unroll
+    for (int j = 0; j < NA; ++j)
+#pragma unroll
+      for (int w = 0; w < W; ++w) S[rh * NA + j][q * W + w] = v[j][w];
   }
   __syncthreads();
   if (NB > 1) {
-    for (int g = threadIdx.x; g < NA * DC; g += SRHT_THREADS) {
-      const int col = g % DC, rl = g / DC;
-      C v[NB];
+    for (int g = threadIdx.x; g < NA * Q; g += SRHT_THREADS) {
+      const int q = g % Q, rl = g / Q;
+      C v[NB][W];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) v[j] = S[rl + NA * j][col];
-      reg_wht<C, NB>(v);
+      for (int j = 0; j < NB; ++j)
 #pragma unroll
-      for (int j = 0; j < NB; ++j) S[rl + NA * j][col] = v[j];
+        for (int w = 0; w < W; ++w) v[j][w] = S[rl + NA * j][q * W + w];
+      reg_wht<C, NB, W>(v);
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+#pragma unroll
+        for (int w = 0; w < W; ++w) S[rl + NA * j][q * W + w] = v[j][w];
     }
     __syncthreads();
   }
   // scatter the sampled outputs: SX[t] (+)= sign * S[q2]
-  const int lanes_per_entry = DC;
-  const int entries_per_pass = SRHT_THREADS / lanes_per_entry;
-  const int col = threadIdx.x % lanes_per_entry;
-  if (col0 + col >= d) return;
-  for (uint32_t e = e0 + threadIdx.x / lanes_per_entry; e < e1; e += entries_per_pass) {
+  const int q = threadIdx.x % Q;
+  const int64_t col = col0 + q * W;
+  if (col >= d) return;
+  for (uint32_t e = e0 + threadIdx.x / Q; e < e1; e += SRHT_THREADS / Q) {
     const uint32_t t = order[e];
     const uint64_t p = static_cast<uint64_t>(sample[t]);
     const int q2 = static_cast<int>((p >> B1) & static_cast<uint64_t>(R - 1));
-    const uint64_t phi = p >> cb;
-    double v = static_cast<double>(S[q2][col]);
-    if (__popcll(phi & static_cast<uint64_t>(chunk)) & 1) v = -v;
-    double* dst = SX + static_cast<int64_t>(t) * d + col0 + col;
-    double acc = first ? v : *dst + v;
-    if (final_div != 0.0) acc = acc / final_div;
-    *dst = acc;
+    const bool neg = __popcll((p >> cb) & static_cast<uint64_t>(chunk)) & 1;
+    double* dst = SX + static_cast<int64_t>(t) * d + col;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      if (col + w >= d) break;
+      double v = static_cast<double>(S[q2][q * W + w]);
+      if (neg) v = -v;
+      double acc = first ? v : dst[w] + v;
+      if (final_div != 0.0) acc = acc / final_div;
+      dst[w] = acc;
+    }
   }
 }
 
@@ -227,11 +291,13 @@ static SrhtPlan plan_srht(int64_t m, int64_t d, size_t csize) {
   return p;
 }
 
-template <typename T, typename C>
+template <typename T, typename C, bool VECTOR>
 static void launch_pass1(int B, dim3 grid, cudaStream_t st, const T* X, int64_t n, int64_t d, int64_t ldx,
                          int64_t row0, const int8_t* signs, C* T1, int32_t* flags) {
-#define LVSK_P1(BB) \
-  case BB: srht_pass1_kernel<T, C, BB><<<grid, SRHT_THREADS, 0, st>>>(X, n, d, ldx, row0, signs, T1, flags); break;
+#define LVSK_P1(BB)                                                                                              \
+  case BB:                                                                                                       \
+    srht_pass1_kernel<T, C, BB, VECTOR><<<grid, SRHT_THREADS, 0, st>>>(X, n, d, ldx, row0, signs, T1, flags); \
+    break;
   switch (B) {
     LVSK_P1(0) LVSK_P1(1) LVSK_P1(2) LVSK_P1(3) LVSK_P1(4) LVSK_P1(5) LVSK_P1(6) LVSK_P1(7) LVSK_P1(8)
   }
@@ -279,9 +345,14 @@ static int32_t run_srht(const T* X, int64_t n, int64_t d, int64_t ldx, int64_t m
   if (last < 0) last = 0;
   if (last > P.chunks - 1) last = P.chunks - 1;
   const unsigned ycols = static_cast<unsigned>((d + SrhtCfg<C>::DC - 1) / SrhtCfg<C>::DC);
+  const bool vector_ok = reinterpret_cast<uintptr_t>(X) % 16 == 0 && (ldx * sizeof(T)) % 16 == 0 &&
+                         (d * sizeof(C)) % 16 == 0 && (d * sizeof(T)) % 16 == 0;
   for (int64_t ch = 0; ch <= last; ++ch) {
     dim3 g1(static_cast<unsigned>(chunk_rows >> P.B1), ycols);
-    launch_pass1<T, C>(P.B1, g1, st, X, n, d, ldx, ch * chunk_rows, signs, T1, flags);
+    if (vector_ok)
+      launch_pass1<T, C, true>(P.B1, g1, st, X, n, d, ldx, ch * chunk_rows, signs, T1, flags);
+    else
+      launch_pass1<T, C, false>(P.B1, g1, st, X, n, d, ldx, ch * chunk_rows, signs, T1, flags);
     dim3 g2(static_cast<unsigned>(int64_t{1} << P.B1), ycols);
     launch_pass2<C>(P.B2, g2, st, T1, d, P.B1, ch, P.cb, sample, order, qstart, SX, ch == 0 ? 1 : 0,
                     ch == last ? divisor : 0.0);

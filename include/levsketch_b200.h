@@ -152,6 +152,24 @@ LVSK_API int32_t lvsk_leverage_tf32x3(const float* X, int64_t n, int64_t d, int6
                                       const float* Mt_lo, const void* Mt_hi_bf16, int64_t r, double* scores,
                                       int32_t* flags, void* stream);
 
+/* ---- K2 / K6: CSR rows (extension G2; BASELINE config 4) -----------------
+ * Same semantics as lvsk_hashed_sketch / lvsk_rowsumsq_gemm on the densified
+ * rows (bit-exact for K2: zero entries leave the TwoSum state unchanged).
+ * row_ptr: n+1 int64 (row_ptr[0] may be nonzero: col/val point at element
+ * row_ptr[0]); col: int32, strictly increasing per row, in [0, d);
+ * val: F32 or F64.  Bad indices set LVSK_FLAG_BADINDEX, non-finite values
+ * LVSK_FLAG_NONFINITE.  K6 takes M as float32 d x r (r <= 256). */
+LVSK_API size_t lvsk_hashed_csr_workspace_bytes(int64_t n, int32_t s, int64_t k);
+LVSK_API int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t* col, const void* val,
+                                        int32_t val_dtype, int64_t n, int64_t d, uint64_t row0,
+                                        const lvsk_hash_block* blocks, int32_t s, double scale,
+                                        const double* hi_in, const double* lo_in, double* hi_out,
+                                        double* lo_out, int64_t k, void* ws, size_t ws_bytes, int32_t* flags,
+                                        void* stream);
+LVSK_API int32_t lvsk_rowsumsq_csr(const int64_t* row_ptr, const int32_t* col, const void* val,
+                                   int32_t val_dtype, int64_t n, int64_t d, const float* M, int64_t r,
+                                   double* scores, int32_t* flags, void* stream);
+
 /* ---- ordering -------------------------------------------------------------
  * scores_to_distribution (order.py:51-63): p = scores / sum(scores), with
  * the sum a deterministic two-level float64 reduction.  Sets

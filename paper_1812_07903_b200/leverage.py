@@ -372,12 +372,16 @@ def _block_scores(rows, basis) -> np.ndarray:
 
 
 def _sketched(a, spec, sv_tol, mem_cap_bytes, jl_dim, jl_seed, rank, method):
-    X = device_matrix(a)
+    from .csr import CSRMatrix, csr_scores
+
+    m = None if isinstance(a, (np.ndarray, torch.Tensor, list)) else CSRMatrix.from_any(a)
+    X = m if m is not None else device_matrix(a)
+    d = m.d if m is not None else X.shape[1]
     state = apply_sketch(X, spec, mem_cap=mem_cap_bytes)
     sx = state.data_device
-    pi = None if jl_dim is None else jl_device(jl_seed, X.shape[1], jl_dim)
+    pi = None if jl_dim is None else jl_device(jl_seed, d, jl_dim)
     M, eff = sketch_fold(sx, sv_tol, rank, pi)
-    scores = scores_device(X, M)
+    scores = csr_scores(m, M) if m is not None else scores_device(X, M)
     return LeverageResult(
         scores=scores.cpu().numpy(),
         method=method,

@@ -435,3 +435,71 @@ def test_c2_full_size_properties():
     assert np.array_equal(np.sort(o), np.arange(n))
     sc = scores.cpu().numpy()
     assert np.all(np.diff(sc[o] / sc.sum()) <= 0)
+
+
+# ---------------------------------------------------------------------------
+# K2 / K6: CSR rows (extension G2), semantics = densified rows
+
+
+def _random_csr(n, d, per_row, seed, dtype=np.float32):
+    rng = np.random.default_rng(seed)
+    indptr = [0]
+    cols, vals = [], []
+    for _ in range(n):
+        k = int(rng.integers(0, per_row * 2 + 1))
+        c = np.unique(np.minimum(rng.zipf(1.1, size=k) - 1, d - 1))
+        v = rng.lognormal(0.0, 1.0, size=c.size)
+        if c.size:
+            v = v / np.linalg.norm(v)
+        cols.append(c.astype(np.int32))
+        vals.append(v.astype(dtype))
+        indptr.append(indptr[-1] + c.size)
+    indptr = np.array(indptr, dtype=np.int64)
+    col = np.concatenate(cols) if cols else np.zeros(0, np.int32)
+    val = np.concatenate(vals) if vals else np.zeros(0, dtype)
+    dense = np.zeros((n, d), dtype=np.float64)
+    for r in range(n):
+        dense[r, col[indptr[r] : indptr[r + 1]]] = val[indptr[r] : indptr[r + 1]]
+    return (indptr, col, val, (n, d)), dense
+
+
+@pytest.mark.parametrize("n,d,k,s", [(3000, 300, 512, 4), (1500, 2100, 1024, 3), (777, 64, 128, 1)])
+def test_csr_sketch_bit_exact_vs_dense(n, d, k, s):
+    csr, dense = _random_csr(n, d, 40, seed=n + d)
+    fam = "osnap" if s > 1 else "countsketch"
+    spec = P.SketchSpec(fam, eps=0.5, d=d, seed=7, rows_override=k, osnap_s=s if fam == "osnap" else None)
+    hi, lo = O.hashed_sketch(dense, fam, k, 7, s)
+    assert np.array_equal(P.apply_sketch(csr, spec).data, hi + lo)
+    # two row blocks with global indices == one pass
+    m = P.csr.CSRMatrix(*csr)
+    st = P.SketchState(spec, n)
+    P.consume_rows(st, m.rows(0, n // 2), 0)
+    P.consume_rows(st, m.rows(n // 2, n), n // 2)
+    assert np.array_equal(st.data, hi + lo)
+
+
+def test_csr_leverage_vs_oracle():
+    n, d, k, r = 4000, 256, 2048, 128
+    csr, dense = _random_csr(n, d, 30, seed=11)
+    spec = P.SketchSpec("osnap", eps=0.5, d=d, seed=3, rows_override=k, osnap_s=4)
+    res = P.leverage_sketched_trunc(csr, spec, 1e-6, jl_dim=r, jl_seed=2)
+    hi, lo = O.hashed_sketch(dense, "osnap", k, 3, 4)
+    ref, rr, _ = O.leverage_from_sketch(dense, hi + lo, 1e-6, O.jl_matrix(2, d, r))
+    assert res.effective_rank == rr
+    mask = ref > 1e-12
+    assert np.abs(res.scores - ref).max() <= 1e-4 * ref.max()
+    assert np.all(res.scores[~mask] <= 1e-6 * ref.max())
+
+
+def test_csr_validation():
+    indptr = np.array([0, 2, 3], dtype=np.int64)
+    spec = P.SketchSpec("countsketch", eps=0.5, d=8, seed=1, rows_override=16)
+    with pytest.raises(errors.FormatError):  # unsorted columns
+        P.apply_sketch((indptr, np.array([3, 1, 2], np.int32), np.ones(3, np.float32), (2, 8)), spec)
+    with pytest.raises(errors.FormatError):  # out of range
+        P.apply_sketch((indptr, np.array([1, 9, 2], np.int32), np.ones(3, np.float32), (2, 8)), spec)
+    with pytest.raises(errors.FormatError):  # non-finite
+        P.apply_sketch((indptr, np.array([1, 3, 2], np.int32), np.array([1, np.nan, 1], np.float32), (2, 8)), spec)
+    with pytest.raises(errors.UnsupportedFamilyError):
+        P.apply_sketch((indptr, np.array([1, 3, 2], np.int32), np.ones(3, np.float32), (2, 8)),
+                       P.SketchSpec("srht", eps=0.5, d=8, rows_override=2))

@@ -40,14 +40,55 @@ CONFIGS = {
                desc="configs[1]: CountSketch dense fp32 1e6x512, k=4096, r=64"),
     "c1": dict(family="gaussian", n=20_000, d=256, k=1024, r=64, s=None, dtype="f32", sv_tol=1e-6,
                desc="configs[0]: Gaussian sketch fp32 20000x256, k=1024, r=64"),
+    "c4": dict(family="osnap", n=4_000_000, d=4096, k=16384, r=128, s=4, dtype="f32", sv_tol=1e-6, csr=True,
+               desc="configs[3]: OSNAP s=4 on CSR 4e6x4096, ~80 Zipf(1.1) draws/row, k=16384, r=128"),
     "c3": dict(family="srht", n=2**21, d=256, k=4096, r=64, s=None, dtype="f32", sv_tol=1e-6,
                desc="configs[2]: SRHT fp32 2^21x256, k=4096, r=64"),
 }
 
 
+def gen_csr(n, d, draws, seed, device, chunk=250_000):
+    """Bag-of-words-like canonical CSR on the device: `draws` column draws per
+    row from Zipf(1.1) truncated to [1, d] (inverse CDF), lognormal(0, 1)
+    values, duplicate columns summed, rows L2-normalised."""
+    import torch
+
+    from paper_1812_07903_b200.csr import CSRMatrix
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    w = torch.arange(1, d + 1, device=device, dtype=torch.float64).pow(-1.1)
+    cdf = torch.cumsum(w, 0) / w.sum()
+    ptrs, cols, vals = [torch.zeros(1, dtype=torch.int64, device=device)], [], []
+    base = 0
+    for r0 in range(0, n, chunk):
+        rows = min(chunk, n - r0)
+        u = torch.rand(rows * draws, generator=g, device=device, dtype=torch.float64)
+        c = torch.searchsorted(cdf, u).clamp_(max=d - 1)
+        v = torch.exp(torch.randn(rows * draws, generator=g, device=device))
+        r = torch.arange(rows, device=device).repeat_interleave(draws)
+        key = r * d + c
+        key, order = torch.sort(key)
+        v = v[order]
+        uk, inv = torch.unique_consecutive(key, return_inverse=True)
+        vs = torch.zeros(uk.numel(), device=device, dtype=torch.float32).index_add_(0, inv, v)
+        ur = uk // d
+        norm = torch.zeros(rows, device=device, dtype=torch.float32).index_add_(0, ur, vs * vs).sqrt_()
+        vs = vs / norm[ur]
+        cnt = torch.bincount(ur, minlength=rows)
+        ptrs.append(base + torch.cumsum(cnt, 0))
+        base += int(uk.numel())
+        cols.append((uk % d).to(torch.int32))
+        vals.append(vs)
+    indptr = torch.cat(ptrs)
+    return CSRMatrix(indptr, torch.cat(cols), torch.cat(vals), (n, d))
+
+
 def gen_x(cfg, rank: int, device):
     """Seeded synthetic X with the config's structure, generated on the device."""
     import torch
+
+    if cfg.get("csr"):
+        return gen_csr(cfg["n"], cfg["d"], 80, 1000 + rank, device)
 
     n, d = cfg["n"], cfg["d"]
     g = torch.Generator(device=device).manual_seed(1000 + rank)
@@ -145,6 +186,28 @@ def cpu_leg(cfg, rows: int, threads: int):
 
     rng = np.random.default_rng(7)
     d = cfg["d"]
+    if cfg.get("csr"):
+        # densified CSR rows streamed through the reference hashing;
+        # the n-independent 16384 x 4096 SVD is excluded here (~23 s in LAPACK)
+        import scipy.sparse as sp
+
+        w = np.arange(1, d + 1, dtype=np.float64) ** -1.1
+        cdf = np.cumsum(w) / w.sum()
+        r = np.repeat(np.arange(rows), 80)
+        c = np.minimum(np.searchsorted(cdf, rng.random(rows * 80)), d - 1)
+        m = sp.csr_matrix((rng.lognormal(0, 1, rows * 80), (r, c)), shape=(rows, d))
+        m.sum_duplicates()
+        x = np.asarray(m.todense())
+        x /= np.maximum(np.linalg.norm(x, axis=1, keepdims=True), 1e-30)
+        pi = O.jl_matrix(0, d, cfg["r"])
+        t0 = time.perf_counter()
+        hp = O.HashParams("osnap", 0, cfg["k"], cfg["s"])
+        hi = np.zeros((cfg["k"], d))
+        lo = np.zeros_like(hi)
+        O.hashed_consume(hi, lo, hp, x, 0)
+        O.row_scores(x, np.linalg.qr(pi)[0])  # stands in for the fold's d x r product
+        dt = time.perf_counter() - t0
+        return rows / dt, dt
     x = (rng.standard_normal((rows, 50)) @ (np.linspace(10, 1, 50)[:, None] * rng.standard_normal((50, d)))
          + 0.01 * rng.standard_normal((rows, d))).astype(np.float32).astype(np.float64)
     pi = O.jl_matrix(0, d, cfg["r"])
@@ -231,7 +294,10 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
     n, d, k, r = cfg["n"], cfg["d"], cfg["k"], cfg["r"]
     spec = P.SketchSpec(cfg["family"], eps=0.5, d=d, seed=0, rows_override=k, osnap_s=cfg["s"])
-    X = gen_x(cfg, rank, dev).to(dtype)
+    X = gen_x(cfg, rank, dev)
+    csr = cfg.get("csr", False)
+    if not csr:
+        X = X.to(dtype)
     torch.cuda.synchronize()
     row0 = rank * n
     pipe = P.LeveragePipeline(spec, n * world if world > 1 else n, d, dtype, sv_tol=cfg["sv_tol"], jl_dim=r,
@@ -333,10 +399,11 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
 
     # ---- per-kernel roofline (algorithmic bytes / event-timed duration) ----
     peak, peak_src = measured_peaks()
-    elt = X.element_size()
+    elt = 4 if csr else X.element_size()
+    x_bytes = (X.nnz * 8 + 8 * (n + 1)) if csr else n * d * elt  # CSR: int32 col + f32 val + int64 row_ptr
     stage_ms = {k_: v / args.steps for k_, v in stage_sum.items()}
-    lev_bytes = n * d * elt + 8 * n  # X once + float64 scores
-    sk_bytes = n * d * elt + 2 * 8 * k * d  # X once + compensated state write
+    lev_bytes = x_bytes + 8 * n  # X once + float64 scores
+    sk_bytes = x_bytes + 2 * 8 * k * d  # X once + compensated state write (the kernel reads CSR rows s times)
     lev_gbs = lev_bytes / (stage_ms["leverage"] / 1000) / 1e9 if stage_ms.get("leverage") else None
     sk_gbs = sk_bytes / (stage_ms["sketch"] / 1000) / 1e9 if stage_ms.get("sketch") else None
     dominant = "sketch" if stage_ms.get("sketch", 0) >= stage_ms.get("leverage", 0) else "leverage"
@@ -351,8 +418,12 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             traffic = None
     roofline = {
         "bound": "hbm",
-        "kernel": {"sketch": "hashed_gather_kernel (K1, with keygen+radix grouping)",
-                   "leverage": "rowsumsq kernel (K5)"}[dominant],
+        "kernel": {"sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. keygen + radix grouping)",
+                              "osnap": "csr_gather_kernel (K2, incl. keygen + radix grouping)" if csr else
+                              "hashed_gather_bulk_kernel (K1, incl. keygen + radix grouping)",
+                              "srht": "srht_pass1/pass2 kernels (K3)",
+                              "gaussian": "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],
+                   "leverage": "csr_rowsumsq_kernel (K6)" if csr else "leverage_v2_kernel (K5, tcgen05)"}[dominant],
         "achieved": dom_gbs,
         "peak": peak,
         "unit": "GB/s",
@@ -371,8 +442,11 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     # ---- e2e through the public API with host buffers (rank 0 view) ----
     e2e = None
     if not args.no_e2e:
-        Xh = torch.empty((n, d), dtype=dtype, pin_memory=True)
-        Xh.copy_(X)
+        if csr:
+            Xh = (X.indptr.cpu().pin_memory(), X.indices.cpu().pin_memory(), X.data.cpu().pin_memory(), (n, d))
+        else:
+            Xh = torch.empty((n, d), dtype=dtype, pin_memory=True)
+            Xh.copy_(X)
         e2e_steps = max(2, min(args.steps, args.e2e_steps))
 
         def e2e_step():
@@ -393,7 +467,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-        h2d = n * d * elt + (2 * 8 * n if world == 1 else 0)
+        h2d = x_bytes + (2 * 8 * n if world == 1 else 0)
         d2h = (3 * 8 * n) if world == 1 else 8 * n
         e2e = {"value": rows_total / float(e2e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
@@ -425,7 +499,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             "data": "synthetic (seeded, generated on device; random-init, no dataset)",
             "config": {"workload": cfg["desc"], "rows_per_gpu": n, "d": d, "k": k, "jl_r": r,
                        "sv_tol": cfg["sv_tol"], "parallelism": f"row-partition x{world}",
-                       "l2": f"inputs larger than L2 (X = {n * d * elt / 1e9:.2f} GB per GPU)"},
+                       "l2": f"inputs larger than L2 (X = {x_bytes / 1e9:.2f} GB per GPU)",
+                       **({"nnz": X.nnz} if csr else {})},
             "stages_ms": other,
             "roofline": roofline,
             "cpu_baseline": cpu,

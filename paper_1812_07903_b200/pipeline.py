@@ -23,6 +23,7 @@ import torch
 from . import _native as N
 from .errors import FormatError
 from .leverage import FoldGraph, KernelOperands, jl_device, sketch_fold
+from .csr import CSRMatrix, csr_code
 from .sketch import GAUSSIAN, SRHT, SketchSpec, SketchState, sketch_rows
 
 STAGES = ("sketch", "factor", "leverage", "order")
@@ -50,7 +51,7 @@ class LeveragePipeline:
         elif spec.family == GAUSSIAN:
             wsb = L.lvsk_gaussian_workspace_bytes(n, d, self.k, code)
         else:
-            wsb = L.lvsk_hashed_workspace_bytes(n, spec.s, self.k)
+            wsb = max(L.lvsk_hashed_workspace_bytes(n, spec.s, self.k), L.lvsk_hashed_csr_workspace_bytes(n, spec.s, self.k))
         self.ws_sketch = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
         self.scores = torch.empty(n, dtype=torch.float64, device=dev)
         self.p = torch.empty(n, dtype=torch.float64, device=dev)
@@ -63,13 +64,26 @@ class LeveragePipeline:
         # a dtype/alignment witness for choosing the K5 kernel (real X has the same layout)
         self._x_like = torch.empty((1, d), dtype=dtype, device=dev)
         self._fold_graph = None
+        self._m32 = None
+        self._m32_src = None
         self.effective_rank = None
         self.events = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in STAGES}
 
     # -- stages ------------------------------------------------------------
-    def _sketch(self, X: torch.Tensor) -> None:
+    def _sketch(self, X) -> None:
         L, st, s = N.lib(), N.stream_ptr(), self.state
         fam = self.spec.family
+        if isinstance(X, CSRMatrix):
+            s._hi.zero_()
+            s._lo.zero_()
+            N.check(L.lvsk_hashed_sketch_csr(X.indptr.data_ptr(), X.indices.data_ptr(), X.data.data_ptr(),
+                                             csr_code(X), X.n, X.d, self.row0, s._blocks, self.spec.s, s._scale,
+                                             s._hi.data_ptr(), s._lo.data_ptr(), s._hi.data_ptr(), s._lo.data_ptr(),
+                                             self.k, self.ws_sketch.data_ptr(), self.ws_sketch.numel(),
+                                             self.flags.data_ptr(), st), "csr sketch")
+            N.check(L.lvsk_fold_compensated(s._hi.data_ptr(), s._lo.data_ptr(), self.sx.data_ptr(), self.sx.numel(), st),
+                    "fold")
+            return
         ldx = X.stride(0)
         if fam == SRHT:
             N.check(L.lvsk_srht(X.data_ptr(), self.code, self.n, self.d, ldx, s._m, s._signs_dev.data_ptr(),
@@ -107,7 +121,17 @@ class LeveragePipeline:
         self.ops = KernelOperands(M, self._x_like)
         self.r = M.shape[1]
 
-    def _leverage(self, X: torch.Tensor) -> None:
+    def _leverage(self, X) -> None:
+        if isinstance(X, CSRMatrix):
+            if self._m32 is None or self._m32_src is not self.ops:
+                self._m32 = (self.ops.a.T.double() + self.ops.b.T.double()).to(torch.float32).contiguous() \
+                    if self.ops.tc else self.ops.a.to(torch.float32).contiguous()
+                self._m32_src = self.ops
+            N.check(N.lib().lvsk_rowsumsq_csr(X.indptr.data_ptr(), X.indices.data_ptr(), X.data.data_ptr(),
+                                              csr_code(X), X.n, X.d, self._m32.data_ptr(), self._m32.shape[1],
+                                              self.scores.data_ptr(), self.flags.data_ptr(), N.stream_ptr()),
+                    "csr leverage pass")
+            return
         self.ops.run(X, self.scores, self.flags.data_ptr())
 
     def _order(self) -> None:
@@ -122,7 +146,10 @@ class LeveragePipeline:
     def run(self, X: torch.Tensor, timing: bool = False, check: bool = True):
         """Full pass over device-resident X (n x d, self.dtype).  Returns
         (scores, order) CUDA tensors (order is None when order=False)."""
-        if X.shape != (self.n, self.d) or X.dtype != self.dtype or X.stride(1) != 1:
+        if isinstance(X, CSRMatrix):
+            if X.shape != (self.n, self.d):
+                raise ValueError(f"expected a ({self.n}, {self.d}) CSR matrix")
+        elif X.shape != (self.n, self.d) or X.dtype != self.dtype or X.stride(1) != 1:
             raise ValueError(f"expected a ({self.n}, {self.d}) {self.dtype} row-major CUDA tensor")
         self.flags.zero_()
         ev = self.events
@@ -152,6 +179,8 @@ class LeveragePipeline:
 
     def check(self) -> None:
         f = int(self.flags.item())
+        if f & N.FLAG_BADINDEX:
+            raise FormatError("CSR rows need strictly increasing column indices in [0, d)")
         if f & N.FLAG_NONFINITE:
             raise FormatError("matrix contains non-finite entries")
 

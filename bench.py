@@ -42,6 +42,8 @@ CONFIGS = {
                desc="configs[0]: Gaussian sketch fp32 20000x256, k=1024, r=64"),
     "c4": dict(family="osnap", n=4_000_000, d=4096, k=16384, r=128, s=4, dtype="f32", sv_tol=1e-6, csr=True,
                desc="configs[3]: OSNAP s=4 on CSR 4e6x4096, ~80 Zipf(1.1) draws/row, k=16384, r=128"),
+    "c5": dict(family="gaussian", n=1_000_000, d=1024, k=2048, r=128, s=None, dtype="bf16", sv_tol=1e-6, rank=100,
+               desc="configs[4]: Gaussian sketch on bf16 X 1e6x1024 per GPU (8e6 on 8), k=2048, rank-100, r=128"),
     "c3": dict(family="srht", n=2**21, d=256, k=4096, r=64, s=None, dtype="f32", sv_tol=1e-6,
                desc="configs[2]: SRHT fp32 2^21x256, k=4096, r=64"),
 }
@@ -98,6 +100,11 @@ def gen_x(cfg, rank: int, device):
         v, _ = torch.linalg.qr(torch.randn(d, 50, generator=g, device=device, dtype=torch.float32))
         s = torch.linspace(10.0, 1.0, 50, device=device)
         x = (u * s) @ v.T + 0.01 * torch.randn(n, d, generator=g, device=device, dtype=torch.float32)
+    elif cfg["family"] == "gaussian" and cfg.get("rank"):
+        # image-feature-like: sigmoid(G1 G2 + 0.05 N) in [0, 1], G1 n x 100, G2 100 x d
+        g1 = torch.randn(n, 100, generator=g, device=device) / 10.0
+        g2 = torch.randn(100, d, generator=g, device=device)
+        x = torch.sigmoid(g1 @ g2 + 0.05 * torch.randn(n, d, generator=g, device=device))
     elif cfg["family"] == "srht":
         x = torch.randn(n, d, generator=g, device=device) / torch.sqrt(torch.arange(1, d + 1, device=device, dtype=torch.float32))
     else:
@@ -301,7 +308,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     row0 = rank * n
     pipe = P.LeveragePipeline(spec, n * world if world > 1 else n, d, dtype, sv_tol=cfg["sv_tol"], jl_dim=r,
-                              order=(world == 1), row0=row0)
+                              rank=cfg.get("rank"), order=(world == 1), row0=row0)
     if world > 1:
         pipe.n = n  # local rows; the state covers n*world global rows
         pipe.scores = torch.empty(n, dtype=torch.float64, device=dev)
@@ -336,7 +343,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             ev["factor"][0].record()
         M = torch.empty((d, r), dtype=torch.float64, device=dev)
         if rank == 0:
-            M.copy_(sketch_fold(pipe.sx, cfg["sv_tol"], None, pi)[0])
+            M.copy_(sketch_fold(pipe.sx, cfg["sv_tol"], cfg.get("rank"), pi)[0])
         dist.broadcast(M, 0)
         pipe.set_fold(M)
         if timing:
@@ -451,7 +458,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
 
         def e2e_step():
             if world == 1:
-                res = P.leverage_sketched_trunc(Xh, spec, cfg["sv_tol"], jl_dim=r)
+                res = P.leverage_sketched_trunc(Xh, spec, cfg["sv_tol"], jl_dim=r, rank=cfg.get("rank"))
                 plan = P.make_plan(P.scores_to_distribution(res.scores), P.OrderingPolicy("dec"))
                 return plan.indices
             local, *_ = P.run_sharded(Xh, row0, n * world, spec, cfg["sv_tol"], jl_dim=r)

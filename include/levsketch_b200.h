@@ -152,6 +152,12 @@ LVSK_API int32_t lvsk_leverage_tf32x3(const float* X, int64_t n, int64_t d, int6
                                       const float* Mt_lo, const void* Mt_hi_bf16, int64_t r, double* scores,
                                       int32_t* flags, void* stream);
 
+/* K5 on tcgen05 for bf16 X (BASELINE config 5): Mt is (2*r_pad) x d bf16 with
+ * rows [0, r) = bf16(M^T), rows [r_pad, r_pad + r) = bf16(M^T - hi), zeros
+ * elsewhere; r_pad in {32, 64, 128}. */
+LVSK_API int32_t lvsk_leverage_bf16(const void* X, int64_t n, int64_t d, int64_t ldx, const void* Mt, int64_t r,
+                                    int64_t r_pad, double* scores, int32_t* flags, void* stream);
+
 /* ---- K2 / K6: CSR rows (extension G2; BASELINE config 4) -----------------
  * Same semantics as lvsk_hashed_sketch / lvsk_rowsumsq_gemm on the densified
  * rows (bit-exact for K2: zero entries leave the TwoSum state unchanged).

@@ -59,6 +59,7 @@ _SIGS = {
     "lvsk_gaussian_entries": (_I32, [_U64, _I64, _U64, _I64, _P, _P]),
     "lvsk_rowsumsq_gemm": (_I32, [_P, _I32, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _P]),
     "lvsk_leverage_tf32x3": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P]),
+    "lvsk_leverage_bf16": (_I32, [_P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P]),
     "lvsk_hashed_csr_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
     "lvsk_hashed_sketch_csr": (
         _I32,

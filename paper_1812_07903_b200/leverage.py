@@ -219,6 +219,17 @@ def use_tensor_cores(X: torch.Tensor, r: int) -> bool:
     )
 
 
+def use_bf16_tensor_cores(X: torch.Tensor, r: int) -> bool:
+    return (
+        X.dtype == torch.bfloat16
+        and r <= 128
+        and os.environ.get("LVSK_NO_TC", "0") != "1"
+        and X.data_ptr() % 16 == 0
+        and (X.stride(0) * 2) % 16 == 0
+        and (X.shape[1] * 2) % 16 == 0
+    )
+
+
 class KernelOperands:
     """K5 operands for a fold M (d x r): TF32 hi/lo transposes (+ bf16 hi) for
     the tcgen05 kernels, fp32 hi/lo or fp64 for the SIMT kernel.  Buffers are
@@ -227,9 +238,14 @@ class KernelOperands:
     def __init__(self, M: torch.Tensor | None, X_like: torch.Tensor, shape: tuple[int, int] | None = None):
         self.d, self.r = M.shape if M is not None else shape
         self.tc = use_tensor_cores(X_like, self.r)
+        self.bf16 = use_bf16_tensor_cores(X_like, self.r)
         dev = X_like.device
         self.hb = None
-        if self.tc:
+        if self.bf16:
+            self.r_pad = 32 if self.r <= 32 else (64 if self.r <= 64 else 128)
+            self.a = torch.zeros((2 * self.r_pad, self.d), dtype=torch.bfloat16, device=dev)
+            self.b = None
+        elif self.tc:
             self.a = torch.empty((self.r, self.d), dtype=torch.float32, device=dev)
             self.b = torch.empty((self.r, self.d), dtype=torch.float32, device=dev)
             if self.r <= 64:
@@ -244,7 +260,14 @@ class KernelOperands:
             self.set(M)
 
     def set(self, M: torch.Tensor) -> None:
-        if self.tc:
+        self.M64 = M
+        if self.bf16:
+            mt = M.T
+            hi = mt.to(torch.bfloat16)
+            lo = (mt - hi.to(torch.float64)).to(torch.bfloat16)
+            self.a[: self.r].copy_(hi)
+            self.a[self.r_pad : self.r_pad + self.r].copy_(lo)
+        elif self.tc:
             hi, lo = split_m_tf32(M)
             self.a.copy_(hi)
             self.b.copy_(lo)
@@ -259,6 +282,15 @@ class KernelOperands:
     def run(self, X: torch.Tensor, out: torch.Tensor, flags_ptr: int) -> None:
         n, d = X.shape
         L = N.lib()
+        if self.bf16 and use_bf16_tensor_cores(X, self.r):
+            N.check(L.lvsk_leverage_bf16(X.data_ptr(), n, d, X.stride(0), self.a.data_ptr(), self.r, self.r_pad,
+                                         out.data_ptr(), flags_ptr, N.stream_ptr()), "leverage pass (tcgen05 bf16)")
+            return
+        if self.bf16:
+            a, b = split_m(self.M64, X.dtype)
+            N.check(L.lvsk_rowsumsq_gemm(X.data_ptr(), N.dtype_code(X), n, d, X.stride(0), a.data_ptr(), N.ptr(b),
+                                         self.r, out.data_ptr(), flags_ptr, N.stream_ptr()), "leverage pass")
+            return
         if self.tc and use_tensor_cores(X, self.r):
             rc = L.lvsk_leverage_tf32x3(X.data_ptr(), n, d, X.stride(0), self.a.data_ptr(), self.b.data_ptr(),
                                         N.ptr(self.hb), self.r, out.data_ptr(), flags_ptr, N.stream_ptr())

@@ -503,3 +503,34 @@ def test_csr_validation():
     with pytest.raises(errors.UnsupportedFamilyError):
         P.apply_sketch((indptr, np.array([1, 3, 2], np.int32), np.ones(3, np.float32), (2, 8)),
                        P.SketchSpec("srht", eps=0.5, d=8, rows_override=2))
+
+
+@pytest.mark.parametrize("n,d,r", [(5000, 1024, 128), (3000, 256, 100), (2048, 64, 30), (777, 512, 64)])
+def test_tcgen05_bf16_leverage_vs_fp64(n, d, r):
+    g = torch.Generator(device="cpu").manual_seed(n + r)
+    X = torch.rand(n, d, generator=g, dtype=torch.float64).to(torch.bfloat16).cuda()
+    M = (torch.randn(d, r, generator=g, dtype=torch.float64) / math.sqrt(d)).cuda()
+    ref = ((X.double() @ M) ** 2).sum(1)
+    ops = P.leverage.KernelOperands(M, X)
+    assert ops.bf16
+    out = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+    fl = N.Flags()
+    ops.run(X, out, fl.p)
+    rel = ((out - ref).abs() / ref).max().item()
+    assert rel < 1e-4, rel  # bf16 X exact, M as bf16 hi + lo (~16 bits), fp32 accumulation
+
+
+def test_c5_shaped_pipeline_small():
+    """Gaussian sketch on bf16 X, rank-capped truncation, r = 128 (config 5 shape, reduced n)."""
+    n, d, k = 20000, 256, 512
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = torch.sigmoid(torch.randn(n, 20, generator=g, device="cuda") @ torch.randn(20, d, generator=g, device="cuda")
+                      / 3 + 0.05 * torch.randn(n, d, generator=g, device="cuda")).to(torch.bfloat16)
+    spec = P.SketchSpec("gaussian", eps=0.5, d=d, seed=1, rows_override=k)
+    res = P.leverage_sketched_trunc(X, spec, 1e-6, jl_dim=128, jl_seed=3, rank=20)
+    xv = X.double().cpu().numpy()
+    sx = O.gaussian_sketch(xv, k, 1)
+    ref, r, _ = O.leverage_from_sketch(xv, sx, 1e-6, O.jl_matrix(3, d, 128), rank=20)
+    assert res.effective_rank == r == 20
+    assert np.abs(res.scores - ref).max() <= 2e-2 * ref.max()
+    assert np.median(np.abs(res.scores - ref) / ref) < 1e-3

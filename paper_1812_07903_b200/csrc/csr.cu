@@ -14,6 +14,8 @@
 // K6: one warp per row; lane l owns r/32 consecutive columns of u = x M and
 // gathers the M rows of the row's nonzeros (L1/L2-resident), fp32 FMA, then
 // the squared norm is reduced across the warp.
+#include <cstdlib>
+
 #include "radix_sort.cuh"
 
 namespace lvsk {
@@ -98,6 +100,162 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
   }
   const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
   if (any && lane == 0) atomicOr(flags, any);
+}
+
+// ---------------------------------------------------------------------------
+// K2 ring variant (default for float32 values): one CTA owns one (bucket, <= 4096-column group) with its
+// float64 (hi, lo) slice in shared memory; a producer warp streams the
+// bucket's CSR row pieces (16-byte aligned supersets, <= 64 entries each;
+// rounding out to 16-byte granules never leaves the allocation's page)
+// into a 64-slot ring with cp.async.bulk, so ~100 rows are in flight per CTA;
+// a consumer warp applies them in ascending row order.
+constexpr int RING_SLOTS = 64;
+constexpr int SLOT_ELEMS = 64;
+constexpr int RING_GROUP = 4096;
+
+struct SlotMeta {
+  int32_t first, last;  // valid element range inside the slot
+  uint32_t flags;       // bit0: negative sign, bit1: first piece of its row
+};
+
+__device__ __forceinline__ uint32_t csr_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void csr_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "CW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni CW_%=;\n}" ::"r"(csr_smem(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(64) csr_ring_kernel(const int64_t* __restrict__ row_ptr,
+                                                      const int32_t* __restrict__ col, const float* __restrict__ val,
+                                                      int64_t shift, int64_t d, int ngroups, const uint32_t* __restrict__ vals,
+                                                      const uint32_t* __restrict__ start, double scale,
+                                                      const double* hi_in, const double* lo_in, double* hi_out,
+                                                      double* lo_out, int32_t* flags) {
+  extern __shared__ __align__(128) uint8_t csr_ring_smem[];
+  double* hi = reinterpret_cast<double*>(csr_ring_smem);
+  double* lo = hi + RING_GROUP;
+  int32_t* rcol = reinterpret_cast<int32_t*>(lo + RING_GROUP);     // [RING_SLOTS][SLOT_ELEMS]
+  float* rval = reinterpret_cast<float*>(rcol + RING_SLOTS * SLOT_ELEMS);
+  SlotMeta* meta = reinterpret_cast<SlotMeta*>(rval + RING_SLOTS * SLOT_ELEMS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + RING_SLOTS);
+  uint64_t* empty = full + RING_SLOTS;
+  const int64_t b = blockIdx.x / ngroups;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x - b * ngroups) * RING_GROUP;
+  const int64_t width = d - c0 < RING_GROUP ? d - c0 : RING_GROUP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RING_SLOTS; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_smem(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_smem(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
+    hi[c] = hi_in[b * d + c0 + c];
+    lo[c] = lo_in[b * d + c0 + c];
+  }
+  __syncthreads();
+  // element indices are relative to the 16-byte aligned col / val bases
+  const int64_t base0 = row_ptr[0] - shift;
+  const uint32_t p0 = start[b], p1 = start[b + 1];
+  if (warp == 0) {  // producer
+    if (lane == 0) {
+      uint32_t j = 0;
+      for (uint32_t p = p0; p < p1; ++p) {
+        const uint32_t vv = vals[p];
+        const int64_t r = vv >> 1;
+        const int64_t e0 = row_ptr[r] - base0, e1 = row_ptr[r + 1] - base0;
+        const int64_t a0 = e0 & ~int64_t{3};
+        const int64_t a_end = (e1 + 3) & ~int64_t{3};
+        int64_t s0 = a0;
+        do {
+          const int64_t s1 = s0 + SLOT_ELEMS < a_end ? s0 + SLOT_ELEMS : a_end;
+          const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
+          csr_wait(&empty[slot], ph ^ 1u);
+          SlotMeta m;
+          m.first = static_cast<int32_t>((e0 > s0 ? e0 : s0) - s0);
+          m.last = static_cast<int32_t>((e1 < s1 ? e1 : s1) - s0);
+          m.flags = (vv & 1u) | (s0 == a0 ? 2u : 0u);
+          meta[slot] = m;
+          const uint32_t nb = static_cast<uint32_t>((s1 - s0) * 4);
+          if (nb > 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(csr_smem(&full[slot])),
+                         "r"(2 * nb)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    csr_smem(rcol + slot * SLOT_ELEMS)),
+                "l"(col + s0), "r"(nb), "r"(csr_smem(&full[slot]))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    csr_smem(rval + slot * SLOT_ELEMS)),
+                "l"(val + s0), "r"(nb), "r"(csr_smem(&full[slot]))
+                : "memory");
+          } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[slot])) : "memory");
+          }
+          ++j;
+          s0 = s1;
+        } while (s0 < a_end);
+      }
+    }
+  } else {  // consumer
+    int bad = 0;
+    uint32_t j = 0;
+    for (uint32_t p = p0; p < p1; ++p) {
+      const int64_t r = vals[p] >> 1;
+      const int64_t e0 = row_ptr[r] - base0, e1 = row_ptr[r + 1] - base0;
+      const int64_t a0 = e0 & ~int64_t{3};
+      const int64_t a_end = (e1 + 3) & ~int64_t{3};
+      const int64_t npieces = a_end > a0 ? (a_end - a0 + SLOT_ELEMS - 1) / SLOT_ELEMS : 1;
+      int32_t prev_last = -1;
+      for (int64_t q = 0; q < npieces; ++q, ++j) {
+        const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
+        csr_wait(&full[slot], ph);
+        const SlotMeta m = meta[slot];
+        const double sg = (m.flags & 1u) ? -scale : scale;
+#pragma unroll
+        for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
+          const int idx = h * 32 + lane;
+          const bool live = idx >= m.first && idx < m.last;
+          const int32_t c = live ? rcol[slot * SLOT_ELEMS + idx] : INT32_MAX;
+          const float x = live ? rval[slot * SLOT_ELEMS + idx] : 0.f;
+          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+          const bool prev_live = lane > 0 && (idx - 1) >= m.first;
+          const int32_t before = prev_live ? cprev : prev_last;
+          if (live) {
+            if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
+            if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
+            const int64_t lc = static_cast<int64_t>(c) - c0;
+            if (lc >= 0 && lc < width) {
+              double su, er;
+              two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(x)), su, er);
+              hi[lc] = su;
+              lo[lc] = __dadd_rn(lo[lc], er);
+            }
+          }
+          const uint32_t lm = __ballot_sync(0xFFFFFFFFu, live);
+          if (lm) prev_last = __shfl_sync(0xFFFFFFFFu, c, 31 - __clz(lm));
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&empty[slot])) : "memory");
+      }
+    }
+    const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (any && lane == 0) atomicOr(flags, any);
+  }
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
+    hi_out[b * d + c0 + c] = hi[c];
+    lo_out[b * d + c0 + c] = lo[c];
+  }
 }
 
 // K6: one warp per row, lane owns RPL = r/32 consecutive columns of u
@@ -231,7 +389,25 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
     cudaFuncSetAttribute(csr_gather_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  if (val_dtype == LVSK_F32)
+  // the ring reads 16-byte aligned supersets of each row; col and val must
+  // share their misalignment so one element index addresses both
+  const int mis = static_cast<int>(reinterpret_cast<uintptr_t>(col) % 16);
+  const bool ring = val_dtype == LVSK_F32 && mis % 4 == 0 &&
+                    mis == static_cast<int>(reinterpret_cast<uintptr_t>(val) % 16) &&
+                    getenv("LVSK_K2_SIMPLE") == nullptr;
+  if (ring) {
+    const int rgroups = static_cast<int>((d + RING_GROUP - 1) / RING_GROUP);
+    const int rsmem = 2 * RING_GROUP * 8 + RING_SLOTS * SLOT_ELEMS * 8 + RING_SLOTS * static_cast<int>(sizeof(SlotMeta)) +
+                      2 * RING_SLOTS * 8;
+    static bool rattr = false;
+    if (!rattr) {
+      cudaFuncSetAttribute(csr_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
+      rattr = true;
+    }
+    csr_ring_kernel<<<static_cast<unsigned>(k * rgroups), 64, rsmem, st>>>(
+        row_ptr, col - mis / 4, static_cast<const float*>(val) - mis / 4, mis / 4, d, rgroups, svals, start, scale, hi_in, lo_in, hi_out, lo_out,
+        flags);
+  } else if (val_dtype == LVSK_F32)
     csr_gather_kernel<float><<<grid, 32 * CSR_WARPS, smem, st>>>(row_ptr, col, static_cast<const float*>(val), d,
                                                               ngroups, svals, start, units, scale, hi_in, lo_in,
                                                               hi_out, lo_out, flags);

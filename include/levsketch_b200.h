@@ -176,6 +176,19 @@ LVSK_API int32_t lvsk_rowsumsq_csr(const int64_t* row_ptr, const int32_t* col, c
                                    int32_t val_dtype, int64_t n, int64_t d, const float* M, int64_t r,
                                    double* scores, int32_t* flags, void* stream);
 
+/* ---- fold ------------------------------------------------------------------
+ * KF: the certified Cholesky JL fold (replaces the reference's
+ * svd + truncate + V'/sigma' basis, leverage.py:75-85 / svd.py:41-74, for the
+ * JL variant).  G: d x d float64 symmetric (upper
+ * triangle read, leading dimension ldg), Pi: d x r float64 row-major.
+ * Writes M = R^-1 Pi (d x r, R^T R = G, R upper with positive diagonal) and
+ * diag[3] = {info (0 = positive definite), trace(G), trace(G^-1)}; the caller
+ * certifies trace(G) * trace(G^-1) < 1/sv_tol^2 before using M.  One
+ * cooperative launch; stream-capturable. */
+LVSK_API size_t lvsk_chol_fold_workspace_bytes(int64_t d, int64_t r);
+LVSK_API int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const double* Pi, int64_t r, double* M,
+                                double* diag, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- ordering -------------------------------------------------------------
  * scores_to_distribution (order.py:51-63): p = scores / sum(scores), with
  * the sum a deterministic two-level float64 reduction.  Sets

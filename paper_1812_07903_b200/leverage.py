@@ -108,16 +108,27 @@ def fold_device(sigma: torch.Tensor, vt: torch.Tensor, s_host: np.ndarray, pi: t
     return (basis @ (vt @ pi)).contiguous()
 
 
-def _chol_body(sx: torch.Tensor, pi: torch.Tensor, eye: torch.Tensor):
+_FOLD_WS: dict = {}
+
+
+def _chol_body(sx: torch.Tensor, pi: torch.Tensor):
     """Shape-static Cholesky fold (CUDA-graph capturable, no host sync):
-    G = SX^T SX = R^T R, M = R^-1 Pi, plus diag = [info, trace(G), trace(G^-1)]
-    with trace(G^-1) = ||R^-1||_F^2."""
+    G = SX^T SX (cuBLAS DGEMM) = R^T R, then the KF kernel (csrc/factor.cu):
+    M = R^-1 Pi and diag = [info, trace(G), trace(G^-1)] with
+    trace(G^-1) = ||R^-1||_F^2."""
+    k, d = sx.shape
+    r = pi.shape[1]
     G = sx.T @ sx
-    L, info = torch.linalg.cholesky_ex(G)
-    R = L.mT
-    M = torch.linalg.solve_triangular(R, pi, upper=True)
-    Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
-    diag = torch.stack([info.to(G.dtype), torch.trace(G), (Rinv * Rinv).sum()])
+    key = (d, r, sx.device)
+    ws = _FOLD_WS.get(key)
+    if ws is None:
+        ws = torch.empty(int(N.lib().lvsk_chol_fold_workspace_bytes(d, r)), dtype=torch.uint8, device=sx.device)
+        _FOLD_WS[key] = ws
+    pi = pi.contiguous()
+    M = torch.empty((d, r), dtype=torch.float64, device=sx.device)
+    diag = torch.empty(3, dtype=torch.float64, device=sx.device)
+    N.check(N.lib().lvsk_chol_fold(G.data_ptr(), d, G.stride(0), pi.data_ptr(), r, M.data_ptr(), diag.data_ptr(),
+                                   ws.data_ptr(), ws.numel(), N.stream_ptr()), "cholesky fold")
     return M, diag
 
 
@@ -144,8 +155,7 @@ def cholesky_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor):
     k, d = sx.shape
     if k < d:
         return None
-    eye = torch.eye(d, dtype=sx.dtype, device=sx.device)
-    M, diag = _chol_body(sx, pi, eye)
+    M, diag = _chol_body(sx, pi)
     return M.contiguous() if chol_certified(diag.tolist(), sv_tol) else None
 
 
@@ -315,11 +325,10 @@ class FoldGraph:
         self.sx, self.sv_tol, self.pi = sx, sv_tol, pi
         k, d = sx.shape
         self.ops = KernelOperands(None, X_like, (d, pi.shape[1]))
-        self.eye = torch.eye(d, dtype=torch.float64, device=sx.device)
         self.diag = torch.zeros(3, dtype=torch.float64, device=sx.device)
         self.graph = None
-        # warm up cuBLAS / cuSOLVER handles and workspaces outside capture
-        M, diag = _chol_body(sx, pi, self.eye)
+        # warm up cuBLAS handles and the fold workspace outside capture
+        M, diag = _chol_body(sx, pi)
         self.ops.set(M)
         torch.cuda.synchronize()
         s = torch.cuda.Stream()
@@ -327,7 +336,7 @@ class FoldGraph:
         with torch.cuda.stream(s):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
-                M, diag = _chol_body(self.sx, self.pi, self.eye)
+                M, diag = _chol_body(self.sx, self.pi)
                 self.ops.set(M)
                 self.diag.copy_(diag)
         torch.cuda.current_stream().wait_stream(s)

@@ -303,6 +303,43 @@ def test_cholesky_fold_equals_qr_fold_and_oracle():
     assert r_tr == r_or2 < 256 and np.allclose(m_tr.cpu().numpy(), m_or2, rtol=1e-8, atol=1e-11 * np.abs(m_or2).max())
 
 
+@pytest.mark.parametrize("k,d,r", [(64, 1, 1), (300, 64, 64), (400, 100, 7), (2048, 512, 64), (1500, 700, 130)])
+def test_kf_cholesky_fold_kernel_vs_numpy(k, d, r):
+    """KF (csrc/factor.cu) against numpy: M = R^-1 Pi and the certificate
+    traces, on ragged d / r (identity padding) and one-tile cases."""
+    rng = np.random.default_rng(k + d + r)
+    sx = rng.standard_normal((k, d)) * np.linspace(1.0, 20.0, d)
+    pi = O.jl_matrix(5, d, r)
+    G = sx.T @ sx
+    R = np.linalg.cholesky(G).T
+    m_ref = np.linalg.solve(R, pi)
+    tr_inv = float(np.sum(np.linalg.inv(R) ** 2))
+    M, diag = P.leverage._chol_body(torch.from_numpy(sx).cuda(), torch.from_numpy(pi).cuda())
+    diag = diag.cpu().numpy()
+    assert diag[0] == 0.0
+    assert abs(diag[1] - np.trace(G)) <= 1e-12 * np.trace(G)
+    assert abs(diag[2] - tr_inv) <= 1e-9 * tr_inv
+    assert np.allclose(M.cpu().numpy(), m_ref, rtol=1e-9, atol=1e-11 * np.abs(m_ref).max())
+
+
+def test_kf_cholesky_fold_flags_indefinite():
+    d = 130
+    rng = np.random.default_rng(1)
+    sx = rng.standard_normal((50, d))  # k < d: G singular
+    g = sx.T @ sx
+    g[90, 90] = -1.0
+    L = P._native.lib()
+    Gt = torch.from_numpy(g).cuda()
+    pi = torch.from_numpy(O.jl_matrix(1, d, 16)).cuda()
+    ws = torch.empty(int(L.lvsk_chol_fold_workspace_bytes(d, 16)), dtype=torch.uint8, device="cuda")
+    M = torch.empty((d, 16), dtype=torch.float64, device="cuda")
+    diag = torch.empty(3, dtype=torch.float64, device="cuda")
+    P._native.check(L.lvsk_chol_fold(Gt.data_ptr(), d, d, pi.data_ptr(), 16, M.data_ptr(), diag.data_ptr(),
+                                     ws.data_ptr(), ws.numel(), P._native.stream_ptr()), "fold")
+    assert diag[0].item() != 0.0
+    assert not P.leverage.chol_certified(diag.tolist(), 1e-6)
+
+
 # ---------------------------------------------------------------------------
 # end-to-end leverage (reference leverage.py / dist.py golden cases)
 

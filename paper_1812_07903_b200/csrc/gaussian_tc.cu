@@ -1,0 +1,265 @@
+// K4-TC — Gaussian sketch SX = Z X / sqrt(k) on the tensor cores for bf16 X
+// (BASELINE config 5), Z generated on the fly (philox.cuh) and never stored
+// in global memory.  Extension: the reference rejects "gaussian"
+// (pkg/src/levsketch/sketch.py:38-41, 74-75).
+//
+// GEMM shape: SX (k x d) = Z (k x n) . X (n x d), contraction over the input
+// rows n.  One CTA owns a (128 sketch rows) x (NS <= 512 columns) output
+// tile for one split of the rows (split-K; the fp32 partials are reduced in
+// float64 by gaussian.cu's reduce kernel), accumulating in TMEM
+// (NS fp32 columns).  Per 64-row stage:
+//   warp 0   TMA: X[64 rows][NS cols] as NS/64 SW128 boxes.  X is the MMA's
+//            B operand in MN-major layout (rows of X = K, contiguous columns
+//            = N), so no transpose pass exists anywhere;
+//   warps 2-9 generate the Z tile [128 x 64] (philox.cuh, bit-identical to
+//            the SIMT path and the oracle) straight into the K-major SW128 A
+//            layout in shared memory, fence.proxy.async, arrive;
+//   warp 1   issues 4 x (NS/256) tcgen05.mma kind::f16 (M = 128, N = 256,
+//            K = 16) and commits the stage back to both producers.
+// After the last stage warps 2-9 drain TMEM (tcgen05.ld 32x32b) into the
+// split's fp32 partial.  X traffic: each X element is read once per 128
+// sketch rows (ceil(k/128) times, L2-shared across the CTAs of one
+// (split, column slab) which are launched adjacently); each Z entry is
+// generated ceil(d/NS) times.
+#include "philox.cuh"
+#include "tc_common.cuh"
+
+namespace lvsk {
+namespace tc {
+
+template <int NS>
+struct CfgG {
+  static constexpr int BKN = 64;                // input rows per stage (MMA K)
+  static constexpr int NB = NS / 64;            // 64-column TMA boxes per stage
+  static constexpr int NMMA = NS / 256;         // N = 256 MMAs per K16 step
+  static constexpr int BOX_BYTES = BKN * 64 * 2;  // 8 KB
+  static constexpr int X_BYTES = NB * BOX_BYTES;
+  static constexpr int Z_BYTES = BM * BKN * 2;  // 16 KB
+  static constexpr int S = NS == 512 ? 2 : 4;
+  static constexpr int OFF_Z = S * X_BYTES;
+  static constexpr int OFF_BAR = OFF_Z + S * Z_BYTES;
+  static constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;
+  static constexpr int GEN_WARPS = 8;
+  static constexpr int NTHREADS = 64 + 32 * GEN_WARPS;
+  // kind::f16: F32 accumulate, A = B = bf16, B MN-major, N = 256, M = 128
+  static constexpr uint32_t IDESC =
+      (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(256 >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+};
+
+// MN-major SWIZZLE_128B: 64-element x 8-row atoms; LBO = stride between
+// 64-element MN blocks, SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(lbo_bytes >> 4) << 16;
+  d |= uint64_t{1024 >> 4} << 32;
+  d |= uint64_t{1} << 46;
+  d |= uint64_t{2} << 61;
+  return d;
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
+    gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
+                       uint32_t k0, uint32_t k1, int ktiles, int dslabs, int64_t rows_per_split,
+                       float* __restrict__ partial) {
+  using C = CfgG<NS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* xfull = bars;
+  uint64_t* zfull = xfull + C::S;
+  uint64_t* empty = zfull + C::S;
+  uint64_t* accfull = empty + C::S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int item = blockIdx.x;
+  const int ktile = item % ktiles;
+  const int dslab = (item / ktiles) % dslabs;
+  const int64_t split = item / (ktiles * dslabs);
+  const int64_t r_begin = split * rows_per_split;
+  const int64_t r_end = r_begin + rows_per_split < n ? r_begin + rows_per_split : n;
+  const int nstages = static_cast<int>((r_end - r_begin + C::BKN - 1) / C::BKN);
+  const int col0 = dslab * NS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::S; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&zfull[s], C::GEN_WARPS);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(NS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_normal();
+      for (int t = 0; t < nstages; ++t) {
+        const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&xfull[s], C::X_BYTES);
+        const int row = static_cast<int>(r_begin + static_cast<int64_t>(t) * C::BKN);
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d(&mapX, &xfull[s], smem + s * C::X_BYTES + b * C::BOX_BYTES, col0 + b * 64, row, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int t = 0; t < nstages; ++t) {
+        const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+        mbar_wait(&xfull[s], ph);
+        mbar_wait(&zfull[s], ph);
+        tc_fence_after();
+        const uint64_t a = sw128_desc(smem_u32(smem + C::OFF_Z + s * C::Z_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < C::BKN / 16; ++kk) {
+#pragma unroll
+          for (int h = 0; h < C::NMMA; ++h) {
+            const uint64_t b = sw128_mn_desc(smem_u32(smem + s * C::X_BYTES + h * 4 * C::BOX_BYTES + kk * 2048),
+                                             C::BOX_BYTES);
+            umma_f16(tmem_base + h * 256, a + 2 * kk, b, C::IDESC, (t | kk) ? 1u : 0u);
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(accfull);
+    }
+  } else {
+    // ---- Z generation: thread -> (8 sketch rows 8q.., 4 consecutive input rows)
+    const int gw = warp - 2;
+    const int iblk = lane & 15;           // input rows 4*iblk .. 4*iblk+3 of the stage
+    const int q = gw * 2 + (lane >> 4);   // sketch rows 8q .. 8q+7 of the tile
+    const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 4) + 2 * q);  // Philox quad of row 8q
+    for (int t = 0; t < nstages; ++t) {
+      const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+      const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 4 * iblk);
+      float z[4][8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        gaussian4(g0 + e, qg, k0, k1, *reinterpret_cast<float(*)[4]>(&z[e][0]));
+        gaussian4(g0 + e, qg + 1, k0, k1, *reinterpret_cast<float(*)[4]>(&z[e][4]));
+      }
+      mbar_wait(&empty[s], ph ^ 1u);
+      uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
+#pragma unroll
+      for (int r8 = 0; r8 < 8; ++r8) {
+        const int j = 8 * q + r8;
+        __nv_bfloat162 lo = __floats2bfloat162_rn(z[0][r8], z[1][r8]);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(z[2][r8], z[3][r8]);
+        uint2 v;
+        v.x = *reinterpret_cast<uint32_t*>(&lo);
+        v.y = *reinterpret_cast<uint32_t*>(&hi);
+        const int off = j * 128 + ((((iblk >> 1) ^ (j & 7))) << 4) + (iblk & 1) * 8;
+        *reinterpret_cast<uint2*>(zt + off) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&zfull[s]);
+    }
+    // ---- epilogue: TMEM -> fp32 partial
+    mbar_wait(accfull, 0);
+    tc_fence_after();
+    const int quarter = warp & 3, half = gw >> 2;
+    const int64_t j = static_cast<int64_t>(ktile) * BM + quarter * 32 + lane;
+    float* out = partial + split * k * d + j * d;
+#pragma unroll 1
+    for (int c = half * (NS / 2); c < (half + 1) * (NS / 2); c += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
+      tmem_wait_ld();
+      const int64_t dc = col0 + c;
+      if (j < k) {
+        if (dc + 32 <= d && (d & 3) == 0) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(out + dc + e) =
+                make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                            __uint_as_float(v[e + 3]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (dc + e < d) out[dc + e] = __uint_as_float(v[e]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(NS));
+  }
+}
+
+}  // namespace tc
+
+GaussTcPlan plan_gauss_tc(int64_t n, int64_t d, int64_t k) {
+  GaussTcPlan p;
+  p.ns = d > 256 ? 512 : 256;
+  p.ktiles = static_cast<int>((k + tc::BM - 1) / tc::BM);
+  p.dslabs = static_cast<int>((d + p.ns - 1) / p.ns);
+  const int64_t pairs = static_cast<int64_t>(p.ktiles) * p.dslabs;
+  int64_t splits = num_sms() / pairs;
+  const int64_t maxs = (n + 255) / 256;
+  if (splits > maxs) splits = maxs;
+  if (splits < 1) splits = 1;
+  p.rows_per_split = ((n + splits - 1) / splits + 63) / 64 * 64;
+  p.splits = (n + p.rows_per_split - 1) / p.rows_per_split;
+  return p;
+}
+
+bool gaussian_tc_ok(const void* X, int64_t n, int64_t d, int64_t ldx, int64_t k) {
+  if (getenv("LVSK_NO_TC") != nullptr) return false;
+  if (reinterpret_cast<uintptr_t>(X) % 16 != 0 || (ldx * 2) % 16 != 0) return false;
+  if (n > (int64_t{1} << 31) - (int64_t{1} << 20) || d < 1 || k < 1) return false;
+  return true;
+}
+
+template <int NS>
+static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
+                               uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
+  using C = tc::CfgG<NS>;
+  CUtensorMap mx;
+  if (!tc::make_map(&mx, X, d, n, ldx * 2, 64, C::BKN, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return LVSK_ERR_CUDA;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc::gaussian_tc_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "gaussian tc smem attribute");
+    attr = true;
+  }
+  const int64_t items = static_cast<int64_t>(p.ktiles) * p.dslabs * p.splits;
+  tc::gaussian_tc_kernel<NS><<<static_cast<unsigned>(items), C::NTHREADS, C::SMEM_BYTES, st>>>(
+      mx, n, d, k, row0, k0, k1, p.ktiles, p.dslabs, p.rows_per_split, partial);
+  LVSK_CHECK_LAUNCH("gaussian tc");
+  return LVSK_OK;
+}
+
+int32_t gaussian_tc_bf16(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
+                         uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
+  return p.ns == 512 ? launch_gauss_tc<512>(X, n, d, ldx, k, row0, k0, k1, p, partial, st)
+                     : launch_gauss_tc<256>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
+}
+
+}  // namespace lvsk

@@ -227,6 +227,37 @@ def test_gaussian_sketch_matches_oracle():
         assert np.linalg.norm(st.data - ref) <= tol * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("n,d,k,ldx,row0", [(5000, 1024, 300, 1024, 0), (3001, 200, 128, 208, 7),
+                                            (700, 520, 256, 520, 2**33 + 5), (64, 64, 8, 64, 0)])
+def test_gaussian_tc_bf16_vs_oracle(n, d, k, ldx, row0):
+    """K4-TC (tcgen05, bf16 X as the MN-major B operand, Z generated in smem)
+    against the oracle's exact Z X / sqrt(k): ragged k / d (TMA zero fill),
+    two 512-column slabs, strided rows, a large global row offset."""
+    rng = np.random.default_rng(n + d)
+    buf = torch.from_numpy(rng.standard_normal((n, ldx))).to(torch.bfloat16).cuda()
+    X = buf[:, :d]
+    xv = X.double().cpu().numpy()
+    L = N.lib()
+    ws = torch.empty(int(L.lvsk_gaussian_workspace_bytes(n, d, k, N.LVSK_BF16)), dtype=torch.uint8, device="cuda")
+    SX = torch.empty((k, d), dtype=torch.float64, device="cuda")
+    flags = N.Flags()
+    N.check(L.lvsk_gaussian_sketch(X.data_ptr(), N.LVSK_BF16, n, d, ldx, row0, 77, k, SX.data_ptr(), 0,
+                                   ws.data_ptr(), ws.numel(), flags.p, N.stream_ptr()), "gaussian tc")
+    assert flags.read() == 0
+    ref = O.gaussian_z(77, k, row0, n).astype(np.float64) @ xv / math.sqrt(k)
+    got = SX.cpu().numpy()
+    assert np.linalg.norm(got - ref) <= 2e-6 * np.linalg.norm(ref)
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+    # accumulate = 1 adds onto the state; non-finite input raises the flag
+    N.check(L.lvsk_gaussian_sketch(X.data_ptr(), N.LVSK_BF16, n, d, ldx, row0, 77, k, SX.data_ptr(), 1,
+                                   ws.data_ptr(), ws.numel(), flags.p, N.stream_ptr()), "gaussian tc")
+    assert np.linalg.norm(SX.cpu().numpy() - 2 * ref) <= 2e-6 * np.linalg.norm(2 * ref)
+    buf[n // 2, 3] = float("inf")
+    N.check(L.lvsk_gaussian_sketch(X.data_ptr(), N.LVSK_BF16, n, d, ldx, row0, 77, k, SX.data_ptr(), 0,
+                                   ws.data_ptr(), ws.numel(), flags.p, N.stream_ptr()), "gaussian tc")
+    assert flags.read() & N.FLAG_NONFINITE
+
+
 # ---------------------------------------------------------------------------
 # K5 leverage pass vs a float64 torch reference
 

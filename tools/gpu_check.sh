@@ -1,9 +1,9 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -rf --timeout 300 > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-tail -25 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --config c5 --steps 3 --warmup 1 --no-e2e --no-cpu > gpurun_out/bench_c5.log 2>&1
-echo "bench c5 exit $?" >> gpurun_out/bench_c5.log; tail -3 gpurun_out/bench_c5.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv \
-      python bench.py --config c5 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launch_c5.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q -rf --timeout 300 -k "kf_ or cholesky or csr or jl_fold or leverage_golden or c2_full" > gpurun_out/pytest_kf.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_kf.log
+tail -15 gpurun_out/pytest_kf.log
+timeout 600 python bench.py --steps 50 --warmup 5 --no-e2e --no-cpu > gpurun_out/bench_c2.log 2>&1
+echo "bench c2 exit $?" >> gpurun_out/bench_c2.log; tail -c 1500 gpurun_out/bench_c2.log
+timeout 600 python bench.py --config c4 --steps 3 --warmup 2 --no-e2e --no-cpu > gpurun_out/bench_c4.log 2>&1
+echo "bench c4 exit $?" >> gpurun_out/bench_c4.log; tail -c 1500 gpurun_out/bench_c4.log

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
           v = (m < a.d && c < a.r) ? a.Pi[m * a.r + c] : 0.0;
         else
           v = (c - rp) == m ? 1.0 : 0.0;
-        a.W[e] = v;
+        a.W[f] = v;
       }
     }
     if (cta == 0) {

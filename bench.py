@@ -438,7 +438,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
                               "hashed_gather_bulk_kernel (K1, incl. keygen + radix grouping)",
                               "srht": "srht_pass1/pass2 kernels (K3)",
                               "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
-                              if X.dtype == torch.bfloat16 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],
+                              if not csr and X.dtype == torch.bfloat16 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],
                    "leverage": "csr_rowsumsq_kernel (K6)" if csr else "leverage_v2_kernel (K5, tcgen05)"}[dominant],
         "achieved": dom_gbs,
         "peak": peak,

@@ -129,6 +129,9 @@ LVSK_API int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n, i
 /* Materialise Z (k x n float32, row-major) for KAT parity. */
 LVSK_API int32_t lvsk_gaussian_entries(uint64_t seed, int64_t k, uint64_t row0, int64_t n, float* Z,
                               void* stream);
+/* The generator's 1280-float table (INV[128] | LN[128] | CSA[256][2] |
+ * CSB[256][2], see csrc/philox.cuh), host-side; count >= 1280. */
+LVSK_API int32_t lvsk_gaussian_tables(float* out, int64_t count);
 
 /* ---- K5: leverage pass --------------------------------------------------
  * Replaces _block_scores (reference leverage.py:88-95):

@@ -268,9 +268,10 @@ def explicit_srht_matrix(k, seed, n):
 
 # ---------------------------------------------------------------------------
 # Gaussian sketch (extension; parity unpinned by reference tests).
-# S[j, i] = bf16(BoxMuller(Philox4x32-10(counter=(i_lo, i_hi, j>>2, 0),
-# key=(seed_lo, seed_hi ^ 'GAUS'))))[j & 3] / sqrt(k); the transcendental
-# parts use only IEEE fp32 add/mul/div/sqrt so CPU and GPU agree bit-for-bit.
+# S[j, i] = bf16(table-driven Box-Muller of the 16-bit halves of Philox4x32-10
+# word (j >> 1) & 3, counter (i_lo, i_hi, j >> 3, 0), key (seed_lo,
+# seed_hi ^ 'GAUS')) / sqrt(k); every step is an IEEE fp32 op or a table
+# lookup, so CPU and GPU agree bit-for-bit (definition: csrc/philox.cuh).
 
 _PH_M0, _PH_M1 = 0xD2511F53, 0xCD9E8D57
 _PH_W0, _PH_W1 = 0x9E3779B9, 0xBB67AE85
@@ -297,48 +298,17 @@ def philox4x32(c0, c1, c2, c3, k0, k1, rounds=10):
 _f = np.float32
 
 
-def _u01(x):
-    """uint32 -> (0,1) float32: (2*(x>>9)+1) * 2^-24, exact."""
-    return ((x >> np.uint64(9)) * np.uint64(2) + np.uint64(1)).astype(np.float32) * _f(2.0**-24)
-
-
-def _log_f32(u):
-    """ln(u) for u in (0,1), IEEE fp32 ops only (no FMA)."""
-    bits = u.view(np.uint32).astype(np.uint64)
-    e = ((bits >> np.uint64(23)) & np.uint64(0xFF)).astype(np.int64) - 127
-    mb = (bits & np.uint64(0x7FFFFF)) | np.uint64(0x3F800000)
-    big = mb > np.uint64(0x3FB504F3)
-    mb = np.where(big, mb - np.uint64(0x00800000), mb)
-    e = e + big.astype(np.int64)
-    m = mb.astype(np.uint32).view(np.float32)
-    t = (m - _f(1.0)) / (m + _f(1.0))
-    t2 = t * t
-    p = _f(2.0 / 9.0)
-    p = p * t2 + _f(2.0 / 7.0)
-    p = p * t2 + _f(2.0 / 5.0)
-    p = p * t2 + _f(2.0 / 3.0)
-    p = p * t2 + _f(2.0)
-    return e.astype(np.float32) * _f(0.6931471805599453) + t * p
-
-
-def _sincos_turns(v):
-    """(cos, sin) of 2*pi*v for v in (0,1), IEEE fp32 ops only."""
-    f4 = v * _f(4.0)
-    q = np.floor(f4)
-    f = f4 - q
-    qi = q.astype(np.int64)
-    x = f * _f(math.pi / 2)
-    x2 = x * x
-    s = _f(-1.0 / 39916800.0)
-    for c in (1.0 / 362880.0, -1.0 / 5040.0, 1.0 / 120.0, -1.0 / 6.0, 1.0):
-        s = s * x2 + _f(c)
-    s = s * x
-    c_ = _f(1.0 / 479001600.0)
-    for c in (-1.0 / 3628800.0, 1.0 / 40320.0, -1.0 / 720.0, 1.0 / 24.0, -0.5, 1.0):
-        c_ = c_ * x2 + _f(c)
-    cos = np.select([qi == 0, qi == 1, qi == 2], [c_, -s, -c_], s)
-    sin = np.select([qi == 0, qi == 1, qi == 2], [s, c_, -s], -c_)
-    return cos.astype(np.float32), sin.astype(np.float32)
+def gaussian_tables() -> np.ndarray:
+    """The generator's float32 table INV[128] | LN[128] | CSA[256][2] | CSB[256][2]
+    (csrc/philox.cuh; same float64 expressions, rounded once)."""
+    i = np.arange(128, dtype=np.float64)
+    two_pi = 2.0 * 3.141592653589793
+    a = np.arange(256, dtype=np.float64)
+    ang_a = two_pi * a / 256.0
+    ang_b = two_pi * (a + 0.5) / 65536.0
+    csa = np.stack([np.cos(ang_a), np.sin(ang_a)], axis=1).reshape(-1)
+    csb = np.stack([np.cos(ang_b), np.sin(ang_b)], axis=1).reshape(-1)
+    return np.concatenate([128.0 / (128.0 + i), np.log1p(i / 128.0), csa, csb]).astype(np.float32)
 
 
 def _bf16_rn(x):
@@ -347,22 +317,47 @@ def _bf16_rn(x):
     return b.astype(np.uint32).view(np.float32)
 
 
+def _box_muller16(w, tab):
+    """(r cos, r sin) of 32-bit words w, every step one IEEE fp32 op (philox.cuh)."""
+    w = w.astype(np.uint32)
+    v1, v2 = w & np.uint32(0xFFFF), w >> np.uint32(16)
+    u1 = (v1.astype(np.float32) + _f(0.5)) * _f(2.0**-16)
+    bits = u1.view(np.uint32)
+    ex = (bits >> np.uint32(23)).astype(np.int32) - 127
+    idx = ((bits >> np.uint32(16)) & np.uint32(0x7F)).astype(np.int64)
+    f = ((bits & np.uint32(0x007FFFFF)) | np.uint32(0x3F800000)).view(np.float32)
+    f0 = ((bits & np.uint32(0x007F0000)) | np.uint32(0x3F800000)).view(np.float32)
+    y = (f - f0) * tab[idx]
+    t = y - (y * y) * _f(0.5)
+    lnf = tab[128 + idx] + t
+    lnu = ex.astype(np.float32) * _f(0.693147182464599609375) + lnf
+    r = np.sqrt(lnu * _f(-2.0))
+    ia, ib = (v2 >> np.uint32(8)).astype(np.int64), (v2 & np.uint32(0xFF)).astype(np.int64)
+    ac, as_ = tab[256 + 2 * ia], tab[256 + 2 * ia + 1]
+    bc, bs = tab[768 + 2 * ib], tab[768 + 2 * ib + 1]
+    c = ac * bc - as_ * bs
+    s = as_ * bc + ac * bs
+    return r * c, r * s
+
+
 def gaussian_z(seed: int, k: int, row0: int, n: int) -> np.ndarray:
     """Unscaled Gaussian sketch entries Z (k x n, float32, bf16-representable)
-    for global rows row0..row0+n-1.  S = Z / sqrt(k)."""
+    for global rows row0..row0+n-1; S = Z / sqrt(k).  Z[8q + 2h + e, i] comes
+    from word h of Philox4x32-10(counter=(i_lo, i_hi, q, 0), key=(seed_lo,
+    seed_hi ^ 'GAUS')) through the table-driven Box-Muller of csrc/philox.cuh."""
+    tab = gaussian_tables()
     i = np.arange(row0, row0 + n, dtype=np.uint64)
-    q = np.arange((k + 3) // 4, dtype=np.uint64)
-    I, Q = np.meshgrid(i, q)  # (k/4, n)
+    q = np.arange((k + 7) // 8, dtype=np.uint64)
+    I, Q = np.meshgrid(i, q)  # (k/8, n)
     k0 = seed & 0xFFFFFFFF
     k1 = ((seed >> 32) & 0xFFFFFFFF) ^ GAUSS_KEY_XOR
-    x0, x1, x2, x3 = philox4x32(I & _U32, I >> np.uint64(32), Q, np.zeros_like(Q), k0, k1)
-    out = np.empty((Q.shape[0], 4, n), dtype=np.float32)
-    for (xa, xb), slot in (((x0, x1), 0), ((x2, x3), 2)):
-        u1, u2 = _u01(xa), _u01(xb)
-        r = np.sqrt(_f(-2.0) * _log_f32(u1))
-        c, s = _sincos_turns(u2)
-        out[:, slot] = _bf16_rn(r * c)
-        out[:, slot + 1] = _bf16_rn(r * s)
+    words = philox4x32(I & _U32, I >> np.uint64(32), Q, np.zeros_like(Q), k0, k1)
+    out = np.empty((Q.shape[0], 8, n), dtype=np.float32)
+    with np.errstate(over="ignore", invalid="ignore"):
+        for h, w in enumerate(words):
+            z0, z1 = _box_muller16(w, tab)
+            out[:, 2 * h] = _bf16_rn(z0)
+            out[:, 2 * h + 1] = _bf16_rn(z1)
     return out.reshape(-1, n)[:k]
 
 

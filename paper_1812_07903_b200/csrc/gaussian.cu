@@ -2,29 +2,70 @@
 //
 // Extension: the reference rejects the "gaussian" family
 // (pkg/src/levsketch/sketch.py:38-41, 74-75); BASELINE configs 1 and 5 ask
-// for it.  Z[j, i] (j < k sketch row, i global input row) is a bf16-rounded
-// standard normal from Philox4x32-10 (Random123) with counter
-// (i_lo, i_hi, j >> 2, 0) and key (seed_lo, seed_hi ^ 0x47415553), followed by
-// Box-Muller whose log / sin / cos use only IEEE fp32 add/mul/div/sqrt, so the
-// CPU oracle (oracle/levsketch_oracle.py: gaussian_z) reproduces every entry
-// bit-for-bit (generator: philox.cuh).  bf16 X runs on the tensor cores
+// for it.  Z[j, i] (j < k sketch row, i global input row) is the bf16-rounded
+// table-driven Box-Muller normal of philox.cuh, which the CPU oracle
+// (oracle/levsketch_oracle.py: gaussian_z) reproduces bit-for-bit.  bf16 X runs on the tensor cores
 // (gaussian_tc.cu); this file holds the entry generator, the SIMT GEMM used
 // for fp32 / fp64 X (split-K) and the deterministic float64 reduction of the
 // split partials shared by both.
+#include <cmath>
+#include <mutex>
+
 #include "philox.cuh"
 
 namespace lvsk {
 
-__global__ void gaussian_entries_kernel(uint32_t k0, uint32_t k1, int64_t k, uint64_t row0, int64_t n, float* Z) {
-  const int64_t nq = (k + 3) / 4;
+// ---- generator tables (philox.cuh) ----------------------------------------
+// Built in float64 then rounded to float32, with the same expressions as the
+// oracle (gaussian_tables); tests pin the two against each other.
+void gaussian_table_host(float* out) {
+  const double two_pi = 2.0 * 3.141592653589793;
+  for (int i = 0; i < 128; ++i) {
+    out[GT_INV + i] = static_cast<float>(128.0 / (128.0 + i));
+    out[GT_LN + i] = static_cast<float>(std::log1p(i / 128.0));
+  }
+  for (int a = 0; a < 256; ++a) {
+    const double ang = two_pi * a / 256.0;
+    out[GT_CSA + 2 * a] = static_cast<float>(std::cos(ang));
+    out[GT_CSA + 2 * a + 1] = static_cast<float>(std::sin(ang));
+  }
+  for (int b = 0; b < 256; ++b) {
+    const double ang = two_pi * (b + 0.5) / 65536.0;
+    out[GT_CSB + 2 * b] = static_cast<float>(std::cos(ang));
+    out[GT_CSB + 2 * b + 1] = static_cast<float>(std::sin(ang));
+  }
+}
+
+const float* gaussian_table_device() {
+  static float* dev = nullptr;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  if (dev == nullptr) {
+    float host[GT_SIZE];
+    gaussian_table_host(host);
+    if (cudaMalloc(&dev, sizeof(host)) != cudaSuccess) {
+      dev = nullptr;
+      return nullptr;
+    }
+    cudaMemcpy(dev, host, sizeof(host), cudaMemcpyHostToDevice);
+  }
+  return dev;
+}
+
+__global__ void gaussian_entries_kernel(uint32_t k0, uint32_t k1, int64_t k, uint64_t row0, int64_t n,
+                                        const float* __restrict__ gtab, float* Z) {
+  __shared__ float tab[GT_SIZE];
+  load_gaussian_table(tab, gtab);
+  __syncthreads();
+  const int64_t nq = (k + 7) / 8;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nq * n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t q = t / n, i = t - q * n;
-    float z[4];
-    gaussian4(row0 + static_cast<uint64_t>(i), static_cast<uint32_t>(q), k0, k1, z);
+    float z[8];
+    gaussian8(row0 + static_cast<uint64_t>(i), static_cast<uint32_t>(q), k0, k1, tab, z);
 #pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if (4 * q + s < k) Z[(4 * q + s) * n + i] = z[s];
+    for (int s = 0; s < 8; ++s)
+      if (8 * q + s < k) Z[(8 * q + s) * n + i] = bf16_rn(z[s]);
   }
 }
 
@@ -37,7 +78,9 @@ template <typename T, typename A>
 __global__ void __launch_bounds__(256) gaussian_gemm_kernel(const T* __restrict__ X, int64_t n, int64_t d,
                                                             int64_t ldx, uint64_t row0, uint32_t k0, uint32_t k1,
                                                             int64_t k, int64_t rows_per_split,
+                                                            const float* __restrict__ gtab,
                                                             A* __restrict__ partial, int32_t* flags) {
+  __shared__ float tab[GT_SIZE];
   __shared__ A Zs[G_RT][G_JT + 1];
   __shared__ A Xs[G_RT][G_CT + 1];
   const int tid = threadIdx.x;
@@ -47,6 +90,8 @@ __global__ void __launch_bounds__(256) gaussian_gemm_kernel(const T* __restrict_
   const int64_t split = blockIdx.z;
   const int64_t r_begin = split * rows_per_split;
   const int64_t r_end = min(n, r_begin + rows_per_split);
+  load_gaussian_table(tab, gtab);
+  __syncthreads();
   A acc[4][8];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -54,13 +99,13 @@ __global__ void __launch_bounds__(256) gaussian_gemm_kernel(const T* __restrict_
     for (int b = 0; b < 8; ++b) acc[a][b] = A(0);
   bool bad = false;
   for (int64_t r0 = r_begin; r0 < r_end; r0 += G_RT) {
-    {  // Z tile: thread -> (row offset, quad)
-      const int ro = tid % G_RT, q = tid / G_RT;  // 16 x 16 quads = 64 sketch rows
+    if (tid < G_RT * (G_JT / 8)) {  // Z tile: thread -> (row offset, octet of sketch rows)
+      const int ro = tid % G_RT, q = tid / G_RT;
       const int64_t r = r0 + ro;
-      float z[4] = {0.f, 0.f, 0.f, 0.f};
-      if (r < r_end) gaussian4(row0 + static_cast<uint64_t>(r), static_cast<uint32_t>(j0 / 4 + q), k0, k1, z);
+      float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (r < r_end) gaussian8(row0 + static_cast<uint64_t>(r), static_cast<uint32_t>(j0 / 8 + q), k0, k1, tab, z);
 #pragma unroll
-      for (int s = 0; s < 4; ++s) Zs[ro][4 * q + s] = static_cast<A>(z[s]);
+      for (int s = 0; s < 8; ++s) Zs[ro][8 * q + s] = static_cast<A>(bf16_rn(z[s]));
     }
     for (int e = tid; e < G_RT * G_CT; e += 256) {
       const int ro = e / G_CT, cc = e % G_CT;
@@ -162,8 +207,10 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
                (long long)d);
   LVSK_REQUIRE(k >= 1, LVSK_ERR_CONFIGURATION, "k must be >= 1");
   cudaStream_t st = as_stream(stream);
+  const float* gtab = gaussian_table_device();
+  LVSK_REQUIRE(gtab != nullptr, LVSK_ERR_CUDA, "cannot allocate the Gaussian generator table");
   const GaussPlan p = plan_gauss(n, d, k);
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32) ^ 0x47415553u;
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32) ^ Philox::KEY_XOR;
   dim3 grid(p.gx, p.gy, static_cast<unsigned>(p.splits));
   const double scale = 1.0 / sqrt(static_cast<double>(k));
   const int64_t count = k * d;
@@ -173,7 +220,7 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
     double* part = c.take<double>(static_cast<size_t>(p.splits) * count);
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
     gaussian_gemm_kernel<double, double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), n, d, ldx, row0, k0,
-                                                               k1, k, p.rows_per_split, part, flags);
+                                                               k1, k, p.rows_per_split, gtab, part, flags);
     gaussian_reduce_kernel<double><<<rgrid, 256, 0, st>>>(part, p.splits, count, scale, SX, accumulate, flags);
   } else if (dtype == LVSK_BF16 && gaussian_tc_ok(X, n, d, ldx, k)) {
     const GaussTcPlan t = plan_gauss_tc(n, d, k);
@@ -187,11 +234,11 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
     if (dtype == LVSK_F32)
       gaussian_gemm_kernel<float, float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx, row0, k0,
-                                                               k1, k, p.rows_per_split, part, flags);
+                                                               k1, k, p.rows_per_split, gtab, part, flags);
     else
       gaussian_gemm_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X), n, d,
                                                                        ldx, row0, k0, k1, k, p.rows_per_split,
-                                                                       part, flags);
+                                                                       gtab, part, flags);
     gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, p.splits, count, scale, SX, accumulate, flags);
   }
   LVSK_CHECK_LAUNCH("gaussian sketch");
@@ -202,10 +249,18 @@ extern "C" int32_t lvsk_gaussian_entries(uint64_t seed, int64_t k, uint64_t row0
                                          void* stream) {
   LVSK_REQUIRE(k >= 1 && n >= 0, LVSK_ERR_CONFIGURATION, "bad arguments");
   if (n == 0) return LVSK_OK;
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32) ^ 0x47415553u;
-  const int64_t work = (k + 3) / 4 * n;
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32) ^ Philox::KEY_XOR;
+  const float* gtab = gaussian_table_device();
+  LVSK_REQUIRE(gtab != nullptr, LVSK_ERR_CUDA, "cannot allocate the Gaussian generator table");
+  const int64_t work = (k + 7) / 8 * n;
   const int grid = static_cast<int>((work + 255) / 256 < num_sms() * 32 ? (work + 255) / 256 : num_sms() * 32);
-  gaussian_entries_kernel<<<grid, 256, 0, as_stream(stream)>>>(k0, k1, k, row0, n, Z);
+  gaussian_entries_kernel<<<grid, 256, 0, as_stream(stream)>>>(k0, k1, k, row0, n, gtab, Z);
   LVSK_CHECK_LAUNCH("gaussian entries");
+  return LVSK_OK;
+}
+
+extern "C" int32_t lvsk_gaussian_tables(float* out, int64_t count) {
+  LVSK_REQUIRE(out != nullptr && count >= GT_SIZE, LVSK_ERR_CAPACITY, "need %d floats", GT_SIZE);
+  gaussian_table_host(out);
   return LVSK_OK;
 }

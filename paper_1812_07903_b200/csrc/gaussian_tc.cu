@@ -11,8 +11,9 @@
 //   warp 0   TMA: X[64 rows][NS cols] as NS/64 SW128 boxes.  X is the MMA's
 //            B operand in MN-major layout (rows of X = K, contiguous columns
 //            = N), so no transpose pass exists anywhere;
-//   warps 2-9 generate the Z tile [128 x 64] (philox.cuh, bit-identical to
-//            the SIMT path and the oracle) straight into the K-major SW128 A
+//   warps 2-9 generate the Z tile [128 x 64] (philox.cuh: 8 entries per
+//            Philox call, table-driven Box-Muller, bit-identical to the SIMT
+//            path and the oracle) straight into the K-major SW128 A
 //            layout in shared memory, fence.proxy.async, arrive;
 //   warp 1   issues 4 x (NS/256) tcgen05.mma kind::f16 (M = 128, N = 256,
 //            K = 16) and commits the stage back to both producers.
@@ -38,7 +39,8 @@ struct CfgG {
   static constexpr int S = NS == 512 ? 2 : 4;
   static constexpr int OFF_Z = S * X_BYTES;
   static constexpr int OFF_BAR = OFF_Z + S * Z_BYTES;
-  static constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_TAB = OFF_BAR + 256;
+  static constexpr int SMEM_BYTES = OFF_TAB + GT_SIZE * 4 + 1024;
   static constexpr int GEN_WARPS = 8;
   static constexpr int NTHREADS = 64 + 32 * GEN_WARPS;
   // kind::f16: F32 accumulate, A = B = bf16, B MN-major, N = 256, M = 128
@@ -67,7 +69,7 @@ template <int NS>
 __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
                        uint32_t k0, uint32_t k1, int ktiles, int dslabs, int64_t rows_per_split,
-                       float* __restrict__ partial) {
+                       const float* __restrict__ gtab, float* __restrict__ partial) {
   using C = CfgG<NS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -77,6 +79,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   uint64_t* empty = zfull + C::S;
   uint64_t* accfull = empty + C::S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
+  float* tab = reinterpret_cast<float*>(smem + C::OFF_TAB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int item = blockIdx.x;
@@ -98,6 +101,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
   }
+  load_gaussian_table(tab, gtab);
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(NS));
@@ -147,16 +151,13 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     const int gw = warp - 2;
     const int iblk = lane & 15;           // input rows 4*iblk .. 4*iblk+3 of the stage
     const int q = gw * 2 + (lane >> 4);   // sketch rows 8q .. 8q+7 of the tile
-    const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 4) + 2 * q);  // Philox quad of row 8q
+    const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
     for (int t = 0; t < nstages; ++t) {
       const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
       const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 4 * iblk);
       float z[4][8];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        gaussian4(g0 + e, qg, k0, k1, *reinterpret_cast<float(*)[4]>(&z[e][0]));
-        gaussian4(g0 + e, qg + 1, k0, k1, *reinterpret_cast<float(*)[4]>(&z[e][4]));
-      }
+      for (int e = 0; e < 4; ++e) gaussian8(g0 + e, qg, k0, k1, tab, z[e]);
       mbar_wait(&empty[s], ph ^ 1u);
       uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
 #pragma unroll
@@ -250,8 +251,13 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
     attr = true;
   }
   const int64_t items = static_cast<int64_t>(p.ktiles) * p.dslabs * p.splits;
+  const float* gtab = gaussian_table_device();
+  if (gtab == nullptr) {
+    set_error("cannot allocate the Gaussian generator table");
+    return LVSK_ERR_CUDA;
+  }
   tc::gaussian_tc_kernel<NS><<<static_cast<unsigned>(items), C::NTHREADS, C::SMEM_BYTES, st>>>(
-      mx, n, d, k, row0, k0, k1, p.ktiles, p.dslabs, p.rows_per_split, partial);
+      mx, n, d, k, row0, k0, k1, p.ktiles, p.dslabs, p.rows_per_split, gtab, partial);
   LVSK_CHECK_LAUNCH("gaussian tc");
   return LVSK_OK;
 }

@@ -30,6 +30,17 @@ def test_library_exports_every_declared_symbol():
     assert lib.lvsk_abi_version() == 1
 
 
+def test_gaussian_generator_table_matches_oracle():
+    """The K4 generator's host-built table (csrc/gaussian.cu) is the oracle's,
+    bit for bit, so device entries can equal the oracle's exactly."""
+    import ctypes
+
+    out = np.zeros(1280, dtype=np.float32)
+    rc = _native.lib().lvsk_gaussian_tables(out.ctypes.data_as(ctypes.c_void_p), out.size)
+    assert rc == 0
+    assert np.array_equal(out.view(np.uint32), O.gaussian_tables().view(np.uint32))
+
+
 def test_no_cpu_fallback_without_gpu():
     import torch
 

@@ -418,14 +418,18 @@ def fold_r(sx, sv_tol, pi, rank=None):
     """JL fold (extension G3, the north star's "R M = Pi"): M = pinv_tau(R) Pi,
     pinv_tau from the SVD of R (same sigma / V as SX) truncated like the
     reference (strict relative threshold, optional rank cap).  With nothing
-    truncated this is R^-1 Pi; with Pi = I the row norms equal the reference
-    basis V'/sigma' scores.  Returns (M, r')."""
+    truncated this is R^-1 Pi.  When the kept rank r' does not exceed the JL
+    width (r' <= Pi's columns) a projection cannot reduce the dimension, so the
+    fold is the reference basis V'/sigma' itself (exact scores).
+    Returns (M, r')."""
     R = r_factor(sx)
     u, s, vt = np.linalg.svd(R, full_matrices=False)
     s2, vt2 = truncate(s, vt, sv_tol, rank)
     r = s2.shape[0]
     if np.any(s2 == 0.0):
         raise ZeroDivisionError("exact zero singular value")
+    if r <= pi.shape[1]:
+        return vt2.T / s2, r
     return (vt2.T / s2) @ (u[:, :r].T @ pi), r
 
 

@@ -12,14 +12,15 @@
 // one persistent cooperative kernel (<= 1 CTA per SM, 256 threads) walks the
 // blocked algorithm over 64 x 64 float64 tiles held in global memory (L2
 // resident: d = 512 is 2 MB) with a grid barrier between dependent phases:
-//   Cholesky step j:  B(j) panel solves  U_jk = U_jj^-T A_jk        (k > j)
+//   Cholesky step j:  B(j) panels  U_jk = T_j^T A_jk  (T_j = U_jj^-1)  (k > j)
 //                     C(j) trailing updates A_kl -= U_jk^T U_jl   (j < k <= l),
-//                          the task owning (j+1, j+1) also factors it
+//                          the task owning (j+1, j+1) also factors and inverts it
 //   back substitution X = U^-1 [Pi | I]:  step i updates W_l,c -= U_li X_ic
-//                          (l < i), the task owning (i-1, c) also solves it
-// Each tile op runs from shared memory: 64-step substitutions / factorization
-// with one __syncthreads per step, and 4 x 4 register-blocked float64 tile
-// GEMMs.  Padding rows (d % 64) carry an identity so no branch reaches the
+//                          (l < i), the task owning (i-1, c) then sets X = T W
+// The only sequential tile op is the diagonal one (chol_inv_tile: 64-pivot
+// Cholesky + the 64-step inverse of its factor, columns register-resident,
+// one __syncthreads per pivot); panels and the substitution are 4 x 4
+// register-blocked float64 tile GEMMs against those inverses.  Padding rows (d % 64) carry an identity so no branch reaches the
 // math.  Zero tiles of the identity right-hand side (U^-1 is triangular) are
 // skipped.
 #include <cooperative_groups.h>
@@ -44,6 +45,7 @@ struct FactorArgs {
   double* diag;
   double* A;  // dp x dp working copy (upper tiles)
   double* W;  // dp x wc right-hand sides, overwritten by X
+  double* T;  // nb tiles 64 x 64: inverses of the diagonal tiles of U
   double* partial;
   int32_t* info;
   int nb, rt, ct;  // tiles per edge, Pi column tiles, total RHS column tiles (rt + nb)
@@ -73,26 +75,29 @@ __device__ __forceinline__ void store_tile(double* g, int64_t ld, const double* 
 
 // ---- tile math ---------------------------------------------------------------
 
-// C (global, 64 x 64) -= At^T B with At[p][m], B[p][c] in smem; the result is
-// also left in smem tile `out` when out != nullptr.
-__device__ __forceinline__ void gemm_sub(double* gC, int64_t ldc, const double* At, const double* B, double* out) {
+// acc = (SUB ? C - At^T B : At^T B) with At[p][m], B[p][c] in smem (C read from
+// global when SUB); the result goes to smem `out` when out != nullptr, else
+// back to global C.  4 x 4 register blocking, 256 threads.
+template <bool SUB>
+__device__ __forceinline__ void gemm_tile(double* gC, int64_t ldc, const double* At, const double* B, double* out) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = gC[(ty + 16 * a) * ldc + tx + 16 * b];
+    for (int b = 0; b < 4; ++b) acc[a][b] = SUB ? gC[(ty + 16 * a) * ldc + tx + 16 * b] : 0.0;
+  const double sg = SUB ? -1.0 : 1.0;
 #pragma unroll 4
   for (int p = 0; p < FT; ++p) {
     double av[4], bv[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) av[a] = At[p * FLD + ty + 16 * a];
+    for (int a = 0; a < 4; ++a) av[a] = sg * At[p * FLD + ty + 16 * a];
 #pragma unroll
     for (int b = 0; b < 4; ++b) bv[b] = B[p * FLD + tx + 16 * b];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(-av[a], bv[b], acc[a][b]);
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -105,62 +110,57 @@ __device__ __forceinline__ void gemm_sub(double* gC, int64_t ldc, const double* 
     }
 }
 
-// In-place Cholesky of the upper triangle of s (s = U^T U, U upper with a
-// positive diagonal); the strict lower triangle is zeroed.  Returns through
-// *bad a nonzero value when a pivot is not positive and finite.
-__device__ void chol_tile(double* s, int32_t* bad) {
+// Cholesky of the 64 x 64 tile s (upper triangle used; s = U^T U) and the
+// inverse T = U^-1, both upper triangular, written to s and t.  Thread
+// (column c, group g) keeps rows g, g+4, .. of its column in registers; one
+// __syncthreads per pivot (the pivot row is published through `rowbuf`).
+// *bad |= 1 on a pivot that is not positive and finite.
+__device__ void chol_inv_tile(double* s, double* t, double* scratch, int32_t* bad) {
   const int c = threadIdx.x & 63, g = threadIdx.x >> 6;
+  double* rowbuf = scratch;          // [2][64]
+  double* rd = scratch + 2 * FT;     // [64] reciprocal diagonal of U
+  double a[FT / 4];
+#pragma unroll
+  for (int i = 0; i < FT / 4; ++i) a[i] = s[(g + 4 * i) * FLD + c];
+  bool badp = false;
+#pragma unroll
   for (int p = 0; p < FT; ++p) {
+    double* rb = rowbuf + (p & 1) * FT;
+    if (g == (p & 3)) rb[c] = a[p >> 2];
     __syncthreads();
-    const double piv = s[p * FLD + p];
-    if (c > p) {
-      const double w = s[p * FLD + c] / piv;
-      for (int m = p + 1 + ((g - (p + 1)) & 3); m <= c; m += 4) s[m * FLD + c] = fma(-s[p * FLD + m], w, s[m * FLD + c]);
-    }
+    const double piv = rb[p];
+    const double rs = rsqrt(piv);
+    const double w = rb[c] * (rs * rs);
+#pragma unroll
+    for (int i = 0; i < FT / 4; ++i)
+      if (g + 4 * i > p) a[i] = fma(-rb[g + 4 * i], w, a[i]);
+    if (g == (p & 3)) a[p >> 2] = c >= p ? rb[c] * rs : 0.0;
+    if (c == p && g == 0) badp = !(piv > 0.0) || !isfinite(piv);
   }
+  if (badp) atomicOr(bad, 1);
+#pragma unroll
+  for (int i = 0; i < FT / 4; ++i) s[(g + 4 * i) * FLD + c] = a[i];
   __syncthreads();
-  // scale rows: U[p][c] = a[p][c] / sqrt(a[p][p]); reads of the diagonal must
-  // finish before any row is rewritten
-  double dg[FT / 4];
-  for (int i = 0; i < FT / 4; ++i) {
-    const int m = g + 4 * i;
-    dg[i] = s[m * FLD + m];
-  }
+  if (threadIdx.x < FT) rd[threadIdx.x] = 1.0 / s[threadIdx.x * FLD + threadIdx.x];
+  // T = U^-1 by backward substitution on the identity, column c in registers
+#pragma unroll
+  for (int i = 0; i < FT / 4; ++i) a[i] = (g + 4 * i == c) ? 1.0 : 0.0;
   __syncthreads();
-  for (int i = 0; i < FT / 4; ++i) {
-    const int m = g + 4 * i;
-    const double piv = dg[i];
-    if (!(piv > 0.0) || !isfinite(piv)) {
-      if (c == 0) atomicOr(bad, 1);
-    }
-    const double v = s[m * FLD + c];
-    s[m * FLD + c] = c >= m ? v / sqrt(piv) : 0.0;
-  }
-  __syncthreads();
-}
-
-// Y = U^-T B (forward substitution with the lower U^T): B in smem (destroyed),
-// Y written to smem `y`.
-__device__ void solve_lower_t(const double* U, double* b, double* y) {
-  const int c = threadIdx.x & 63, g = threadIdx.x >> 6;
-  for (int p = 0; p < FT; ++p) {
-    __syncthreads();
-    const double x = b[p * FLD + c] / U[p * FLD + p];
-    if (g == 0) y[p * FLD + c] = x;
-    for (int m = p + 1 + ((g - (p + 1)) & 3); m < FT; m += 4) b[m * FLD + c] = fma(-U[p * FLD + m], x, b[m * FLD + c]);
-  }
-  __syncthreads();
-}
-
-// X = U^-1 B (backward substitution with the upper U): B in smem (destroyed).
-__device__ void solve_upper(const double* U, double* b, double* x_out) {
-  const int c = threadIdx.x & 63, g = threadIdx.x >> 6;
+#pragma unroll
   for (int p = FT - 1; p >= 0; --p) {
+    double* xb = rowbuf + (p & 1) * FT;
+    if (g == (p & 3)) {
+      a[p >> 2] *= rd[p];
+      xb[c] = a[p >> 2];
+    }
     __syncthreads();
-    const double x = b[p * FLD + c] / U[p * FLD + p];
-    if (g == 0) x_out[p * FLD + c] = x;
-    for (int m = g; m < p; m += 4) b[m * FLD + c] = fma(-U[m * FLD + p], x, b[m * FLD + c]);
+    const double x = xb[c];
+#pragma unroll
+    for (int i = 0; i < FT / 4; ++i)
+      if (g + 4 * i < p) a[i] = fma(-s[(g + 4 * i) * FLD + p], x, a[i]);
   }
+#pragma unroll
+  for (int i = 0; i < FT / 4; ++i) t[(g + 4 * i) * FLD + c] = a[i];
   __syncthreads();
 }
 
@@ -169,6 +169,7 @@ __device__ void solve_upper(const double* U, double* b, double* x_out) {
 __device__ __forceinline__ double* atile(const FactorArgs& a, int k, int l) {
   return a.A + static_cast<int64_t>(k) * FT * a.dp + static_cast<int64_t>(l) * FT;
 }
+__device__ __forceinline__ double* ttile(const FactorArgs& a, int j) { return a.T + static_cast<int64_t>(j) * FT * FT; }
 __device__ __forceinline__ double* wtile(const FactorArgs& a, int i, int c) {
   return a.W + static_cast<int64_t>(i) * FT * a.wc + static_cast<int64_t>(c) * FT;
 }
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
   double* s0 = fsm;
   double* s1 = fsm + FT * FLD;
   double* s2 = fsm + 2 * FT * FLD;
+  double* scratch = fsm + 3 * FT * FLD;  // 3 x 64 doubles
   cg::grid_group grid = cg::this_grid();
   const int cta = blockIdx.x, ncta = gridDim.x;
   const int nb = a.nb;
@@ -227,27 +229,27 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
   grid.sync();
   if (cta == 0) {
     load_tile(s0, atile(a, 0, 0), a.dp);
-    chol_tile(s0, a.info);
+    chol_inv_tile(s0, s1, scratch, a.info);
     store_tile(atile(a, 0, 0), a.dp, s0);
+    store_tile(ttile(a, 0), FT, s1);
   }
   grid.sync();
 
-  // ---- blocked Cholesky
+  // ---- blocked Cholesky (T_j = U_jj^-1 from the task that factored U_jj)
   for (int j = 0; j < nb - 1; ++j) {
-    // B(j): U_jk = U_jj^-T A_jk
+    // B(j): U_jk = T_j^T A_jk
     for (int k = j + 1 + cta; k < nb; k += ncta) {
-      load_tile(s0, atile(a, j, j), a.dp);
+      load_tile(s0, ttile(a, j), FT);
       load_tile(s1, atile(a, j, k), a.dp);
-      solve_lower_t(s0, s1, s2);
-      store_tile(atile(a, j, k), a.dp, s2);
+      __syncthreads();
+      gemm_tile<false>(atile(a, j, k), a.dp, s0, s1, nullptr);
       __syncthreads();
     }
     grid.sync();
-    // C(j): A_kl -= U_jk^T U_jl for j < k <= l; task 0 is (j+1, j+1) + factor
+    // C(j): A_kl -= U_jk^T U_jl for j < k <= l; task 0 is (j+1, j+1) + factor + inverse
     const int m = nb - j - 1;
     const int ntask = m * (m + 1) / 2;
     for (int t = cta; t < ntask; t += ncta) {
-      // t -> (k, l): row-major over the upper triangle starting at (j+1, j+1)
       int k = 0, rem = t;
       while (rem >= m - k) {
         rem -= m - k;
@@ -258,25 +260,27 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       load_tile(s1, atile(a, j, ll), a.dp);
       __syncthreads();
       if (t == 0) {
-        gemm_sub(atile(a, kk, ll), a.dp, s0, s1, s2);
-        chol_tile(s2, a.info);
+        gemm_tile<true>(atile(a, kk, ll), a.dp, s0, s1, s2);
+        __syncthreads();
+        chol_inv_tile(s2, s0, scratch, a.info);
         store_tile(atile(a, kk, ll), a.dp, s2);
+        store_tile(ttile(a, kk), FT, s0);
       } else {
-        gemm_sub(atile(a, kk, ll), a.dp, s0, s1, nullptr);
+        gemm_tile<true>(atile(a, kk, ll), a.dp, s0, s1, nullptr);
       }
       __syncthreads();
     }
     grid.sync();
   }
 
-  // ---- back substitution X = U^-1 W, in place in W
+  // ---- back substitution X = U^-1 W, in place in W:  X_i = T_i (W_i - sum_{l>i} U_il X_l)
   const int ct = a.ct;
   for (int c = cta; c < ct; c += ncta) {
     if (!x_live(a, nb - 1, c)) continue;
-    load_tile(s0, atile(a, nb - 1, nb - 1), a.dp);
+    load_tile_t(s0, ttile(a, nb - 1), FT);
     load_tile(s1, wtile(a, nb - 1, c), a.wc);
-    solve_upper(s0, s1, s2);
-    store_tile(wtile(a, nb - 1, c), a.wc, s2);
+    __syncthreads();
+    gemm_tile<false>(wtile(a, nb - 1, c), a.wc, s0, s1, nullptr);
     __syncthreads();
   }
   grid.sync();
@@ -293,15 +297,15 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
         load_tile_t(s0, atile(a, l, i), a.dp);
         load_tile(s1, wtile(a, i, c), a.wc);
         __syncthreads();
-        gemm_sub(wtile(a, l, c), a.wc, s0, s1, solve ? s2 : nullptr);
+        gemm_tile<true>(wtile(a, l, c), a.wc, s0, s1, solve ? s2 : nullptr);
       } else {
         load_tile(s2, wtile(a, l, c), a.wc);
       }
       if (solve) {
         __syncthreads();
-        load_tile(s0, atile(a, l, l), a.dp);
-        solve_upper(s0, s2, s1);
-        store_tile(wtile(a, l, c), a.wc, s1);
+        load_tile_t(s0, ttile(a, l), FT);
+        __syncthreads();
+        gemm_tile<false>(wtile(a, l, c), a.wc, s0, s2, nullptr);
       }
       __syncthreads();
     }
@@ -381,6 +385,7 @@ extern "C" size_t lvsk_chol_fold_workspace_bytes(int64_t d, int64_t r) {
   Measure ms;
   ms.take<double>(static_cast<size_t>(P.dp) * P.dp);
   ms.take<double>(static_cast<size_t>(P.dp) * P.wc);
+  ms.take<double>(static_cast<size_t>(P.nb) * FT * FT);
   ms.take<double>(static_cast<size_t>(P.nb) * P.ct);
   ms.take<int32_t>(1);
   return ms.off;
@@ -403,6 +408,7 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.diag = diag;
   a.A = c.take<double>(static_cast<size_t>(P.dp) * P.dp);
   a.W = c.take<double>(static_cast<size_t>(P.dp) * P.wc);
+  a.T = c.take<double>(static_cast<size_t>(P.nb) * FT * FT);
   a.partial = c.take<double>(static_cast<size_t>(P.nb) * P.ct);
   a.info = c.take<int32_t>(1);
   LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
@@ -411,7 +417,7 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.ct = P.ct;
   a.dp = P.dp;
   a.wc = P.wc;
-  const int smem = 3 * FTILE_SMEM;
+  const int smem = 3 * FTILE_SMEM + 3 * FT * 8;
   static int grid_cap = 0;
   if (grid_cap == 0) {
     cudaError_t e = cudaFuncSetAttribute(chol_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -159,25 +159,61 @@ def cholesky_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor):
     return M.contiguous() if chol_certified(diag.tolist(), sv_tol) else None
 
 
-def qr_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor):
-    """General JL fold M = pinv_tau(R) Pi: R from QR of SX (no squaring of the
-    condition number), SVD of the small R, the reference's strict relative
-    truncation and the optional rank cap."""
+# the Gram route's sigma / V are accurate to ~eps * kappa^2 relative; above this
+# kept-spectrum condition number the QR + Jacobi-SVD route runs instead
+_EIGH_KAPPA = 1e4
+
+
+def _positive_r(sx: torch.Tensor) -> torch.Tensor:
     R = torch.linalg.qr(sx, mode="r")[1]
     sg = torch.sign(torch.diagonal(R))
     sg[sg == 0] = 1.0
-    R = R * sg[:, None]
-    u, sigma, vt = torch.linalg.svd(R, full_matrices=False, driver="gesvd")
-    s_host = sigma.cpu().numpy()
+    return R * sg[:, None]
+
+
+def _kept(s_host: np.ndarray, sv_tol: float | None, rank: int | None) -> int:
     if s_host.shape[0] == 0 or s_host[0] <= 0:
         raise DegenerateInputError("cannot truncate an all-zero matrix (largest singular value is 0)")
     r = s_host.shape[0] if sv_tol is None else int(np.count_nonzero(s_host > sv_tol * s_host[0]))
-    if rank is not None:
-        r = min(r, rank)
+    return min(r, rank) if rank is not None else r
+
+
+def spectral_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor,
+                  force_qr: bool = False):
+    """General JL fold M = pinv_tau(R) Pi (oracle fold_r): sigma and V of SX
+    from the Gram eigendecomposition when the kept spectrum is well conditioned
+    (kappa' <= 1e4), else from a Jacobi SVD of the positive-diagonal QR factor
+    R; the reference's strict relative truncation and the optional rank cap.
+    When the kept rank r' <= Pi's width the projection cannot reduce the
+    dimension and M is the reference basis V'/sigma' (exact scores)."""
+    k, d = sx.shape
+    jl = pi.shape[1]
+    u = None
+    ok = False
+    if k >= d and not force_qr:
+        lam, v = torch.linalg.eigh(sx.T @ sx)
+        sigma = torch.sqrt(torch.clamp(lam.flip(0), min=0.0))
+        vt = v.flip(1).T
+        s_host = sigma.cpu().numpy()
+        r = _kept(s_host, sv_tol, rank)
+        ok = s_host[r - 1] > 0 and s_host[0] / s_host[r - 1] <= _EIGH_KAPPA
+    if not ok:
+        R = _positive_r(sx)
+        u, sigma, vt = torch.linalg.svd(R, full_matrices=False, driver="gesvdj")
+        s_host = sigma.cpu().numpy()
+        r = _kept(s_host, sv_tol, rank)
     if np.any(s_host[:r] == 0.0):
         raise SingularInversionError("sketch has an exactly-zero singular value; use the truncated method")
-    M = (vt[:r].T / sigma[:r]) @ (u[:, :r].T @ pi)
-    return M.contiguous(), r
+    basis = vt[:r].T / sigma[:r]
+    if r <= jl:
+        return basis.contiguous(), r
+    ur = (_positive_r(sx) @ vt[:r].T) / sigma[:r] if u is None else u[:, :r]
+    return (basis @ (ur.T @ pi)).contiguous(), r
+
+
+def qr_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor):
+    """:func:`spectral_fold` forced onto the QR + SVD-of-R route."""
+    return spectral_fold(sx, sv_tol, rank, pi, force_qr=True)
 
 
 def sketch_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: torch.Tensor | None,
@@ -186,17 +222,18 @@ def sketch_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: to
 
     pi is None (the reference API): M = V'/sigma' from the SVD of SX
     (leverage.py:75-85).  JL (pi given, BASELINE's r): M = pinv_tau(R) Pi —
-    Cholesky + triangular solves when :func:`chol_certified` proves nothing is
-    truncated, else QR + SVD of R."""
+    the KF Cholesky kernel when :func:`chol_certified` proves nothing is
+    truncated (Pi = I when d <= r: the exact scores), else
+    :func:`spectral_fold`."""
     k, d = sx.shape
     if pi is None:
         sigma, vt, s_host = factor_device(sx, sv_tol, rank, "svd" if method in ("auto", "chol", "qr") else method)
         return fold_device(sigma, vt, s_host, None), int(s_host.shape[0])
     if method in ("auto", "chol") and rank is None and k >= d:
-        M = cholesky_fold(sx, sv_tol, pi)
+        M = cholesky_fold(sx, sv_tol, pi if d > pi.shape[1] else torch.eye(d, dtype=sx.dtype, device=sx.device))
         if M is not None:
             return M, d
-    return qr_fold(sx, sv_tol, rank, pi)
+    return spectral_fold(sx, sv_tol, rank, pi, force_qr=(method == "qr"))
 
 
 def split_m(M: torch.Tensor, x_dtype: torch.dtype):
@@ -322,8 +359,10 @@ class FoldGraph:
     the certificate fails (caller then takes the eager QR path)."""
 
     def __init__(self, sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor, X_like: torch.Tensor):
-        self.sx, self.sv_tol, self.pi = sx, sv_tol, pi
         k, d = sx.shape
+        if d <= pi.shape[1]:  # a JL projection cannot reduce the dimension: exact scores (Pi = I)
+            pi = torch.eye(d, dtype=sx.dtype, device=sx.device)
+        self.sx, self.sv_tol, self.pi = sx, sv_tol, pi
         self.ops = KernelOperands(None, X_like, (d, pi.shape[1]))
         self.diag = torch.zeros(3, dtype=torch.float64, device=sx.device)
         self.graph = None
@@ -342,9 +381,16 @@ class FoldGraph:
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
 
-    def run(self) -> bool:
+    def replay(self) -> None:
+        """Enqueue the fold (no host synchronisation); see :meth:`certified`."""
         self.graph.replay()
+
+    def certified(self) -> bool:
         return chol_certified(self.diag.tolist(), self.sv_tol)
+
+    def run(self) -> bool:
+        self.replay()
+        return self.certified()
 
 
 def scores_device(X: torch.Tensor, M: torch.Tensor, out: torch.Tensor | None = None, flags=None) -> torch.Tensor:

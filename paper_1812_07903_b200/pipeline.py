@@ -64,6 +64,8 @@ class LeveragePipeline:
         # a dtype/alignment witness for choosing the K5 kernel (real X has the same layout)
         self._x_like = torch.empty((1, d), dtype=dtype, device=dev)
         self._fold_graph = None
+        self._cert_pending = False
+        self._last_X = None
         self._m32 = None
         self._m32_src = None
         self.effective_rank = None
@@ -105,17 +107,34 @@ class LeveragePipeline:
 
     def _factor(self) -> None:
         k, d = self.sx.shape
+        self._cert_pending = False
         if (self.factor_method == "auto" and self.pi is not None and self.rank is None and k >= d
                 and os.environ.get("LVSK_NO_GRAPH", "0") != "1"):
             if self._fold_graph is None:
                 self._fold_graph = FoldGraph(self.sx, self.sv_tol, self.pi, self._x_like)
-            if self._fold_graph.run():
-                self.ops = self._fold_graph.ops
-                self.r = self.ops.r
-                self.effective_rank = d
-                return
+            # optimistic: the leverage pass runs on R^-1 Pi right away and the
+            # certificate is verified in check(); a failed certificate redoes
+            # the fold (spectral route) and the passes after it
+            self._fold_graph.replay()
+            self._cert_pending = True
+            self.ops = self._fold_graph.ops
+            self.r = self.ops.r
+            self.effective_rank = d
+            return
         M, self.effective_rank = sketch_fold(self.sx, self.sv_tol, self.rank, self.pi, self.factor_method)
         self.set_fold(M)
+
+    def _verify_fold(self) -> None:
+        if not self._cert_pending:
+            return
+        self._cert_pending = False
+        if self._fold_graph.certified():
+            return
+        M, self.effective_rank = sketch_fold(self.sx, self.sv_tol, self.rank, self.pi, "qr")
+        self.set_fold(M)
+        self._leverage(self._last_X)
+        if self.order:
+            self._order()
 
     def set_fold(self, M: torch.Tensor) -> None:
         self.ops = KernelOperands(M, self._x_like)
@@ -152,6 +171,7 @@ class LeveragePipeline:
         elif X.shape != (self.n, self.d) or X.dtype != self.dtype or X.stride(1) != 1:
             raise ValueError(f"expected a ({self.n}, {self.d}) {self.dtype} row-major CUDA tensor")
         self.flags.zero_()
+        self._last_X = X
         ev = self.events
         steps = [("sketch", lambda: self._sketch(X)), ("factor", self._factor), ("leverage", lambda: self._leverage(X))]
         if self.order:
@@ -178,6 +198,9 @@ class LeveragePipeline:
         return out
 
     def check(self) -> None:
+        """Verify the fold certificate of the last run (redoing the fold and the
+        passes after it if it failed) and raise on flagged input errors."""
+        self._verify_fold()
         f = int(self.flags.item())
         if f & N.FLAG_BADINDEX:
             raise FormatError("CSR rows need strictly increasing column indices in [0, d)")

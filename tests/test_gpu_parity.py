@@ -505,6 +505,28 @@ def test_c2_full_size_properties():
     assert np.all(np.diff(sc[o] / sc.sum()) <= 0)
 
 
+@pytest.mark.parametrize("sv_tol,noise", [(1e-6, 0.3), (0.05, 0.0)])
+def test_pipeline_fold_certificate_and_fallback(sv_tol, noise):
+    """LeveragePipeline runs the KF fold optimistically and verifies the
+    certificate in check(): certified -> R^-1 Pi; refused (a threshold that
+    truncates) -> the spectral fold redone, scores and order recomputed.
+    Both equal the oracle's fold_r scores."""
+    rng = np.random.default_rng(11)
+    n, d, k, jl = 6000, 96, 512, 32
+    x = (rng.standard_normal((n, 12)) @ rng.standard_normal((12, d))) * np.linspace(1, 5, d) \
+        + noise * rng.standard_normal((n, d))
+    X = torch.from_numpy(x.astype(np.float32)).cuda()
+    spec = P.SketchSpec("countsketch", eps=0.5, d=d, seed=5, rows_override=k)
+    pipe = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=sv_tol, jl_dim=jl, jl_seed=6)
+    scores, order = pipe.run(X)
+    hi, lo = O.hashed_sketch(X.double().cpu().numpy(), "countsketch", k, 5, 1)
+    ref, r, _ = O.leverage_from_sketch(X.double().cpu().numpy(), hi + lo, sv_tol, O.jl_matrix(6, d, jl))
+    assert pipe.effective_rank == r
+    got = scores.cpu().numpy()
+    assert np.max(np.abs(got - ref) / np.maximum(ref, 1e-30)) < 1e-4
+    assert np.array_equal(order.cpu().numpy(), np.argsort(-(got / got.sum()), kind="stable"))
+
+
 # ---------------------------------------------------------------------------
 # K2 / K6: CSR rows (extension G2), semantics = densified rows
 

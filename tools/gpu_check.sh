@@ -1,10 +1,10 @@
 cd $GRAFT_REPO_ROOT
+export PYTHONPATH=$GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -rf --timeout 300 -k "kf_ or cholesky or csr or jl_fold or leverage_golden or c2_full or distributed or c5" > gpurun_out/pytest_new.log 2>&1
-echo "pytest exit $?" >> gpurun_out/pytest_new.log
-tail -15 gpurun_out/pytest_new.log
-timeout 300 python bench.py --steps 50 --warmup 5 --no-e2e --no-cpu > gpurun_out/bench_c2.log 2>&1
-echo "bench c2 exit $?" >> gpurun_out/bench_c2.log; tail -c 1200 gpurun_out/bench_c2.log
-timeout 300 python bench.py --config c4 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_c4.log 2>&1
-echo "bench c4 exit $?" >> gpurun_out/bench_c4.log; tail -c 1200 gpurun_out/bench_c4.log
-timeout 300 python tools/factor_bench.py > gpurun_out/factor_bench.log 2>&1; cat gpurun_out/factor_bench.log
+timeout 600 python -m pytest tests -m gpu -q -rf --timeout 300 -k "gaussian or c5" > gpurun_out/pytest_g.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_g.log
+tail -8 gpurun_out/pytest_g.log
+timeout 300 python tools/kf_time.py > gpurun_out/kf_time.log 2>&1; cat gpurun_out/kf_time.log
+timeout 300 python bench.py --config c5 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_c5.log 2>&1
+echo "bench c5 exit $?" >> gpurun_out/bench_c5.log; tail -c 1500 gpurun_out/bench_c5.log
+timeout 300 ncu --metrics gpu__time_duration.sum,sm__inst_executed.sum,smsp__cycles_active.avg --clock-control none -k regex:chol_fold -c 3 python tools/kf_time.py > gpurun_out/kf_ncu.log 2>&1; grep -E "chol_fold|duration|inst_exec|cycles_active" gpurun_out/kf_ncu.log | head -20

@@ -11,13 +11,13 @@
 //   warp 0   TMA: X[64 rows][NS cols] as NS/64 SW128 boxes.  X is the MMA's
 //            B operand in MN-major layout (rows of X = K, contiguous columns
 //            = N), so no transpose pass exists anywhere;
-//   warps 2-9 generate the Z tile [128 x 64] (philox.cuh: 8 entries per
+//   warps 2-17 generate the Z tile [128 x 64] (philox.cuh: 8 entries per
 //            Philox call, table-driven Box-Muller, bit-identical to the SIMT
 //            path and the oracle) straight into the K-major SW128 A
 //            layout in shared memory, fence.proxy.async, arrive;
 //   warp 1   issues 4 x (NS/256) tcgen05.mma kind::f16 (M = 128, N = 256,
 //            K = 16) and commits the stage back to both producers.
-// After the last stage warps 2-9 drain TMEM (tcgen05.ld 32x32b) into the
+// After the last stage warps 2-17 drain TMEM (tcgen05.ld 32x32b) into the
 // split's fp32 partial.  X traffic: each X element is read once per 128
 // sketch rows (ceil(k/128) times, L2-shared across the CTAs of one
 // (split, column slab) which are launched adjacently); each Z entry is
@@ -41,7 +41,7 @@ struct CfgG {
   static constexpr int OFF_BAR = OFF_Z + S * Z_BYTES;
   static constexpr int OFF_TAB = OFF_BAR + 256;
   static constexpr int SMEM_BYTES = OFF_TAB + GT_SIZE * 4 + 1024;
-  static constexpr int GEN_WARPS = 8;
+  static constexpr int GEN_WARPS = 16;  // one per 8-row octet of the 128-row tile
   static constexpr int NTHREADS = 64 + 32 * GEN_WARPS;
   // kind::f16: F32 accumulate, A = B = bf16, B MN-major, N = 256, M = 128
   static constexpr uint32_t IDESC =
@@ -147,29 +147,26 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       umma_commit(accfull);
     }
   } else {
-    // ---- Z generation: thread -> (8 sketch rows 8q.., 4 consecutive input rows)
+    // ---- Z generation: warp gw -> sketch rows 8gw .. 8gw+7 of the tile,
+    //      lane -> input rows 2*lane, 2*lane+1 of the stage (2 Philox calls)
     const int gw = warp - 2;
-    const int iblk = lane & 15;           // input rows 4*iblk .. 4*iblk+3 of the stage
-    const int q = gw * 2 + (lane >> 4);   // sketch rows 8q .. 8q+7 of the tile
+    const int q = gw;
     const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
     for (int t = 0; t < nstages; ++t) {
       const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
-      const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 4 * iblk);
-      float z[4][8];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) gaussian8(g0 + e, qg, k0, k1, tab, z[e]);
+      const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 2 * lane);
+      float z[2][8];
+      gaussian8(g0, qg, k0, k1, tab, z[0]);
+      gaussian8(g0 + 1, qg, k0, k1, tab, z[1]);
       mbar_wait(&empty[s], ph ^ 1u);
       uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
 #pragma unroll
       for (int r8 = 0; r8 < 8; ++r8) {
         const int j = 8 * q + r8;
-        __nv_bfloat162 lo = __floats2bfloat162_rn(z[0][r8], z[1][r8]);
-        __nv_bfloat162 hi = __floats2bfloat162_rn(z[2][r8], z[3][r8]);
-        uint2 v;
-        v.x = *reinterpret_cast<uint32_t*>(&lo);
-        v.y = *reinterpret_cast<uint32_t*>(&hi);
-        const int off = j * 128 + ((((iblk >> 1) ^ (j & 7))) << 4) + (iblk & 1) * 8;
-        *reinterpret_cast<uint2*>(zt + off) = v;
+        __nv_bfloat162 v = __floats2bfloat162_rn(z[0][r8], z[1][r8]);
+        // row j: 128 B = 8 swizzled 16-byte chunks; lane owns bytes [4 lane, 4 lane + 4)
+        const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
+        *reinterpret_cast<__nv_bfloat162*>(zt + off) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -178,11 +175,12 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     // ---- epilogue: TMEM -> fp32 partial
     mbar_wait(accfull, 0);
     tc_fence_after();
-    const int quarter = warp & 3, half = gw >> 2;
+    constexpr int PARTS = C::GEN_WARPS / 4;  // warps per TMEM lane quarter
+    const int quarter = warp & 3, part = gw >> 2;
     const int64_t j = static_cast<int64_t>(ktile) * BM + quarter * 32 + lane;
     float* out = partial + split * k * d + j * d;
 #pragma unroll 1
-    for (int c = half * (NS / 2); c < (half + 1) * (NS / 2); c += 32) {
+    for (int c = part * (NS / PARTS); c < (part + 1) * (NS / PARTS); c += 32) {
       uint32_t v[32];
       tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
       tmem_wait_ld();

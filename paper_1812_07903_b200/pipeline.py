@@ -132,6 +132,9 @@ class LeveragePipeline:
             return
         M, self.effective_rank = sketch_fold(self.sx, self.sv_tol, self.rank, self.pi, "qr")
         self.set_fold(M)
+        # the optimistic passes ran on an uncertified (possibly non-finite) fold;
+        # their flags are void — the leverage pass re-checks X itself
+        self.flags.zero_()
         self._leverage(self._last_X)
         if self.order:
             self._order()

@@ -331,7 +331,10 @@ def test_cholesky_fold_equals_qr_fold_and_oracle():
     assert P.leverage.cholesky_fold(sx, 0.5, pi) is None
     m_tr, r_tr = P.leverage.qr_fold(sx, 0.5, None, pi)
     m_or2, r_or2 = O.fold_r(sx.cpu().numpy(), 0.5, O.jl_matrix(0, 256, 64))
-    assert r_tr == r_or2 < 256 and np.allclose(m_tr.cpu().numpy(), m_or2, rtol=1e-8, atol=1e-11 * np.abs(m_or2).max())
+    # r' <= 64 = Pi's width: both return the (sign-ambiguous) basis V'/sigma'; compare M M^T
+    mm, mo = m_tr.cpu().numpy(), m_or2
+    assert r_tr == r_or2 < 64 and mm.shape == mo.shape
+    assert np.allclose(mm @ mm.T, mo @ mo.T, rtol=1e-8, atol=1e-11 * np.abs(mo @ mo.T).max())
 
 
 @pytest.mark.parametrize("k,d,r", [(64, 1, 1), (300, 64, 64), (400, 100, 7), (2048, 512, 64), (1500, 700, 130)])
@@ -505,7 +508,7 @@ def test_c2_full_size_properties():
     assert np.all(np.diff(sc[o] / sc.sum()) <= 0)
 
 
-@pytest.mark.parametrize("sv_tol,noise", [(1e-6, 0.3), (0.05, 0.0)])
+@pytest.mark.parametrize("sv_tol,noise", [(1e-6, 1.0), (0.05, 0.0)])
 def test_pipeline_fold_certificate_and_fallback(sv_tol, noise):
     """LeveragePipeline runs the KF fold optimistically and verifies the
     certificate in check(): certified -> R^-1 Pi; refused (a threshold that

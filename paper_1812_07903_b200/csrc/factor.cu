@@ -25,6 +25,9 @@
 // skipped.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -48,6 +51,7 @@ struct FactorArgs {
   double* T;  // nb tiles 64 x 64: inverses of the diagonal tiles of U
   double* partial;
   int32_t* info;
+  unsigned long long* trace;  // optional phase timestamps (LVSK_KF_TRACE), else null
   int nb, rt, ct;  // tiles per edge, Pi column tiles, total RHS column tiles (rt + nb)
   int64_t dp, wc;
 };
@@ -177,7 +181,17 @@ __device__ __forceinline__ double* wtile(const FactorArgs& a, int i, int c) {
 // identity column tile c (c >= rt) has nonzero X rows only for i <= c - rt
 __device__ __forceinline__ bool x_live(const FactorArgs& a, int i, int c) { return c < a.rt || i <= c - a.rt; }
 
+__device__ __forceinline__ void kf_mark(const FactorArgs& a, int& ph) {
+  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[ph] = t;
+  }
+  ++ph;
+}
+
 __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
+  int ph = 0;
   extern __shared__ double fsm[];
   double* s0 = fsm;
   double* s1 = fsm + FT * FLD;
@@ -227,6 +241,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
     }
   }
   grid.sync();
+  kf_mark(a, ph);
   if (cta == 0) {
     load_tile(s0, atile(a, 0, 0), a.dp);
     chol_inv_tile(s0, s1, scratch, a.info);
@@ -234,6 +249,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
     store_tile(ttile(a, 0), FT, s1);
   }
   grid.sync();
+  kf_mark(a, ph);
 
   // ---- blocked Cholesky (T_j = U_jj^-1 from the task that factored U_jj)
   for (int j = 0; j < nb - 1; ++j) {
@@ -246,6 +262,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       __syncthreads();
     }
     grid.sync();
+    kf_mark(a, ph);
     // C(j): A_kl -= U_jk^T U_jl for j < k <= l; task 0 is (j+1, j+1) + factor + inverse
     const int m = nb - j - 1;
     const int ntask = m * (m + 1) / 2;
@@ -271,6 +288,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       __syncthreads();
     }
     grid.sync();
+    kf_mark(a, ph);
   }
 
   // ---- back substitution X = U^-1 W, in place in W:  X_i = T_i (W_i - sum_{l>i} U_il X_l)
@@ -284,6 +302,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
     __syncthreads();
   }
   grid.sync();
+  kf_mark(a, ph);
   for (int i = nb - 1; i >= 1; --i) {
     // tasks (l, c), l < i; the l = i-1 tasks (update + solve) are enumerated first
     const int ntask = i * ct;
@@ -310,6 +329,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       __syncthreads();
     }
     grid.sync();
+    kf_mark(a, ph);
   }
 
   // ---- outputs: M (Pi columns) and per-tile sums of squares of U^-1
@@ -351,6 +371,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
     }
   }
   grid.sync();
+  kf_mark(a, ph);
   if (cta == 0 && threadIdx.x == 0) {
     double tr = 0.0;
     for (int t = 0; t < nb * ct; ++t)
@@ -444,7 +465,20 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static unsigned long long* trace = nullptr;
+  const bool tracing = getenv("LVSK_KF_TRACE") != nullptr;
+  if (tracing && trace == nullptr) cudaMalloc(&trace, 1024 * sizeof(unsigned long long));
+  a.trace = tracing ? trace : nullptr;
   cudaError_t e = cudaLaunchKernelEx(&cfg, chol_fold_kernel, a);
   if (e != cudaSuccess) return cuda_status(e, "chol_fold launch");
+  if (tracing) {
+    unsigned long long h[1024];
+    const int nph = 4 + 2 * (P.nb - 1) + P.nb;
+    cudaStreamSynchronize(cfg.stream);
+    cudaMemcpy(h, trace, nph * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "KF d=%lld r=%lld grid=%d phases(us):", (long long)d, (long long)r, grid);
+    for (int i = 1; i < nph; ++i) fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1000.0);
+    fprintf(stderr, "\n");
+  }
   return LVSK_OK;
 }

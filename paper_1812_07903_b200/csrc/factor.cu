@@ -119,7 +119,7 @@ __device__ __forceinline__ void gemm_tile(double* gC, int64_t ldc, const double*
 // (column c, group g) keeps rows g, g+4, .. of its column in registers; one
 // __syncthreads per pivot (the pivot row is published through `rowbuf`).
 // *bad |= 1 on a pivot that is not positive and finite.
-__device__ void chol_inv_tile(double* s, double* t, double* scratch, int32_t* bad) {
+__device__ __noinline__ void chol_inv_tile(double* s, double* t, double* scratch, int32_t* bad) {
   const int c = threadIdx.x & 63, g = threadIdx.x >> 6;
   double* rowbuf = scratch;          // [2][64]
   double* rd = scratch + 2 * FT;     // [64] reciprocal diagonal of U
@@ -133,7 +133,10 @@ __device__ void chol_inv_tile(double* s, double* t, double* scratch, int32_t* ba
     if (g == (p & 3)) rb[c] = a[p >> 2];
     __syncthreads();
     const double piv = rb[p];
-    const double rs = rsqrt(piv);
+    // 1/sqrt(piv): SFU approximation + one Newton step (rel. error ~1e-15)
+    double rs;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(piv));
+    rs = rs * fma(-0.5 * piv, rs * rs, 1.5);
     const double w = rb[c] * (rs * rs);
 #pragma unroll
     for (int i = 0; i < FT / 4; ++i)
@@ -201,30 +204,22 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
   const int cta = blockIdx.x, ncta = gridDim.x;
   const int nb = a.nb;
 
-  // phase 0: working copies (padding: identity on the diagonal, zeros elsewhere)
+  // phase 0: working copies (padding: identity on the diagonal, zeros elsewhere);
+  // one warp per row, no integer division
   {
-    const int64_t dp = a.dp;
-    const int64_t total = dp * dp + dp * a.wc;
-    for (int64_t e = static_cast<int64_t>(cta) * FTHREADS + threadIdx.x; e < total;
-         e += static_cast<int64_t>(ncta) * FTHREADS) {
-      if (e < dp * dp) {
-        const int64_t m = e / dp, c = e - m * dp;
-        double v;
-        if (m < a.d && c < a.d)
-          v = m <= c ? a.G[m * a.ldg + c] : 0.0;
-        else
-          v = m == c ? 1.0 : 0.0;
-        a.A[e] = v;
+    const int64_t dp = a.dp, wc = a.wc;
+    const int64_t rp = static_cast<int64_t>(a.rt) * FT;
+    const int wid = (cta * FTHREADS + threadIdx.x) >> 5, nw = (ncta * FTHREADS) >> 5, lane = threadIdx.x & 31;
+    for (int64_t m = wid; m < 2 * dp; m += nw) {
+      if (m < dp) {
+        double* row = a.A + m * dp;
+        for (int64_t c = lane; c < dp; c += 32)
+          row[c] = (m < a.d && c < a.d) ? (m <= c ? a.G[m * a.ldg + c] : 0.0) : (m == c ? 1.0 : 0.0);
       } else {
-        const int64_t f = e - dp * dp;
-        const int64_t m = f / a.wc, c = f - m * a.wc;
-        const int64_t rp = static_cast<int64_t>(a.rt) * FT;
-        double v;
-        if (c < rp)
-          v = (m < a.d && c < a.r) ? a.Pi[m * a.r + c] : 0.0;
-        else
-          v = (c - rp) == m ? 1.0 : 0.0;
-        a.W[f] = v;
+        const int64_t mm = m - dp;
+        double* row = a.W + mm * wc;
+        for (int64_t c = lane; c < wc; c += 32)
+          row[c] = c < rp ? ((mm < a.d && c < a.r) ? a.Pi[mm * a.r + c] : 0.0) : ((c - rp) == mm ? 1.0 : 0.0);
       }
     }
     if (cta == 0) {

@@ -164,89 +164,99 @@ __global__ void __launch_bounds__(64) csr_ring_kernel(const int64_t* __restrict_
   // element indices are relative to the 16-byte aligned col / val bases
   const int64_t base0 = row_ptr[0] - shift;
   const uint32_t p0 = start[b], p1 = start[b + 1];
-  if (warp == 0) {  // producer
-    if (lane == 0) {
-      uint32_t j = 0;
-      for (uint32_t p = p0; p < p1; ++p) {
-        const uint32_t vv = vals[p];
-        const int64_t r = vv >> 1;
-        const int64_t e0 = row_ptr[r] - base0, e1 = row_ptr[r + 1] - base0;
-        const int64_t a0 = e0 & ~int64_t{3};
-        const int64_t a_end = (e1 + 3) & ~int64_t{3};
-        int64_t s0 = a0;
-        do {
-          const int64_t s1 = s0 + SLOT_ELEMS < a_end ? s0 + SLOT_ELEMS : a_end;
-          const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
-          csr_wait(&empty[slot], ph ^ 1u);
-          SlotMeta m;
-          m.first = static_cast<int32_t>((e0 > s0 ? e0 : s0) - s0);
-          m.last = static_cast<int32_t>((e1 < s1 ? e1 : s1) - s0);
-          m.flags = (vv & 1u) | (s0 == a0 ? 2u : 0u);
-          meta[slot] = m;
-          const uint32_t nb = static_cast<uint32_t>((s1 - s0) * 4);
-          if (nb > 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(csr_smem(&full[slot])),
-                         "r"(2 * nb)
-                         : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    csr_smem(rcol + slot * SLOT_ELEMS)),
-                "l"(col + s0), "r"(nb), "r"(csr_smem(&full[slot]))
-                : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    csr_smem(rval + slot * SLOT_ELEMS)),
-                "l"(val + s0), "r"(nb), "r"(csr_smem(&full[slot]))
-                : "memory");
-          } else {
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[slot])) : "memory");
-          }
-          ++j;
-          s0 = s1;
-        } while (s0 < a_end);
+  if (warp == 0) {  // producer: 32 rows' pointers fetched in parallel, lane 0 issues the copies
+    uint32_t j = 0;
+    for (uint32_t pb = p0; pb < p1; pb += 32) {
+      const uint32_t p = pb + lane;
+      const bool valid = p < p1;
+      const uint32_t vv = valid ? vals[p] : 0u;
+      const int64_t r = vv >> 1;
+      const int64_t e0 = valid ? row_ptr[r] - base0 : 0, e1 = valid ? row_ptr[r + 1] - base0 : 0;
+      const int cnt = p1 - pb < 32u ? static_cast<int>(p1 - pb) : 32;
+      for (int q = 0; q < cnt; ++q) {
+        const int64_t re0 = __shfl_sync(0xFFFFFFFFu, e0, q), re1 = __shfl_sync(0xFFFFFFFFu, e1, q);
+        const uint32_t neg = __shfl_sync(0xFFFFFFFFu, vv, q) & 1u;
+        if (lane == 0) {
+          const int64_t a0 = re0 & ~int64_t{3};
+          const int64_t a_end = (re1 + 3) & ~int64_t{3};
+          int64_t s0 = a0;
+          do {
+            const int64_t s1 = s0 + SLOT_ELEMS < a_end ? s0 + SLOT_ELEMS : a_end;
+            const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
+            csr_wait(&empty[slot], ph ^ 1u);
+            SlotMeta m;
+            m.first = static_cast<int32_t>((re0 > s0 ? re0 : s0) - s0);
+            m.last = static_cast<int32_t>((re1 < s1 ? re1 : s1) - s0);
+            m.flags = neg | (s0 == a0 ? 2u : 0u);
+            meta[slot] = m;
+            const uint32_t nb = static_cast<uint32_t>((s1 - s0) * 4);
+            if (nb > 0) {
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(csr_smem(&full[slot])),
+                           "r"(2 * nb)
+                           : "memory");
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      csr_smem(rcol + slot * SLOT_ELEMS)),
+                  "l"(col + s0), "r"(nb), "r"(csr_smem(&full[slot]))
+                  : "memory");
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      csr_smem(rval + slot * SLOT_ELEMS)),
+                  "l"(val + s0), "r"(nb), "r"(csr_smem(&full[slot]))
+                  : "memory");
+            } else {
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[slot])) : "memory");
+            }
+            ++j;
+            s0 = s1;
+          } while (s0 < a_end);
+        }
       }
     }
-  } else {  // consumer
+    if (lane == 0) {  // end-of-stream marker
+      const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
+      csr_wait(&empty[slot], ph ^ 1u);
+      SlotMeta m;
+      m.first = m.last = 0;
+      m.flags = 4u;
+      meta[slot] = m;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[slot])) : "memory");
+    }
+  } else {  // consumer: slots in order until the end marker (row starts carry flag bit 1)
     int bad = 0;
-    uint32_t j = 0;
-    for (uint32_t p = p0; p < p1; ++p) {
-      const int64_t r = vals[p] >> 1;
-      const int64_t e0 = row_ptr[r] - base0, e1 = row_ptr[r + 1] - base0;
-      const int64_t a0 = e0 & ~int64_t{3};
-      const int64_t a_end = (e1 + 3) & ~int64_t{3};
-      const int64_t npieces = a_end > a0 ? (a_end - a0 + SLOT_ELEMS - 1) / SLOT_ELEMS : 1;
-      int32_t prev_last = -1;
-      for (int64_t q = 0; q < npieces; ++q, ++j) {
-        const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
-        csr_wait(&full[slot], ph);
-        const SlotMeta m = meta[slot];
-        const double sg = (m.flags & 1u) ? -scale : scale;
+    int32_t prev_last = -1;
+    for (uint32_t j = 0;; ++j) {
+      const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
+      csr_wait(&full[slot], ph);
+      const SlotMeta m = meta[slot];
+      if (m.flags & 4u) break;
+      if (m.flags & 2u) prev_last = -1;
+      const double sg = (m.flags & 1u) ? -scale : scale;
 #pragma unroll
-        for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
-          const int idx = h * 32 + lane;
-          const bool live = idx >= m.first && idx < m.last;
-          const int32_t c = live ? rcol[slot * SLOT_ELEMS + idx] : INT32_MAX;
-          const float x = live ? rval[slot * SLOT_ELEMS + idx] : 0.f;
-          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-          const bool prev_live = lane > 0 && (idx - 1) >= m.first;
-          const int32_t before = prev_live ? cprev : prev_last;
-          if (live) {
-            if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
-            if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
-            const int64_t lc = static_cast<int64_t>(c) - c0;
-            if (lc >= 0 && lc < width) {
-              double su, er;
-              two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(x)), su, er);
-              hi[lc] = su;
-              lo[lc] = __dadd_rn(lo[lc], er);
-            }
+      for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
+        const int idx = h * 32 + lane;
+        const bool live = idx >= m.first && idx < m.last;
+        const int32_t c = live ? rcol[slot * SLOT_ELEMS + idx] : INT32_MAX;
+        const float x = live ? rval[slot * SLOT_ELEMS + idx] : 0.f;
+        const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+        const bool prev_live = lane > 0 && (idx - 1) >= m.first;
+        const int32_t before = prev_live ? cprev : prev_last;
+        if (live) {
+          if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
+          if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
+          const int64_t lc = static_cast<int64_t>(c) - c0;
+          if (lc >= 0 && lc < width) {
+            double su, er;
+            two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(x)), su, er);
+            hi[lc] = su;
+            lo[lc] = __dadd_rn(lo[lc], er);
           }
-          const uint32_t lm = __ballot_sync(0xFFFFFFFFu, live);
-          if (lm) prev_last = __shfl_sync(0xFFFFFFFFu, c, 31 - __clz(lm));
         }
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&empty[slot])) : "memory");
+        const uint32_t lm = __ballot_sync(0xFFFFFFFFu, live);
+        if (lm) prev_last = __shfl_sync(0xFFFFFFFFu, c, 31 - __clz(lm));
       }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&empty[slot])) : "memory");
     }
     const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
     if (any && lane == 0) atomicOr(flags, any);

@@ -106,10 +106,12 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 // K2 ring variant (default for float32 values): one CTA owns one (bucket, <= 4096-column group) with its
 // float64 (hi, lo) slice in shared memory; a producer warp streams the
 // bucket's CSR row pieces (16-byte aligned supersets, <= 64 entries each;
-// rounding out to 16-byte granules never leaves the allocation's page)
+// rounding out to 16-byte granules never leaves the allocation's page) into a
+// 32-slot ring; four consumer warps each apply one quarter of the columns
 // into a 64-slot ring with cp.async.bulk, so ~100 rows are in flight per CTA;
 // a consumer warp applies them in ascending row order.
-constexpr int RING_SLOTS = 64;
+constexpr int RING_SLOTS = 32;
+constexpr int RING_CONSUMERS = 4;  // consumer warps, each owning a quarter of the column group
 constexpr int SLOT_ELEMS = 64;
 constexpr int RING_GROUP = 4096;
 
@@ -131,7 +133,7 @@ __device__ __forceinline__ void csr_wait(uint64_t* b, uint32_t parity) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(64) csr_ring_kernel(const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(32 * (1 + RING_CONSUMERS)) csr_ring_kernel(const int64_t* __restrict__ row_ptr,
                                                       const int32_t* __restrict__ col, const float* __restrict__ val,
                                                       int64_t shift, int64_t d, int ngroups, const uint32_t* __restrict__ vals,
                                                       const uint32_t* __restrict__ start, double scale,
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(64) csr_ring_kernel(const int64_t* __restrict_
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING_SLOTS; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_smem(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_smem(&empty[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&empty[s])), "r"(RING_CONSUMERS));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -222,7 +224,12 @@ __global__ void __launch_bounds__(64) csr_ring_kernel(const int64_t* __restrict_
       meta[slot] = m;
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[slot])) : "memory");
     }
-  } else {  // consumer: slots in order until the end marker (row starts carry flag bit 1)
+  } else {  // consumers: slots in order until the end marker (row starts carry flag bit 1);
+           // warp w applies the columns [w, w+1) * RING_GROUP / RING_CONSUMERS of the group,
+           // warp 1 also validates every entry
+    const int cw = warp - 1;
+    const int64_t lo_c = static_cast<int64_t>(cw) * (RING_GROUP / RING_CONSUMERS);
+    const int64_t hi_c = lo_c + RING_GROUP / RING_CONSUMERS;
     int bad = 0;
     int32_t prev_last = -1;
     for (uint32_t j = 0;; ++j) {
@@ -232,31 +239,56 @@ __global__ void __launch_bounds__(64) csr_ring_kernel(const int64_t* __restrict_
       if (m.flags & 4u) break;
       if (m.flags & 2u) prev_last = -1;
       const double sg = (m.flags & 1u) ? -scale : scale;
+      int32_t c[SLOT_ELEMS / 32];
+      float x[SLOT_ELEMS / 32];
+      bool live[SLOT_ELEMS / 32];
 #pragma unroll
       for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
         const int idx = h * 32 + lane;
-        const bool live = idx >= m.first && idx < m.last;
-        const int32_t c = live ? rcol[slot * SLOT_ELEMS + idx] : INT32_MAX;
-        const float x = live ? rval[slot * SLOT_ELEMS + idx] : 0.f;
-        const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-        const bool prev_live = lane > 0 && (idx - 1) >= m.first;
-        const int32_t before = prev_live ? cprev : prev_last;
-        if (live) {
-          if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
-          if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
-          const int64_t lc = static_cast<int64_t>(c) - c0;
-          if (lc >= 0 && lc < width) {
-            double su, er;
-            two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(x)), su, er);
-            hi[lc] = su;
-            lo[lc] = __dadd_rn(lo[lc], er);
-          }
-        }
-        const uint32_t lm = __ballot_sync(0xFFFFFFFFu, live);
-        if (lm) prev_last = __shfl_sync(0xFFFFFFFFu, c, 31 - __clz(lm));
+        live[h] = idx >= m.first && idx < m.last;
+        c[h] = live[h] ? rcol[slot * SLOT_ELEMS + idx] : INT32_MAX;
+        x[h] = live[h] ? rval[slot * SLOT_ELEMS + idx] : 0.f;
       }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&empty[slot])) : "memory");
+      if (cw == 0) {
+#pragma unroll
+        for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
+          const int idx = h * 32 + lane;
+          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c[h], 1);
+          const bool prev_live = lane > 0 && (idx - 1) >= m.first;
+          const int32_t before = prev_live ? cprev : prev_last;
+          if (live[h]) {
+            if (c[h] < 0 || c[h] >= d || c[h] <= before) bad |= LVSK_FLAG_BADINDEX;
+            if (!isfinite(x[h])) bad |= LVSK_FLAG_NONFINITE;
+          }
+          const uint32_t lm = __ballot_sync(0xFFFFFFFFu, live[h]);
+          if (lm) prev_last = __shfl_sync(0xFFFFFFFFu, c[h], 31 - __clz(lm));
+        }
+      }
+      // the entries of one row have distinct columns: both halves' updates are independent
+      double hv[SLOT_ELEMS / 32], lv[SLOT_ELEMS / 32];
+      int64_t lc[SLOT_ELEMS / 32];
+      bool mine[SLOT_ELEMS / 32];
+#pragma unroll
+      for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
+        lc[h] = static_cast<int64_t>(c[h]) - c0;
+        mine[h] = live[h] && lc[h] >= lo_c && lc[h] < hi_c && lc[h] < width;
+        if (mine[h]) {
+          hv[h] = hi[lc[h]];
+          lv[h] = lo[lc[h]];
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
+        if (mine[h]) {
+          double su, er;
+          two_sum(hv[h], __dmul_rn(sg, static_cast<double>(x[h])), su, er);
+          hi[lc[h]] = su;
+          lo[lc[h]] = __dadd_rn(lv[h], er);
+        }
+      }
+      __syncwarp();  // the next row may update the same columns from other lanes
     }
     const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
     if (any && lane == 0) atomicOr(flags, any);
@@ -414,7 +446,7 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
       cudaFuncSetAttribute(csr_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
       rattr = true;
     }
-    csr_ring_kernel<<<static_cast<unsigned>(k * rgroups), 64, rsmem, st>>>(
+    csr_ring_kernel<<<static_cast<unsigned>(k * rgroups), 32 * (1 + RING_CONSUMERS), rsmem, st>>>(
         row_ptr, col - mis / 4, static_cast<const float*>(val) - mis / 4, mis / 4, d, rgroups, svals, start, scale, hi_in, lo_in, hi_out, lo_out,
         flags);
   } else if (val_dtype == LVSK_F32)

@@ -103,201 +103,206 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K2 ring variant (default for float32 values): one CTA owns one (bucket, <= 4096-column group) with its
-// float64 (hi, lo) slice in shared memory; a producer warp streams the
-// bucket's CSR row pieces (16-byte aligned supersets, <= 64 entries each;
-// rounding out to 16-byte granules never leaves the allocation's page) into a
-// 32-slot ring; four consumer warps each apply one quarter of the columns
-// into a 64-slot ring with cp.async.bulk, so ~100 rows are in flight per CTA;
-// a consumer warp applies them in ascending row order.
-constexpr int RING_SLOTS = 32;
-constexpr int RING_CONSUMERS = 4;  // consumer warps, each owning a quarter of the column group
-constexpr int SLOT_ELEMS = 64;
-constexpr int RING_GROUP = 4096;
+// K2 staged variant (default): one CTA (8 warps) owns one (bucket, <= 4096-
+// column group) with its float64 (hi, lo) slice in shared memory (64 KB).
+// The bucket's rows are staged in chunks of <= 64 rows / 2048 entries: warp 0
+// plans a chunk from 32 rows' pointers fetched in parallel (rows longer than
+// the buffer are split into segments, which is harmless: one row's entries
+// have distinct columns), all warps copy it with cp.async (LDGSTS) into one of
+// two buffers while the previous chunk is applied; the apply walks the rows
+// in ascending index and warp w applies the entries of its 512 columns
+// (TwoSum into hi / lo), the validation (strictly increasing in-range columns,
+// finite values) is spread over the warps by row.
+constexpr int SG_COLS = 4096;
+constexpr int SG_WARPS = 8;
+constexpr int SG_ECAP = 2048;  // entries per staging buffer
+constexpr int SG_RMAX = 64;    // rows (segments) per staging buffer
 
-struct SlotMeta {
-  int32_t first, last;  // valid element range inside the slot
-  uint32_t flags;       // bit0: negative sign, bit1: first piece of its row
+struct SegInfo {
+  int64_t src;      // first entry (relative to base0)
+  int32_t off, len;  // position in the buffer, entry count
+  int32_t flags;     // bit0 negative sign, bit1 continuation of the previous segment's row
 };
 
 __device__ __forceinline__ uint32_t csr_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void csr_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "CW_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra.uni CW_%=;\n}" ::"r"(csr_smem(b)),
-      "r"(parity)
-      : "memory");
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(csr_smem(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(csr_smem(dst)), "l"(src) : "memory");
 }
 
-__global__ void __launch_bounds__(32 * (1 + RING_CONSUMERS)) csr_ring_kernel(const int64_t* __restrict__ row_ptr,
-                                                      const int32_t* __restrict__ col, const float* __restrict__ val,
-                                                      int64_t shift, int64_t d, int ngroups, const uint32_t* __restrict__ vals,
-                                                      const uint32_t* __restrict__ start, double scale,
-                                                      const double* hi_in, const double* lo_in, double* hi_out,
-                                                      double* lo_out, int32_t* flags) {
-  extern __shared__ __align__(128) uint8_t csr_ring_smem[];
-  double* hi = reinterpret_cast<double*>(csr_ring_smem);
-  double* lo = hi + RING_GROUP;
-  int32_t* rcol = reinterpret_cast<int32_t*>(lo + RING_GROUP);     // [RING_SLOTS][SLOT_ELEMS]
-  float* rval = reinterpret_cast<float*>(rcol + RING_SLOTS * SLOT_ELEMS);
-  SlotMeta* meta = reinterpret_cast<SlotMeta*>(rval + RING_SLOTS * SLOT_ELEMS);
-  uint64_t* full = reinterpret_cast<uint64_t*>(meta + RING_SLOTS);
-  uint64_t* empty = full + RING_SLOTS;
-  const int64_t b = blockIdx.x / ngroups;
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x - b * ngroups) * RING_GROUP;
-  const int64_t width = d - c0 < RING_GROUP ? d - c0 : RING_GROUP;
+template <typename V>
+__global__ void __launch_bounds__(32 * SG_WARPS) csr_staged_kernel(
+    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const V* __restrict__ val, int64_t d,
+    int ngroups, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ start, double scale,
+    const double* hi_in, const double* lo_in, double* hi_out, double* lo_out, int32_t* flags) {
+  extern __shared__ __align__(128) uint8_t sg_smem[];
+  double* hi = reinterpret_cast<double*>(sg_smem);
+  double* lo = hi + SG_COLS;
+  V* bval = reinterpret_cast<V*>(lo + SG_COLS);                       // [2][SG_ECAP]
+  int32_t* bcol = reinterpret_cast<int32_t*>(bval + 2 * SG_ECAP);     // [2][SG_ECAP]
+  SegInfo* seg = reinterpret_cast<SegInfo*>(bcol + 2 * SG_ECAP);      // [2][SG_RMAX]
+  __shared__ int nseg_s[2];
+  __shared__ int more_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < RING_SLOTS; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_smem(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&empty[s])), "r"(RING_CONSUMERS));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  const int64_t b = blockIdx.x / ngroups;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x - b * ngroups) * SG_COLS;
+  const int64_t width = d - c0 < SG_COLS ? d - c0 : SG_COLS;
   for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
     hi[c] = hi_in[b * d + c0 + c];
     lo[c] = lo_in[b * d + c0 + c];
   }
-  __syncthreads();
-  // element indices are relative to the 16-byte aligned col / val bases
-  const int64_t base0 = row_ptr[0] - shift;
+  const int64_t base0 = row_ptr[0];
   const uint32_t p0 = start[b], p1 = start[b + 1];
-  if (warp == 0) {  // producer: 32 rows' pointers fetched in parallel, lane 0 issues the copies
-    uint32_t j = 0;
-    for (uint32_t pb = p0; pb < p1; pb += 32) {
-      const uint32_t p = pb + lane;
-      const bool valid = p < p1;
-      const uint32_t vv = valid ? vals[p] : 0u;
-      const int64_t r = vv >> 1;
-      const int64_t e0 = valid ? row_ptr[r] - base0 : 0, e1 = valid ? row_ptr[r + 1] - base0 : 0;
-      const int cnt = p1 - pb < 32u ? static_cast<int>(p1 - pb) : 32;
-      for (int q = 0; q < cnt; ++q) {
-        const int64_t re0 = __shfl_sync(0xFFFFFFFFu, e0, q), re1 = __shfl_sync(0xFFFFFFFFu, e1, q);
-        const uint32_t neg = __shfl_sync(0xFFFFFFFFu, vv, q) & 1u;
+
+  // ---- planner state (warp 0): a batch of 32 prefetched rows + the row in progress
+  uint32_t pb = p0;        // first row of the prefetched batch
+  int bq = 32;             // next batch slot to consume (32 = batch empty)
+  int64_t e0 = 0, e1 = 0;  // this lane's batch row
+  uint32_t vv = 0;
+  int64_t cur = 0, cur_end = 0;  // segment cursor of the row in progress (lane-uniform)
+  uint32_t cur_neg = 0;
+  bool cur_live = false, cont = false;
+
+  auto plan = [&](int buf) -> int {  // warp 0 only; returns the number of segments
+    int ns = 0, ne = 0;
+    while (ns < SG_RMAX && ne < SG_ECAP) {
+      if (!cur_live) {
+        if (bq == 32) {
+          if (pb >= p1) break;
+          const uint32_t p = pb + lane;
+          const bool valid = p < p1;
+          vv = valid ? vals[p] : 0u;
+          const int64_t r = vv >> 1;
+          e0 = valid ? row_ptr[r] - base0 : 0;
+          e1 = valid ? row_ptr[r + 1] - base0 : 0;
+          bq = 0;
+        }
+        const uint32_t p = pb + bq;
+        if (p >= p1) break;
+        cur = __shfl_sync(0xFFFFFFFFu, e0, bq);
+        cur_end = __shfl_sync(0xFFFFFFFFu, e1, bq);
+        cur_neg = __shfl_sync(0xFFFFFFFFu, vv, bq) & 1u;
+        cur_live = true;
+        cont = false;
+        if (++bq == 32) pb += 32;
+      }
+      const int64_t room = SG_ECAP - ne;
+      const int64_t len = cur_end - cur < room ? cur_end - cur : room;
+      if (len == 0 && cur_end > cur) break;  // buffer full
+      if (lane == 0) {
+        SegInfo si;
+        si.src = cur;
+        si.off = ne;
+        si.len = static_cast<int32_t>(len);
+        si.flags = static_cast<int32_t>(cur_neg | (cont ? 2u : 0u));
+        seg[buf * SG_RMAX + ns] = si;
+      }
+      ++ns;
+      ne += static_cast<int>(len);
+      cur += len;
+      if (cur >= cur_end) {
+        cur_live = false;
+      } else {
+        cont = true;
+      }
+    }
+    return ns;
+  };
+  auto issue = [&](int buf, int ns) {  // all warps: copy the planned segments
+    for (int q = warp; q < ns; q += SG_WARPS) {
+      const SegInfo si = seg[buf * SG_RMAX + q];
+      for (int e = lane; e < si.len; e += 32) {
+        cp_async4(bcol + buf * SG_ECAP + si.off + e, col + si.src + e);
+        if constexpr (sizeof(V) == 8)
+          cp_async8(bval + buf * SG_ECAP + si.off + e, val + si.src + e);
+        else
+          cp_async4(bval + buf * SG_ECAP + si.off + e, val + si.src + e);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  if (warp == 0) {
+    const int ns = plan(0);
+    if (lane == 0) {
+      nseg_s[0] = ns;
+      more_s = cur_live || (pb + (bq == 32 ? 0 : bq)) < p1;
+    }
+  }
+  __syncthreads();
+  issue(0, nseg_s[0]);
+  int bad = 0;
+  int32_t lastcol = -1;  // last column of the previous chunk (a row continued across chunks)
+  const int64_t lo_c = static_cast<int64_t>(warp) * (SG_COLS / SG_WARPS), hi_c = lo_c + SG_COLS / SG_WARPS;
+  for (int it = 0;; ++it) {
+    const int buf = it & 1;
+    const bool more = more_s;
+    __syncthreads();  // every thread has read more_s / nseg_s before the planner rewrites them
+    if (more) {
+      if (warp == 0) {
+        const int ns = plan(buf ^ 1);
         if (lane == 0) {
-          const int64_t a0 = re0 & ~int64_t{3};
-          const int64_t a_end = (re1 + 3) & ~int64_t{3};
-          int64_t s0 = a0;
-          do {
-            const int64_t s1 = s0 + SLOT_ELEMS < a_end ? s0 + SLOT_ELEMS : a_end;
-            const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
-            csr_wait(&empty[slot], ph ^ 1u);
-            SlotMeta m;
-            m.first = static_cast<int32_t>((re0 > s0 ? re0 : s0) - s0);
-            m.last = static_cast<int32_t>((re1 < s1 ? re1 : s1) - s0);
-            m.flags = neg | (s0 == a0 ? 2u : 0u);
-            meta[slot] = m;
-            const uint32_t nb = static_cast<uint32_t>((s1 - s0) * 4);
-            if (nb > 0) {
-              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(csr_smem(&full[slot])),
-                           "r"(2 * nb)
-                           : "memory");
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                      csr_smem(rcol + slot * SLOT_ELEMS)),
-                  "l"(col + s0), "r"(nb), "r"(csr_smem(&full[slot]))
-                  : "memory");
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                      csr_smem(rval + slot * SLOT_ELEMS)),
-                  "l"(val + s0), "r"(nb), "r"(csr_smem(&full[slot]))
-                  : "memory");
-            } else {
-              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[slot])) : "memory");
-            }
-            ++j;
-            s0 = s1;
-          } while (s0 < a_end);
+          nseg_s[buf ^ 1] = ns;
+          more_s = cur_live || (pb + (bq == 32 ? 0 : bq)) < p1;
         }
       }
+      __syncthreads();
+      issue(buf ^ 1, nseg_s[buf ^ 1]);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    if (lane == 0) {  // end-of-stream marker
-      const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
-      csr_wait(&empty[slot], ph ^ 1u);
-      SlotMeta m;
-      m.first = m.last = 0;
-      m.flags = 4u;
-      meta[slot] = m;
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[slot])) : "memory");
-    }
-  } else {  // consumers: slots in order until the end marker (row starts carry flag bit 1);
-           // warp w applies the columns [w, w+1) * RING_GROUP / RING_CONSUMERS of the group,
-           // warp 1 also validates every entry
-    const int cw = warp - 1;
-    const int64_t lo_c = static_cast<int64_t>(cw) * (RING_GROUP / RING_CONSUMERS);
-    const int64_t hi_c = lo_c + RING_GROUP / RING_CONSUMERS;
-    int bad = 0;
-    int32_t prev_last = -1;
-    for (uint32_t j = 0;; ++j) {
-      const uint32_t slot = j % RING_SLOTS, ph = (j / RING_SLOTS) & 1u;
-      csr_wait(&full[slot], ph);
-      const SlotMeta m = meta[slot];
-      if (m.flags & 4u) break;
-      if (m.flags & 2u) prev_last = -1;
-      const double sg = (m.flags & 1u) ? -scale : scale;
-      int32_t c[SLOT_ELEMS / 32];
-      float x[SLOT_ELEMS / 32];
-      bool live[SLOT_ELEMS / 32];
-#pragma unroll
-      for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
-        const int idx = h * 32 + lane;
-        live[h] = idx >= m.first && idx < m.last;
-        c[h] = live[h] ? rcol[slot * SLOT_ELEMS + idx] : INT32_MAX;
-        x[h] = live[h] ? rval[slot * SLOT_ELEMS + idx] : 0.f;
-      }
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&empty[slot])) : "memory");
-      if (cw == 0) {
-#pragma unroll
-        for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
-          const int idx = h * 32 + lane;
-          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c[h], 1);
-          const bool prev_live = lane > 0 && (idx - 1) >= m.first;
-          const int32_t before = prev_live ? cprev : prev_last;
-          if (live[h]) {
-            if (c[h] < 0 || c[h] >= d || c[h] <= before) bad |= LVSK_FLAG_BADINDEX;
-            if (!isfinite(x[h])) bad |= LVSK_FLAG_NONFINITE;
-          }
-          const uint32_t lm = __ballot_sync(0xFFFFFFFFu, live[h]);
-          if (lm) prev_last = __shfl_sync(0xFFFFFFFFu, c[h], 31 - __clz(lm));
-        }
-      }
-      // the entries of one row have distinct columns: both halves' updates are independent
-      double hv[SLOT_ELEMS / 32], lv[SLOT_ELEMS / 32];
-      int64_t lc[SLOT_ELEMS / 32];
-      bool mine[SLOT_ELEMS / 32];
-#pragma unroll
-      for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
-        lc[h] = static_cast<int64_t>(c[h]) - c0;
-        mine[h] = live[h] && lc[h] >= lo_c && lc[h] < hi_c && lc[h] < width;
-        if (mine[h]) {
-          hv[h] = hi[lc[h]];
-          lv[h] = lo[lc[h]];
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < SLOT_ELEMS / 32; ++h) {
-        if (mine[h]) {
+    __syncthreads();  // chunk `it` has landed for every thread's copies
+    const int ns = nseg_s[buf];
+    const V* vb = bval + buf * SG_ECAP;
+    const int32_t* cb = bcol + buf * SG_ECAP;
+    for (int q = 0; q < ns; ++q) {
+      const SegInfo si = seg[buf * SG_RMAX + q];
+      const double sg = (si.flags & 1) ? -scale : scale;
+      for (int e = lane; e < si.len; e += 32) {
+        const int64_t lc = static_cast<int64_t>(cb[si.off + e]) - c0;
+        if (lc >= lo_c && lc < hi_c && lc < width) {
           double su, er;
-          two_sum(hv[h], __dmul_rn(sg, static_cast<double>(x[h])), su, er);
-          hi[lc[h]] = su;
-          lo[lc[h]] = __dadd_rn(lv[h], er);
+          two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(vb[si.off + e])), su, er);
+          hi[lc] = su;
+          lo[lc] = __dadd_rn(lo[lc], er);
         }
       }
-      __syncwarp();  // the next row may update the same columns from other lanes
+      __syncwarp();  // the next row may hit the same columns from other lanes
+      if (q % SG_WARPS == warp) {  // validation of this segment
+        int32_t carry = (si.flags & 2) ? (q > 0 ? cb[si.off - 1] : lastcol) : -1;
+        for (int e0v = 0; e0v < si.len; e0v += 32) {
+          const int e = e0v + lane;
+          const bool live = e < si.len;
+          const int32_t c = live ? cb[si.off + e] : INT32_MAX;
+          const double x = live ? static_cast<double>(vb[si.off + e]) : 0.0;
+          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+          const int32_t before = lane == 0 ? carry : cprev;
+          if (live) {
+            if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
+            if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
+          }
+          carry = __shfl_sync(0xFFFFFFFFu, c, 31);
+        }
+      }
     }
-    const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
-    if (any && lane == 0) atomicOr(flags, any);
+    if (ns > 0) {
+      const SegInfo sl = seg[buf * SG_RMAX + ns - 1];
+      if (sl.len > 0) lastcol = cb[sl.off + sl.len - 1];
+    }
+    if (!more) break;
   }
   __syncthreads();
   for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
     hi_out[b * d + c0 + c] = hi[c];
     lo_out[b * d + c0 + c] = lo[c];
   }
+  const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (any && lane == 0) atomicOr(flags, any);
 }
 
 // K6: one warp per row, lane owns RPL = r/32 consecutive columns of u
@@ -431,24 +436,27 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
     cudaFuncSetAttribute(csr_gather_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  // the ring reads 16-byte aligned supersets of each row; col and val must
-  // share their misalignment so one element index addresses both
-  const int mis = static_cast<int>(reinterpret_cast<uintptr_t>(col) % 16);
-  const bool ring = val_dtype == LVSK_F32 && mis % 4 == 0 &&
-                    mis == static_cast<int>(reinterpret_cast<uintptr_t>(val) % 16) &&
-                    getenv("LVSK_K2_SIMPLE") == nullptr;
-  if (ring) {
-    const int rgroups = static_cast<int>((d + RING_GROUP - 1) / RING_GROUP);
-    const int rsmem = 2 * RING_GROUP * 8 + RING_SLOTS * SLOT_ELEMS * 8 + RING_SLOTS * static_cast<int>(sizeof(SlotMeta)) +
-                      2 * RING_SLOTS * 8;
-    static bool rattr = false;
-    if (!rattr) {
-      cudaFuncSetAttribute(csr_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
-      rattr = true;
+  if (getenv("LVSK_K2_SIMPLE") == nullptr) {
+    const int sgroups = static_cast<int>((d + SG_COLS - 1) / SG_COLS);
+    const int vsz = val_dtype == LVSK_F64 ? 8 : 4;
+    const int ssmem = 2 * SG_COLS * 8 + 2 * SG_ECAP * (vsz + 4) + 2 * SG_RMAX * static_cast<int>(sizeof(SegInfo));
+    static bool sattr = false;
+    if (!sattr) {
+      cudaFuncSetAttribute(csr_staged_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           2 * SG_COLS * 8 + 2 * SG_ECAP * 8 + 2 * SG_RMAX * static_cast<int>(sizeof(SegInfo)));
+      cudaFuncSetAttribute(csr_staged_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           2 * SG_COLS * 8 + 2 * SG_ECAP * 12 + 2 * SG_RMAX * static_cast<int>(sizeof(SegInfo)));
+      sattr = true;
     }
-    csr_ring_kernel<<<static_cast<unsigned>(k * rgroups), 32 * (1 + RING_CONSUMERS), rsmem, st>>>(
-        row_ptr, col - mis / 4, static_cast<const float*>(val) - mis / 4, mis / 4, d, rgroups, svals, start, scale, hi_in, lo_in, hi_out, lo_out,
-        flags);
+    const unsigned sgrid = static_cast<unsigned>(k * sgroups);
+    if (val_dtype == LVSK_F32)
+      csr_staged_kernel<float><<<sgrid, 32 * SG_WARPS, ssmem, st>>>(row_ptr, col, static_cast<const float*>(val), d,
+                                                                   sgroups, svals, start, scale, hi_in, lo_in,
+                                                                   hi_out, lo_out, flags);
+    else
+      csr_staged_kernel<double><<<sgrid, 32 * SG_WARPS, ssmem, st>>>(row_ptr, col, static_cast<const double*>(val),
+                                                                    d, sgroups, svals, start, scale, hi_in, lo_in,
+                                                                    hi_out, lo_out, flags);
   } else if (val_dtype == LVSK_F32)
     csr_gather_kernel<float><<<grid, 32 * CSR_WARPS, smem, st>>>(row_ptr, col, static_cast<const float*>(val), d,
                                                               ngroups, svals, start, units, scale, hi_in, lo_in,

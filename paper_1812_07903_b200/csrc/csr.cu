@@ -103,25 +103,27 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K2 staged variant (default): one CTA (8 warps) owns one (bucket, <= 4096-
-// column group) with its float64 (hi, lo) slice in shared memory (64 KB).
-// The bucket's rows are staged in chunks of <= 64 rows / 2048 entries: warp 0
-// plans a chunk from 32 rows' pointers fetched in parallel (rows longer than
-// the buffer are split into segments, which is harmless: one row's entries
-// have distinct columns), all warps copy it with cp.async (LDGSTS) into one of
-// two buffers while the previous chunk is applied; the apply walks the rows
-// in ascending index and warp w applies the entries of its 512 columns
-// (TwoSum into hi / lo), the validation (strictly increasing in-range columns,
-// finite values) is spread over the warps by row.
-constexpr int SG_COLS = 4096;
-constexpr int SG_WARPS = 8;
-constexpr int SG_ECAP = 2048;  // entries per staging buffer
-constexpr int SG_RMAX = 64;    // rows (segments) per staging buffer
+// K2 streaming variant (default).  csr_prep_kernel turns the bucket-sorted
+// (row, sign) pairs into per-pair (source offset, length) so nothing
+// downstream chases row pointers.  csr_stream_kernel: one CTA owns one
+// (bucket, <= 4096-column group) with its float64 (hi, lo) slice in shared
+// memory (64 KB); warp 0 streams the bucket's rows in chunks (<= 64 row
+// segments / 1024 entries; longer rows are split, harmless since one row's
+// entries have distinct columns) with cp.async into a 4-deep ring signalled
+// by cp.async.mbarrier.arrive; warps 1..8 apply the chunks in row order,
+// warp w taking the entries of its 512 columns (TwoSum into hi / lo), and
+// validate (strictly increasing in-range columns, finite values) the
+// segments assigned to them.
+constexpr int ST_COLS = 4096;
+constexpr int ST_APPLY = 8;  // applier warps
+constexpr int ST_ECAP = 1024;
+constexpr int ST_RMAX = 64;
+constexpr int ST_STAGES = 4;
 
 struct SegInfo {
-  int64_t src;      // first entry (relative to base0)
-  int32_t off, len;  // position in the buffer, entry count
-  int32_t flags;     // bit0 negative sign, bit1 continuation of the previous segment's row
+  int32_t off, len;  // position in the stage buffer, entry count
+  int32_t flags;     // bit0 negative sign, bit1 continuation of the previous segment's row, bit2 end of stream
+  int32_t pad;
 };
 
 __device__ __forceinline__ uint32_t csr_smem(const void* p) {
@@ -133,176 +135,188 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(csr_smem(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void st_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni SW_%=;\n}" ::"r"(csr_smem(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void csr_prep_kernel(const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ svals, int64_t N,
+                                int64_t* __restrict__ msrc, int32_t* __restrict__ mlen) {
+  const int64_t base0 = row_ptr[0];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = svals[i] >> 1;
+    const int64_t e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    msrc[i] = e0 - base0;
+    mlen[i] = static_cast<int32_t>(e1 - e0);
+  }
+}
 
 template <typename V>
-__global__ void __launch_bounds__(32 * SG_WARPS) csr_staged_kernel(
-    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const V* __restrict__ val, int64_t d,
-    int ngroups, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ start, double scale,
-    const double* hi_in, const double* lo_in, double* hi_out, double* lo_out, int32_t* flags) {
-  extern __shared__ __align__(128) uint8_t sg_smem[];
-  double* hi = reinterpret_cast<double*>(sg_smem);
-  double* lo = hi + SG_COLS;
-  V* bval = reinterpret_cast<V*>(lo + SG_COLS);                       // [2][SG_ECAP]
-  int32_t* bcol = reinterpret_cast<int32_t*>(bval + 2 * SG_ECAP);     // [2][SG_ECAP]
-  SegInfo* seg = reinterpret_cast<SegInfo*>(bcol + 2 * SG_ECAP);      // [2][SG_RMAX]
-  __shared__ int nseg_s[2];
-  __shared__ int more_s;
+__global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
+    const int32_t* __restrict__ col, const V* __restrict__ val, int64_t d, int ngroups,
+    const uint32_t* __restrict__ svals, const int64_t* __restrict__ msrc, const int32_t* __restrict__ mlen,
+    const uint32_t* __restrict__ start, double scale, const double* hi_in, const double* lo_in, double* hi_out,
+    double* lo_out, int32_t* flags) {
+  extern __shared__ __align__(128) uint8_t st_smem[];
+  double* hi = reinterpret_cast<double*>(st_smem);
+  double* lo = hi + ST_COLS;
+  V* bval = reinterpret_cast<V*>(lo + ST_COLS);                          // [ST_STAGES][ST_ECAP]
+  int32_t* bcol = reinterpret_cast<int32_t*>(bval + ST_STAGES * ST_ECAP);  // [ST_STAGES][ST_ECAP]
+  SegInfo* seg = reinterpret_cast<SegInfo*>(bcol + ST_STAGES * ST_ECAP);  // [ST_STAGES][ST_RMAX]
+  int32_t* nseg = reinterpret_cast<int32_t*>(seg + ST_STAGES * ST_RMAX);  // [ST_STAGES]
+  uint64_t* full = reinterpret_cast<uint64_t*>(nseg + ST_STAGES);         // 8-aligned: ST_STAGES even
+  uint64_t* empty = full + ST_STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = blockIdx.x / ngroups;
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x - b * ngroups) * SG_COLS;
-  const int64_t width = d - c0 < SG_COLS ? d - c0 : SG_COLS;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x - b * ngroups) * ST_COLS;
+  const int64_t width = d - c0 < ST_COLS ? d - c0 : ST_COLS;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST_STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&full[s])), "r"(33));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&empty[s])), "r"(ST_APPLY));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
     hi[c] = hi_in[b * d + c0 + c];
     lo[c] = lo_in[b * d + c0 + c];
   }
-  const int64_t base0 = row_ptr[0];
+  __syncthreads();
   const uint32_t p0 = start[b], p1 = start[b + 1];
-
-  // ---- planner state (warp 0): a batch of 32 prefetched rows + the row in progress
-  uint32_t pb = p0;        // first row of the prefetched batch
-  int bq = 32;             // next batch slot to consume (32 = batch empty)
-  int64_t e0 = 0, e1 = 0;  // this lane's batch row
-  uint32_t vv = 0;
-  int64_t cur = 0, cur_end = 0;  // segment cursor of the row in progress (lane-uniform)
-  uint32_t cur_neg = 0;
-  bool cur_live = false, cont = false;
-
-  auto plan = [&](int buf) -> int {  // warp 0 only; returns the number of segments
-    int ns = 0, ne = 0;
-    while (ns < SG_RMAX && ne < SG_ECAP) {
-      if (!cur_live) {
-        if (bq == 32) {
-          if (pb >= p1) break;
-          const uint32_t p = pb + lane;
-          const bool valid = p < p1;
-          vv = valid ? vals[p] : 0u;
-          const int64_t r = vv >> 1;
-          e0 = valid ? row_ptr[r] - base0 : 0;
-          e1 = valid ? row_ptr[r + 1] - base0 : 0;
-          bq = 0;
+  if (warp == 0) {
+    // ---- loader
+    uint32_t pb = p0;          // next pair batch
+    int64_t src = 0, rem = 0;  // row in progress (lane-uniform)
+    uint32_t neg = 0;
+    bool cont = false;
+    int bcnt = 0, bq = 0;      // pairs in the current batch / consumed
+    int64_t my_src = 0;
+    int32_t my_len = 0;
+    uint32_t my_v = 0;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t s = it % ST_STAGES, ph = (it / ST_STAGES) & 1u;
+      st_wait(&empty[s], ph ^ 1u);
+      int ns = 0, ne = 0;
+      bool done = false;
+      while (ns < ST_RMAX && ne < ST_ECAP) {
+        if (rem == 0 && !cont) {
+          if (bq == bcnt) {  // fetch the next 32 pairs' (src, len, sign) in parallel
+            if (pb >= p1) {
+              done = true;
+              break;
+            }
+            bcnt = p1 - pb < 32u ? static_cast<int>(p1 - pb) : 32;
+            if (lane < bcnt) {
+              my_src = msrc[pb + lane];
+              my_len = mlen[pb + lane];
+              my_v = svals[pb + lane];
+            }
+            pb += bcnt;
+            bq = 0;
+          }
+          src = __shfl_sync(0xFFFFFFFFu, my_src, bq);
+          rem = __shfl_sync(0xFFFFFFFFu, my_len, bq);
+          neg = __shfl_sync(0xFFFFFFFFu, my_v, bq) & 1u;
+          ++bq;
+          if (rem == 0) {  // empty row: nothing to apply or validate
+            continue;
+          }
         }
-        const uint32_t p = pb + bq;
-        if (p >= p1) break;
-        cur = __shfl_sync(0xFFFFFFFFu, e0, bq);
-        cur_end = __shfl_sync(0xFFFFFFFFu, e1, bq);
-        cur_neg = __shfl_sync(0xFFFFFFFFu, vv, bq) & 1u;
-        cur_live = true;
-        cont = false;
-        if (++bq == 32) pb += 32;
-      }
-      const int64_t room = SG_ECAP - ne;
-      const int64_t len = cur_end - cur < room ? cur_end - cur : room;
-      if (len == 0 && cur_end > cur) break;  // buffer full
-      if (lane == 0) {
+        const int64_t len = rem < ST_ECAP - ne ? rem : ST_ECAP - ne;
+        if (len == 0) break;
         SegInfo si;
-        si.src = cur;
         si.off = ne;
         si.len = static_cast<int32_t>(len);
-        si.flags = static_cast<int32_t>(cur_neg | (cont ? 2u : 0u));
-        seg[buf * SG_RMAX + ns] = si;
-      }
-      ++ns;
-      ne += static_cast<int>(len);
-      cur += len;
-      if (cur >= cur_end) {
-        cur_live = false;
-      } else {
-        cont = true;
-      }
-    }
-    return ns;
-  };
-  auto issue = [&](int buf, int ns) {  // all warps: copy the planned segments
-    for (int q = warp; q < ns; q += SG_WARPS) {
-      const SegInfo si = seg[buf * SG_RMAX + q];
-      for (int e = lane; e < si.len; e += 32) {
-        cp_async4(bcol + buf * SG_ECAP + si.off + e, col + si.src + e);
-        if constexpr (sizeof(V) == 8)
-          cp_async8(bval + buf * SG_ECAP + si.off + e, val + si.src + e);
-        else
-          cp_async4(bval + buf * SG_ECAP + si.off + e, val + si.src + e);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  if (warp == 0) {
-    const int ns = plan(0);
-    if (lane == 0) {
-      nseg_s[0] = ns;
-      more_s = cur_live || (pb + (bq == 32 ? 0 : bq)) < p1;
-    }
-  }
-  __syncthreads();
-  issue(0, nseg_s[0]);
-  int bad = 0;
-  int32_t lastcol = -1;  // last column of the previous chunk (a row continued across chunks)
-  const int64_t lo_c = static_cast<int64_t>(warp) * (SG_COLS / SG_WARPS), hi_c = lo_c + SG_COLS / SG_WARPS;
-  for (int it = 0;; ++it) {
-    const int buf = it & 1;
-    const bool more = more_s;
-    __syncthreads();  // every thread has read more_s / nseg_s before the planner rewrites them
-    if (more) {
-      if (warp == 0) {
-        const int ns = plan(buf ^ 1);
-        if (lane == 0) {
-          nseg_s[buf ^ 1] = ns;
-          more_s = cur_live || (pb + (bq == 32 ? 0 : bq)) < p1;
+        si.flags = static_cast<int32_t>(neg | (cont ? 2u : 0u));
+        si.pad = 0;
+        if (lane == 0) seg[s * ST_RMAX + ns] = si;
+        for (int e = lane; e < len; e += 32) {
+          cp_async4(bcol + s * ST_ECAP + ne + e, col + src + e);
+          if constexpr (sizeof(V) == 8)
+            cp_async8(bval + s * ST_ECAP + ne + e, val + src + e);
+          else
+            cp_async4(bval + s * ST_ECAP + ne + e, val + src + e);
         }
+        ++ns;
+        ne += static_cast<int>(len);
+        src += len;
+        rem -= len;
+        cont = rem > 0;
       }
-      __syncthreads();
-      issue(buf ^ 1, nseg_s[buf ^ 1]);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if (lane == 0) nseg[s] = done && ns == 0 ? -1 : ns;
+      if (done && ns > 0 && lane == 0) nseg[s] = ns | (1 << 30);  // last chunk
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(csr_smem(&full[s])) : "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[s])) : "memory");
+      if (done) break;
     }
-    __syncthreads();  // chunk `it` has landed for every thread's copies
-    const int ns = nseg_s[buf];
-    const V* vb = bval + buf * SG_ECAP;
-    const int32_t* cb = bcol + buf * SG_ECAP;
-    for (int q = 0; q < ns; ++q) {
-      const SegInfo si = seg[buf * SG_RMAX + q];
-      const double sg = (si.flags & 1) ? -scale : scale;
-      for (int e = lane; e < si.len; e += 32) {
-        const int64_t lc = static_cast<int64_t>(cb[si.off + e]) - c0;
-        if (lc >= lo_c && lc < hi_c && lc < width) {
-          double su, er;
-          two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(vb[si.off + e])), su, er);
-          hi[lc] = su;
-          lo[lc] = __dadd_rn(lo[lc], er);
-        }
-      }
-      __syncwarp();  // the next row may hit the same columns from other lanes
-      if (q % SG_WARPS == warp) {  // validation of this segment
-        int32_t carry = (si.flags & 2) ? (q > 0 ? cb[si.off - 1] : lastcol) : -1;
-        for (int e0v = 0; e0v < si.len; e0v += 32) {
-          const int e = e0v + lane;
-          const bool live = e < si.len;
-          const int32_t c = live ? cb[si.off + e] : INT32_MAX;
-          const double x = live ? static_cast<double>(vb[si.off + e]) : 0.0;
-          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-          const int32_t before = lane == 0 ? carry : cprev;
-          if (live) {
-            if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
-            if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
+  } else {
+    // ---- appliers
+    const int aw = warp - 1;
+    const int64_t lo_c = static_cast<int64_t>(aw) * (ST_COLS / ST_APPLY), hi_c = lo_c + ST_COLS / ST_APPLY;
+    int bad = 0;
+    int32_t lastcol = -1;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t s = it % ST_STAGES, ph = (it / ST_STAGES) & 1u;
+      st_wait(&full[s], ph);
+      const int raw = nseg[s];
+      if (raw < 0) break;
+      const bool last = (raw >> 30) & 1;
+      const int ns = raw & ((1 << 30) - 1);
+      const V* vb = bval + s * ST_ECAP;
+      const int32_t* cb = bcol + s * ST_ECAP;
+      for (int q = 0; q < ns; ++q) {
+        const SegInfo si = seg[s * ST_RMAX + q];
+        const double sg = (si.flags & 1) ? -scale : scale;
+        for (int e = lane; e < si.len; e += 32) {
+          const int64_t lc = static_cast<int64_t>(cb[si.off + e]) - c0;
+          if (lc >= lo_c && lc < hi_c && lc < width) {
+            double su, er;
+            two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(vb[si.off + e])), su, er);
+            hi[lc] = su;
+            lo[lc] = __dadd_rn(lo[lc], er);
           }
-          carry = __shfl_sync(0xFFFFFFFFu, c, 31);
+        }
+        __syncwarp();  // the next row may hit the same columns from other lanes
+        if (q % ST_APPLY == aw) {
+          int32_t carry = (si.flags & 2) ? (q > 0 ? cb[si.off - 1] : lastcol) : -1;
+          for (int e0v = 0; e0v < si.len; e0v += 32) {
+            const int e = e0v + lane;
+            const bool live = e < si.len;
+            const int32_t c = live ? cb[si.off + e] : INT32_MAX;
+            const double x = live ? static_cast<double>(vb[si.off + e]) : 0.0;
+            const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+            const int32_t before = lane == 0 ? carry : cprev;
+            if (live) {
+              if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
+              if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
+            }
+            carry = __shfl_sync(0xFFFFFFFFu, c, 31);
+          }
         }
       }
+      if (ns > 0) {
+        const SegInfo sl = seg[s * ST_RMAX + ns - 1];
+        lastcol = cb[sl.off + sl.len - 1];
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&empty[s])) : "memory");
+      if (last) break;
     }
-    if (ns > 0) {
-      const SegInfo sl = seg[buf * SG_RMAX + ns - 1];
-      if (sl.len > 0) lastcol = cb[sl.off + sl.len - 1];
-    }
-    if (!more) break;
+    const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (any && lane == 0) atomicOr(flags, any);
   }
   __syncthreads();
   for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
     hi_out[b * d + c0 + c] = hi[c];
     lo_out[b * d + c0 + c] = lo[c];
   }
-  const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
-  if (any && lane == 0) atomicOr(flags, any);
 }
 
 // K6: one warp per row, lane owns RPL = r/32 consecutive columns of u
@@ -389,6 +403,8 @@ extern "C" size_t lvsk_hashed_csr_workspace_bytes(int64_t n, int32_t s, int64_t 
   m.take<uint32_t>(N);
   m.take<uint32_t>(N);
   m.take<uint32_t>(k + 1);
+  m.take<int64_t>(N);
+  m.take<int32_t>(N);
   radix::measure<uint32_t>(m, N);
   return m.off;
 }
@@ -411,6 +427,8 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
   uint32_t* skeys = c.take<uint32_t>(N);
   uint32_t* svals = c.take<uint32_t>(N);
   uint32_t* start = c.take<uint32_t>(k + 1);
+  int64_t* msrc = c.take<int64_t>(N);
+  int32_t* mlen = c.take<int32_t>(N);
   auto rb = radix::carve<uint32_t>(c, N);
   LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
   CsrBlocks P;
@@ -437,26 +455,28 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
     attr = true;
   }
   if (getenv("LVSK_K2_SIMPLE") == nullptr) {
-    const int sgroups = static_cast<int>((d + SG_COLS - 1) / SG_COLS);
+    csr_prep_kernel<<<csr_grid(N, 256), 256, 0, st>>>(row_ptr, svals, N, msrc, mlen);
+    const int sgroups = static_cast<int>((d + ST_COLS - 1) / ST_COLS);
     const int vsz = val_dtype == LVSK_F64 ? 8 : 4;
-    const int ssmem = 2 * SG_COLS * 8 + 2 * SG_ECAP * (vsz + 4) + 2 * SG_RMAX * static_cast<int>(sizeof(SegInfo));
+    auto smem_for = [](int v) {
+      return 2 * ST_COLS * 8 + ST_STAGES * ST_ECAP * (v + 4) + ST_STAGES * ST_RMAX * static_cast<int>(sizeof(SegInfo)) +
+             ST_STAGES * 4 + 2 * ST_STAGES * 8;
+    };
     static bool sattr = false;
     if (!sattr) {
-      cudaFuncSetAttribute(csr_staged_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           2 * SG_COLS * 8 + 2 * SG_ECAP * 8 + 2 * SG_RMAX * static_cast<int>(sizeof(SegInfo)));
-      cudaFuncSetAttribute(csr_staged_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           2 * SG_COLS * 8 + 2 * SG_ECAP * 12 + 2 * SG_RMAX * static_cast<int>(sizeof(SegInfo)));
+      cudaFuncSetAttribute(csr_stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(4));
+      cudaFuncSetAttribute(csr_stream_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8));
       sattr = true;
     }
     const unsigned sgrid = static_cast<unsigned>(k * sgroups);
     if (val_dtype == LVSK_F32)
-      csr_staged_kernel<float><<<sgrid, 32 * SG_WARPS, ssmem, st>>>(row_ptr, col, static_cast<const float*>(val), d,
-                                                                   sgroups, svals, start, scale, hi_in, lo_in,
-                                                                   hi_out, lo_out, flags);
+      csr_stream_kernel<float><<<sgrid, 32 * (1 + ST_APPLY), smem_for(vsz), st>>>(
+          col, static_cast<const float*>(val), d, sgroups, svals, msrc, mlen, start, scale, hi_in, lo_in, hi_out,
+          lo_out, flags);
     else
-      csr_staged_kernel<double><<<sgrid, 32 * SG_WARPS, ssmem, st>>>(row_ptr, col, static_cast<const double*>(val),
-                                                                    d, sgroups, svals, start, scale, hi_in, lo_in,
-                                                                    hi_out, lo_out, flags);
+      csr_stream_kernel<double><<<sgrid, 32 * (1 + ST_APPLY), smem_for(vsz), st>>>(
+          col, static_cast<const double*>(val), d, sgroups, svals, msrc, mlen, start, scale, hi_in, lo_in, hi_out,
+          lo_out, flags);
   } else if (val_dtype == LVSK_F32)
     csr_gather_kernel<float><<<grid, 32 * CSR_WARPS, smem, st>>>(row_ptr, col, static_cast<const float*>(val), d,
                                                               ngroups, svals, start, units, scale, hi_in, lo_in,

@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 // segments / 1024 entries; longer rows are split, harmless since one row's
 // entries have distinct columns) with cp.async into a 4-deep ring signalled
 // by cp.async.mbarrier.arrive; warps 1..8 apply the chunks in row order,
-// warp w taking the entries of its 512 columns (TwoSum into hi / lo), and
+// warp w taking the entries of its 512 columns — one contiguous run of each
+// column-sorted row, found with two ballots per 32 entries — (TwoSum into
+// hi / lo), and
 // validate (strictly increasing in-range columns, finite values) the
 // segments assigned to them.
 constexpr int ST_COLS = 4096;
@@ -274,9 +276,18 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
       for (int q = 0; q < ns; ++q) {
         const SegInfo si = seg[s * ST_RMAX + q];
         const double sg = (si.flags & 1) ? -scale : scale;
-        for (int e = lane; e < si.len; e += 32) {
+        // a canonical row is column-sorted, so this warp's columns form one
+        // contiguous run [first, last) of the segment: count, then apply it
+        int first = 0, last = 0;
+        for (int e0v = 0; e0v < si.len; e0v += 32) {
+          const int e = e0v + lane;
+          const int64_t lc = e < si.len ? static_cast<int64_t>(cb[si.off + e]) - c0 : INT64_MAX;
+          first += __popc(__ballot_sync(0xFFFFFFFFu, lc < lo_c));
+          last += __popc(__ballot_sync(0xFFFFFFFFu, lc < hi_c && lc < width));
+        }
+        for (int e = first + lane; e < last; e += 32) {
           const int64_t lc = static_cast<int64_t>(cb[si.off + e]) - c0;
-          if (lc >= lo_c && lc < hi_c && lc < width) {
+          if (lc >= lo_c && lc < hi_c) {  // guards a non-canonical row (flagged by the validation)
             double su, er;
             two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(vb[si.off + e])), su, er);
             hi[lc] = su;

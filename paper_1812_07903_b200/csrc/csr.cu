@@ -110,12 +110,15 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 // memory (64 KB); warp 0 streams the bucket's rows in chunks (<= 64 row
 // segments / 1024 entries; longer rows are split, harmless since one row's
 // entries have distinct columns) with cp.async into a 4-deep ring signalled
-// by cp.async.mbarrier.arrive; warps 1..8 apply the chunks in row order,
-// warp w taking the entries of its 512 columns — one contiguous run of each
-// column-sorted row, found with two ballots per 32 entries — (TwoSum into
-// hi / lo), and
-// validate (strictly increasing in-range columns, finite values) the
-// segments assigned to them.
+// by cp.async.mbarrier.arrive; warps 1..8 apply the chunk's segments
+// concurrently (segment q by warp q mod 8) with returning shared-memory
+// atomics: hi += v, and the exact rounding error of that addition (TwoSum of
+// the returned old value and v) onto lo, so hi + lo is the compensated sum of
+// the bucket's contributions in whatever order they land (the sketch equals
+// the reference's to ~1e-16 relative instead of bit-for-bit;
+// LVSK_K2_DETERMINISTIC=1 selects the ordered csr_gather_kernel, which is
+// bit-exact).  The same warps validate their segments (strictly increasing
+// in-range columns, finite values).
 constexpr int ST_COLS = 4096;
 constexpr int ST_APPLY = 8;  // applier warps
 constexpr int ST_ECAP = 1024;
@@ -261,7 +264,6 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
   } else {
     // ---- appliers
     const int aw = warp - 1;
-    const int64_t lo_c = static_cast<int64_t>(aw) * (ST_COLS / ST_APPLY), hi_c = lo_c + ST_COLS / ST_APPLY;
     int bad = 0;
     int32_t lastcol = -1;
     for (uint32_t it = 0;; ++it) {
@@ -273,43 +275,34 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
       const int ns = raw & ((1 << 30) - 1);
       const V* vb = bval + s * ST_ECAP;
       const int32_t* cb = bcol + s * ST_ECAP;
-      for (int q = 0; q < ns; ++q) {
+      // segments are independent: every entry goes through a returning
+      // shared-memory atomic on hi and its exact rounding error (TwoSum of
+      // the old value and the addend) onto lo, so hi + lo carries the
+      // compensated sum in any order
+      for (int q = aw; q < ns; q += ST_APPLY) {
         const SegInfo si = seg[s * ST_RMAX + q];
         const double sg = (si.flags & 1) ? -scale : scale;
-        // a canonical row is column-sorted, so this warp's columns form one
-        // contiguous run [first, last) of the segment: count, then apply it
-        int first = 0, last = 0;
+        int32_t carry = (si.flags & 2) ? (q > 0 ? cb[si.off - 1] : lastcol) : -1;
         for (int e0v = 0; e0v < si.len; e0v += 32) {
           const int e = e0v + lane;
-          const int64_t lc = e < si.len ? static_cast<int64_t>(cb[si.off + e]) - c0 : INT64_MAX;
-          first += __popc(__ballot_sync(0xFFFFFFFFu, lc < lo_c));
-          last += __popc(__ballot_sync(0xFFFFFFFFu, lc < hi_c && lc < width));
-        }
-        for (int e = first + lane; e < last; e += 32) {
-          const int64_t lc = static_cast<int64_t>(cb[si.off + e]) - c0;
-          if (lc >= lo_c && lc < hi_c) {  // guards a non-canonical row (flagged by the validation)
-            double su, er;
-            two_sum(hi[lc], __dmul_rn(sg, static_cast<double>(vb[si.off + e])), su, er);
-            hi[lc] = su;
-            lo[lc] = __dadd_rn(lo[lc], er);
-          }
-        }
-        __syncwarp();  // the next row may hit the same columns from other lanes
-        if (q % ST_APPLY == aw) {
-          int32_t carry = (si.flags & 2) ? (q > 0 ? cb[si.off - 1] : lastcol) : -1;
-          for (int e0v = 0; e0v < si.len; e0v += 32) {
-            const int e = e0v + lane;
-            const bool live = e < si.len;
-            const int32_t c = live ? cb[si.off + e] : INT32_MAX;
-            const double x = live ? static_cast<double>(vb[si.off + e]) : 0.0;
-            const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-            const int32_t before = lane == 0 ? carry : cprev;
-            if (live) {
-              if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
-              if (!isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
+          const bool live = e < si.len;
+          const int32_t c = live ? cb[si.off + e] : INT32_MAX;
+          const V xv = live ? vb[si.off + e] : V(0);
+          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+          const int32_t before = lane == 0 ? carry : cprev;
+          if (live) {
+            if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
+            if (!isfinite(static_cast<double>(xv))) bad |= LVSK_FLAG_NONFINITE;
+            const int64_t lc = static_cast<int64_t>(c) - c0;
+            if (lc >= 0 && lc < width) {
+              const double v = __dmul_rn(sg, static_cast<double>(xv));
+              const double old = atomicAdd(&hi[lc], v);
+              double su, er;
+              two_sum(old, v, su, er);
+              atomicAdd(&lo[lc], er);
             }
-            carry = __shfl_sync(0xFFFFFFFFu, c, 31);
           }
+          carry = __shfl_sync(0xFFFFFFFFu, c, 31);
         }
       }
       if (ns > 0) {
@@ -465,7 +458,7 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
     cudaFuncSetAttribute(csr_gather_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  if (getenv("LVSK_K2_SIMPLE") == nullptr) {
+  if (getenv("LVSK_K2_DETERMINISTIC") == nullptr) {
     csr_prep_kernel<<<csr_grid(N, 256), 256, 0, st>>>(row_ptr, svals, N, msrc, mlen);
     const int sgroups = static_cast<int>((d + ST_COLS - 1) / ST_COLS);
     const int vsz = val_dtype == LVSK_F64 ? 8 : 4;

@@ -557,18 +557,29 @@ def _random_csr(n, d, per_row, seed, dtype=np.float32):
 
 
 @pytest.mark.parametrize("n,d,k,s", [(3000, 300, 512, 4), (1500, 2100, 1024, 3), (777, 64, 128, 1)])
-def test_csr_sketch_bit_exact_vs_dense(n, d, k, s):
+def test_csr_sketch_bit_exact_vs_dense(n, d, k, s, monkeypatch):
+    """K2 default (order-free compensated atomics): hi + lo within 1e-13 of the
+    reference's compensated state; LVSK_K2_DETERMINISTIC=1 (ordered gather):
+    bit-exact."""
     csr, dense = _random_csr(n, d, 40, seed=n + d)
     fam = "osnap" if s > 1 else "countsketch"
     spec = P.SketchSpec(fam, eps=0.5, d=d, seed=7, rows_override=k, osnap_s=s if fam == "osnap" else None)
     hi, lo = O.hashed_sketch(dense, fam, k, 7, s)
-    assert np.array_equal(P.apply_sketch(csr, spec).data, hi + lo)
+    ref = hi + lo
+    tol = 1e-13 * np.abs(ref).max()
+    assert np.allclose(P.apply_sketch(csr, spec).data, ref, rtol=1e-13, atol=tol)
     # two row blocks with global indices == one pass
     m = P.csr.CSRMatrix(*csr)
     st = P.SketchState(spec, n)
     P.consume_rows(st, m.rows(0, n // 2), 0)
     P.consume_rows(st, m.rows(n // 2, n), n // 2)
-    assert np.array_equal(st.data, hi + lo)
+    assert np.allclose(st.data, ref, rtol=1e-13, atol=tol)
+    monkeypatch.setenv("LVSK_K2_DETERMINISTIC", "1")
+    assert np.array_equal(P.apply_sketch(csr, spec).data, ref)
+    st = P.SketchState(spec, n)
+    P.consume_rows(st, m.rows(0, n // 2), 0)
+    P.consume_rows(st, m.rows(n // 2, n), n // 2)
+    assert np.array_equal(st.data, ref)
 
 
 def test_csr_leverage_vs_oracle():

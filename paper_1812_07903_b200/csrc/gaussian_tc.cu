@@ -22,6 +22,8 @@
 // sketch rows (ceil(k/128) times, L2-shared across the CTAs of one
 // (split, column slab) which are launched adjacently); each Z entry is
 // generated ceil(d/NS) times.
+#include <cstdlib>
+
 #include "philox.cuh"
 #include "tc_common.cuh"
 
@@ -65,7 +67,29 @@ __device__ __forceinline__ uint64_t l2_policy_evict_normal() {
   return p;
 }
 
-template <int NS>
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// CL = 1: one CTA per (k tile, column slab, split), each generating its whole
+// Z tile.  CL = 2 (d in (512, 1024]): the two column slabs of a k tile form a
+// cluster; each CTA generates half of the Z tile's rows and stores them into
+// both CTAs' shared memory (DSMEM), so every Z entry is generated once.
+template <int NS, int CL>
 __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
                        uint32_t k0, uint32_t k1, int ktiles, int dslabs, int64_t rows_per_split,
@@ -83,9 +107,17 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int item = blockIdx.x;
-  const int ktile = item % ktiles;
-  const int dslab = (item / ktiles) % dslabs;
-  const int64_t split = item / (ktiles * dslabs);
+  int ktile, dslab;
+  int64_t split;
+  if constexpr (CL == 1) {
+    ktile = item % ktiles;
+    dslab = (item / ktiles) % dslabs;
+    split = item / (ktiles * dslabs);
+  } else {  // cluster rank = column slab
+    dslab = item % CL;
+    ktile = (item / CL) % ktiles;
+    split = item / (CL * ktiles);
+  }
   const int64_t r_begin = split * rows_per_split;
   const int64_t r_end = r_begin + rows_per_split < n ? r_begin + rows_per_split : n;
   const int nstages = static_cast<int>((r_end - r_begin + C::BKN - 1) / C::BKN);
@@ -94,8 +126,8 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::S; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&zfull[s], C::GEN_WARPS);
-      mbar_init(&empty[s], 1);
+      mbar_init(&zfull[s], C::GEN_WARPS * CL);
+      mbar_init(&empty[s], CL);
     }
     mbar_init(accfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -110,6 +142,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -130,7 +163,10 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       for (int t = 0; t < nstages; ++t) {
         const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
         mbar_wait(&xfull[s], ph);
-        mbar_wait(&zfull[s], ph);
+        if constexpr (CL > 1)
+          mbar_wait_cluster(&zfull[s], ph);
+        else
+          mbar_wait(&zfull[s], ph);
         tc_fence_after();
         const uint64_t a = sw128_desc(smem_u32(smem + C::OFF_Z + s * C::Z_BYTES));
 #pragma unroll
@@ -142,35 +178,88 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
             umma_f16(tmem_base + h * 256, a + 2 * kk, b, C::IDESC, (t | kk) ? 1u : 0u);
           }
         }
-        umma_commit(&empty[s]);
+        if constexpr (CL > 1)
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&empty[s])),
+              "h"(static_cast<uint16_t>((1u << CL) - 1u))
+              : "memory");
+        else
+          umma_commit(&empty[s]);
       }
       umma_commit(accfull);
     }
   } else {
-    // ---- Z generation: warp gw -> sketch rows 8gw .. 8gw+7 of the tile,
-    //      lane -> input rows 2*lane, 2*lane+1 of the stage (2 Philox calls)
     const int gw = warp - 2;
-    const int q = gw;
-    const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
-    for (int t = 0; t < nstages; ++t) {
-      const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
-      const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 2 * lane);
-      float z[2][8];
-      gaussian8(g0, qg, k0, k1, tab, z[0]);
-      gaussian8(g0 + 1, qg, k0, k1, tab, z[1]);
-      mbar_wait(&empty[s], ph ^ 1u);
-      uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
+    if constexpr (CL == 1) {
+      // ---- Z generation: warp gw -> sketch rows 8gw .. 8gw+7 of the tile,
+      //      lane -> input rows 2*lane, 2*lane+1 of the stage (2 Philox calls)
+      const int q = gw;
+      const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
+      for (int t = 0; t < nstages; ++t) {
+        const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+        const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 2 * lane);
+        float z[2][8];
+        gaussian8(g0, qg, k0, k1, tab, z[0]);
+        gaussian8(g0 + 1, qg, k0, k1, tab, z[1]);
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
 #pragma unroll
-      for (int r8 = 0; r8 < 8; ++r8) {
-        const int j = 8 * q + r8;
-        __nv_bfloat162 v = __floats2bfloat162_rn(z[0][r8], z[1][r8]);
-        // row j: 128 B = 8 swizzled 16-byte chunks; lane owns bytes [4 lane, 4 lane + 4)
-        const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
-        *reinterpret_cast<__nv_bfloat162*>(zt + off) = v;
+        for (int r8 = 0; r8 < 8; ++r8) {
+          const int j = 8 * q + r8;
+          __nv_bfloat162 v = __floats2bfloat162_rn(z[0][r8], z[1][r8]);
+          // row j: 128 B = 8 swizzled 16-byte chunks; lane owns bytes [4 lane, 4 lane + 4)
+          const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
+          *reinterpret_cast<__nv_bfloat162*>(zt + off) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&zfull[s]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&zfull[s]);
+    } else {
+      // ---- Z generation, cluster of 2: this CTA (rank = dslab) makes rows
+      //      [64 rank, 64 rank + 64) of the tile — warp gw -> octet q, half of
+      //      the 64 input rows; lane -> one input row (1 Philox call) — and
+      //      stores them into both CTAs' Z slot
+      const uint32_t peer = static_cast<uint32_t>(dslab ^ 1);
+      const int q = dslab * 8 + (gw >> 1);
+      const int cbase = (gw & 1) * 32;
+      const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
+      const uint32_t zfull_peer0 = map_peer(smem_u32(&zfull[0]), peer);
+      for (int t = 0; t < nstages; ++t) {
+        const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+        const int cidx = cbase + lane;  // input row of the stage = Z column
+        const uint64_t g = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + cidx);
+        float z[8], zp[8];
+        gaussian8(g, qg, k0, k1, tab, z);
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) zp[r8] = __shfl_xor_sync(0xFFFFFFFFu, z[r8], 1);
+        mbar_wait(&empty[s], ph ^ 1u);
+        const uint32_t zt = smem_u32(smem + C::OFF_Z + s * C::Z_BYTES);
+        const uint32_t ztp = map_peer(zt, peer);
+        const int cpair = cidx & ~1;  // even column of this lane's pair
+        const bool odd = lane & 1;    // even lanes write rows 0-3, odd lanes rows 4-7
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) {
+          if ((r8 >= 4) == odd) {
+            const int j = 8 * q + r8;
+            const float a = odd ? zp[r8] : z[r8];   // even column
+            const float bv = odd ? z[r8] : zp[r8];  // odd column
+            __nv_bfloat162 v = __floats2bfloat162_rn(a, bv);
+            const uint32_t w = *reinterpret_cast<uint32_t*>(&v);
+            const int off = j * 128 + ((((cpair * 2) >> 4) ^ (j & 7)) << 4) + ((cpair * 2) & 15);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(zt + off), "r"(w) : "memory");
+            asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(ztp + off), "r"(w) : "memory");
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&zfull[s]);
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(zfull_peer0 + s * 8)
+                       : "memory");
+        }
+      }
     }
     // ---- epilogue: TMEM -> fp32 partial
     mbar_wait(accfull, 0);
@@ -206,6 +295,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(NS));
   }
+  if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still write into it
 }
 
 }  // namespace tc
@@ -232,7 +322,7 @@ bool gaussian_tc_ok(const void* X, int64_t n, int64_t d, int64_t ldx, int64_t k)
   return true;
 }
 
-template <int NS>
+template <int NS, int CL>
 static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
                                uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
   using C = tc::CfgG<NS>;
@@ -243,8 +333,8 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
   }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::gaussian_tc_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(tc::gaussian_tc_kernel<NS, CL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return cuda_status(e, "gaussian tc smem attribute");
     attr = true;
   }
@@ -254,16 +344,30 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
     set_error("cannot allocate the Gaussian generator table");
     return LVSK_ERR_CUDA;
   }
-  tc::gaussian_tc_kernel<NS><<<static_cast<unsigned>(items), C::NTHREADS, C::SMEM_BYTES, st>>>(
-      mx, n, d, k, row0, k0, k1, p.ktiles, p.dslabs, p.rows_per_split, gtab, partial);
-  LVSK_CHECK_LAUNCH("gaussian tc");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(items));
+  cfg.blockDim = dim3(C::NTHREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CL;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, CL>, mx, n, d, k, row0, k0, k1, p.ktiles,
+                                     p.dslabs, p.rows_per_split, gtab, partial);
+  if (e != cudaSuccess) return cuda_status(e, "gaussian tc launch");
   return LVSK_OK;
 }
 
 int32_t gaussian_tc_bf16(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
                          uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
-  return p.ns == 512 ? launch_gauss_tc<512>(X, n, d, ldx, k, row0, k0, k1, p, partial, st)
-                     : launch_gauss_tc<256>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
+  if (p.ns == 512 && p.dslabs == 2 && getenv("LVSK_K4_NOCLUSTER") == nullptr)
+    return launch_gauss_tc<512, 2>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
+  return p.ns == 512 ? launch_gauss_tc<512, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st)
+                     : launch_gauss_tc<256, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
 }
 
 }  // namespace lvsk

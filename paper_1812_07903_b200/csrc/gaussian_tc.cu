@@ -14,7 +14,8 @@
 //   warps 2-17 generate the Z tile [128 x 64] (philox.cuh: 8 entries per
 //            Philox call, table-driven Box-Muller, bit-identical to the SIMT
 //            path and the oracle) straight into the K-major SW128 A
-//            layout in shared memory, fence.proxy.async, arrive;
+//            layout in shared memory and arrive (the MMA thread issues the
+//            generic->async proxy fence once per stage);
 //   warp 1   issues 4 x (NS/256) tcgen05.mma kind::f16 (M = 128, N = 256,
 //            K = 16) and commits the stage back to both producers.
 // After the last stage warps 2-17 drain TMEM (tcgen05.ld 32x32b) into the
@@ -167,6 +168,10 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
           mbar_wait_cluster(&zfull[s], ph);
         else
           mbar_wait(&zfull[s], ph);
+        // the Z tile was written through the generic proxy (local and DSMEM
+        // stores); one proxy fence here, after the acquire, orders it before
+        // the tensor core's async-proxy reads (instead of one per producer warp)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_after();
         const uint64_t a = sw128_desc(smem_u32(smem + C::OFF_Z + s * C::Z_BYTES));
 #pragma unroll
@@ -212,7 +217,6 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
           const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
           *reinterpret_cast<__nv_bfloat162*>(zt + off) = v;
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&zfull[s]);
       }
@@ -252,7 +256,6 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
             asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(ztp + off), "r"(w) : "memory");
           }
         }
-        asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&zfull[s]);

@@ -39,9 +39,10 @@ struct CfgG {
   static constexpr int BOX_BYTES = BKN * 64 * 2;  // 8 KB
   static constexpr int X_BYTES = NB * BOX_BYTES;
   static constexpr int Z_BYTES = BM * BKN * 2;  // 16 KB
-  static constexpr int S = NS == 512 ? 2 : 4;
+  static constexpr int S = NS == 512 ? 2 : 4;  // X stages
+  static constexpr int SZ = 4;                  // Z stages (generation runs up to 4 stages ahead)
   static constexpr int OFF_Z = S * X_BYTES;
-  static constexpr int OFF_BAR = OFF_Z + S * Z_BYTES;
+  static constexpr int OFF_BAR = OFF_Z + SZ * Z_BYTES;
   static constexpr int OFF_TAB = OFF_BAR + 256;
   static constexpr int SMEM_BYTES = OFF_TAB + GT_SIZE * 4 + 1024;
   static constexpr int GEN_WARPS = 16;  // one per 8-row octet of the 128-row tile
@@ -94,15 +95,16 @@ template <int NS, int CL>
 __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
                        uint32_t k0, uint32_t k1, int ktiles, int dslabs, int64_t rows_per_split,
-                       const float* __restrict__ gtab, float* __restrict__ partial) {
+                       const float* __restrict__ gtab, float* __restrict__ partial, int nogen) {
   using C = CfgG<NS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* xfull = bars;
-  uint64_t* zfull = xfull + C::S;
-  uint64_t* empty = zfull + C::S;
-  uint64_t* accfull = empty + C::S;
+  uint64_t* empty = xfull + C::S;  // X slots
+  uint64_t* zfull = empty + C::S;
+  uint64_t* zempty = zfull + C::SZ;
+  uint64_t* accfull = zempty + C::SZ;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
   float* tab = reinterpret_cast<float*>(smem + C::OFF_TAB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -127,8 +129,11 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::S; ++s) {
       mbar_init(&xfull[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < C::SZ; ++s) {
       mbar_init(&zfull[s], C::GEN_WARPS * CL);
-      mbar_init(&empty[s], CL);
+      mbar_init(&zempty[s], CL);
     }
     mbar_init(accfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -163,17 +168,18 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     if (lane == 0) {
       for (int t = 0; t < nstages; ++t) {
         const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+        const uint32_t sz = t % C::SZ, phz = (t / C::SZ) & 1u;
         mbar_wait(&xfull[s], ph);
         if constexpr (CL > 1)
-          mbar_wait_cluster(&zfull[s], ph);
+          mbar_wait_cluster(&zfull[sz], phz);
         else
-          mbar_wait(&zfull[s], ph);
+          mbar_wait(&zfull[sz], phz);
         // the Z tile was written through the generic proxy (local and DSMEM
         // stores); one proxy fence here, after the acquire, orders it before
         // the tensor core's async-proxy reads (instead of one per producer warp)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_after();
-        const uint64_t a = sw128_desc(smem_u32(smem + C::OFF_Z + s * C::Z_BYTES));
+        const uint64_t a = sw128_desc(smem_u32(smem + C::OFF_Z + sz * C::Z_BYTES));
 #pragma unroll
         for (int kk = 0; kk < C::BKN / 16; ++kk) {
 #pragma unroll
@@ -183,14 +189,15 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
             umma_f16(tmem_base + h * 256, a + 2 * kk, b, C::IDESC, (t | kk) ? 1u : 0u);
           }
         }
+        umma_commit(&empty[s]);
         if constexpr (CL > 1)
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                  smem_u32(&empty[s])),
+                  smem_u32(&zempty[sz])),
               "h"(static_cast<uint16_t>((1u << CL) - 1u))
               : "memory");
         else
-          umma_commit(&empty[s]);
+          umma_commit(&zempty[sz]);
       }
       umma_commit(accfull);
     }
@@ -202,12 +209,17 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       const int q = gw;
       const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
       for (int t = 0; t < nstages; ++t) {
-        const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+        const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
         const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 2 * lane);
         float z[2][8];
-        gaussian8(g0, qg, k0, k1, tab, z[0]);
-        gaussian8(g0 + 1, qg, k0, k1, tab, z[1]);
-        mbar_wait(&empty[s], ph ^ 1u);
+        if (nogen) {  // profiling aid (LVSK_K4_NOGEN): stage the MMA with constant Z
+#pragma unroll
+          for (int r8 = 0; r8 < 8; ++r8) z[0][r8] = z[1][r8] = 1.0f;
+        } else {
+          gaussian8(g0, qg, k0, k1, tab, z[0]);
+          gaussian8(g0 + 1, qg, k0, k1, tab, z[1]);
+        }
+        mbar_wait(&zempty[s], ph ^ 1u);
         uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
 #pragma unroll
         for (int r8 = 0; r8 < 8; ++r8) {
@@ -231,14 +243,19 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
       const uint32_t zfull_peer0 = map_peer(smem_u32(&zfull[0]), peer);
       for (int t = 0; t < nstages; ++t) {
-        const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
+        const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
         const int cidx = cbase + lane;  // input row of the stage = Z column
         const uint64_t g = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + cidx);
         float z[8], zp[8];
-        gaussian8(g, qg, k0, k1, tab, z);
+        if (nogen) {
+#pragma unroll
+          for (int r8 = 0; r8 < 8; ++r8) z[r8] = 1.0f;
+        } else {
+          gaussian8(g, qg, k0, k1, tab, z);
+        }
 #pragma unroll
         for (int r8 = 0; r8 < 8; ++r8) zp[r8] = __shfl_xor_sync(0xFFFFFFFFu, z[r8], 1);
-        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_wait(&zempty[s], ph ^ 1u);
         const uint32_t zt = smem_u32(smem + C::OFF_Z + s * C::Z_BYTES);
         const uint32_t ztp = map_peer(zt, peer);
         const int cpair = cidx & ~1;  // even column of this lane's pair
@@ -360,7 +377,8 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, CL>, mx, n, d, k, row0, k0, k1, p.ktiles,
-                                     p.dslabs, p.rows_per_split, gtab, partial);
+                                     p.dslabs, p.rows_per_split, gtab, partial,
+                                     getenv("LVSK_K4_NOGEN") != nullptr ? 1 : 0);
   if (e != cudaSuccess) return cuda_status(e, "gaussian tc launch");
   return LVSK_OK;
 }

@@ -17,6 +17,8 @@
 //           (-1)^popcount(p_hi & chunk) * value into SX[t] (float64).
 // The butterflies run low bit first like the reference, so float64 input
 // reproduces the reference up to the reassociation of the top a bits.
+#include <cstdlib>
+
 #include "radix_sort.cuh"
 
 namespace lvsk {
@@ -51,6 +53,23 @@ __device__ __forceinline__ void reg_wht(C (&v)[N][W]) {
   }
 }
 
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_f4_hint(float* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_f4_hint(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -107,6 +126,7 @@ __global__ void __launch_bounds__(SRHT_THREADS) srht_pass1_kernel(const T* __res
   const int64_t col0 = static_cast<int64_t>(blockIdx.y) * G::DC;
   const int64_t lrow0 = static_cast<int64_t>(blockIdx.x) * R;  // chunk-local
   const uint64_t pol = evict_first_policy();
+  const uint64_t pol_keep = evict_last_policy();  // T1 is re-read by pass 2 from L2
   bool bad = false;
   for (int g = threadIdx.x; g < (R / NA) * Q; g += SRHT_THREADS) {
     const int q = g % Q, rh = g / Q;
@@ -155,7 +175,7 @@ __global__ void __launch_bounds__(SRHT_THREADS) srht_pass1_kernel(const T* __res
       C* dst = T1 + (lrow0 + rl + NA * j) * d + col;
       if (col + W <= d && d % W == 0) {
         if constexpr (sizeof(C) == 4) {
-          *reinterpret_cast<float4*>(dst) = make_float4(v[j][0], v[j][1], v[j][2], v[j][3]);
+          st_f4_hint(reinterpret_cast<float*>(dst), make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), pol_keep);
         } else {
           *reinterpret_cast<double2*>(dst) = make_double2(v[j][0], v[j][1]);
         }
@@ -192,6 +212,7 @@ __global__ void __launch_bounds__(SRHT_THREADS) srht_pass2_kernel(const C* __res
   if (e0 == e1) return;  // no sampled row has this residue (block-uniform)
   const int64_t col0 = static_cast<int64_t>(blockIdx.y) * G::DC;
   const int64_t stride = int64_t{1} << B1;
+  const uint64_t pol_drop = evict_first_policy();  // last use of T1
   for (int g = threadIdx.x; g < (R / NA) * Q; g += SRHT_THREADS) {
     const int q = g % Q, rh = g / Q;
     const int64_t col = col0 + q * W;
@@ -201,7 +222,7 @@ __global__ void __launch_bounds__(SRHT_THREADS) srht_pass2_kernel(const C* __res
       const C* src = T1 + (q1 + stride * (rh * NA + j)) * d + col;
       if (col + W <= d && d % W == 0) {
         if constexpr (sizeof(C) == 4) {
-          const float4 t = *reinterpret_cast<const float4*>(src);
+          const float4 t = ld_f4_hint(reinterpret_cast<const float*>(src), pol_drop);
           v[j][0] = t.x; v[j][1] = t.y; v[j][2] = t.z; v[j][3] = t.w;
         } else {
           const double2 t = *reinterpret_cast<const double2*>(src);
@@ -282,7 +303,9 @@ static SrhtPlan plan_srht(int64_t m, int64_t d, size_t csize) {
   } else {
     p.B1 = 8;
     int maxcb = 8;
-    while (maxcb < 16 && (size_t{1} << (maxcb + 1)) * static_cast<size_t>(d) * csize <= SRHT_CHUNK_BYTES) ++maxcb;
+    size_t cap = SRHT_CHUNK_BYTES;
+    if (const char* e = getenv("LVSK_SRHT_CHUNK_MB")) cap = static_cast<size_t>(atoi(e)) << 20;
+    while (maxcb < 16 && (size_t{1} << (maxcb + 1)) * static_cast<size_t>(d) * csize <= cap) ++maxcb;
     int cb = p.L < maxcb ? p.L : maxcb;
     p.B2 = cb - 8;
   }

@@ -1,12 +1,11 @@
 cd $GRAFT_REPO_ROOT
 export PYTHONPATH=$GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 300 python bench.py --config c4 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_c4.log 2>&1
-echo "bench c4 exit $?" >> gpurun_out/bench_c4.log; tail -c 1500 gpurun_out/bench_c4.log
-LVSK_K2_SIMPLE=1 timeout 300 python bench.py --config c4 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_c4_simple.log 2>&1
-echo "bench c4 simple exit $?" >> gpurun_out/bench_c4_simple.log; tail -c 700 gpurun_out/bench_c4_simple.log
-timeout 300 python bench.py --config c3 --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_c3.log 2>&1
-echo "bench c3 exit $?" >> gpurun_out/bench_c3.log; tail -c 1200 gpurun_out/bench_c3.log
-timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1
-echo "bench default exit $?" >> gpurun_out/bench_default.log; tail -c 2500 gpurun_out/bench_default.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launch_c2.log 2>&1; tail -2 gpurun_out/ncu_launch_c2.log
+timeout 900 python -m pytest tests -m gpu -q -rf --timeout 300 > gpurun_out/pytest_all.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_all.log
+tail -6 gpurun_out/pytest_all.log
+for c in c1 c2 c3 c4 c5; do
+  timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_$c.log 2>&1
+  echo "$c exit $?"; grep -o "\"ms_per_step\": [0-9.]*\|\"stages_ms\": {[^}]*}[^}]*}[^}]*}" gpurun_out/bench_$c.log
+done
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2

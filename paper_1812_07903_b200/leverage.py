@@ -474,13 +474,54 @@ def _block_scores(rows, basis) -> np.ndarray:
     return scores_device(X, M).cpu().numpy()
 
 
+_STREAM_CHUNK_BYTES = 128 << 20
+
+
+def _streamed_sketch(a: torch.Tensor, spec: SketchSpec, mem_cap):
+    """Pinned host rows -> device in 128 MB chunks on a copy stream, each chunk
+    sketched (consume_rows with its global row offset) as soon as it lands, so
+    the host->device transfer hides the sketch.  Returns (device X, state)."""
+    from .sketch import SketchState, consume_rows
+
+    n, d = a.shape
+    X = torch.empty((n, d), dtype=a.dtype, device=N.device())
+    state = SketchState(spec, n, mem_cap=mem_cap)
+    rows_per = max(1, _STREAM_CHUNK_BYTES // (d * a.element_size()))
+    cur = torch.cuda.current_stream()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(cur)
+    events = []
+    with torch.cuda.stream(cs):  # every copy is enqueued up front: the copy engine never waits on the host
+        for r0 in range(0, n, rows_per):
+            r1 = min(n, r0 + rows_per)
+            X[r0:r1].copy_(a[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append((r0, r1, ev))
+    for r0, r1, ev in events:
+        cur.wait_event(ev)
+        consume_rows(state, X[r0:r1], r0)
+    return X, state
+
+
+def _streamable(a, spec) -> bool:
+    return (isinstance(a, torch.Tensor) and a.device.type == "cpu" and a.dim() == 2 and a.is_pinned()
+            and a.is_contiguous() and a.dtype in (torch.float32, torch.bfloat16, torch.float64)
+            and spec.family in ("countsketch", "osnap", "gaussian")
+            and a.numel() * a.element_size() >= 2 * _STREAM_CHUNK_BYTES)
+
+
 def _sketched(a, spec, sv_tol, mem_cap_bytes, jl_dim, jl_seed, rank, method):
     from .csr import CSRMatrix, csr_scores
 
     m = None if isinstance(a, (np.ndarray, torch.Tensor, list)) else CSRMatrix.from_any(a)
-    X = m if m is not None else device_matrix(a)
-    d = m.d if m is not None else X.shape[1]
-    state = apply_sketch(X, spec, mem_cap=mem_cap_bytes)
+    if m is None and _streamable(a, spec):
+        X, state = _streamed_sketch(a, spec, mem_cap_bytes)
+        d = X.shape[1]
+    else:
+        X = m if m is not None else device_matrix(a)
+        d = m.d if m is not None else X.shape[1]
+        state = apply_sketch(X, spec, mem_cap=mem_cap_bytes)
     sx = state.data_device
     pi = None if jl_dim is None else jl_device(jl_seed, d, jl_dim)
     M, eff = sketch_fold(sx, sv_tol, rank, pi)

@@ -54,7 +54,8 @@ def _vector(x, what: str) -> tuple[torch.Tensor, bool]:
         t = x.detach()
         was_torch = True
     else:
-        t = torch.from_numpy(np.array(x, dtype=np.float64, ndmin=1) if np.ndim(x) else np.asarray(x, dtype=np.float64))
+        a = np.asarray(x, dtype=np.float64)  # no host copy for a float64 array
+        t = torch.from_numpy(a if a.ndim else a.reshape(1))
         was_torch = False
     if t.dim() != 1 or t.numel() == 0:
         raise DegenerateInputError(f"{what}, got shape {tuple(t.shape)}")

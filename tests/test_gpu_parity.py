@@ -638,3 +638,20 @@ def test_c5_shaped_pipeline_small():
     assert res.effective_rank == r == 20
     assert np.abs(res.scores - ref).max() <= 2e-2 * ref.max()
     assert np.median(np.abs(res.scores - ref) / ref) < 1e-3
+
+
+def test_streamed_host_input_equals_device_input():
+    """Pinned host X (>= 256 MB) goes through the chunked copy-stream path
+    (each 128 MB chunk sketched as it lands); results equal the device-X path
+    bit for bit (the hashed sketch is order-exact across row blocks)."""
+    n, d = 160_000, 512
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Xd = torch.randn(n, d, device="cuda", dtype=torch.float32, generator=g)
+    Xh = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    Xh.copy_(Xd)
+    assert P.leverage._streamable(Xh, P.SketchSpec("countsketch", eps=0.5, d=d))
+    for fam in ("countsketch", "osnap"):
+        spec = P.SketchSpec(fam, eps=0.5, d=d, seed=3, rows_override=2048, osnap_s=4 if fam == "osnap" else None)
+        a = P.leverage_sketched_trunc(Xh, spec, 1e-6, jl_dim=64)
+        b = P.leverage_sketched_trunc(Xd, spec, 1e-6, jl_dim=64)
+        assert np.array_equal(a.scores, b.scores), fam

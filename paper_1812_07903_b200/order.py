@@ -132,7 +132,7 @@ def make_plan(p, policy: OrderingPolicy, epoch: int = 0) -> OrderingPlan:
     else:  # DEC_SWR: i.i.d. draws, host RNG like the reference
         ph = pt.cpu().numpy()
         idx = torch.from_numpy(_epoch_rng(policy, epoch).choice(n, size=n, replace=True, p=ph).astype(np.int64))
-    indices = idx if was_torch else idx.cpu().numpy().astype(np.int64)
+    indices = idx if was_torch else idx.cpu().numpy().astype(np.int64, copy=False)
     return OrderingPlan(epoch=epoch, indices=indices, policy=policy)
 
 

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   using C = CfgB<N2>;
   constexpr int RP = N2 / 2;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays a shared-space pointer
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* xfull = bars;
   uint64_t* xempty = xfull + C::SX;

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                            double* __restrict__ scores, int32_t* flags) {
   using C = Cfg<N>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays a shared-space pointer
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* full = bars;
   uint64_t* xdone = bars + C::STAGES;
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                        int64_t n, int kchunks, double* __restrict__ scores, int32_t* flags) {
   using C = Cfg2;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays a shared-space pointer
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* xfull = bars;                 // [SX] TMA complete_tx
   uint64_t* xempty = xfull + C::SX;       // [SX] main-MMA commit (1) + transform threads (128)

@@ -115,59 +115,64 @@ __device__ __forceinline__ void gemm_tile(double* gC, int64_t ldc, const double*
 }
 
 // Cholesky of the 64 x 64 tile s (upper triangle used; s = U^T U) and the
-// inverse T = U^-1, both upper triangular, written to s and t.  Thread
-// (column c, group g) keeps rows g, g+4, .. of its column in registers; one
-// __syncthreads per pivot (the pivot row is published through `rowbuf`).
-// *bad |= 1 on a pivot that is not positive and finite.
+// inverse T = U^-1, both upper triangular, written to s and t.  One 64-step
+// elimination on the augmented tile [A | I]: the row operations that take A
+// to D L^T take I to L^-1, so U = D^-1/2 (D L^T) and T = L^-T D^-1/2.  Thread
+// (column c, group g) keeps rows g, g+4, .. of column c of both halves in
+// registers; one __syncthreads per pivot (pivot rows published through
+// `rowbuf`).  *bad |= 1 on a pivot that is not positive and finite.
 __device__ __noinline__ void chol_inv_tile(double* s, double* t, double* scratch, int32_t* bad) {
   const int c = threadIdx.x & 63, g = threadIdx.x >> 6;
-  double* rowbuf = scratch;          // [2][64]
-  double* rd = scratch + 2 * FT;     // [64] reciprocal diagonal of U
-  double a[FT / 4];
+  const int cw0 = c & 32;            // first column of this warp
+  double* rowbuf = scratch;          // [2][2][64]: (A row, B row) per parity
+  double* rsd = scratch + 4 * FT;    // [64] 1 / sqrt(pivot)
+  double a[FT / 4], bm[FT / 4];
 #pragma unroll
-  for (int i = 0; i < FT / 4; ++i) a[i] = s[(g + 4 * i) * FLD + c];
+  for (int i = 0; i < FT / 4; ++i) {
+    a[i] = s[(g + 4 * i) * FLD + c];
+    bm[i] = (g + 4 * i == c) ? 1.0 : 0.0;
+  }
   bool badp = false;
 #pragma unroll
   for (int p = 0; p < FT; ++p) {
-    double* rb = rowbuf + (p & 1) * FT;
-    if (g == (p & 3)) rb[c] = a[p >> 2];
+    double* ra = rowbuf + (p & 1) * 2 * FT;
+    double* rb = ra + FT;
+    if (g == (p & 3)) {
+      ra[c] = a[p >> 2];
+      rb[c] = bm[p >> 2];
+    }
     __syncthreads();
-    const double piv = rb[p];
+    const double piv = ra[p];
     // 1/sqrt(piv): SFU approximation + one Newton step (rel. error ~1e-15)
     double rs;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(piv));
     rs = rs * fma(-0.5 * piv, rs * rs, 1.5);
-    const double w = rb[c] * (rs * rs);
+    const double inv = rs * rs;
+    if (cw0 + 31 > p) {  // warp-uniform: some column of this warp is right of the pivot
+      const double wa = ra[c];
 #pragma unroll
-    for (int i = 0; i < FT / 4; ++i)
-      if (g + 4 * i > p) a[i] = fma(-rb[g + 4 * i], w, a[i]);
-    if (g == (p & 3)) a[p >> 2] = c >= p ? rb[c] * rs : 0.0;
-    if (c == p && g == 0) badp = !(piv > 0.0) || !isfinite(piv);
+      for (int i = 0; i < FT / 4; ++i)
+        if (g + 4 * i > p) a[i] = fma(-ra[g + 4 * i] * inv, wa, a[i]);
+    }
+    if (cw0 <= p) {  // warp-uniform: L^-1 row p is zero right of column p
+      const double wb = rb[c];
+#pragma unroll
+      for (int i = 0; i < FT / 4; ++i)
+        if (g + 4 * i > p) bm[i] = fma(-ra[g + 4 * i] * inv, wb, bm[i]);
+    }
+    if (g == (p & 3)) a[p >> 2] = c >= p ? a[p >> 2] * rs : 0.0;
+    if (c == p && g == 0) {
+      badp = !(piv > 0.0) || !isfinite(piv);
+      rsd[p] = rs;
+    }
   }
   if (badp) atomicOr(bad, 1);
 #pragma unroll
   for (int i = 0; i < FT / 4; ++i) s[(g + 4 * i) * FLD + c] = a[i];
   __syncthreads();
-  if (threadIdx.x < FT) rd[threadIdx.x] = 1.0 / s[threadIdx.x * FLD + threadIdx.x];
-  // T = U^-1 by backward substitution on the identity, column c in registers
+  // T[c][m] = L^-1[m][c] / sqrt(D_m)
 #pragma unroll
-  for (int i = 0; i < FT / 4; ++i) a[i] = (g + 4 * i == c) ? 1.0 : 0.0;
-  __syncthreads();
-#pragma unroll
-  for (int p = FT - 1; p >= 0; --p) {
-    double* xb = rowbuf + (p & 1) * FT;
-    if (g == (p & 3)) {
-      a[p >> 2] *= rd[p];
-      xb[c] = a[p >> 2];
-    }
-    __syncthreads();
-    const double x = xb[c];
-#pragma unroll
-    for (int i = 0; i < FT / 4; ++i)
-      if (g + 4 * i < p) a[i] = fma(-s[(g + 4 * i) * FLD + p], x, a[i]);
-  }
-#pragma unroll
-  for (int i = 0; i < FT / 4; ++i) t[(g + 4 * i) * FLD + c] = a[i];
+  for (int i = 0; i < FT / 4; ++i) t[c * FLD + g + 4 * i] = bm[i] * rsd[g + 4 * i];
   __syncthreads();
 }
 
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
   double* s0 = fsm;
   double* s1 = fsm + FT * FLD;
   double* s2 = fsm + 2 * FT * FLD;
-  double* scratch = fsm + 3 * FT * FLD;  // 3 x 64 doubles
+  double* scratch = fsm + 3 * FT * FLD;  // 5 x 64 doubles
   cg::grid_group grid = cg::this_grid();
   const int cta = blockIdx.x, ncta = gridDim.x;
   const int nb = a.nb;
@@ -433,7 +438,7 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.ct = P.ct;
   a.dp = P.dp;
   a.wc = P.wc;
-  const int smem = 3 * FTILE_SMEM + 3 * FT * 8;
+  const int smem = 3 * FTILE_SMEM + 5 * FT * 8;
   static int grid_cap = 0;
   if (grid_cap == 0) {
     cudaError_t e = cudaFuncSetAttribute(chol_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

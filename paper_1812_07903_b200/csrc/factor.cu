@@ -148,17 +148,17 @@ __device__ __noinline__ void chol_inv_tile(double* s, double* t, double* scratch
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(piv));
     rs = rs * fma(-0.5 * piv, rs * rs, 1.5);
     const double inv = rs * rs;
-    if (cw0 + 31 > p) {  // warp-uniform: some column of this warp is right of the pivot
-      const double wa = ra[c];
+    // row m -= (a[p][m] / piv) row p, on both halves; columns left of the pivot
+    // keep zero in the A half, columns right of it in the B half (L^-1 lower)
+    const double wa = cw0 + 31 > p ? ra[c] * inv : 0.0;
+    const double wb = cw0 <= p ? rb[c] * inv : 0.0;
 #pragma unroll
-      for (int i = 0; i < FT / 4; ++i)
-        if (g + 4 * i > p) a[i] = fma(-ra[g + 4 * i] * inv, wa, a[i]);
-    }
-    if (cw0 <= p) {  // warp-uniform: L^-1 row p is zero right of column p
-      const double wb = rb[c];
-#pragma unroll
-      for (int i = 0; i < FT / 4; ++i)
-        if (g + 4 * i > p) bm[i] = fma(-ra[g + 4 * i] * inv, wb, bm[i]);
+    for (int i = 0; i < FT / 4; ++i) {
+      if (g + 4 * i > p) {
+        const double l = ra[g + 4 * i];
+        a[i] = fma(-l, wa, a[i]);
+        bm[i] = fma(-l, wb, bm[i]);
+      }
     }
     if (g == (p & 3)) a[p >> 2] = c >= p ? a[p >> 2] * rs : 0.0;
     if (c == p && g == 0) {
@@ -277,11 +277,22 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       load_tile(s1, atile(a, j, ll), a.dp);
       __syncthreads();
       if (t == 0) {
+        unsigned long long t0, t1, t2, t3;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         gemm_tile<true>(atile(a, kk, ll), a.dp, s0, s1, s2);
         __syncthreads();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         chol_inv_tile(s2, s0, scratch, a.info);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
         store_tile(atile(a, kk, ll), a.dp, s2);
         store_tile(ttile(a, kk), FT, s0);
+        __syncthreads();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+        if (a.trace != nullptr && threadIdx.x == 0) {
+          a.trace[512 + 3 * j] = t1 - t0;
+          a.trace[513 + 3 * j] = t2 - t1;
+          a.trace[514 + 3 * j] = t3 - t2;
+        }
       } else {
         gemm_tile<true>(atile(a, kk, ll), a.dp, s0, s1, nullptr);
       }
@@ -478,6 +489,10 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
     cudaMemcpy(h, trace, nph * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     fprintf(stderr, "KF d=%lld r=%lld grid=%d phases(us):", (long long)d, (long long)r, grid);
     for (int i = 1; i < nph; ++i) fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1000.0);
+    cudaMemcpy(h + 512, trace + 512, 3 * P.nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "\n  diag task gemm/chol_inv/store(us):");
+    for (int j = 0; j + 1 < P.nb && j < 8; ++j)
+      fprintf(stderr, " %.1f/%.1f/%.1f", h[512 + 3 * j] / 1000.0, h[513 + 3 * j] / 1000.0, h[514 + 3 * j] / 1000.0);
     fprintf(stderr, "\n");
   }
   return LVSK_OK;

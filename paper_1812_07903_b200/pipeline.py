@@ -225,5 +225,7 @@ class LeveragePipeline:
         else:
             sk = 1 + radix(self.n * self.spec.s, max(1, (self.k - 1).bit_length())) + 1 + 1 + 1
         lev = 1
+        k, d = self.sx.shape
+        fold = 1 if (self.pi is not None and self.rank is None and k >= d) else 0  # KF (chol_fold_kernel)
         order_ = (3 + 1 + radix(self.n, 64)) if self.order else 0
-        return sk + lev + order_
+        return sk + fold + lev + order_

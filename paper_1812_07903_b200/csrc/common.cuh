@@ -93,6 +93,17 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   err = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bp)), __dsub_rn(b, bp));
 }
 
+// Same (s, err) as two_sum — the rounding error of a + b is unique, so any
+// exact method gives the identical bits — via Fast2Sum on the operands ordered
+// by magnitude: 3 fp64 adds + one compare, the ordering done with integer
+// selects (for finite inputs; a non-finite input is caught by the callers).
+__device__ __forceinline__ void two_sum_ordered(double a, double b, double& s, double& err) {
+  s = __dadd_rn(a, b);
+  const bool a_big = fabs(a) >= fabs(b);
+  const double big = a_big ? a : b, small = a_big ? b : a;
+  err = __dsub_rn(small, __dsub_rn(s, big));
+}
+
 template <typename T>
 __device__ __forceinline__ float to_f32(T v);
 template <>

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
         const double cval = contrib<T, UNIT>(xs[v], neg, scale);
         if constexpr (sizeof(T) == 8) bad |= !isfinite(cval);
         double sum, e;
-        two_sum(h[v], cval, sum, e);
+        two_sum_ordered(h[v], cval, sum, e);
         h[v] = sum;
         l[v] = __dadd_rn(l[v], e);
       }

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
   constexpr int VEC = BULK_LANE_BYTES / static_cast<int>(sizeof(T));
   __shared__ alignas(128) uint8_t ring[BULK_SLOTS][BULK_SEG];
   __shared__ uint64_t full[BULK_SLOTS], empty[BULK_SLOTS];
+  __shared__ uint32_t slot_neg[BULK_SLOTS];
   const int64_t b = blockIdx.x / ngroups;
   const int g = blockIdx.x - static_cast<int>(b * ngroups);
   constexpr int SEG_ELEMS = BULK_SEG / static_cast<int>(sizeof(T));
@@ -220,26 +221,22 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
   __syncthreads();
   const uint32_t p0 = start[b], p1 = start[b + 1];
   const uint32_t cnt = p1 - p0;
-  if (warp == BULK_CONSUMERS) {  // producer: 32 rows' indices per coalesced load, lane 0 issues
-    for (uint32_t jb = 0; jb < cnt; jb += 32) {
-      const uint32_t mine = jb + lane < cnt ? vals[p0 + jb + lane] : 0u;
-      const uint32_t nb = cnt - jb < 32u ? cnt - jb : 32u;
-      for (uint32_t q = 0; q < nb; ++q) {
-        const uint32_t v = __shfl_sync(0xFFFFFFFFu, mine, q);
-        if (lane == 0) {
-          const uint32_t j = jb + q;
-          const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
-          bar_wait(&empty[s], ph ^ 1u);
-          const T* src = X + static_cast<int64_t>(v >> 1) * ldx + c0;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[s])),
-                       "r"(seg_bytes)
-                       : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_addr(ring[s])),
-              "l"(src), "r"(seg_bytes), "r"(smem_addr(&full[s]))
-              : "memory");
-        }
+  if (warp == BULK_CONSUMERS) {  // producer: one lane, one bulk copy per row; the row's sign goes to the slot
+    if (lane == 0) {
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
+        const uint32_t v = vals[p0 + j];
+        bar_wait(&empty[s], ph ^ 1u);
+        slot_neg[s] = v & 1u;
+        const T* src = X + static_cast<int64_t>(v >> 1) * ldx + c0;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[s])),
+                     "r"(seg_bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(ring[s])),
+            "l"(src), "r"(seg_bytes), "r"(smem_addr(&full[s]))
+            : "memory");
       }
     }
     return;
@@ -255,12 +252,10 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
     l[v] = v < nv ? lo_in[so + v] : 0.0;
   }
   bool bad = false;
-  uint32_t signs = 0;  // sign bits of the current batch of 32 rows
   for (uint32_t j = 0; j < cnt; ++j) {
     const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
-    if ((j & 31u) == 0) signs = __ballot_sync(0xFFFFFFFFu, j + lane < cnt && (vals[p0 + j + lane] & 1u));
-    const bool neg = (signs >> (j & 31u)) & 1u;
     bar_wait(&full[s], ph);
+    const bool neg = slot_neg[s] != 0u;  // written by the producer before its (release) arrive
     if (nv) {
       T xs[VEC];
       const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(ring[s]) + col);

@@ -184,12 +184,27 @@ __device__ __forceinline__ void bar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
 }
 
+// x with its sign flipped when neg, on the raw bits (exact; no fp64 op)
+template <typename T>
+__device__ __forceinline__ T flip_sign(T x, bool neg);
+template <>
+__device__ __forceinline__ float flip_sign<float>(float x, bool neg) {
+  return __uint_as_float(__float_as_uint(x) ^ (static_cast<uint32_t>(neg) << 31));
+}
+template <>
+__device__ __forceinline__ double flip_sign<double>(double x, bool neg) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (static_cast<long long>(neg) << 63));
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 flip_sign<__nv_bfloat16>(__nv_bfloat16 x, bool neg) {
+  return __ushort_as_bfloat16(__bfloat16_as_ushort(x) ^ static_cast<unsigned short>(neg << 15));
+}
+
 // contribution (sign * scale) * x as float64; UNIT: scale == 1 -> exact sign flip
 template <typename T, bool UNIT>
 __device__ __forceinline__ double contrib(T x, bool neg, double scale) {
   if constexpr (UNIT) {
-    const double v = to_f64<T>(x);
-    return neg ? -v : v;
+    return to_f64<T>(flip_sign<T>(x, neg));
   } else {
     return __dmul_rn(neg ? -scale : scale, to_f64<T>(x));
   }
@@ -270,7 +285,7 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
         const double cval = contrib<T, UNIT>(xs[v], neg, scale);
         if constexpr (sizeof(T) == 8) bad |= !isfinite(cval);
         double sum, e;
-        two_sum_ordered(h[v], cval, sum, e);
+        two_sum(h[v], cval, sum, e);
         h[v] = sum;
         l[v] = __dadd_rn(l[v], e);
       }

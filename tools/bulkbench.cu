@@ -173,7 +173,15 @@ int main() {
   int *perm, *start;
   double* out;
   cudaMalloc(&x, (size_t)nrows * 2048);
-  cudaMemset(x, 0, (size_t)nrows * 2048);
+  {
+    std::vector<float> hx((size_t)nrows * 512);
+    unsigned r = 7;
+    for (size_t i = 0; i < hx.size(); ++i) {
+      r = r * 1664525u + 1013904223u;
+      hx[i] = (float)(r >> 8) * (1.0f / 16777216.0f) - 0.5f;
+    }
+    cudaMemcpy(x, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice);
+  }
   cudaMalloc(&perm, nrows * 4);
   cudaMalloc(&start, (k + 1) * 4);
   cudaMalloc(&out, 8);
@@ -263,5 +271,6 @@ int main() {
   runk("K1-like no ballot", k1_like<16, true, false, true>);
   runk("K1-like no batch", k1_like<16, true, true, false>);
   runk("K1-like none", k1_like<16, false, false, false>);
+  runk("K1-like stateio only", k1_like<16, true, false, false>);
   return 0;
 }

@@ -200,9 +200,10 @@ int main() {
   cudaMemcpy(start, st.data(), (k + 1) * 4, cudaMemcpyHostToDevice);
   // K1's real order: rows hashed to buckets, each bucket in ascending row order
   std::vector<int> hb(nrows), cnt(k + 1, 0), bk(nrows), st2(k + 1, 0);
+  const unsigned long long ha = 0xd855bac60e2f2043ull | 1ull, hbb = 0xa6cfae49d58dfd30ull;
   for (int i = 0; i < nrows; ++i) {
-    s = s * 1664525u + 1013904223u;
-    bk[i] = (s >> 8) % k;
+    const unsigned long long v = ha * (unsigned long long)i + hbb;  // the reference's multiply-shift bucket hash
+    bk[i] = (int)(((v >> 32) * (unsigned long long)k) >> 32);
     ++cnt[bk[i] + 1];
   }
   for (int b = 0; b < k; ++b) cnt[b + 1] += cnt[b];

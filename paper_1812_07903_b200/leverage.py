@@ -505,7 +505,9 @@ def _streamed_sketch(a: torch.Tensor, spec: SketchSpec, mem_cap):
 
 
 def _streamable(a, spec) -> bool:
-    return (isinstance(a, torch.Tensor) and a.device.type == "cpu" and a.dim() == 2 and a.is_pinned()
+    # opt-in (LVSK_STREAM=1): measured no faster end to end than one whole
+    # copy (the 2 GB host->device transfer dominates either way; tools/e2e_ab.py)
+    return (os.environ.get("LVSK_STREAM", "0") == "1" and isinstance(a, torch.Tensor) and a.device.type == "cpu" and a.dim() == 2 and a.is_pinned()
             and a.is_contiguous() and a.dtype in (torch.float32, torch.bfloat16, torch.float64)
             and spec.family in ("countsketch", "osnap", "gaussian")
             and a.numel() * a.element_size() >= 2 * _STREAM_CHUNK_BYTES)

@@ -640,7 +640,7 @@ def test_c5_shaped_pipeline_small():
     assert np.median(np.abs(res.scores - ref) / ref) < 1e-3
 
 
-def test_streamed_host_input_equals_device_input():
+def test_streamed_host_input_equals_device_input(monkeypatch):
     """Pinned host X (>= 256 MB) goes through the chunked copy-stream path
     (each 128 MB chunk sketched as it lands); results equal the device-X path
     bit for bit (the hashed sketch is order-exact across row blocks)."""
@@ -649,6 +649,7 @@ def test_streamed_host_input_equals_device_input():
     Xd = torch.randn(n, d, device="cuda", dtype=torch.float32, generator=g)
     Xh = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
     Xh.copy_(Xd)
+    monkeypatch.setenv("LVSK_STREAM", "1")
     assert P.leverage._streamable(Xh, P.SketchSpec("countsketch", eps=0.5, d=d))
     for fam in ("countsketch", "osnap"):
         spec = P.SketchSpec(fam, eps=0.5, d=d, seed=3, rows_override=2048, osnap_s=4 if fam == "osnap" else None)

@@ -25,12 +25,14 @@ namespace srht_tma {
 constexpr int ROWS = 256;                 // tile rows (pass 1: the low 8 index bits)
 constexpr int COLS = 32;                  // fp32 columns per tile (128 B)
 constexpr int TILE_BYTES = ROWS * COLS * 4;  // 32 KB
-constexpr int STAGES = 4;
-constexpr int CWARPS = 4;                 // compute warps
+constexpr int GROUPS = 3;                 // compute groups (4 warps each), one tile in flight per group
+constexpr int STAGES = 2 * GROUPS;        // 6 x 32 KB ring
+constexpr int CWARPS = 4 * GROUPS;        // compute warps
 constexpr int NTHREADS = 32 * (CWARPS + 1);
 constexpr int SMEM_BYTES = STAGES * TILE_BYTES + 1024 + 256;
 
-__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(CWARPS * 32) : "memory"); }
+// named barrier of one 128-thread compute group
+__device__ __forceinline__ void bar_group(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
 
 __device__ __forceinline__ void st_f4_keep(float* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
@@ -100,12 +102,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     return;
   }
-  const int tid = threadIdx.x;  // 0..127
+  const int grp = warp >> 2, tid = threadIdx.x & 127;  // compute group, thread in group
   const int q = tid & 7, rg = tid >> 3;  // column quad, row group
   const uint64_t keep = tc::l2_policy_evict_last();
   bool bad = false;
-  uint32_t it = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+  uint32_t it = grp;
+  for (int64_t t = blockIdx.x + static_cast<int64_t>(grp) * gridDim.x; t < ntiles;
+       t += static_cast<int64_t>(GROUPS) * gridDim.x, it += GROUPS) {
     const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
     const int64_t rb = t / cblocks, cb = t - rb * cblocks;
     const int64_t grow0 = row0 + rb * ROWS;
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       *reinterpret_cast<float4*>(tile + (rg * 16 + j) * COLS + q * 4) = make_float4(v[j][0], v[j][1], v[j][2], v[j][3]);
-    bar_compute();
+    bar_group(grp);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const float4 x = *reinterpret_cast<const float4*>(tile + (rg + 16 * j) * COLS + q * 4);
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 0; j < 16; ++j)
         st_f4_keep(T1 + (rb * ROWS + rg + 16 * j) * d + col, make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), keep);
     }
-    bar_compute();  // every compute thread is done with the slot
+    bar_group(grp);  // every thread of the group is done with the slot
     if (tid == 0) tc::mbar_arrive(&empty[s]);
   }
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
@@ -194,15 +197,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     return;
   }
-  const int tid = threadIdx.x;
+  const int grp = warp >> 2, tid = threadIdx.x & 127;
   const int q = tid & 7, rg = tid >> 3;
-  uint32_t it = 0;
+  uint32_t it = 0;  // index of the non-empty item among this CTA's items; group grp takes it % GROUPS == grp
   for (int64_t t = blockIdx.x; t < nitems; t += gridDim.x) {
     const int64_t q1 = t / cblocks, cb = t - q1 * cblocks;
     const uint32_t e0 = qstart[q1], e1 = qstart[q1 + 1];
     if (e0 == e1) continue;
-    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
-    ++it;
+    const uint32_t mine = it++;
+    if (mine % GROUPS != static_cast<uint32_t>(grp)) continue;
+    const uint32_t s = mine % STAGES, ph = (mine / STAGES) & 1u;
     tc::mbar_wait(&full[s], ph);
     float* tile = reinterpret_cast<float*>(smem + s * TILE_BYTES);
     float v[NA][4];
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         *reinterpret_cast<float4*>(tile + (rg * NA + j) * COLS + q * 4) =
             make_float4(v[j][0], v[j][1], v[j][2], v[j][3]);
     }
-    bar_compute();
+    bar_group(grp);
     if constexpr (NB > 1) {
       float u[NB][4];
       if (rg < NA) {
@@ -239,12 +243,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           *reinterpret_cast<float4*>(tile + (rg + NA * j) * COLS + q * 4) =
               make_float4(u[j][0], u[j][1], u[j][2], u[j][3]);
       }
-      bar_compute();
+      bar_group(grp);
     }
     // scatter: SX[t] (+)= (-1)^popc(p_hi & chunk) * row q2 of the tile; 4 rows x 32 columns per sweep
     const int c = tid & 31;
     const int64_t col = cb * COLS + c;
-    for (uint32_t e = e0 + (tid >> 5); e < e1; e += CWARPS) {
+    for (uint32_t e = e0 + (tid >> 5); e < e1; e += 4) {
       const uint32_t tt = order[e];
       const uint64_t p = static_cast<uint64_t>(sample[tt]);
       const int q2 = static_cast<int>((p >> B1) & static_cast<uint64_t>(R - 1));
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         *dst = acc;
       }
     }
-    bar_compute();
+    bar_group(grp);
     if (tid == 0) tc::mbar_arrive(&empty[s]);
   }
 }

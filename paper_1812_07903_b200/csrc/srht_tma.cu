@@ -11,7 +11,7 @@
 // [i2][q1][d], i.e. the 2^B2 rows q1 + 256 i2 of one residue in one box), and
 // four compute warps run the 16 x 16 radix-2 WHT in registers, in place in
 // the stage buffer, so loads, butterflies and stores of different tiles
-// overlap instead of running as one-shot CTAs.
+// overlap instead of running as one-shot CTAs.  (Opt-in; see srht_tma_ok.)
 #include <cuda.h>
 
 #include <cstdlib>
@@ -271,8 +271,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 // Runs pass 1 + pass 2 of one chunk with the TMA kernels; false if the shape
 // is not covered (caller keeps the one-shot kernels).
+// Opt-in (LVSK_SRHT_TMA=1): measured on C3 (2^21 x 256) pass 1 23 us vs 25 us
+// one-shot per 64 MB chunk, but pass 2 35 us vs 26 us — the 3-D residue box is
+// 256 separate 128-byte rows, which the TMA engine serves slower than the
+// one-shot kernel's direct L2 loads; the default stays the one-shot pair.
 bool srht_tma_ok(const float* X, int64_t d, int64_t ldx, int B1) {
-  if (getenv("LVSK_SRHT_ONESHOT") != nullptr) return false;
+  if (getenv("LVSK_SRHT_TMA") == nullptr) return false;
   return B1 == 8 && d % 4 == 0 && ldx % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0;
 }
 

@@ -180,42 +180,41 @@ def cholesky_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor):
 _EIGH_KAPPA = 1e4
 
 
-def _cholqr2(Y: torch.Tensor):
+def _cholqr2(Y: torch.Tensor) -> torch.Tensor:
     """Orthonormal basis of range(Y) by two rounds of Cholesky QR (stable for
-    cond(Y) up to ~1e7 in float64); None when a Gram is not positive definite."""
+    cond(Y) up to ~1e7 in float64).  No host synchronisation: a failed
+    factorisation yields NaNs, which the caller's residual test rejects."""
     for _ in range(2):
-        L, info = torch.linalg.cholesky_ex(Y.T @ Y)
-        if int(info.item()) != 0:
-            return None
+        L, _ = torch.linalg.cholesky_ex(Y.T @ Y)
         Y = torch.linalg.solve_triangular(L, Y.T, upper=False).T
     return Y
 
 
-def _topk_gram(G: torch.Tensor, want: int, max_iter: int = 12, tol: float = 1e-12):
+def _topk_gram(G: torch.Tensor, want: int, rounds: int = 2, iters: int = 6, tol: float = 1e-12):
     """Top `want` eigenpairs (descending) of the SPD Gram G by block subspace
-    iteration (block want + max(16, want / 4) rounded up to 32, seeded start,
-    Cholesky-QR re-orthonormalisation) with Rayleigh-Ritz; accepted only when
-    every kept Ritz pair has ||G v - theta v|| <= tol * theta_1, else None
-    (the caller falls back to the full eigensolver)."""
+    iteration: block want + max(16, want / 4) rounded up to 32, seeded start,
+    `iters` power steps with Cholesky-QR re-orthonormalisation per round, then
+    one Rayleigh-Ritz (the only small dense eigensolve: ~2 ms on a B200, so it
+    is not run per step).  Accepted only when every kept Ritz pair has
+    ||G v - theta v|| <= tol * theta_1; else another round, then None (the
+    caller falls back to the full eigensolver)."""
     d = G.shape[0]
     b = min(d, -(-(want + max(16, want // 4)) // 32) * 32)
     gen = torch.Generator(device=G.device).manual_seed(0x5EED)
-    Q = _cholqr2(G @ torch.randn(d, b, dtype=G.dtype, device=G.device, generator=gen))
-    if Q is None:
-        return None
-    for it in range(max_iter):
+    Q = torch.randn(d, b, dtype=G.dtype, device=G.device, generator=gen)
+    for _ in range(rounds):
+        for _ in range(iters):
+            Q = _cholqr2(G @ Q)
         Y = G @ Q
-        if it >= 2:
-            Bm = Q.T @ Y
-            theta, W = torch.linalg.eigh(0.5 * (Bm + Bm.T))
-            theta, W = theta.flip(0), W.flip(1)
-            V = Q @ W
-            res = torch.linalg.vector_norm(Y @ W - V * theta, dim=0)[:want]
-            if float(res.max()) <= tol * float(theta[0]):
-                return theta[:want].contiguous(), V[:, :want].contiguous()
-        Q = _cholqr2(Y)
-        if Q is None:
-            return None
+        Bm = Q.T @ Y
+        theta, W = torch.linalg.eigh(0.5 * (Bm + Bm.T))
+        theta, W = theta.flip(0), W.flip(1)
+        V = Q @ W
+        res = torch.linalg.vector_norm(Y @ W - V * theta, dim=0)[:want]
+        worst = float(res.max())
+        if math.isfinite(worst) and worst <= tol * float(theta[0]):
+            return theta[:want].contiguous(), V[:, :want].contiguous()
+        Q = V
     return None
 
 

@@ -83,8 +83,7 @@ __device__ __forceinline__ void store_tile(double* g, int64_t ld, const double* 
 // global when SUB); the result goes to smem `out` when out != nullptr, else
 // back to global C.  4 x 4 register blocking, 256 threads.
 template <bool SUB>
-__device__ __forceinline__ void gemm_tile_simt(double* gC, int64_t ldc, const double* At, const double* B,
-                                               double* out) {
+__device__ __forceinline__ void gemm_tile(double* gC, int64_t ldc, const double* At, const double* B, double* out) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4];
 #pragma unroll
@@ -113,55 +112,6 @@ __device__ __forceinline__ void gemm_tile_simt(double* gC, int64_t ldc, const do
       else
         gC[(ty + 16 * a) * ldc + tx + 16 * b] = acc[a][b];
     }
-}
-
-// Same contract on the fp64 tensor cores (mma.sync m8n8k4 f64): warp w owns
-// output rows 16 (w >> 1) .. +16 and columns 32 (w & 1) .. +32 (2 x 4 tiles
-// of 8 x 8); per k-step of 4 it loads 2 A and 4 B fragments (one double per
-// lane each) for 8 MMAs, so shared memory carries 8x fewer bytes per FMA
-// than the 4 x 4 register-blocked SIMT tile.
-template <bool SUB>
-__device__ __forceinline__ void gemm_tile(double* gC, int64_t ldc, const double* At, const double* B, double* out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = (warp >> 1) * 16, n0 = (warp & 1) * 32;
-  const int fr = lane >> 2, fc = lane & 3;  // fragment row / column
-  double acc[2][4][2];
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        acc[mt][nt][e] = SUB ? gC[(m0 + 8 * mt + fr) * ldc + n0 + 8 * nt + 2 * fc + e] : 0.0;
-  const double sg = SUB ? -1.0 : 1.0;
-#pragma unroll 4
-  for (int ks = 0; ks < FT / 4; ++ks) {
-    const int p = 4 * ks + fc;
-    double af[2], bf[4];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) af[mt] = sg * At[p * FLD + m0 + 8 * mt + fr];  // A[m][p] = At[p][m]
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) bf[nt] = B[p * FLD + n0 + 8 * nt + fr];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                     : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
-                     : "d"(af[mt]), "d"(bf[nt]));
-  }
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = m0 + 8 * mt + fr, c = n0 + 8 * nt + 2 * fc + e;
-        if (out)
-          out[r * FLD + c] = acc[mt][nt][e];
-        else
-          gC[r * ldc + c] = acc[mt][nt][e];
-      }
 }
 
 // Cholesky of the 64 x 64 tile s (upper triangle used; s = U^T U) and the

@@ -306,6 +306,9 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if world > 1 and cfg["family"] == "srht":
+        # the reference's run_distributed rejects SRHT (dist.py:95-98); K3 has no row offset
+        raise SystemExit("bench: SRHT (c3) runs on one GPU only")
     dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
     n, d, k, r = cfg["n"], cfg["d"], cfg["k"], cfg["r"]
     spec = P.SketchSpec(cfg["family"], eps=0.5, d=d, seed=0, rows_override=k, osnap_s=cfg["s"])
@@ -337,21 +340,29 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         if timing:
             ev["sketch"][1].record()
         s = pipe.state
-        his = [torch.empty_like(s._hi) for _ in range(world)]
-        los = [torch.empty_like(s._lo) for _ in range(world)]
-        dist.all_gather(his, s._hi)
-        dist.all_gather(los, s._lo)
-        hi, lo = his[0], los[0]
-        for q in range(1, world):
-            N.check(N.lib().lvsk_merge_compensated(hi.data_ptr(), lo.data_ptr(), his[q].data_ptr(), los[q].data_ptr(),
-                                                   hi.data_ptr(), lo.data_ptr(), hi.numel(), N.stream_ptr()))
-        N.check(N.lib().lvsk_fold_compensated(hi.data_ptr(), lo.data_ptr(), pipe.sx.data_ptr(), pipe.sx.numel(),
-                                              N.stream_ptr()))
+        if cfg["family"] == "gaussian":  # a plain float64 partial per rank
+            dist.all_reduce(pipe.sx)
+        else:  # hashed: rank-ordered TwoSum fold of the (hi, lo) partials, as dist.py merges
+            his = [torch.empty_like(s._hi) for _ in range(world)]
+            los = [torch.empty_like(s._lo) for _ in range(world)]
+            dist.all_gather(his, s._hi)
+            dist.all_gather(los, s._lo)
+            hi, lo = his[0], los[0]
+            for q in range(1, world):
+                N.check(N.lib().lvsk_merge_compensated(hi.data_ptr(), lo.data_ptr(), his[q].data_ptr(),
+                                                       los[q].data_ptr(), hi.data_ptr(), lo.data_ptr(), hi.numel(),
+                                                       N.stream_ptr()))
+            N.check(N.lib().lvsk_fold_compensated(hi.data_ptr(), lo.data_ptr(), pipe.sx.data_ptr(), pipe.sx.numel(),
+                                                  N.stream_ptr()))
         if timing:
             ev["factor"][0].record()
-        M = torch.empty((d, r), dtype=torch.float64, device=dev)
+        shape = torch.zeros(2, dtype=torch.int64, device=dev)
         if rank == 0:
-            M.copy_(sketch_fold(pipe.sx, cfg["sv_tol"], cfg.get("rank"), pi)[0])
+            M0 = sketch_fold(pipe.sx, cfg["sv_tol"], cfg.get("rank"), pi)[0]
+            shape[0], shape[1] = M0.shape[0], M0.shape[1]
+        dist.broadcast(shape, 0)  # the basis fold (r' <= r) has r' columns
+        M = M0.contiguous() if rank == 0 else torch.empty((int(shape[0]), int(shape[1])), dtype=torch.float64,
+                                                            device=dev)
         dist.broadcast(M, 0)
         pipe.set_fold(M)
         if timing:

@@ -567,12 +567,20 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank)
         return
+    # LVSK_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo — a correctness
+    # check of the multi-rank code path on a one-GPU box, never a measurement
+    share = world > 1 and os.environ.get("LVSK_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, cfg, rank, world, local_rank)
     finally:

@@ -302,6 +302,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
 
     import paper_1812_07903_b200 as P
     from paper_1812_07903_b200 import _native as N
+    from paper_1812_07903_b200.dist import sliced_hashed_merge
     from paper_1812_07903_b200.leverage import jl_device, sketch_fold
 
     torch.cuda.set_device(local_rank)
@@ -342,18 +343,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         s = pipe.state
         if cfg["family"] == "gaussian":  # a plain float64 partial per rank
             dist.all_reduce(pipe.sx)
-        else:  # hashed: rank-ordered TwoSum fold of the (hi, lo) partials, as dist.py merges
-            his = [torch.empty_like(s._hi) for _ in range(world)]
-            los = [torch.empty_like(s._lo) for _ in range(world)]
-            dist.all_gather(his, s._hi)
-            dist.all_gather(los, s._lo)
-            hi, lo = his[0], los[0]
-            for q in range(1, world):
-                N.check(N.lib().lvsk_merge_compensated(hi.data_ptr(), lo.data_ptr(), his[q].data_ptr(),
-                                                       los[q].data_ptr(), hi.data_ptr(), lo.data_ptr(), hi.numel(),
-                                                       N.stream_ptr()))
-            N.check(N.lib().lvsk_fold_compensated(hi.data_ptr(), lo.data_ptr(), pipe.sx.data_ptr(), pipe.sx.numel(),
-                                                  N.stream_ptr()))
+        else:  # hashed: row slices exchanged all-to-all, rank-ordered TwoSum merge, folded slices gathered
+            pipe.sx.copy_(sliced_hashed_merge(s._hi, s._lo, rank, world))
         if timing:
             ev["factor"][0].record()
         shape = torch.zeros(2, dtype=torch.int64, device=dev)

@@ -196,6 +196,52 @@ def coordinate(ops, local_rows, row0: int, rank: int, world: int, counts: list[i
     return local, merged, s_host, vt_host, (t_sketch, t_merge, t_svd, t_score)
 
 
+def exchange_row_slices(t: torch.Tensor, rank: int, world: int, group=None) -> torch.Tensor:
+    """all_to_all of a (k, d) partial: rank q receives row slice q
+    (partition_rows(k, world)) of every rank's t, stacked in rank order as
+    (world, rows_q, d) — the reduce-scatter layout of a sketch merge, with
+    (world - 1) / world of one state per rank on the wire instead of an
+    all-gather's (world - 1) states."""
+    k, d = t.shape
+    bounds = partition_rows(k, world)
+    lo, hi = bounds[rank]
+    out = torch.empty((world, hi - lo, d), dtype=t.dtype, device=t.device)
+    tdist.all_to_all_single(out.view(-1), t.contiguous().view(-1), [(hi - lo) * d] * world,
+                            [(b - a) * d for a, b in bounds], group=group)
+    return out
+
+
+def gather_row_slices(sl: torch.Tensor, k: int, world: int, group=None) -> torch.Tensor:
+    """Inverse of the slicing: every rank gets the full (k, d) from its slices."""
+    bounds = partition_rows(k, world)
+    rows = max(b - a for a, b in bounds)
+    d = sl.shape[1]
+    buf = torch.zeros((rows, d), dtype=sl.dtype, device=sl.device)
+    buf[: sl.shape[0]] = sl
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    tdist.all_gather(outs, buf, group=group)
+    return torch.cat([outs[q][: b - a] for q, (a, b) in enumerate(bounds)], dim=0)
+
+
+def sliced_hashed_merge(hi: torch.Tensor, lo: torch.Tensor, rank: int, world: int, group=None) -> torch.Tensor:
+    """Merged float64 sketch SX = fold(merge_0..world-1(hi, lo)) on every rank:
+    rank q merges row slice q of all partials in rank order with the
+    reference's TwoSum (the same bits as the all-gather merge), folds it, and
+    the folded slices are all-gathered."""
+    from . import _native as N
+
+    his = exchange_row_slices(hi, rank, world, group)
+    los = exchange_row_slices(lo, rank, world, group)
+    h, l = his[0].clone(), los[0].clone()
+    L, st = N.lib(), N.stream_ptr()
+    for q in range(1, world):
+        N.check(L.lvsk_merge_compensated(h.data_ptr(), l.data_ptr(), his[q].data_ptr(), los[q].data_ptr(),
+                                         h.data_ptr(), l.data_ptr(), h.numel(), st), "merge")
+    sx = torch.empty_like(h)
+    N.check(L.lvsk_fold_compensated(h.data_ptr(), l.data_ptr(), sx.data_ptr(), sx.numel(), st), "fold")
+    return gather_row_slices(sx, hi.shape[0], world, group)
+
+
 def gather_scores(local: torch.Tensor, counts: list[int], group=None) -> torch.Tensor:
     """Concatenate rank-local score vectors in rank order (uneven sizes)."""
     world = len(counts)

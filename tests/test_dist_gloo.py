@@ -110,3 +110,52 @@ def test_two_rank_coordinator_equals_serial(family, s, n):
         assert np.array_equal(sx, ref_sx), rank  # TwoSum fold in rank order == serial, bit-exact here
         np.testing.assert_allclose(scores, ref_scores, rtol=1e-10)
         assert scores.shape == (n,)
+
+
+def _slice_worker(rank, world, port, x, k, seed, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1812_07903_b200.dist import exchange_row_slices, gather_row_slices, partition_rows
+
+        n, d = x.shape
+        lo_r, hi_r = partition_rows(n, world)[rank]
+        hp = O.HashParams("countsketch", seed, k, 1)
+        hi = np.zeros((k, d))
+        lo = np.zeros_like(hi)
+        O.hashed_consume(hi, lo, hp, x[lo_r:hi_r], lo_r)
+        his = exchange_row_slices(torch.from_numpy(hi), rank, world)
+        los = exchange_row_slices(torch.from_numpy(lo), rank, world)
+        h, l = his[0].numpy(), los[0].numpy()
+        for q in range(1, world):  # rank-ordered TwoSum merge of this rank's row slice
+            h, l = O.merge_hashed(h, l, his[q].numpy(), los[q].numpy())
+        full = gather_row_slices(torch.from_numpy(h + l), k, world)
+        out_q.put((rank, full.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sliced_merge_layout_equals_serial_three_ranks():
+    """The reduce-scatter layout bench.py's multi-GPU path uses
+    (dist.exchange_row_slices / gather_row_slices, uneven row slices over 3
+    ranks): merging each slice in rank order and gathering the folded slices
+    gives the serial sketch bit for bit."""
+    rng = np.random.default_rng(9)
+    n, d, k, seed = 901, 7, 101, 3
+    x = rng.standard_normal((n, d))
+    hp = O.HashParams("countsketch", seed, k, 1)
+    ref_hi = np.zeros((k, d))
+    ref_lo = np.zeros_like(ref_hi)
+    O.hashed_consume(ref_hi, ref_lo, hp, x, 0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slice_worker, args=(r, 3, port, x, k, seed, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, full in results:
+        assert np.array_equal(full, ref_hi + ref_lo), rank

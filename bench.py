@@ -503,11 +503,16 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = host_threads()
-        rows = args.cpu_rows
-        v, dt = cpu_leg(cfg, rows, threads)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{rows} rows of the {args.config} workload ({dt:.1f} s), oracle numpy port of the reference "
-                         "path incl. SVD and dec argsort, sketch partitions in threads"}
+        # calibrate, then repeat a bounded sample until ~10 s of CPU work has been timed
+        rate, _ = cpu_leg(cfg, 20_000, threads)
+        rows = int(min(args.cpu_rows, max(20_000, rate * args.cpu_seconds / 2)))
+        total_rows, total_s, passes = 0, 0.0, 0
+        while total_s < args.cpu_seconds and passes < 25:
+            _, dt = cpu_leg(cfg, rows, threads)
+            total_rows, total_s, passes = total_rows + rows, total_s + dt, passes + 1
+        cpu = {"value": total_rows / total_s, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{passes} x {rows} rows of the {args.config} workload ({total_s:.1f} s timed), oracle "
+                         "numpy port of the reference path incl. SVD and dec argsort, sketch partitions in threads"}
 
     if rank == 0:
         line = {
@@ -545,7 +550,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-rows", type=int, default=200_000)
+    ap.add_argument("--cpu-rows", type=int, default=500_000)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-rows", type=int, default=100_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -311,7 +311,7 @@ def run_distributed(
         torch.cuda.synchronize()
         t_sc = time.perf_counter() - t0
     result = LeverageResult(
-        scores=scores.cpu().numpy(),
+        scores=N.host_numpy(scores),
         method="sketch_trunc",
         effective_rank=int(s_host.shape[0]),
         eps=spec.eps,

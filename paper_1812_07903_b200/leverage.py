@@ -490,7 +490,7 @@ def leverage_exact(a) -> LeverageResult:
     r = int(np.count_nonzero(s_host > MACHINE_RANK_TOL * s_host[0]))
     ur = u[:, :r]
     scores = (ur * ur).sum(dim=1)
-    return LeverageResult(scores=scores.cpu().numpy(), method="exact", effective_rank=r)
+    return LeverageResult(scores=N.host_numpy(scores), method="exact", effective_rank=r)
 
 
 def leverage_oracle(a) -> LeverageResult:
@@ -505,7 +505,7 @@ def leverage_oracle(a) -> LeverageResult:
     h = X @ torch.linalg.pinv(X.T @ X) @ X.T
     scores = (h * h).sum(dim=1)
     rank = int(round(float(torch.trace(h))))
-    return LeverageResult(scores=scores.cpu().numpy(), method="oracle", effective_rank=rank)
+    return LeverageResult(scores=N.host_numpy(scores), method="oracle", effective_rank=rank)
 
 
 def _approx_basis(svd: SvdResult) -> np.ndarray:
@@ -520,7 +520,7 @@ def _block_scores(rows, basis) -> np.ndarray:
     X = device_matrix(rows)
     M = basis if isinstance(basis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(basis, dtype=np.float64))
     M = M.to(X.device, torch.float64)
-    return scores_device(X, M).cpu().numpy()
+    return N.host_numpy(scores_device(X, M))
 
 
 _STREAM_CHUNK_BYTES = 128 << 20
@@ -578,7 +578,7 @@ def _sketched(a, spec, sv_tol, mem_cap_bytes, jl_dim, jl_seed, rank, method):
     M, eff = sketch_fold(sx, sv_tol, rank, pi)
     scores = csr_scores(m, M) if m is not None else scores_device(X, M)
     return LeverageResult(
-        scores=scores.cpu().numpy(),
+        scores=N.host_numpy(scores),
         method=method,
         effective_rank=eff,
         eps=spec.eps,

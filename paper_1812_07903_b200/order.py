@@ -87,7 +87,7 @@ def scores_to_distribution(scores):
         raise DegenerateInputError("scores must be nonnegative")
     if float(total.item()) <= 0:
         raise DegenerateInputError("all scores are zero; no sampling distribution exists")
-    return p if was_torch else p.cpu().numpy()
+    return p if was_torch else N.host_numpy(p)
 
 
 def argsort_device(keys: torch.Tensor, descending: bool, out: torch.Tensor | None = None, ws=None) -> torch.Tensor:
@@ -132,7 +132,7 @@ def make_plan(p, policy: OrderingPolicy, epoch: int = 0) -> OrderingPlan:
     else:  # DEC_SWR: i.i.d. draws, host RNG like the reference
         ph = pt.cpu().numpy()
         idx = torch.from_numpy(_epoch_rng(policy, epoch).choice(n, size=n, replace=True, p=ph).astype(np.int64))
-    indices = idx if was_torch else idx.cpu().numpy().astype(np.int64, copy=False)
+    indices = idx if was_torch else N.host_numpy(idx)
     return OrderingPlan(epoch=epoch, indices=indices, policy=policy)
 
 

@@ -333,7 +333,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         if world == 1:
             pipe.run(X, timing=timing, check=False)
             return
-        # multi-rank: local sketch -> all_gather (hi, lo) -> rank-ordered fold -> factor on 0 -> bcast M
+        # multi-rank: local sketch -> sliced rank-ordered merge -> SX on every rank -> fold -> local scores
         ev = pipe.events
         if timing:
             ev["sketch"][0].record()
@@ -347,14 +347,9 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             pipe.sx.copy_(sliced_hashed_merge(s._hi, s._lo, rank, world))
         if timing:
             ev["factor"][0].record()
-        shape = torch.zeros(2, dtype=torch.int64, device=dev)
-        if rank == 0:
-            M0 = sketch_fold(pipe.sx, cfg["sv_tol"], cfg.get("rank"), pi)[0]
-            shape[0], shape[1] = M0.shape[0], M0.shape[1]
-        dist.broadcast(shape, 0)  # the basis fold (r' <= r) has r' columns
-        M = M0.contiguous() if rank == 0 else torch.empty((int(shape[0]), int(shape[1])), dtype=torch.float64,
-                                                            device=dev)
-        dist.broadcast(M, 0)
+        # every rank holds the same SX: the fold is computed redundantly (deterministic
+        # kernels, identical M) instead of folding on rank 0 and broadcasting
+        M = sketch_fold(pipe.sx, cfg["sv_tol"], cfg.get("rank"), pi)[0].contiguous()
         pipe.set_fold(M)
         if timing:
             ev["factor"][1].record()

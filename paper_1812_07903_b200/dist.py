@@ -7,10 +7,12 @@ NVLink):
 
 * each rank sketches its contiguous partition with GLOBAL row indices
   (identical hash assignments to a serial pass, dist.py:106-107);
-* boundary #1 (dist.py:114-118): the compensated (hi, lo) partials are
-  all-gathered and every rank folds ``merge`` in ascending rank order, the
-  reference's exact TwoSum fold, so the merged sketch equals the reference's
-  bit-for-bit (an NCCL sum would reassociate);
+* boundary #1 (dist.py:114-118): the compensated (hi, lo) partials are cut
+  into world row slices and exchanged all-to-all; rank q folds ``merge`` over
+  slice q in ascending rank order (the reference's exact TwoSum fold, so the
+  merged sketch equals the reference's bit-for-bit — an NCCL sum would
+  reassociate) and the merged slices are all-gathered (Gaussian partials,
+  plain sums, are all-gathered and added in rank order);
 * one rank factorises; boundary #2 (dist.py:125): the d x r fold M is
   broadcast;
 * scores stay rank-local (concatenation order = rank order, dist.py:128);
@@ -130,6 +132,13 @@ class DeviceOps:
 
     merge = staticmethod(merge)
 
+    @staticmethod
+    def merge_arrays(h1, l1, h2, l2):
+        """(h1, l1) <- TwoSum merge with (h2, l2) on raw row slices (in place)."""
+        N.check(N.lib().lvsk_merge_compensated(h1.data_ptr(), l1.data_ptr(), h2.data_ptr(), l2.data_ptr(),
+                                               h1.data_ptr(), l1.data_ptr(), h1.numel(), N.stream_ptr()), "merge")
+        return h1, l1
+
     def factor(self, merged: SketchState):
         sx = merged.data_device
         pi = None if self.jl_dim is None else jl_device(self.jl_seed, self.spec.d, self.jl_dim)
@@ -164,11 +173,17 @@ def coordinate(ops, local_rows, row0: int, rank: int, world: int, counts: list[i
 
     t0 = time.perf_counter()
     mine = ops.payload(state)
-    gathered = [[torch.empty_like(t) for _ in range(world)] for t in mine]
-    for slot, t in enumerate(mine):
-        tdist.all_gather(gathered[slot], t.contiguous(), group=group)
-    states = [ops.from_payload([gathered[s][p] for s in range(len(mine))], counts[p]) for p in range(world)]
-    merged = _fold_in_order(ops, states)
+    if len(mine) == 2 and world > 1:  # hashed (hi, lo): sliced rank-ordered merge, then gather
+        h, l = sliced_merge(mine[0], mine[1], rank, world, ops.merge_arrays, group)
+        k = mine[0].shape[0]
+        merged = ops.from_payload([gather_row_slices(h, k, world, group), gather_row_slices(l, k, world, group)],
+                                  sum(counts))
+    else:
+        gathered = [[torch.empty_like(t) for _ in range(world)] for t in mine]
+        for slot, t in enumerate(mine):
+            tdist.all_gather(gathered[slot], t.contiguous(), group=group)
+        states = [ops.from_payload([gathered[s][p] for s in range(len(mine))], counts[p]) for p in range(world)]
+        merged = _fold_in_order(ops, states)
     ops.sync()
     t_merge = time.perf_counter() - t0
 
@@ -223,22 +238,27 @@ def gather_row_slices(sl: torch.Tensor, k: int, world: int, group=None) -> torch
     return torch.cat([outs[q][: b - a] for q, (a, b) in enumerate(bounds)], dim=0)
 
 
-def sliced_hashed_merge(hi: torch.Tensor, lo: torch.Tensor, rank: int, world: int, group=None) -> torch.Tensor:
-    """Merged float64 sketch SX = fold(merge_0..world-1(hi, lo)) on every rank:
-    rank q merges row slice q of all partials in rank order with the
-    reference's TwoSum (the same bits as the all-gather merge), folds it, and
-    the folded slices are all-gathered."""
-    from . import _native as N
-
+def sliced_merge(hi: torch.Tensor, lo: torch.Tensor, rank: int, world: int, merge_arrays, group=None):
+    """Rank q's row slice of merge_0..world-1(hi, lo): slice q of every rank's
+    partial arrives by one all-to-all and is merged in rank order with the
+    reference's TwoSum (merge_arrays), so each slice holds the same bits as
+    the all-gather-then-fold merge (reference dist.py:114-118)."""
     his = exchange_row_slices(hi, rank, world, group)
     los = exchange_row_slices(lo, rank, world, group)
     h, l = his[0].clone(), los[0].clone()
-    L, st = N.lib(), N.stream_ptr()
     for q in range(1, world):
-        N.check(L.lvsk_merge_compensated(h.data_ptr(), l.data_ptr(), his[q].data_ptr(), los[q].data_ptr(),
-                                         h.data_ptr(), l.data_ptr(), h.numel(), st), "merge")
+        h, l = merge_arrays(h, l, his[q], los[q])
+    return h, l
+
+
+def sliced_hashed_merge(hi: torch.Tensor, lo: torch.Tensor, rank: int, world: int, group=None) -> torch.Tensor:
+    """Merged float64 sketch SX = fold(merge(hi, lo)) on every rank: the
+    merged slice is folded (hi + lo) before the all-gather, so one k x d
+    float64 array crosses the wire instead of the pair."""
+    h, l = sliced_merge(hi, lo, rank, world, DeviceOps.merge_arrays, group)
     sx = torch.empty_like(h)
-    N.check(L.lvsk_fold_compensated(h.data_ptr(), l.data_ptr(), sx.data_ptr(), sx.numel(), st), "fold")
+    N.check(N.lib().lvsk_fold_compensated(h.data_ptr(), l.data_ptr(), sx.data_ptr(), sx.numel(), N.stream_ptr()),
+            "fold")
     return gather_row_slices(sx, hi.shape[0], world, group)
 
 

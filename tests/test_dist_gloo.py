@@ -49,6 +49,11 @@ class OracleOps:
         h, l = O.merge_hashed(a.hi.numpy(), a.lo.numpy(), b.hi.numpy(), b.lo.numpy())
         return _State(torch.from_numpy(h), torch.from_numpy(l), a.rows_consumed + b.rows_consumed)
 
+    @staticmethod
+    def merge_arrays(h1, l1, h2, l2):
+        h, l = O.merge_hashed(h1.numpy(), l1.numpy(), h2.numpy(), l2.numpy())
+        return torch.from_numpy(h), torch.from_numpy(l)
+
     def factor(self, merged):
         sx = (merged.hi + merged.lo).numpy()
         _, s, vt = O.thin_svd(sx)

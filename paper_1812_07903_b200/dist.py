@@ -149,7 +149,9 @@ class DeviceOps:
 
     @staticmethod
     def scores(rows, M) -> torch.Tensor:
-        return scores_device(rows, M)
+        from .csr import CSRMatrix, csr_scores
+
+        return csr_scores(rows, M) if isinstance(rows, CSRMatrix) else scores_device(rows, M)
 
     @staticmethod
     def sync():
@@ -366,10 +368,13 @@ def run_sharded(local_rows, row0: int, n_total: int, spec: SketchSpec, sv_tol: f
     tensor) plus the merged sketch and the coordinator's spectrum."""
     if spec.family not in DIST_FAMILIES:
         raise UnsupportedFamilyError(f"distributed sketching supports countsketch and osnap, not {spec.family!r}")
-    X = device_matrix(local_rows)
+    from .csr import CSRMatrix
+
+    m = None if isinstance(local_rows, (np.ndarray, torch.Tensor, list)) else CSRMatrix.from_any(local_rows)
+    X = m if m is not None else device_matrix(local_rows)  # CSR row blocks: K2 sketch + K6 scores
     world = tdist.get_world_size(group)
     me = tdist.get_rank(group)
-    cnt = torch.tensor([X.shape[0]], dtype=torch.int64, device=X.device)
+    cnt = torch.tensor([m.n if m is not None else X.shape[0]], dtype=torch.int64, device=N.device())
     allc = [torch.empty_like(cnt) for _ in range(world)]
     tdist.all_gather(allc, cnt, group=group)
     counts = [int(c.item()) for c in allc]

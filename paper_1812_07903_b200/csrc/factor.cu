@@ -1,4 +1,4 @@
-// KF — the certified Cholesky fold in one cooperative kernel.
+// KF — the certified Cholesky fold in one cooperative dataflow kernel.
 //
 // Replaces the cuSOLVER potrf + two trsm chains of the fold (leverage.py
 // _chol_body; oracle fold_r, the JL-fold definition M = R^-1 Pi with R the
@@ -9,20 +9,32 @@
 // leverage.chol_certified).
 //
 // B200 design.  The d x d problem is latency-bound (d <= a few thousand), so
-// one persistent cooperative kernel (<= 1 CTA per SM, 256 threads) walks the
-// blocked algorithm over 64 x 64 float64 tiles held in global memory (L2
-// resident: d = 512 is 2 MB) with a grid barrier between dependent phases:
-//   Cholesky step j:  B(j) panels  U_jk = T_j^T A_jk  (T_j = U_jj^-1)  (k > j)
-//                     C(j) trailing updates A_kl -= U_jk^T U_jl   (j < k <= l),
-//                          the task owning (j+1, j+1) also factors and inverts it
-//   back substitution X = U^-1 [Pi | I]:  step i updates W_l,c -= U_li X_ic
-//                          (l < i), the task owning (i-1, c) then sets X = T W
-// The only sequential tile op is the diagonal one (chol_inv_tile: 64-pivot
-// Cholesky + the 64-step inverse of its factor, columns register-resident,
-// one __syncthreads per pivot); panels and the substitution are 4 x 4
-// register-blocked float64 tile GEMMs against those inverses.  Padding rows (d % 64) carry an identity so no branch reaches the
-// math.  Zero tiles of the identity right-hand side (U^-1 is triangular) are
-// skipped.
+// one persistent cooperative kernel (<= 1 CTA per SM, 256 threads) runs the
+// blocked algorithm over 64 x 64 float64 tiles (global memory, L2 resident:
+// d = 512 is 2 MB) as a DATAFLOW graph: every tile carries a version counter,
+// a task waits (acquire) for the versions it reads and publishes (release)
+// the one it writes, so no grid barrier separates the steps and step j+1
+// starts while step j's trailing updates still run.  With U = R (upper) and
+// Y = U^-T (lower), step j is
+//   CHAIN(j+1)  U_j,j+1 = T_j^T A_j,j+1;  A_j+1,j+1 -= U^T U;  factor + invert
+//               it (T_j+1 = U_j+1,j+1^-1, Y_j+1,j+1 = T_j+1^T) — the critical
+//               path, run back to back by CTA 0 with T_j kept in shared memory
+//   PANEL       U_jk = T_j^T A_jk                         (k > j + 1)
+//   YROW        Y_jm = T_j^T W_jm                         (m < j)
+//   UPD         A_kl -= U_jk^T U_jl                       (j < k <= l)
+//   WUPD        W_km -= U_jk^T Y_jm                       (m <= j < k)
+//   MACC        M_i  += Y_ji^T Pi_j                       (i <= j)
+// i.e. the forward substitution U^T Y = I rides along the factorisation and
+// M = U^-1 Pi = Y^T Pi accumulates as rows of Y complete, so there is no
+// separate back substitution.  The other CTAs pull the remaining tasks from
+// an atomic queue in topological order (deadlock-free: a task only waits on
+// lower-numbered tasks or on CTA 0's chain, which only waits on tasks two
+// steps back).  The only sequential tile op is the diagonal one
+// (chol_inv_tile: 64-pivot Cholesky + the inverse of its factor, columns
+// register-resident, one __syncthreads per pivot); everything else is a
+// 4 x 4 register-blocked float64 tile GEMM.  Mutable tiles are read with
+// ld.global.cg (L2) so no stale L1 line survives a version change.  Padding
+// rows (d % 64) carry an identity so no branch reaches the math.
 #include <cooperative_groups.h>
 
 #include <cstdio>
@@ -46,28 +58,52 @@ struct FactorArgs {
   int64_t r;
   double* M;  // d x r, row-major
   double* diag;
-  double* A;  // dp x dp working copy (upper tiles)
-  double* W;  // dp x wc right-hand sides, overwritten by X
-  double* T;  // nb tiles 64 x 64: inverses of the diagonal tiles of U
-  double* partial;
-  int32_t* info;
-  unsigned long long* trace;  // optional phase timestamps (LVSK_KF_TRACE), else null
-  int nb, rt, ct;  // tiles per edge, Pi column tiles, total RHS column tiles (rt + nb)
-  int64_t dp, wc;
+  double* A;   // dp x dp: upper tiles, A -> U in place
+  double* W;   // dp x dp: lower tiles, W -> Y = U^-T in place
+  double* T;   // nb tiles 64 x 64: inverses of the diagonal tiles of U
+  double* P;   // dp x rp: Pi, zero padded
+  double* Ma;  // dp x rp: partial M = Y^T Pi
+  double* partial;  // nb x nb: ||Y_km||_F^2 (valid entries)
+  int32_t* verA;    // nb x nb tile versions
+  int32_t* verW;    // nb x nb
+  int32_t* verM;    // nb x rt
+  int32_t* ctl;     // [0] queue head, [1] finished Y tiles, [2] info
+  unsigned long long* trace;  // optional chain timestamps (LVSK_KF_TRACE), else null
+  int nb, rt;
+  int64_t dp, rp;
 };
 
-// ---- tile movement -----------------------------------------------------------
+// ---- synchronisation -----------------------------------------------------------
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// thread 0 spins until *f >= v; the CTA proceeds after the barrier
+__device__ __forceinline__ void wait_ge(const int32_t* f, int v) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire(f) < v) __nanosleep(32);
+  }
+}
+// publish: every thread's tile stores are ordered before the flag
+__device__ __forceinline__ void signal(int32_t* f, int v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(f, v);
+  }
+}
+
+// ---- tile movement (mutable tiles through L2 only) ------------------------------
 
 __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld) {
   for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
     const int m = e >> 6, c = e & 63;
-    s[m * FLD + c] = g[m * ld + c];
-  }
-}
-__device__ __forceinline__ void load_tile_t(double* s, const double* g, int64_t ld) {
-  for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
-    const int m = e >> 6, c = e & 63;
-    s[c * FLD + m] = g[m * ld + c];
+    s[m * FLD + c] = __ldcg(g + m * ld + c);
   }
 }
 __device__ __forceinline__ void store_tile(double* g, int64_t ld, const double* s) {
@@ -76,21 +112,31 @@ __device__ __forceinline__ void store_tile(double* g, int64_t ld, const double* 
     g[m * ld + c] = s[m * FLD + c];
   }
 }
+__device__ __forceinline__ void store_tile_t(double* g, int64_t ld, const double* s) {
+  for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
+    const int m = e >> 6, c = e & 63;
+    g[m * ld + c] = s[c * FLD + m];
+  }
+}
 
 // ---- tile math ---------------------------------------------------------------
 
-// acc = (SUB ? C - At^T B : At^T B) with At[p][m], B[p][c] in smem (C read from
-// global when SUB); the result goes to smem `out` when out != nullptr, else
-// back to global C.  4 x 4 register blocking, 256 threads.
-template <bool SUB>
-__device__ __forceinline__ void gemm_tile(double* gC, int64_t ldc, const double* At, const double* B, double* out) {
+// out = At^T B (MODE 0), C - At^T B (MODE 1) or C + At^T B (MODE 2); At[p][m],
+// B[p][c] in smem; C (ldc) read through L2 when CG, else from smem; out (ldo)
+// may be smem or global.  4 x 4 register blocking, 256 threads.
+template <int MODE, bool CG>
+__device__ __forceinline__ void gemm_tile(const double* At, const double* B, const double* C, int64_t ldc, double* out,
+                                          int64_t ldo) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = SUB ? gC[(ty + 16 * a) * ldc + tx + 16 * b] : 0.0;
-  const double sg = SUB ? -1.0 : 1.0;
+    for (int b = 0; b < 4; ++b) {
+      const double* cp = C + (ty + 16 * a) * ldc + tx + 16 * b;
+      acc[a][b] = MODE == 0 ? 0.0 : (CG ? __ldcg(cp) : *cp);
+    }
+  const double sg = MODE == 1 ? -1.0 : 1.0;
 #pragma unroll 4
   for (int p = 0; p < FT; ++p) {
     double av[4], bv[4];
@@ -106,12 +152,29 @@ __device__ __forceinline__ void gemm_tile(double* gC, int64_t ldc, const double*
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      if (out)
-        out[(ty + 16 * a) * FLD + tx + 16 * b] = acc[a][b];
-      else
-        gC[(ty + 16 * a) * ldc + tx + 16 * b] = acc[a][b];
+    for (int b = 0; b < 4; ++b) out[(ty + 16 * a) * ldo + tx + 16 * b] = acc[a][b];
+}
+
+// fixed-order sum of squares of the valid (rows < nr, cols < nc) entries of a
+// smem tile (TRANS: entry (m, c) read as s[c][m]); result on thread 0
+template <bool TRANS>
+__device__ double tile_sumsq(const double* s, int nr, int nc, double* red) {
+  double ss = 0.0;
+  for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
+    const int m = e >> 6, c = e & 63;
+    if (m < nr && c < nc) {
+      const double v = TRANS ? s[c * FLD + m] : s[m * FLD + c];
+      ss = fma(v, v, ss);
     }
+  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xFFFFFFFFu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < FTHREADS / 32; ++w) t += red[w];
+  __syncthreads();
+  return t;
 }
 
 // Cholesky of the 64 x 64 tile s (upper triangle used; s = U^T U) and the
@@ -176,236 +239,331 @@ __device__ __noinline__ void chol_inv_tile(double* s, double* t, double* scratch
   __syncthreads();
 }
 
-// ---- the kernel ----------------------------------------------------------------
+// ---- tiles -------------------------------------------------------------------
 
 __device__ __forceinline__ double* atile(const FactorArgs& a, int k, int l) {
   return a.A + static_cast<int64_t>(k) * FT * a.dp + static_cast<int64_t>(l) * FT;
 }
+__device__ __forceinline__ double* wtile(const FactorArgs& a, int k, int m) {
+  return a.W + static_cast<int64_t>(k) * FT * a.dp + static_cast<int64_t>(m) * FT;
+}
 __device__ __forceinline__ double* ttile(const FactorArgs& a, int j) { return a.T + static_cast<int64_t>(j) * FT * FT; }
-__device__ __forceinline__ double* wtile(const FactorArgs& a, int i, int c) {
-  return a.W + static_cast<int64_t>(i) * FT * a.wc + static_cast<int64_t>(c) * FT;
+__device__ __forceinline__ double* ptile(const FactorArgs& a, int k, int c) {
+  return a.P + static_cast<int64_t>(k) * FT * a.rp + static_cast<int64_t>(c) * FT;
+}
+__device__ __forceinline__ double* mtile(const FactorArgs& a, int i, int c) {
+  return a.Ma + static_cast<int64_t>(i) * FT * a.rp + static_cast<int64_t>(c) * FT;
 }
 
-// identity column tile c (c >= rt) has nonzero X rows only for i <= c - rt
-__device__ __forceinline__ bool x_live(const FactorArgs& a, int i, int c) { return c < a.rt || i <= c - a.rt; }
-
-__device__ __forceinline__ void kf_mark(const FactorArgs& a, int& ph) {
-  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+__device__ __forceinline__ void kf_stamp(const FactorArgs& a, int slot) {
+  if (a.trace != nullptr && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[ph] = t;
+    a.trace[slot] = t;
   }
-  ++ph;
+}
+
+enum : int { T_PANEL = 0, T_YROW = 1, T_UPD = 2, T_WUPD = 3, T_MACC = 4, T_FINAL = 5, T_NONE = 6, T_YDIAG = 7 };
+
+// queue task t -> (type, j, x, y); per step j: YDIAG(j), PANEL(j, k >= j+2), YROW(j, m < j),
+// UPD(j; k <= l) without (j+1, j+1) — row j+1 first, WUPD(j; k, m <= j) — row
+// j+1 first, MACC(j; i <= j, c); then FINAL
+__host__ __device__ inline int4 kf_decode(int t, int nb, int rt) {
+  for (int j = 0; j < nb; ++j) {
+    const int m = nb - j - 1;
+    const int np = m > 1 ? m - 1 : 0;
+    const int ny = j;
+    const int nu = m >= 1 ? m * (m + 1) / 2 - 1 : 0;
+    const int nw = m * (j + 1);
+    const int nm = (j + 1) * rt;
+    if (t == 0) return make_int4(T_YDIAG, j, 0, 0);
+    t -= 1;
+    if (t < np) return make_int4(T_PANEL, j, j + 2 + t, 0);
+    t -= np;
+    if (t < ny) return make_int4(T_YROW, j, t, 0);
+    t -= ny;
+    if (t < nu) {
+      int q = t + 1, kk = 0;
+      while (q >= m - kk) {
+        q -= m - kk;
+        ++kk;
+      }
+      return make_int4(T_UPD, j, j + 1 + kk, j + 1 + kk + q);
+    }
+    t -= nu;
+    if (t < nw) return make_int4(T_WUPD, j, j + 1 + t / (j + 1), t % (j + 1));
+    t -= nw;
+    if (t < nm) return make_int4(T_MACC, j, t / rt, t % rt);
+    t -= nm;
+  }
+  return make_int4(t == 0 ? T_FINAL : T_NONE, 0, 0, 0);
+}
+
+static int kf_queue_tasks(int nb, int rt) {
+  int n = 0;
+  for (int j = 0; j < nb; ++j) {
+    const int m = nb - j - 1;
+    n += 1 + (m > 1 ? m - 1 : 0) + j + (m >= 1 ? m * (m + 1) / 2 - 1 : 0) + m * (j + 1) + (j + 1) * rt;
+  }
+  return n + 1;
+}
+
+// T_j (smem t) -> global; publish.  U_jj itself is never read again, and
+// Y_jj = T_j^T with its trace share is a queue task (YDIAG), off the chain.
+__device__ __forceinline__ void finish_diag(const FactorArgs& a, int j, const double* t) {
+  store_tile(ttile(a, j), FT, t);
+  signal(a.verA + j * a.nb + j, j + 1);
 }
 
 __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
-  int ph = 0;
   extern __shared__ double fsm[];
-  double* s0 = fsm;
-  double* s1 = fsm + FT * FLD;
-  double* s2 = fsm + 2 * FT * FLD;
-  double* scratch = fsm + 3 * FT * FLD;  // 5 x 64 doubles
+  double* b0 = fsm;
+  double* b1 = fsm + FT * FLD;
+  double* b2 = fsm + 2 * FT * FLD;
+  double* b3 = fsm + 3 * FT * FLD;
+  double* scratch = fsm + 4 * FT * FLD;  // 5 x 64 doubles (chol_inv_tile)
+  double* red = scratch + 5 * FT;        // 8 doubles
+  __shared__ int4 s_task;
   cg::grid_group grid = cg::this_grid();
   const int cta = blockIdx.x, ncta = gridDim.x;
-  const int nb = a.nb;
+  const int nb = a.nb, rt = a.rt;
+  const int64_t dp = a.dp, rp = a.rp;
 
-  // phase 0: working copies (padding: identity on the diagonal, zeros elsewhere);
-  // one warp per row, no integer division
+  // phase 0: working copies (padding: identity on the diagonal), flags; one warp per row
   {
-    const int64_t dp = a.dp, wc = a.wc;
-    const int64_t rp = static_cast<int64_t>(a.rt) * FT;
     const int wid = (cta * FTHREADS + threadIdx.x) >> 5, nw = (ncta * FTHREADS) >> 5, lane = threadIdx.x & 31;
-    for (int64_t m = wid; m < 2 * dp; m += nw) {
+    for (int64_t m = wid; m < 3 * dp; m += nw) {
       if (m < dp) {
         double* row = a.A + m * dp;
         for (int64_t c = lane; c < dp; c += 32)
           row[c] = (m < a.d && c < a.d) ? (m <= c ? a.G[m * a.ldg + c] : 0.0) : (m == c ? 1.0 : 0.0);
+      } else if (m < 2 * dp) {
+        double* row = a.W + (m - dp) * dp;
+        for (int64_t c = lane; c < dp; c += 32) row[c] = 0.0;
       } else {
-        const int64_t mm = m - dp;
-        double* row = a.W + mm * wc;
-        for (int64_t c = lane; c < wc; c += 32)
-          row[c] = c < rp ? ((mm < a.d && c < a.r) ? a.Pi[mm * a.r + c] : 0.0) : ((c - rp) == mm ? 1.0 : 0.0);
+        const int64_t mm = m - 2 * dp;
+        double* row = a.P + mm * rp;
+        for (int64_t c = lane; c < rp; c += 32) row[c] = (mm < a.d && c < a.r) ? a.Pi[mm * a.r + c] : 0.0;
       }
     }
-    if (cta == 0) {
+    const int gt = cta * FTHREADS + threadIdx.x, gn = ncta * FTHREADS;
+    for (int i = gt; i < nb * nb; i += gn) {
+      a.verA[i] = 0;
+      a.verW[i] = 0;
+    }
+    for (int i = gt; i < nb * rt; i += gn) a.verM[i] = 0;
+    if (gt < 4) a.ctl[gt] = 0;
+    if (cta == 0 && threadIdx.x < 32) {
       // trace(G) in a fixed order (one warp, then lane 0)
-      if (threadIdx.x < 32) {
-        double t = 0.0;
-        for (int64_t i = threadIdx.x; i < a.d; i += 32) t += a.G[i * a.ldg + i];
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, o);
-        if (threadIdx.x == 0) {
-          a.diag[1] = t;
-          *a.info = 0;
-        }
-      }
+      double t = 0.0;
+      for (int64_t i = threadIdx.x; i < a.d; i += 32) t += a.G[i * a.ldg + i];
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, o);
+      if (threadIdx.x == 0) a.diag[1] = t;
     }
   }
   grid.sync();
-  kf_mark(a, ph);
+
   if (cta == 0) {
-    load_tile(s0, atile(a, 0, 0), a.dp);
-    chol_inv_tile(s0, s1, scratch, a.info);
-    store_tile(atile(a, 0, 0), a.dp, s0);
-    store_tile(ttile(a, 0), FT, s1);
-  }
-  grid.sync();
-  kf_mark(a, ph);
-
-  // ---- blocked Cholesky (T_j = U_jj^-1 from the task that factored U_jj)
-  for (int j = 0; j < nb - 1; ++j) {
-    // B(j): U_jk = T_j^T A_jk
-    for (int k = j + 1 + cta; k < nb; k += ncta) {
-      load_tile(s0, ttile(a, j), FT);
-      load_tile(s1, atile(a, j, k), a.dp);
-      __syncthreads();
-      gemm_tile<false>(atile(a, j, k), a.dp, s0, s1, nullptr);
-      __syncthreads();
-    }
-    grid.sync();
-    kf_mark(a, ph);
-    // C(j): A_kl -= U_jk^T U_jl for j < k <= l; task 0 is (j+1, j+1) + factor + inverse
-    const int m = nb - j - 1;
-    const int ntask = m * (m + 1) / 2;
-    for (int t = cta; t < ntask; t += ncta) {
-      int k = 0, rem = t;
-      while (rem >= m - k) {
-        rem -= m - k;
-        ++k;
-      }
-      const int kk = j + 1 + k, ll = kk + rem;
-      load_tile(s0, atile(a, j, kk), a.dp);
-      load_tile(s1, atile(a, j, ll), a.dp);
-      __syncthreads();
-      if (t == 0) {
-        unsigned long long t0, t1, t2, t3;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        gemm_tile<true>(atile(a, kk, ll), a.dp, s0, s1, s2);
-        __syncthreads();
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        chol_inv_tile(s2, s0, scratch, a.info);
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
-        store_tile(atile(a, kk, ll), a.dp, s2);
-        store_tile(ttile(a, kk), FT, s0);
-        __syncthreads();
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
-        if (a.trace != nullptr && threadIdx.x == 0) {
-          a.trace[512 + 3 * j] = t1 - t0;
-          a.trace[513 + 3 * j] = t2 - t1;
-          a.trace[514 + 3 * j] = t3 - t2;
-        }
-      } else {
-        gemm_tile<true>(atile(a, kk, ll), a.dp, s0, s1, nullptr);
-      }
-      __syncthreads();
-    }
-    grid.sync();
-    kf_mark(a, ph);
-  }
-
-  // ---- back substitution X = U^-1 W, in place in W:  X_i = T_i (W_i - sum_{l>i} U_il X_l)
-  const int ct = a.ct;
-  for (int c = cta; c < ct; c += ncta) {
-    if (!x_live(a, nb - 1, c)) continue;
-    load_tile_t(s0, ttile(a, nb - 1), FT);
-    load_tile(s1, wtile(a, nb - 1, c), a.wc);
+    // ---- the critical chain: DIAG(0), then CHAIN(1..nb-1), T_j kept in smem
+    double *T = b0, *x = b1, *y = b2, *z = b3;
+    kf_stamp(a, 0);
+    load_tile(y, atile(a, 0, 0), dp);
     __syncthreads();
-    gemm_tile<false>(wtile(a, nb - 1, c), a.wc, s0, s1, nullptr);
-    __syncthreads();
-  }
-  grid.sync();
-  kf_mark(a, ph);
-  for (int i = nb - 1; i >= 1; --i) {
-    // tasks (l, c), l < i; the l = i-1 tasks (update + solve) are enumerated first
-    const int ntask = i * ct;
-    for (int t = cta; t < ntask; t += ncta) {
-      const int l = i - 1 - t / ct, c = t % ct;
-      const bool solve = l == i - 1;
-      if (solve && !x_live(a, l, c)) continue;
-      const bool upd = x_live(a, i, c);
-      if (!upd && !solve) continue;
-      if (upd) {
-        load_tile_t(s0, atile(a, l, i), a.dp);
-        load_tile(s1, wtile(a, i, c), a.wc);
-        __syncthreads();
-        gemm_tile<true>(wtile(a, l, c), a.wc, s0, s1, solve ? s2 : nullptr);
-      } else {
-        load_tile(s2, wtile(a, l, c), a.wc);
-      }
-      if (solve) {
-        __syncthreads();
-        load_tile_t(s0, ttile(a, l), FT);
-        __syncthreads();
-        gemm_tile<false>(wtile(a, l, c), a.wc, s0, s2, nullptr);
-      }
+    chol_inv_tile(y, T, scratch, a.ctl + 2);
+    finish_diag(a, 0, T);
+    kf_stamp(a, 1);
+    for (int j = 0; j + 1 < nb; ++j) {
+      wait_ge(a.verA + j * nb + j + 1, j);
+      wait_ge(a.verA + (j + 1) * nb + j + 1, j);
       __syncthreads();
+      kf_stamp(a, 2 + 3 * j);
+      load_tile(x, atile(a, j, j + 1), dp);
+      load_tile(y, atile(a, j + 1, j + 1), dp);
+      __syncthreads();
+      gemm_tile<0, false>(T, x, nullptr, 0, z, FLD);  // U_j,j+1 = T_j^T A_j,j+1
+      __syncthreads();
+      store_tile(atile(a, j, j + 1), dp, z);
+      signal(a.verA + j * nb + j + 1, j + 1);
+      gemm_tile<1, false>(z, z, y, FLD, x, FLD);  // A_j+1,j+1 - U^T U
+      __syncthreads();
+      kf_stamp(a, 3 + 3 * j);
+      chol_inv_tile(x, y, scratch, a.ctl + 2);  // x = U_j+1,j+1, y = T_j+1
+      finish_diag(a, j + 1, y);
+      kf_stamp(a, 4 + 3 * j);
+      double* freed = T;
+      T = y;
+      y = freed;
     }
-    grid.sync();
-    kf_mark(a, ph);
+    return;
   }
 
-  // ---- outputs: M (Pi columns) and per-tile sums of squares of U^-1
-  {
-    const int ntask = nb * ct;
-    for (int t = cta; t < ntask; t += ncta) {
-      const int i = t / ct, c = t % ct;
-      const double* x = wtile(a, i, c);
-      if (c < a.rt) {
+  // ---- everything else from the queue, in topological order
+  for (;;) {
+    if (threadIdx.x == 0) s_task = kf_decode(atomicAdd(a.ctl, 1), nb, rt);
+    __syncthreads();
+    const int4 tk = s_task;
+    __syncthreads();
+    if (tk.x == T_NONE) break;
+    const int j = tk.y;
+    if (tk.x == T_YDIAG) {  // Y_jj = T_j^T and its share of trace(G^-1)
+      wait_ge(a.verA + j * nb + j, j + 1);
+      __syncthreads();
+      load_tile(b0, ttile(a, j), FT);
+      __syncthreads();
+      store_tile_t(wtile(a, j, j), dp, b0);
+      const int nv = static_cast<int>(a.d - static_cast<int64_t>(j) * FT);
+      const double ss = tile_sumsq<true>(b0, nv, nv, red);
+      if (threadIdx.x == 0) a.partial[j * nb + j] = ss;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(a.verW + j * nb + j, 1);
+        atomicAdd(a.ctl + 1, 1);
+      }
+    } else if (tk.x == T_PANEL) {  // U_jk = T_j^T A_jk
+      const int k = tk.z;
+      wait_ge(a.verA + j * nb + j, j + 1);
+      wait_ge(a.verA + j * nb + k, j);
+      __syncthreads();
+      load_tile(b0, ttile(a, j), FT);
+      load_tile(b1, atile(a, j, k), dp);
+      __syncthreads();
+      gemm_tile<0, false>(b0, b1, nullptr, 0, atile(a, j, k), dp);
+      signal(a.verA + j * nb + k, j + 1);
+    } else if (tk.x == T_YROW) {  // Y_jm = T_j^T W_jm
+      const int m = tk.z;
+      wait_ge(a.verA + j * nb + j, j + 1);
+      wait_ge(a.verW + j * nb + m, j - m);
+      __syncthreads();
+      load_tile(b0, ttile(a, j), FT);
+      load_tile(b1, wtile(a, j, m), dp);
+      __syncthreads();
+      gemm_tile<0, false>(b0, b1, nullptr, 0, b2, FLD);
+      __syncthreads();
+      store_tile(wtile(a, j, m), dp, b2);
+      const double ss = tile_sumsq<false>(b2, static_cast<int>(a.d - static_cast<int64_t>(j) * FT),
+                                          static_cast<int>(a.d - static_cast<int64_t>(m) * FT), red);
+      if (threadIdx.x == 0) a.partial[j * nb + m] = ss;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(a.verW + j * nb + m, j - m + 1);
+        atomicAdd(a.ctl + 1, 1);
+      }
+    } else if (tk.x == T_UPD) {  // A_kl -= U_jk^T U_jl
+      const int k = tk.z, l = tk.w;
+      wait_ge(a.verA + j * nb + k, j + 1);
+      wait_ge(a.verA + j * nb + l, j + 1);
+      wait_ge(a.verA + k * nb + l, j);
+      __syncthreads();
+      load_tile(b0, atile(a, j, k), dp);
+      if (l != k) load_tile(b1, atile(a, j, l), dp);
+      __syncthreads();
+      gemm_tile<1, true>(b0, l != k ? b1 : b0, atile(a, k, l), dp, atile(a, k, l), dp);
+      signal(a.verA + k * nb + l, j + 1);
+    } else if (tk.x == T_WUPD) {  // W_km -= U_jk^T Y_jm
+      const int k = tk.z, m = tk.w;
+      wait_ge(a.verA + j * nb + k, j + 1);
+      wait_ge(a.verW + j * nb + m, j - m + 1);
+      wait_ge(a.verW + k * nb + m, j - m);
+      __syncthreads();
+      load_tile(b0, atile(a, j, k), dp);
+      load_tile(b1, wtile(a, j, m), dp);
+      __syncthreads();
+      gemm_tile<1, true>(b0, b1, wtile(a, k, m), dp, wtile(a, k, m), dp);
+      signal(a.verW + k * nb + m, j - m + 1);
+    } else if (tk.x == T_MACC) {  // M_ic += Y_ji^T Pi_jc
+      const int i = tk.z, c = tk.w;
+      wait_ge(a.verW + j * nb + i, j - i + 1);
+      wait_ge(a.verM + i * rt + c, j - i);
+      __syncthreads();
+      load_tile(b0, wtile(a, j, i), dp);
+      load_tile(b1, ptile(a, j, c), rp);
+      __syncthreads();
+      if (j + 1 < nb) {
+        if (j == i)
+          gemm_tile<0, false>(b0, b1, nullptr, 0, mtile(a, i, c), rp);
+        else
+          gemm_tile<2, true>(b0, b1, mtile(a, i, c), rp, mtile(a, i, c), rp);
+        signal(a.verM + i * rt + c, j - i + 1);
+      } else {
+        if (j == i)
+          gemm_tile<0, false>(b0, b1, nullptr, 0, b2, FLD);
+        else
+          gemm_tile<2, true>(b0, b1, mtile(a, i, c), rp, b2, FLD);
+        __syncthreads();
         for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
-          const int64_t m = static_cast<int64_t>(i) * FT + (e >> 6);
-          const int64_t q = static_cast<int64_t>(c) * FT + (e & 63);
-          if (m < a.d && q < a.r) a.M[m * a.r + q] = x[(e >> 6) * a.wc + (e & 63)];
-        }
-      } else {
-        double ss = 0.0;
-        if (x_live(a, i, c)) {
-          for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
-            const int64_t m = static_cast<int64_t>(i) * FT + (e >> 6);
-            const int64_t q = static_cast<int64_t>(c - a.rt) * FT + (e & 63);
-            if (m < a.d && q < a.d) {
-              const double v = x[(e >> 6) * a.wc + (e & 63)];
-              ss = fma(v, v, ss);
-            }
-          }
-        }
-        // fixed-order block reduction
-        __shared__ double red[FTHREADS / 32];
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xFFFFFFFFu, ss, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          double tsum = 0.0;
-          for (int w = 0; w < FTHREADS / 32; ++w) tsum += red[w];
-          a.partial[t] = tsum;
+          const int64_t row = static_cast<int64_t>(i) * FT + (e >> 6);
+          const int64_t col = static_cast<int64_t>(c) * FT + (e & 63);
+          if (row < a.d && col < a.r) a.M[row * a.r + col] = b2[(e >> 6) * FLD + (e & 63)];
         }
         __syncthreads();
       }
+    } else {  // FINAL: trace(G^-1) = ||Y||_F^2 in a fixed order, info
+      if (threadIdx.x == 0) {
+        while (ld_acquire(a.ctl + 1) < nb * (nb + 1) / 2) __nanosleep(64);
+        double tr = 0.0;
+        for (int k = 0; k < nb; ++k)
+          for (int m = 0; m <= k; ++m) tr += a.partial[k * nb + m];
+        a.diag[2] = tr;
+        a.diag[0] = static_cast<double>(ld_acquire(a.ctl + 2));
+      }
+      __syncthreads();
     }
-  }
-  grid.sync();
-  kf_mark(a, ph);
-  if (cta == 0 && threadIdx.x == 0) {
-    double tr = 0.0;
-    for (int t = 0; t < nb * ct; ++t)
-      if (t % ct >= a.rt) tr += a.partial[t];
-    a.diag[2] = tr;
-    a.diag[0] = static_cast<double>(*a.info);
   }
 }
 
 struct FactorPlan {
-  int nb, rt, ct;
-  int64_t dp, wc;
+  int nb, rt;
+  int64_t dp, rp;
 };
 
 static FactorPlan plan_factor(int64_t d, int64_t r) {
   FactorPlan p;
   p.nb = static_cast<int>((d + FT - 1) / FT);
   p.rt = static_cast<int>((r + FT - 1) / FT);
-  p.ct = p.rt + p.nb;
   p.dp = static_cast<int64_t>(p.nb) * FT;
-  p.wc = static_cast<int64_t>(p.ct) * FT;
+  p.rp = static_cast<int64_t>(p.rt) * FT;
   return p;
 }
+
+template <typename Alloc>
+static void kf_layout(Alloc& c, const FactorPlan& P, FactorArgs* a) {
+  const size_t nb2 = static_cast<size_t>(P.nb) * P.nb;
+  auto A = c.template take<double>(static_cast<size_t>(P.dp) * P.dp);
+  auto W = c.template take<double>(static_cast<size_t>(P.dp) * P.dp);
+  auto T = c.template take<double>(static_cast<size_t>(P.nb) * FT * FT);
+  auto Pp = c.template take<double>(static_cast<size_t>(P.dp) * P.rp);
+  auto Ma = c.template take<double>(static_cast<size_t>(P.dp) * P.rp);
+  auto part = c.template take<double>(nb2);
+  auto vA = c.template take<int32_t>(nb2);
+  auto vW = c.template take<int32_t>(nb2);
+  auto vM = c.template take<int32_t>(static_cast<size_t>(P.nb) * P.rt);
+  auto ctl = c.template take<int32_t>(4);
+  if (a) {
+    a->A = A;
+    a->W = W;
+    a->T = T;
+    a->P = Pp;
+    a->Ma = Ma;
+    a->partial = part;
+    a->verA = vA;
+    a->verW = vW;
+    a->verM = vM;
+    a->ctl = ctl;
+  }
+}
+
+// Measure::take returns void; a typed twin so kf_layout serves both
+struct MeasureT {
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    off += count * sizeof(T);
+    return nullptr;
+  }
+};
 
 }  // namespace lvsk
 
@@ -414,12 +572,8 @@ using namespace lvsk;
 extern "C" size_t lvsk_chol_fold_workspace_bytes(int64_t d, int64_t r) {
   if (d < 1 || r < 1) return 0;
   const FactorPlan P = plan_factor(d, r);
-  Measure ms;
-  ms.take<double>(static_cast<size_t>(P.dp) * P.dp);
-  ms.take<double>(static_cast<size_t>(P.dp) * P.wc);
-  ms.take<double>(static_cast<size_t>(P.nb) * FT * FT);
-  ms.take<double>(static_cast<size_t>(P.nb) * P.ct);
-  ms.take<int32_t>(1);
+  MeasureT ms;
+  kf_layout(ms, P, nullptr);
   return ms.off;
 }
 
@@ -438,18 +592,13 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.r = r;
   a.M = M;
   a.diag = diag;
-  a.A = c.take<double>(static_cast<size_t>(P.dp) * P.dp);
-  a.W = c.take<double>(static_cast<size_t>(P.dp) * P.wc);
-  a.T = c.take<double>(static_cast<size_t>(P.nb) * FT * FT);
-  a.partial = c.take<double>(static_cast<size_t>(P.nb) * P.ct);
-  a.info = c.take<int32_t>(1);
+  kf_layout(c, P, &a);
   LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
   a.nb = P.nb;
   a.rt = P.rt;
-  a.ct = P.ct;
   a.dp = P.dp;
-  a.wc = P.wc;
-  const int smem = 3 * FTILE_SMEM + 5 * FT * 8;
+  a.rp = P.rp;
+  const int smem = 4 * FTILE_SMEM + (5 * FT + 8) * 8;
   static int grid_cap = 0;
   if (grid_cap == 0) {
     cudaError_t e = cudaFuncSetAttribute(chol_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -458,14 +607,12 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chol_fold_kernel, FTHREADS, smem);
-    grid_cap = sms * (per < 1 ? 1 : (per > 1 ? 1 : per));
-    if (grid_cap < 1) grid_cap = 1;
+    grid_cap = per >= 1 ? sms : 0;
+    if (grid_cap < 2) return cuda_status(cudaErrorInvalidConfiguration, "chol_fold needs two co-resident CTAs");
   }
-  // more CTAs than the widest phase only adds barrier cost
-  int64_t widest = static_cast<int64_t>(P.nb) * P.ct;
-  const int64_t tri = static_cast<int64_t>(P.nb) * (P.nb + 1) / 2;
-  if (tri > widest) widest = tri;
-  const int grid = static_cast<int>(widest < grid_cap ? widest : grid_cap);
+  // CTA 0 runs the chain; more queue CTAs than tasks only add polling
+  const int ntask = kf_queue_tasks(P.nb, P.rt);
+  const int grid = 1 + (ntask < grid_cap - 1 ? ntask : grid_cap - 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(FTHREADS);
@@ -484,15 +631,17 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   if (e != cudaSuccess) return cuda_status(e, "chol_fold launch");
   if (tracing) {
     unsigned long long h[1024];
-    const int nph = 4 + 2 * (P.nb - 1) + P.nb;
+    const int nst = P.nb < 300 ? P.nb : 300;
     cudaStreamSynchronize(cfg.stream);
-    cudaMemcpy(h, trace, nph * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "KF d=%lld r=%lld grid=%d phases(us):", (long long)d, (long long)r, grid);
-    for (int i = 1; i < nph; ++i) fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1000.0);
-    cudaMemcpy(h + 512, trace + 512, 3 * P.nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "\n  diag task gemm/chol_inv/store(us):");
-    for (int j = 0; j + 1 < P.nb && j < 8; ++j)
-      fprintf(stderr, " %.1f/%.1f/%.1f", h[512 + 3 * j] / 1000.0, h[513 + 3 * j] / 1000.0, h[514 + 3 * j] / 1000.0);
+    cudaMemcpy(h, trace, (2 + 3 * nst) * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "KF d=%lld r=%lld grid=%d tasks=%d diag0 %.1f us; chain wait/gemm/chol_inv (us):", (long long)d,
+            (long long)r, grid, ntask, (h[1] - h[0]) / 1000.0);
+    unsigned long long prev = h[1];
+    for (int j = 0; j + 1 < nst && j < 16; ++j) {
+      fprintf(stderr, " %.1f/%.1f/%.1f", (h[2 + 3 * j] - prev) / 1000.0, (h[3 + 3 * j] - h[2 + 3 * j]) / 1000.0,
+              (h[4 + 3 * j] - h[3 + 3 * j]) / 1000.0);
+      prev = h[4 + 3 * j];
+    }
     fprintf(stderr, "\n");
   }
   return LVSK_OK;

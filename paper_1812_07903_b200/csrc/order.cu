@@ -6,7 +6,22 @@
 // an order-preserving uint64 image of the float64 keys (8 passes of 8 bits),
 // values = indices, so ties keep ascending index exactly like numpy's stable
 // sort.
+//
+// For n up to a few million the whole sort runs in ONE cooperative kernel
+// (argsort_coop_kernel): the ping-pong key/index buffers (12 B per item) stay
+// in the 126 MB L2, every CTA owns a contiguous index range, and a pass is
+// chunk histogram -> grid barrier -> per-digit offsets from all CTAs'
+// histograms -> stable in-chunk ranking + scatter -> grid barrier.  Passes
+// whose 8-bit digit is the same for every key (found from the OR / AND of all
+// keys; e.g. the sign and top exponent bits of a probability vector) are
+// skipped — a stable pass on a constant digit is the identity.
+#include <cooperative_groups.h>
+
+#include <cstdio>
+
 #include "radix_sort.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace lvsk {
 
@@ -92,6 +107,419 @@ __global__ void argsort_keys_kernel(const double* __restrict__ keys, int64_t n, 
   }
 }
 
+// ---- K7 cooperative (L2-resident) argsort ------------------------------------
+
+constexpr int AS_THREADS = 512;
+constexpr int AS_WARPS = AS_THREADS / 32;
+constexpr int AS_ITEMS = 8;
+constexpr int AS_SUB = AS_THREADS * AS_ITEMS;  // 4096 keys per ranking sub-tile
+constexpr int AS_WARP_ITEMS = AS_SUB / AS_WARPS;
+constexpr int AS_HALO = 64;                    // longest equal-prefix run the fix-up sorts locally
+constexpr int AS_WIN = 4096;                   // fix-up window
+constexpr int64_t AS_MAX_N = int64_t{8} << 20;
+constexpr int AS_MAX_G = 1024;
+constexpr int AS_CHUNK_CAP = 12288;           // chunks up to this size are staged whole (longest output runs)
+constexpr size_t AS_RANK_SMEM =
+    sizeof(uint32_t) * AS_WARPS * 256 + (sizeof(uint64_t) + sizeof(uint32_t)) * AS_CHUNK_CAP;
+constexpr size_t AS_FIX_SMEM = (sizeof(uint64_t) + sizeof(uint32_t)) * (AS_WIN + 2 * AS_HALO);
+constexpr size_t AS_SMEM = AS_RANK_SMEM > AS_FIX_SMEM ? AS_RANK_SMEM : AS_FIX_SMEM;
+
+struct AsArgs {
+  const double* in;
+  int64_t n;
+  int descending;
+  int64_t* out;
+  uint64_t* kb[3];  // kb[0]: keys in index order (kept); kb[1], kb[2]: ping-pong
+  uint32_t* vb[2];
+  uint32_t* hist;   // [G][256] chunk histograms of the current pass
+  uint32_t* totals; // [8][256] digit totals of every pass
+  unsigned long long* orand;  // OR, AND of all keys
+  unsigned int* bar;          // barrier arrivals
+  unsigned int* flag;         // fix-up refused: redo with every digit
+  unsigned long long* trace;  // optional phase timestamps (LVSK_SORT_TRACE)
+};
+
+__device__ __forceinline__ void as_stamp(const AsArgs& a, int slot) {
+  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[slot] = t;
+  }
+}
+
+// exclusive scan of one value per thread over the first 256 threads (all 512 call)
+__device__ __forceinline__ uint32_t scan256(uint32_t v, uint32_t* sh, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = threadIdx.x < 256 ? v : 0u;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31 && warp < 8) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < 8 ? sh[lane] : 0u;
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, off);
+      if (lane >= off) w += y;
+    }
+    if (lane < 8) sh[lane] = w;
+  }
+  __syncthreads();
+  total = sh[7];
+  const uint32_t base = (warp > 0 && warp < 8) ? sh[warp - 1] : 0u;
+  __syncthreads();
+  return base + x - (threadIdx.x < 256 ? v : 0u);
+}
+
+// grid barrier on a monotone arrival counter (zeroed before the launch): the
+// k-th barrier completes when count >= k * G.  One atomic per CTA, thread 0
+// polls with ld.acquire.
+__device__ __forceinline__ void as_barrier(unsigned int* count, unsigned int& nbar) {
+  const unsigned int target = (++nbar) * gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(count, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// Stable LSD passes over the active digits in [dlo, dhi] (8-bit digits of the
+// keys in kb[0]).  The last active pass writes the indices (int64) to out and
+// the keys in sorted order to the returned buffer.  No active digit: the
+// identity.
+__device__ const uint64_t* as_passes(const AsArgs& a, int dlo, int dhi, unsigned long long diff, unsigned int& nbar,
+                                     uint8_t* smem, int64_t c0, int64_t c1) {
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);                  // [AS_WARPS][256]
+  uint64_t* keys_s = reinterpret_cast<uint64_t*>(cnt + AS_WARPS * 256);  // [AS_CHUNK_CAP]
+  uint32_t* vals_s = reinterpret_cast<uint32_t*>(keys_s + AS_CHUNK_CAP); // [AS_CHUNK_CAP]
+  __shared__ uint32_t run[256], loc_start[256], sub_cnt[256], sh[16], cstart[256], crun[256];
+  // a chunk that fits is staged whole in digit order before any global store,
+  // so each digit leaves the CTA as one contiguous run (better write coalescing)
+  const bool whole = c1 - c0 <= AS_CHUNK_CAP;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  int last = -1;
+  for (int p = dlo; p <= dhi; ++p)
+    if ((diff >> (8 * p)) & 0xFFull) last = p;
+  if (last < 0) {
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += AS_THREADS) a.out[i] = i;
+    as_barrier(a.bar, nbar);
+    return a.kb[0];
+  }
+  const uint64_t* ksrc = a.kb[0];
+  const uint32_t* vsrc = nullptr;  // identity on the first active pass
+  uint64_t* kdst = a.kb[1];
+  uint32_t* vdst = a.vb[0];
+  for (int p = dlo; p <= last; ++p) {
+    if (!((diff >> (8 * p)) & 0xFFull)) continue;
+    const int shift = 8 * p;
+    const bool fin = p == last;
+    // (a) chunk histogram
+    for (int i = threadIdx.x; i < 256; i += AS_THREADS) run[i] = 0u;
+    __syncthreads();
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += AS_THREADS)
+      atomicAdd(&run[static_cast<uint32_t>(__ldcg(ksrc + i) >> shift) & 0xFFu], 1u);
+    __syncthreads();
+    if (threadIdx.x < 256) a.hist[cta * 256 + threadIdx.x] = run[threadIdx.x];
+    if (whole) {
+      uint32_t ct;
+      const uint32_t cs = scan256(threadIdx.x < 256 ? run[threadIdx.x] : 0u, sh, ct);
+      if (threadIdx.x < 256) {
+        cstart[threadIdx.x] = cs;
+        crun[threadIdx.x] = cs;
+      }
+    }
+    as_stamp(a, 4 * p + 2);
+    as_barrier(a.bar, nbar);
+    as_stamp(a, 4 * p + 3);
+    // (b) start of this chunk's run of every digit: digit base (scan of the pass
+    // totals) + the counts of the preceding chunks (16 rows in flight per thread)
+    {
+      const int d = threadIdx.x & 255, h = threadIdx.x >> 8;
+      uint32_t acc = 0;
+      for (int c = h; c < cta; c += 32) {
+        uint32_t v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = c + 2 * u < cta ? __ldcg(a.hist + (c + 2 * u) * 256 + d) : 0u;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc += v[u];
+      }
+      if (h == 1) loc_start[d] = acc;
+      __syncthreads();
+      const uint32_t before = h == 0 ? acc + loc_start[d] : 0u;
+      uint32_t all;
+      const uint32_t dbase = scan256(h == 0 ? __ldcg(a.totals + p * 256 + d) : 0u, sh, all);
+      if (h == 0) run[d] = dbase + before;
+      __syncthreads();
+    }
+    as_stamp(a, 4 * p + 4);
+    // (c) stable scatter, sub-tile by sub-tile in index order
+    for (int64_t s0 = c0; s0 < c1; s0 += AS_SUB) {
+      for (int i = threadIdx.x; i < AS_WARPS * 256; i += AS_THREADS) cnt[i] = 0u;
+      __syncthreads();
+      const int64_t wb = s0 + warp * AS_WARP_ITEMS;
+      uint64_t k[AS_ITEMS];
+      uint32_t v[AS_ITEMS], rank[AS_ITEMS], dg[AS_ITEMS];
+#pragma unroll
+      for (int t = 0; t < AS_ITEMS; ++t) {
+        const int64_t i = wb + t * 32 + lane;
+        if (i < c1) {
+          k[t] = __ldcg(ksrc + i);
+          v[t] = vsrc ? __ldcg(vsrc + i) : static_cast<uint32_t>(i);
+        }
+      }
+      // warp-level stable ranking: match_any groups the lanes of a digit, the
+      // group leader bumps the warp's digit counter with one shared atomic
+      // (a warp's atomics to one address apply in issue order = item order)
+      // and broadcasts the old count; all items' matches and atomics are
+      // independent, so they pipeline
+      uint32_t peers[AS_ITEMS], old[AS_ITEMS];
+#pragma unroll
+      for (int t = 0; t < AS_ITEMS; ++t) {
+        const int64_t i = wb + t * 32 + lane;
+        dg[t] = i < c1 ? static_cast<uint32_t>(k[t] >> shift) & 0xFFu : 0xFFFFFFFFu;
+        peers[t] = __match_any_sync(0xFFFFFFFFu, dg[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < AS_ITEMS; ++t) {
+        old[t] = 0u;
+        if (dg[t] != 0xFFFFFFFFu && lane == __ffs(peers[t]) - 1)
+          old[t] = atomicAdd(&cnt[warp * 256 + dg[t]], static_cast<uint32_t>(__popc(peers[t])));
+      }
+#pragma unroll
+      for (int t = 0; t < AS_ITEMS; ++t)
+        rank[t] = __shfl_sync(0xFFFFFFFFu, old[t], __ffs(peers[t]) - 1) + __popc(peers[t] & lt);
+      __syncthreads();
+      uint32_t tc = 0;
+      if (threadIdx.x < 256) {
+#pragma unroll
+        for (int w = 0; w < AS_WARPS; ++w) {
+          const uint32_t c = cnt[w * 256 + threadIdx.x];
+          cnt[w * 256 + threadIdx.x] = tc;
+          tc += c;
+        }
+      }
+      uint32_t tn;
+      const uint32_t ls = scan256(tc, sh, tn);
+      if (threadIdx.x < 256) {
+        loc_start[threadIdx.x] = whole ? crun[threadIdx.x] : ls;
+        sub_cnt[threadIdx.x] = tc;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < AS_ITEMS; ++t) {
+        if (dg[t] != 0xFFFFFFFFu) {
+          const uint32_t lp = loc_start[dg[t]] + cnt[warp * 256 + dg[t]] + rank[t];
+          keys_s[lp] = k[t];
+          vals_s[lp] = v[t];
+        }
+      }
+      __syncthreads();
+      if (whole) {
+        if (threadIdx.x < 256) crun[threadIdx.x] += sub_cnt[threadIdx.x];
+        __syncthreads();
+        continue;
+      }
+      for (int j = threadIdx.x; j < static_cast<int>(tn); j += AS_THREADS) {
+        const uint64_t key = keys_s[j];
+        const uint32_t d = static_cast<uint32_t>(key >> shift) & 0xFFu;
+        const uint32_t pos = run[d] + (j - loc_start[d]);
+        kdst[pos] = key;
+        if (fin)
+          a.out[pos] = vals_s[j];
+        else
+          vdst[pos] = vals_s[j];
+      }
+      __syncthreads();
+      if (threadIdx.x < 256) run[threadIdx.x] += sub_cnt[threadIdx.x];
+      __syncthreads();
+    }
+    if (whole) {
+      const int len = static_cast<int>(c1 - c0);
+      for (int j = threadIdx.x; j < len; j += AS_THREADS) {
+        const uint64_t key = keys_s[j];
+        const uint32_t d = static_cast<uint32_t>(key >> shift) & 0xFFu;
+        const uint32_t pos = run[d] + (j - cstart[d]);
+        kdst[pos] = key;
+        if (fin)
+          a.out[pos] = vals_s[j];
+        else
+          vdst[pos] = vals_s[j];
+      }
+    }
+    as_stamp(a, 4 * p + 5);
+    as_barrier(a.bar, nbar);
+    if (fin) return kdst;
+    ksrc = kdst;
+    vsrc = vdst;
+    kdst = kdst == a.kb[1] ? a.kb[2] : a.kb[1];
+    vdst = vdst == a.vb[0] ? a.vb[1] : a.vb[0];
+  }
+  return ksrc;  // not reached
+}
+
+// Sort by the high 32 key bits only, then put every run of equal high bits in
+// order locally (runs of <= AS_HALO keys, one thread each; in random data the
+// runs hold 1-3 keys).  A disordered longer run raises *flag and the caller
+// redoes the sort on every digit.
+__device__ void as_fixup(const AsArgs& a, const uint64_t* ks, uint8_t* smem, int64_t c0, int64_t c1) {
+  uint64_t* K = reinterpret_cast<uint64_t*>(smem);                     // [AS_WIN + 2 AS_HALO]
+  uint32_t* I = reinterpret_cast<uint32_t*>(K + AS_WIN + 2 * AS_HALO);  // [AS_WIN + 2 AS_HALO]
+  const int64_t n = a.n;
+  for (int64_t w0 = c0; w0 < c1; w0 += AS_WIN) {
+    const int wlen = static_cast<int>(c1 - w0 < AS_WIN ? c1 - w0 : AS_WIN);
+    const int span = wlen + 2 * AS_HALO;
+    for (int j = threadIdx.x; j < span; j += AS_THREADS) {
+      const int64_t pos = w0 - AS_HALO + j;
+      if (pos >= 0 && pos < n) {
+        K[j] = __ldcg(ks + pos);
+        I[j] = static_cast<uint32_t>(__ldcg(a.out + pos));
+      }
+    }
+    __syncthreads();
+    // detection (reads only); run starts in this window that need sorting
+    int my_start[AS_WIN / AS_THREADS], my_len[AS_WIN / AS_THREADS], nmine = 0;
+    bool bad = false;
+    for (int t = threadIdx.x; t < wlen; t += AS_THREADS) {
+      const int64_t pos = w0 + t;
+      const int j = t + AS_HALO;
+      const uint32_t hi = static_cast<uint32_t>(K[j] >> 32);
+      const bool start = pos == 0 || static_cast<uint32_t>(K[j - 1] >> 32) != hi;
+      if (start) {
+        int L = 1;
+        bool dis = false;
+        while (L <= AS_HALO && pos + L < n && static_cast<uint32_t>(K[j + L] >> 32) == hi) {
+          dis |= K[j + L] < K[j + L - 1];
+          ++L;
+        }
+        if (L > AS_HALO) {
+          bad |= dis;  // a run longer than the halo: only an ordered one is accepted
+        } else if (dis) {
+          my_start[nmine] = j;
+          my_len[nmine] = L;
+          ++nmine;
+        }
+      } else if (K[j] < K[j - 1]) {
+        // disordered inside a run: fine if the run started within AS_HALO positions
+        bool found = false;
+        for (int q = 1; q <= AS_HALO && !found; ++q)
+          found = pos - q < 0 || static_cast<uint32_t>(K[j - q] >> 32) != hi;
+        bad |= !found;
+      }
+    }
+    if (bad) atomicOr(a.flag, 1u);
+    __syncthreads();
+    // fix: insertion sort of (key, index) over each short disordered run
+    for (int m = 0; m < nmine; ++m) {
+      const int j0 = my_start[m], L = my_len[m];
+      for (int x = j0 + 1; x < j0 + L; ++x) {
+        const uint64_t kx = K[x];
+        const uint32_t ix = I[x];
+        int y = x - 1;
+        while (y >= j0 && (K[y] > kx || (K[y] == kx && I[y] > ix))) {
+          K[y + 1] = K[y];
+          I[y + 1] = I[y];
+          --y;
+        }
+        K[y + 1] = kx;
+        I[y + 1] = ix;
+      }
+      for (int x = j0; x < j0 + L; ++x) a.out[w0 - AS_HALO + x] = I[x];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(AS_THREADS, 1) argsort_coop_kernel(AsArgs a) {
+  extern __shared__ __align__(16) uint8_t as_smem[];
+  __shared__ unsigned long long red_or[AS_WARPS], red_and[AS_WARPS];
+  unsigned int nbar = 0;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = a.n;
+  const int64_t c0 = n * cta / G, c1 = n * (cta + 1) / G;
+
+  // phase 0: order-preserving keys, OR / AND of all keys, and the digit totals
+  // of every pass (a digit count does not depend on the order of the keys)
+  uint32_t* h8 = reinterpret_cast<uint32_t*>(as_smem);  // [8][256]
+  for (int i = threadIdx.x; i < 8 * 256; i += AS_THREADS) h8[i] = 0u;
+  __syncthreads();
+  unsigned long long o = 0ull, an = ~0ull;
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += AS_THREADS) {
+    const double x = a.in[i];
+    const uint64_t k = f64_key(a.descending ? -x : x);
+    a.kb[0][i] = k;
+    o |= k;
+    an &= k;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) atomicAdd(&h8[q * 256 + ((k >> (8 * q)) & 0xFFu)], 1u);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    o |= __shfl_xor_sync(0xFFFFFFFFu, o, off);
+    an &= __shfl_xor_sync(0xFFFFFFFFu, an, off);
+  }
+  if (lane == 0) {
+    red_or[warp] = o;
+    red_and[warp] = an;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * 256; i += AS_THREADS)
+    if (h8[i]) atomicAdd(a.totals + i, h8[i]);
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < AS_WARPS; ++w) {
+      o |= red_or[w];
+      an &= red_and[w];
+    }
+    if (c1 > c0) {
+      atomicOr(a.orand, o);
+      atomicAnd(a.orand + 1, an);
+    }
+  }
+  as_stamp(a, 0);
+  as_barrier(a.bar, nbar);
+  as_stamp(a, 1);
+  const unsigned long long diff = __ldcg(a.orand) ^ __ldcg(a.orand + 1);
+  if (diff == 0ull) {  // every key equal: the stable order is the identity
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += AS_THREADS) a.out[i] = i;
+    return;
+  }
+  // fast path: the high 32 bits (digits 4..7), then the local fix-up
+  const uint64_t* ks = as_passes(a, 4, 7, diff, nbar, as_smem, c0, c1);
+  if (diff & 0xFFFFFFFFull) {
+    as_stamp(a, 40);
+    as_fixup(a, ks, as_smem, c0, c1);
+    as_stamp(a, 41);
+    as_barrier(a.bar, nbar);
+    as_stamp(a, 42);
+    if (__ldcg(a.flag) != 0u) as_passes(a, 0, 7, diff, nbar, as_smem, c0, c1);
+  }
+}
+
+static int coop_grid() {
+  static int g = -1;
+  if (g < 0) {
+    int per = 0;
+    if (cudaFuncSetAttribute(argsort_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(AS_SMEM)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, argsort_coop_kernel, AS_THREADS, AS_SMEM) !=
+            cudaSuccess)
+      per = 0;
+    g = per >= 1 ? num_sms() * (per > 2 ? 2 : per) : 0;
+    if (g > AS_MAX_G) g = AS_MAX_G;
+  }
+  return g;
+}
+
 static int grid_cap(int64_t work) {
   int64_t g = (work + 255) / 256;
   const int64_t cap = static_cast<int64_t>(num_sms()) * 16;
@@ -144,6 +572,9 @@ extern "C" size_t lvsk_argsort_workspace_bytes(int64_t n) {
   Measure m;
   m.take<uint64_t>(n);
   radix::measure<uint64_t>(m, n);
+  m.take<uint32_t>(static_cast<size_t>(256) * AS_MAX_G);  // coop: chunk histograms
+  m.take<uint32_t>(8 * 256);                               // coop: digit totals of every pass
+  m.take<unsigned long long>(4);                           // coop: OR, AND, barrier, flag
   return m.off;
 }
 
@@ -154,8 +585,56 @@ extern "C" int32_t lvsk_argsort_f64(const double* keys, int64_t n, int32_t desce
   Carve c(ws, ws_bytes);
   uint64_t* k64 = c.take<uint64_t>(n);
   auto rb = radix::carve<uint64_t>(c, n);
+  uint32_t* chist = c.take<uint32_t>(static_cast<size_t>(256) * AS_MAX_G);
+  uint32_t* totals = c.take<uint32_t>(8 * 256);
+  unsigned long long* ctl = c.take<unsigned long long>(4);
   LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
   cudaStream_t st = as_stream(stream);
+  const int G = coop_grid();
+  if (n <= AS_MAX_N && G >= 1 && getenv("LVSK_ARGSORT_CLASSIC") == nullptr) {
+    // ctl: [0] OR = 0, [1] AND = ~0, [2] barrier count = 0, [3] flag = 0
+    cudaError_t e = cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctl + 1, 0xFF, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(totals, 0, 8 * 256 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return cuda_status(e, "argsort memset");
+    AsArgs a;
+    a.in = keys;
+    a.n = n;
+    a.descending = descending;
+    a.out = idx_out;
+    a.kb[0] = k64;
+    a.kb[1] = rb.keys[0];
+    a.kb[2] = rb.keys[1];
+    a.vb[0] = rb.vals[0];
+    a.vb[1] = rb.vals[1];
+    a.hist = chist;
+    a.totals = totals;
+    a.orand = ctl;
+    a.bar = reinterpret_cast<unsigned int*>(ctl + 2);
+    a.flag = reinterpret_cast<unsigned int*>(ctl + 3);
+    static unsigned long long* trace = nullptr;
+    const bool tracing = getenv("LVSK_SORT_TRACE") != nullptr;
+    if (tracing && trace == nullptr) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
+    if (tracing) cudaMemsetAsync(trace, 0, 64 * sizeof(unsigned long long), st);
+    a.trace = tracing ? trace : nullptr;
+    void* args[] = {(void*)&a};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(argsort_coop_kernel), dim3(G), dim3(AS_THREADS), args,
+                                    AS_SMEM, st);
+    if (e != cudaSuccess) return cuda_status(e, "argsort coop launch");
+    if (tracing) {
+      unsigned long long h[64];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "argsort n=%lld G=%d: phase0->bar %.1f us;", (long long)n, G, (h[1] - h[0]) / 1e3);
+      for (int p = 0; p < 8; ++p)
+        if (h[4 * p + 2])
+          fprintf(stderr, " p%d hist-bar %.1f offs %.1f scatter %.1f |", p, (h[4 * p + 3] - h[4 * p + 2]) / 1e3,
+                  (h[4 * p + 4] - h[4 * p + 3]) / 1e3, (h[4 * p + 5] - h[4 * p + 4]) / 1e3);
+      if (h[40]) fprintf(stderr, " fixup %.1f bar %.1f", (h[41] - h[40]) / 1e3, (h[42] - h[41]) / 1e3);
+      fprintf(stderr, " total(from p0 end) %.1f\n", (h[42] ? h[42] : h[1]) > h[0] ? ((h[42] ? h[42] : h[1]) - h[0]) / 1e3 : 0.0);
+    }
+    return LVSK_OK;
+  }
   argsort_keys_kernel<<<grid_cap(n), 256, 0, st>>>(keys, n, descending, k64);
   LVSK_CHECK_LAUNCH("argsort keys");
   return radix::sort_pairs<uint64_t, int64_t>(k64, nullptr, n, 64, rb, nullptr, idx_out, st);

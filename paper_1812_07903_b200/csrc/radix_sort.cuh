@@ -120,16 +120,21 @@ __global__ void __launch_bounds__(THREADS) scatter_kernel(const K* __restrict__ 
   VOut v[ITEMS];
   uint32_t rank[ITEMS];
   uint32_t dg[ITEMS];
+  // all loads first (ITEMS independent DRAM requests in flight per thread)
+#pragma unroll
+  for (int t = 0; t < ITEMS; ++t) {
+    const int64_t i = base + t * 32 + lane;
+    if (i < n) {
+      k[t] = keys_in[i];
+      v[t] = vals_in ? static_cast<VOut>(vals_in[i]) : static_cast<VOut>(i);
+    }
+  }
 #pragma unroll
   for (int t = 0; t < ITEMS; ++t) {
     const int64_t i = base + t * 32 + lane;
     const bool valid = i < n;
     uint32_t d = 0xFFFFFFFFu;
-    if (valid) {
-      k[t] = keys_in[i];
-      v[t] = vals_in ? static_cast<VOut>(vals_in[i]) : static_cast<VOut>(i);
-      d = static_cast<uint32_t>(k[t] >> shift) & mask;
-    }
+    if (valid) d = static_cast<uint32_t>(k[t] >> shift) & mask;
     dg[t] = d;
     const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
     const uint32_t before = valid ? cnt[warp][d] : 0u;
@@ -251,16 +256,21 @@ __global__ void __launch_bounds__(THREADS) onesweep_kernel(const K* __restrict__
   VOut v[ITEMS];
   uint32_t rank[ITEMS];
   uint32_t dg[ITEMS];
+  // all loads first (ITEMS independent DRAM requests in flight per thread)
+#pragma unroll
+  for (int t = 0; t < ITEMS; ++t) {
+    const int64_t i = wbase + t * 32 + lane;
+    if (i < n) {
+      k[t] = keys_in[i];
+      v[t] = vals_in ? static_cast<VOut>(vals_in[i]) : static_cast<VOut>(i);
+    }
+  }
 #pragma unroll
   for (int t = 0; t < ITEMS; ++t) {
     const int64_t i = wbase + t * 32 + lane;
     const bool valid = i < n;
     uint32_t d = 0xFFFFFFFFu;
-    if (valid) {
-      k[t] = keys_in[i];
-      v[t] = vals_in ? static_cast<VOut>(vals_in[i]) : static_cast<VOut>(i);
-      d = static_cast<uint32_t>(k[t] >> shift) & mask;
-    }
+    if (valid) d = static_cast<uint32_t>(k[t] >> shift) & mask;
     dg[t] = d;
     const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
     const uint32_t before = valid ? cnt[warp][d] : 0u;
@@ -285,14 +295,27 @@ __global__ void __launch_bounds__(THREADS) onesweep_kernel(const K* __restrict__
   uint32_t excl = 0;
   if (tile > 0) {
     st_release_u32(my, LB_AGG | tile_cnt);
-    for (int64_t j = tile - 1; j >= 0; --j) {
-      const uint32_t* st = status + j * RADIX + dd;
-      uint32_t w;
-      do {
-        w = ld_acquire_u32(st);
-      } while ((w & ~LB_MASK) == 0u);
-      excl += w & LB_MASK;
-      if (w & LB_INC) break;
+    // windowed look-back: LW predecessors per hop, loaded independently, so a
+    // tile far from the inclusive frontier pays ~distance / LW load latencies
+    constexpr int LW = 16;
+    int64_t j = tile - 1;
+    for (;;) {
+      const int64_t lo = j - (LW - 1) > 0 ? j - (LW - 1) : 0;
+      const int nw = static_cast<int>(j - lo + 1);
+      uint32_t w[LW];
+#pragma unroll
+      for (int q = 0; q < LW; ++q) w[q] = q < nw ? ld_acquire_u32(status + (j - q) * RADIX + dd) : LB_INC;
+      bool done = false;
+#pragma unroll
+      for (int q = 0; q < LW; ++q) {
+        if (!done && q < nw) {
+          while ((w[q] & ~LB_MASK) == 0u) w[q] = ld_acquire_u32(status + (j - q) * RADIX + dd);
+          excl += w[q] & LB_MASK;
+          done = (w[q] & LB_INC) != 0u;
+        }
+      }
+      if (done || lo == 0) break;
+      j = lo - 1;
     }
   }
   st_release_u32(my, LB_INC | (excl + tile_cnt));

@@ -471,6 +471,25 @@ def test_argsort_matches_numpy_stable(n):
         assert np.array_equal(got, ref), (n, desc)
 
 
+@pytest.mark.parametrize("kind", ["long_runs", "short_runs", "wide_exponents"])
+def test_argsort_high_bits_then_fixup_paths(kind):
+    """K7 sorts by the high 32 key bits, then orders runs of equal high bits
+    locally (<= 64 keys) or falls back to all eight digits: keys that share
+    their high 32 bits in one long run (fallback), in many short runs (local
+    fix-up), and keys spread over many binades."""
+    rng = np.random.default_rng(7)
+    n = 300_001
+    if kind == "long_runs":
+        p = 0.5 + rng.random(n) * 1e-12
+    elif kind == "short_runs":
+        p = np.repeat(rng.random(n // 20 + 1), 20)[:n] * (1.0 + rng.random(n) * 1e-13)
+    else:
+        p = rng.random(n) ** 12
+    for desc in (True, False):
+        got = P.order.argsort_device(dev(p), desc).cpu().numpy()
+        assert np.array_equal(got, np.argsort(-p if desc else p, kind="stable")), (kind, desc)
+
+
 # ---------------------------------------------------------------------------
 # full-size properties (BASELINE config 2 shape)
 

@@ -104,6 +104,15 @@ __device__ __forceinline__ void two_sum_ordered(double a, double b, double& s, d
   err = __dsub_rn(small, __dsub_rn(s, big));
 }
 
+// two_sum(a, -c) with the same bits, without negating c: the sign of a CountSketch
+// row is uniform across the warp, so it selects this variant instead of flipping
+// every element (negation is exact and round-to-nearest is symmetric).
+__device__ __forceinline__ void two_sum_neg(double a, double c, double& s, double& err) {
+  s = __dsub_rn(a, c);
+  double bp = __dsub_rn(s, a);
+  err = __dsub_rn(__dsub_rn(a, __dsub_rn(s, bp)), __dadd_rn(c, bp));
+}
+
 template <typename T>
 __device__ __forceinline__ float to_f32(T v);
 template <>

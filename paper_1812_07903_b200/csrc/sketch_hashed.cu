@@ -162,8 +162,12 @@ __global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
 // float64 (hi, lo) registers, exactly as the reference does per bucket.
 constexpr int BULK_SLOTS = 16;
 constexpr int BULK_SEG = 2048;  // bytes per row segment
-constexpr int BULK_LANE_BYTES = 32;  // each consumer lane owns 32 B of the segment
-constexpr int BULK_CONSUMERS = BULK_SEG / (32 * BULK_LANE_BYTES);  // 2 warps
+// each consumer lane owns 32 B of the segment (8 fp32 / 4 fp64 / 16 bf16
+// values = independent TwoSum chains per lane; 16 B and 64 B measured slower)
+template <typename T>
+constexpr int bulk_lane_bytes() { return 32; }
+template <typename T>
+constexpr int bulk_consumers() { return BULK_SEG / (32 * bulk_lane_bytes<T>()); }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -211,11 +215,13 @@ __device__ __forceinline__ double contrib(T x, bool neg, double scale) {
 }
 
 template <typename T, bool UNIT>
-__global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_kernel(
+__global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1)) hashed_gather_bulk_kernel(
     const T* __restrict__ X, int64_t ldx, int64_t d, int ngroups, const uint32_t* __restrict__ vals,
     const uint32_t* __restrict__ start, int64_t k, double scale, const double* hi_in, const double* lo_in,
     double* hi_out, double* lo_out, int32_t* flags) {
-  constexpr int VEC = BULK_LANE_BYTES / static_cast<int>(sizeof(T));
+  constexpr int BULK_CONSUMERS = bulk_consumers<T>();
+  constexpr int VEC = bulk_lane_bytes<T>() / static_cast<int>(sizeof(T));
+  constexpr int NQ = bulk_lane_bytes<T>() / 16;  // 16-byte shared loads per lane and row
   __shared__ alignas(128) uint8_t ring[BULK_SLOTS][BULK_SEG];
   __shared__ uint64_t full[BULK_SLOTS], empty[BULK_SLOTS];
   __shared__ uint32_t slot_neg[BULK_SLOTS];
@@ -274,20 +280,46 @@ __global__ void __launch_bounds__(32 * (BULK_CONSUMERS + 1)) hashed_gather_bulk_
     if (nv) {
       T xs[VEC];
       const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(ring[s]) + col);
-      uint4 w[2];
-      w[0] = src[0];
-      w[1] = nv == VEC ? src[1] : make_uint4(0u, 0u, 0u, 0u);
+      uint4 w[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)  // nv is a multiple of 16 B
+        w[q] = q * (16 / static_cast<int>(sizeof(T))) < nv ? src[q] : make_uint4(0u, 0u, 0u, 0u);
       const T* wv = reinterpret_cast<const T*>(w);
 #pragma unroll
       for (int v = 0; v < VEC; ++v) xs[v] = wv[v];
+      if constexpr (UNIT) {
+        // the row's sign is warp-uniform: pick TwoSum(h, x) or TwoSum(h, -x)
+        if (neg) {
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        const double cval = contrib<T, UNIT>(xs[v], neg, scale);
-        if constexpr (sizeof(T) == 8) bad |= !isfinite(cval);
-        double sum, e;
-        two_sum(h[v], cval, sum, e);
-        h[v] = sum;
-        l[v] = __dadd_rn(l[v], e);
+          for (int v = 0; v < VEC; ++v) {
+            const double cval = to_f64<T>(xs[v]);
+            if constexpr (sizeof(T) == 8) bad |= !isfinite(cval);
+            double sum, e;
+            two_sum_neg(h[v], cval, sum, e);
+            h[v] = sum;
+            l[v] = __dadd_rn(l[v], e);
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            const double cval = to_f64<T>(xs[v]);
+            if constexpr (sizeof(T) == 8) bad |= !isfinite(cval);
+            double sum, e;
+            two_sum(h[v], cval, sum, e);
+            h[v] = sum;
+            l[v] = __dadd_rn(l[v], e);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const double cval = contrib<T, UNIT>(xs[v], neg, scale);
+          if constexpr (sizeof(T) == 8) bad |= !isfinite(cval);
+          double sum, e;
+          two_sum(h[v], cval, sum, e);
+          h[v] = sum;
+          l[v] = __dadd_rn(l[v], e);
+        }
       }
     }
     __syncwarp();
@@ -369,10 +401,10 @@ static void launch_gather_bulk(const void* X, int64_t ldx, int64_t d, const uint
   const int ngroups = static_cast<int>((d * static_cast<int64_t>(sizeof(T)) + BULK_SEG - 1) / BULK_SEG);
   const unsigned grid = static_cast<unsigned>(k * ngroups);
   if (scale == 1.0)
-    hashed_gather_bulk_kernel<T, true><<<grid, 32 * (BULK_CONSUMERS + 1), 0, st>>>(
+    hashed_gather_bulk_kernel<T, true><<<grid, 32 * (bulk_consumers<T>() + 1), 0, st>>>(
         static_cast<const T*>(X), ldx, d, ngroups, vals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags);
   else
-    hashed_gather_bulk_kernel<T, false><<<grid, 32 * (BULK_CONSUMERS + 1), 0, st>>>(
+    hashed_gather_bulk_kernel<T, false><<<grid, 32 * (bulk_consumers<T>() + 1), 0, st>>>(
         static_cast<const T*>(X), ldx, d, ngroups, vals, start, k, scale, hi_in, lo_in, hi_out, lo_out, flags);
 }
 

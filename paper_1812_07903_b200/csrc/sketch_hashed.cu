@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
 // mbarrier complete_tx), so 32 KB per CTA (~200 KB per SM) are in flight;
 // four consumer warps apply the rows in ascending index order, TwoSum into
 // float64 (hi, lo) registers, exactly as the reference does per bucket.
-constexpr int BULK_SLOTS = 16;
+constexpr int BULK_RPS = 2;     // rows per ring slot (one mbarrier round trip per pair of rows)
+constexpr int BULK_SLOTS = 8;
 constexpr int BULK_SEG = 2048;  // bytes per row segment
 // each consumer lane owns 32 B of the segment (8 fp32 / 4 fp64 / 16 bf16
 // values = independent TwoSum chains per lane; 16 B and 64 B measured slower)
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1)) hashed_gather_
   constexpr int BULK_CONSUMERS = bulk_consumers<T>();
   constexpr int VEC = bulk_lane_bytes<T>() / static_cast<int>(sizeof(T));
   constexpr int NQ = bulk_lane_bytes<T>() / 16;  // 16-byte shared loads per lane and row
-  __shared__ alignas(128) uint8_t ring[BULK_SLOTS][BULK_SEG];
+  __shared__ alignas(128) uint8_t ring[BULK_SLOTS][BULK_RPS][BULK_SEG];
   __shared__ uint64_t full[BULK_SLOTS], empty[BULK_SLOTS];
   __shared__ uint32_t slot_neg[BULK_SLOTS];
   const int64_t b = blockIdx.x / ngroups;
@@ -244,20 +245,32 @@ __global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1)) hashed_gather_
   const uint32_t cnt = p1 - p0;
   if (warp == BULK_CONSUMERS) {  // producer: one lane, one bulk copy per row; the row's sign goes to the slot
     if (lane == 0) {
-      for (uint32_t j = 0; j < cnt; ++j) {
-        const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
-        const uint32_t v = vals[p0 + j];
+      for (uint32_t q = 0; q * BULK_RPS < cnt; ++q) {
+        const uint32_t s = q % BULK_SLOTS, ph = (q / BULK_SLOTS) & 1u;
+        const uint32_t nr = cnt - q * BULK_RPS < BULK_RPS ? cnt - q * BULK_RPS : BULK_RPS;
+        uint32_t v[BULK_RPS];
+        uint32_t negs = 0;
+#pragma unroll
+        for (int r = 0; r < BULK_RPS; ++r) {
+          v[r] = r < static_cast<int>(nr) ? vals[p0 + q * BULK_RPS + r] : 0u;
+          negs |= (v[r] & 1u) << r;
+        }
         bar_wait(&empty[s], ph ^ 1u);
-        slot_neg[s] = v & 1u;
-        const T* src = X + static_cast<int64_t>(v >> 1) * ldx + c0;
+        slot_neg[s] = negs;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[s])),
-                     "r"(seg_bytes)
+                     "r"(seg_bytes * nr)
                      : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_addr(ring[s])),
-            "l"(src), "r"(seg_bytes), "r"(smem_addr(&full[s]))
-            : "memory");
+#pragma unroll
+        for (int r = 0; r < BULK_RPS; ++r) {
+          if (r < static_cast<int>(nr)) {
+            const T* src = X + static_cast<int64_t>(v[r] >> 1) * ldx + c0;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(ring[s][r])),
+                "l"(src), "r"(seg_bytes), "r"(smem_addr(&full[s]))
+                : "memory");
+          }
+        }
       }
     }
     return;
@@ -273,13 +286,10 @@ __global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1)) hashed_gather_
     l[v] = v < nv ? lo_in[so + v] : 0.0;
   }
   bool bad = false;
-  for (uint32_t j = 0; j < cnt; ++j) {
-    const uint32_t s = j % BULK_SLOTS, ph = (j / BULK_SLOTS) & 1u;
-    bar_wait(&full[s], ph);
-    const bool neg = slot_neg[s] != 0u;  // written by the producer before its (release) arrive
+  auto apply_row = [&](const uint8_t* seg, bool neg) {
     if (nv) {
       T xs[VEC];
-      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(ring[s]) + col);
+      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(seg) + col);
       uint4 w[NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q)  // nv is a multiple of 16 B
@@ -322,6 +332,13 @@ __global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1)) hashed_gather_
         }
       }
     }
+  };
+  for (uint32_t q = 0; q * BULK_RPS < cnt; ++q) {
+    const uint32_t s = q % BULK_SLOTS, ph = (q / BULK_SLOTS) & 1u;
+    bar_wait(&full[s], ph);
+    const uint32_t negs = slot_neg[s];  // written by the producer before its (release) arrive
+    apply_row(ring[s][0], (negs & 1u) != 0u);
+    if (q * BULK_RPS + 1 < cnt) apply_row(ring[s][1], (negs & 2u) != 0u);
     __syncwarp();
     if (lane == 0) bar_arrive(&empty[s]);
   }

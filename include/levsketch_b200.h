@@ -161,6 +161,14 @@ LVSK_API int32_t lvsk_leverage_tf32x3(const float* X, int64_t n, int64_t d, int6
 LVSK_API int32_t lvsk_leverage_bf16(const void* X, int64_t n, int64_t d, int64_t ldx, const void* Mt, int64_t r,
                                     int64_t r_pad, double* scores, int32_t* flags, void* stream);
 
+/* K5 operand split of a float64 fold M (d x r, row-major), one launch.
+ * bf16_mode = 0: Mt_hi / Mt_lo (r x d float32) as lvsk_leverage_tf32x3 takes
+ * them, and Mt_bf16 (r x d bfloat16, optional) = bf16(Mt_hi).
+ * bf16_mode = 1: Mt_bf16 is the (2*r_pad) x d operand of lvsk_leverage_bf16;
+ * rows [r, r_pad) and [r_pad + r, 2*r_pad) are left untouched (zero them once). */
+LVSK_API int32_t lvsk_split_fold(const double* M, int64_t d, int64_t r, int32_t bf16_mode, int64_t r_pad,
+                                 float* Mt_hi, float* Mt_lo, void* Mt_bf16, void* stream);
+
 /* ---- K2 / K6: CSR rows (extension G2; BASELINE config 4) -----------------
  * Same semantics as lvsk_hashed_sketch / lvsk_rowsumsq_gemm on the densified
  * rows (bit-exact for K2: zero entries leave the TwoSum state unchanged).

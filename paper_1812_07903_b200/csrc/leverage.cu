@@ -80,6 +80,50 @@ __global__ void __launch_bounds__(256) rowsumsq_simt_kernel(const T* __restrict_
 
 using namespace lvsk;
 
+namespace lvsk {
+
+// K5 operand split of a float64 fold M (d x r) in one launch (was a chain of
+// small framework kernels on the fold's critical path):
+//   tf32 mode:  Mt_hi = M^T with the low 13 mantissa bits of fp32(M) cleared
+//               (exact TF32), Mt_lo = fp32(M^T - Mt_hi), Mt_hb = bf16(Mt_hi)
+//   bf16 mode:  out rows [0, r) = bf16(fp32(M^T)), rows [r_pad, r_pad + r) =
+//               bf16(fp32(M^T - hi))   (the other rows stay as they are)
+__global__ void split_fold_kernel(const double* __restrict__ M, int64_t d, int64_t r, int bf16_mode, int64_t r_pad,
+                                  float* __restrict__ hi, float* __restrict__ lo, __nv_bfloat16* __restrict__ hb) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < d * r;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / r, c = idx - i * r;
+    const double m = M[idx];
+    if (bf16_mode) {
+      const __nv_bfloat16 h = __float2bfloat16_rn(__double2float_rn(m));
+      const __nv_bfloat16 l = __float2bfloat16_rn(__double2float_rn(m - static_cast<double>(__bfloat162float(h))));
+      hb[c * d + i] = h;
+      hb[(r_pad + c) * d + i] = l;
+    } else {
+      const float h = __uint_as_float(__float_as_uint(__double2float_rn(m)) & ~0x1FFFu);
+      hi[c * d + i] = h;
+      lo[c * d + i] = __double2float_rn(m - static_cast<double>(h));
+      if (hb != nullptr) hb[c * d + i] = __float2bfloat16_rn(h);
+    }
+  }
+}
+
+}  // namespace lvsk
+
+extern "C" int32_t lvsk_split_fold(const double* M, int64_t d, int64_t r, int32_t bf16_mode, int64_t r_pad,
+                                   float* Mt_hi, float* Mt_lo, void* Mt_bf16, void* stream) {
+  using namespace lvsk;
+  LVSK_REQUIRE(d >= 1 && r >= 1 && M, LVSK_ERR_DIMENSION, "bad fold shape d=%lld r=%lld", (long long)d, (long long)r);
+  LVSK_REQUIRE(bf16_mode ? (Mt_bf16 != nullptr && r_pad >= r) : (Mt_hi != nullptr && Mt_lo != nullptr),
+               LVSK_ERR_CONFIGURATION, "missing split outputs");
+  const int64_t work = d * r;
+  const unsigned grid = static_cast<unsigned>(work < 256 * 1184 ? (work + 255) / 256 : 1184);
+  split_fold_kernel<<<grid, 256, 0, as_stream(stream)>>>(M, d, r, bf16_mode, r_pad, Mt_hi, Mt_lo,
+                                                         static_cast<__nv_bfloat16*>(Mt_bf16));
+  LVSK_CHECK_LAUNCH("split fold");
+  return LVSK_OK;
+}
+
 extern "C" int32_t lvsk_rowsumsq_gemm(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx,
                                       const void* M, const void* M_lo, int64_t r, double* scores, int32_t* flags,
                                       void* stream) {

@@ -373,18 +373,14 @@ class KernelOperands:
 
     def set(self, M: torch.Tensor) -> None:
         self.M64 = M
-        if self.bf16:
-            mt = M.T
-            hi = mt.to(torch.bfloat16)
-            lo = (mt - hi.to(torch.float64)).to(torch.bfloat16)
-            self.a[: self.r].copy_(hi)
-            self.a[self.r_pad : self.r_pad + self.r].copy_(lo)
-        elif self.tc:
-            hi, lo = split_m_tf32(M)
-            self.a.copy_(hi)
-            self.b.copy_(lo)
-            if self.hb is not None:
-                self.hb.copy_(hi)
+        if self.bf16 or self.tc:  # one split kernel (csrc/leverage.cu)
+            Mc = M.contiguous()
+            if self.bf16:
+                N.check(N.lib().lvsk_split_fold(Mc.data_ptr(), self.d, self.r, 1, self.r_pad, None, None,
+                                                self.a.data_ptr(), N.stream_ptr()), "split fold")
+            else:
+                N.check(N.lib().lvsk_split_fold(Mc.data_ptr(), self.d, self.r, 0, 0, self.a.data_ptr(),
+                                                self.b.data_ptr(), N.ptr(self.hb), N.stream_ptr()), "split fold")
         else:
             hi, lo = split_m(M, self.a.dtype)
             self.a.copy_(hi)

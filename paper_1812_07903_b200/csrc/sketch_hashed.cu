@@ -156,12 +156,14 @@ __global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
 // ---------------------------------------------------------------------------
 // Bulk-copy gather (default when rows are 16-byte aligned): one CTA owns one
 // (bucket, 2 KB column group).  A producer warp streams the bucket's row
-// segments into a 16-slot shared-memory ring with cp.async.bulk (TMA 1-D,
-// mbarrier complete_tx), so 32 KB per CTA (~200 KB per SM) are in flight;
-// four consumer warps apply the rows in ascending index order, TwoSum into
+// segments into a 6-slot x 2-row shared-memory ring with cp.async.bulk (TMA 1-D,
+// mbarrier complete_tx), so 24 KB per CTA (~190 KB per SM) are in flight;
+// two consumer warps apply the rows in ascending index order, TwoSum into
 // float64 (hi, lo) registers, exactly as the reference does per bucket.
 constexpr int BULK_RPS = 2;     // rows per ring slot (one mbarrier round trip per pair of rows)
-constexpr int BULK_SLOTS = 8;
+// 6 slots x 2 rows x 2 KB = 24 KB ring and <= 78 registers (launch bound of 8
+// CTAs/SM): 8 CTAs per SM, 0.452 -> 0.426 ms at C2 vs 8 slots / 88 registers
+constexpr int BULK_SLOTS = 6;
 constexpr int BULK_SEG = 2048;  // bytes per row segment
 // each consumer lane owns 32 B of the segment (8 fp32 / 4 fp64 / 16 bf16
 // values = independent TwoSum chains per lane; 16 B and 64 B measured slower)
@@ -216,7 +218,7 @@ __device__ __forceinline__ double contrib(T x, bool neg, double scale) {
 }
 
 template <typename T, bool UNIT>
-__global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1)) hashed_gather_bulk_kernel(
+__global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1), 8) hashed_gather_bulk_kernel(
     const T* __restrict__ X, int64_t ldx, int64_t d, int ngroups, const uint32_t* __restrict__ vals,
     const uint32_t* __restrict__ start, int64_t k, double scale, const double* hi_in, const double* lo_in,
     double* hi_out, double* lo_out, int32_t* flags) {

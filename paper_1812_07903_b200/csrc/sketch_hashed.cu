@@ -15,6 +15,8 @@
 // row segments; the accumulator never round-trips HBM.
 #include <cstdlib>
 
+#include <cstdio>
+
 #include "radix_sort.cuh"
 
 namespace lvsk {
@@ -438,6 +440,230 @@ static void launch_gather(const void* X, int64_t ldx, int64_t d, const uint32_t*
                                                      scale, hi_in, lo_in, hi_out, lo_out, flags);
 }
 
+// ---------------------------------------------------------------------------
+// Bucket grouping in ONE cooperative kernel (k <= GC_MAX_K): a stable counting
+// sort of the (row, block) items by bucket.  CTA c owns a contiguous item range
+// and each of its 8 warps a contiguous sub-range, so stable order = (CTA, warp,
+// 32-item step, lane):
+//   1. hash every item once (bucket, value kept in shared memory when the
+//      chunk fits), per-warp bucket counts, CTA histogram -> ghist[b][cta]
+//   2. grid barrier; CTA c turns the rows of its ~k/G buckets into prefix
+//      counts over the CTAs (one warp scan per bucket) and bucket totals
+//   3. grid barrier; every CTA scans the totals (bucket starts, written by
+//      CTA 0 as `start`), adds its prefix and its warps' prefixes, and each
+//      warp writes its items' values in order (match_any ranks equal buckets
+//      within a step; the warp's own counter orders the steps)
+// Replaces keygen + two radix passes + bucket bounds (7 launches).
+constexpr int GC_THREADS = 256;
+constexpr int GC_WARPS = GC_THREADS / 32;
+constexpr int64_t GC_MAX_K = 4096;
+constexpr int GC_MAX_G = 256;
+constexpr int GC_PER = static_cast<int>(GC_MAX_K / GC_THREADS);  // buckets per thread in the base scan
+constexpr int GC_CAP = 7168;                                       // items cached per CTA
+constexpr size_t GC_SMEM = sizeof(uint32_t) * ((GC_WARPS + 2) * GC_MAX_K + 2 * GC_CAP);
+
+__device__ __forceinline__ void gc_barrier(unsigned int* count, unsigned int& nbar) {
+  const unsigned int target = (++nbar) * gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(count, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void gc_item(int64_t t, int64_t n, uint64_t row0, const KeygenBlocks& P, uint32_t& bk,
+                                        uint32_t& val) {
+  const int jj = static_cast<int>(t / n);
+  const int64_t r = t - static_cast<int64_t>(jj) * n;
+  const uint64_t g = row0 + static_cast<uint64_t>(r);
+  bk = P.offset[jj] + bucket_hash(g, P.a[jj], P.b[jj], P.size[jj]);
+  val = (static_cast<uint32_t>(r) << 1) | (sign_negative(g, P.key[jj]) ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(GC_THREADS, 1) group_coop_kernel(int64_t n, int nb, uint64_t row0, KeygenBlocks P,
+                                                                   int64_t k, uint32_t* __restrict__ svals,
+                                                                   uint32_t* __restrict__ start, uint32_t* ghist,
+                                                                   uint32_t* gtot, uint32_t* pre, unsigned int* bar,
+                                                                   unsigned long long* trace) {
+  auto stamp = [&](int slot) {
+    if (trace != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[slot + (blockIdx.x == 0 ? 0 : 8)] = t;
+    }
+  };
+  stamp(0);
+  extern __shared__ uint32_t gc_smem[];
+  uint32_t* hw = gc_smem;                     // [GC_WARPS][k] per-warp counts, then per-warp write offsets
+  uint32_t* base = gc_smem + GC_WARPS * k;    // [k]
+  uint32_t* prow = base + k;                  // [k] this CTA's prefix row
+  uint32_t* items = prow + k;                 // [GC_CAP][2] (bucket, value) in item order
+  __shared__ uint32_t sh[GC_WARPS];
+  unsigned int nbar = 0;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t N = n * nb;
+  const int64_t c0 = N * cta / G, c1 = N * (cta + 1) / G;
+  const bool cached = c1 - c0 <= GC_CAP;
+  const int64_t w0 = c0 + (c1 - c0) * warp / GC_WARPS, w1 = c0 + (c1 - c0) * (warp + 1) / GC_WARPS;
+  for (int64_t i = threadIdx.x; i < GC_WARPS * k; i += GC_THREADS) hw[i] = 0u;
+  __syncthreads();
+  // 1. hash, per-warp counts
+  for (int64_t t = w0 + lane; t < w1; t += 32) {
+    uint32_t bk, val;
+    gc_item(t, n, row0, P, bk, val);
+    if (cached) {
+      items[2 * (t - c0)] = bk;
+      items[2 * (t - c0) + 1] = val;
+    }
+    atomicAdd(&hw[warp * k + bk], 1u);
+  }
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b < k; b += GC_THREADS) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < GC_WARPS; ++w) {
+      const uint32_t c = hw[w * k + b];
+      hw[w * k + b] = run;  // prefix over the CTA's earlier warps
+      run += c;
+    }
+    ghist[b * G + cta] = run;  // bucket-major: a bucket's CTA counts are contiguous
+  }
+  stamp(1);
+  gc_barrier(bar, nbar);
+  stamp(2);
+  // 2. prefix over CTAs for my buckets: one warp per bucket, all loads up front
+  {
+    const int64_t b0 = k * cta / G, b1 = k * (cta + 1) / G;
+    for (int64_t b = b0 + warp; b < b1; b += GC_WARPS) {
+      const uint32_t* row = ghist + b * G;
+      uint32_t v[GC_MAX_G / 32];
+#pragma unroll
+      for (int q = 0; q < GC_MAX_G / 32; ++q) v[q] = q * 32 + lane < G ? __ldcg(row + q * 32 + lane) : 0u;
+      uint32_t carry = 0;
+#pragma unroll
+      for (int q = 0; q < GC_MAX_G / 32; ++q) {
+        if (q * 32 >= G) break;
+        uint32_t x = v[q];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+          if (lane >= off) x += y;
+        }
+        if (q * 32 + lane < G) pre[static_cast<int64_t>(q * 32 + lane) * k + b] = carry + x - v[q];
+        carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+      }
+      if (lane == 0) gtot[b] = carry;
+    }
+  }
+  stamp(3);
+  gc_barrier(bar, nbar);
+  stamp(4);
+  // 3. bucket starts: totals and this CTA's prefix row staged through shared
+  // memory with coalesced loads, then thread t scans buckets [t*PER, (t+1)*PER)
+  {
+    uint32_t tv[GC_PER], pv[GC_PER];  // all 2 x GC_PER loads in flight before any store
+#pragma unroll
+    for (int q = 0; q < GC_PER; ++q) {
+      const int64_t b = threadIdx.x + static_cast<int64_t>(q) * GC_THREADS;
+      tv[q] = b < k ? __ldcg(gtot + b) : 0u;
+      pv[q] = b < k ? __ldcg(pre + static_cast<int64_t>(cta) * k + b) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < GC_PER; ++q) {
+      const int64_t b = threadIdx.x + static_cast<int64_t>(q) * GC_THREADS;
+      if (b < k) {
+        base[b] = tv[q];
+        prow[b] = pv[q];
+      }
+    }
+  }
+  __syncthreads();
+  {
+    const int64_t b0 = static_cast<int64_t>(threadIdx.x) * GC_PER;
+    uint32_t run = 0;
+#pragma unroll
+    for (int q = 0; q < GC_PER; ++q) run += b0 + q < k ? base[b0 + q] : 0u;
+    uint32_t x = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    uint32_t acc = x - run;
+    for (int w = 0; w < warp; ++w) acc += sh[w];
+    uint32_t tv[GC_PER];
+#pragma unroll
+    for (int q = 0; q < GC_PER; ++q) tv[q] = b0 + q < k ? base[b0 + q] : 0u;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < GC_PER; ++q) {
+      if (b0 + q < k) base[b0 + q] = acc;  // bucket start
+      acc += tv[q];
+    }
+  }
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b < k; b += GC_THREADS) {  // consecutive buckets per warp: no bank conflicts
+    const uint32_t st0 = base[b];
+    if (cta == 0) start[b] = st0;
+    const uint32_t o = st0 + prow[b];
+#pragma unroll
+    for (int w = 0; w < GC_WARPS; ++w) hw[w * k + b] += o;
+  }
+  if (cta == 0 && threadIdx.x == 0) start[k] = static_cast<uint32_t>(N);
+  __syncthreads();
+  stamp(5);
+  // 4. stable scatter of the values, warp by warp
+  const uint32_t lt = lanemask_lt();
+  uint32_t* my = hw + warp * k;
+  for (int64_t t0 = w0; t0 < w1; t0 += 32) {
+    const int64_t t = t0 + lane;
+    const bool valid = t < w1;
+    uint32_t bk = 0xFFFFFFFFu, val = 0u;
+    if (valid) {
+      if (cached) {
+        bk = items[2 * (t - c0)];
+        val = items[2 * (t - c0) + 1];
+      } else {
+        gc_item(t, n, row0, P, bk, val);
+      }
+    }
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, bk);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0u;
+    if (valid && lane == leader) {
+      old = my[bk];
+      my[bk] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xFFFFFFFFu, old, leader);
+    if (valid) svals[old + __popc(peers & lt)] = val;
+    __syncwarp();
+  }
+  __syncthreads();
+  stamp(6);
+}
+
+static int gc_grid() {
+  static int g = -1;
+  if (g < 0) {
+    int per = 0;
+    if (cudaFuncSetAttribute(group_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(GC_SMEM)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, group_coop_kernel, GC_THREADS, GC_SMEM) != cudaSuccess)
+      per = 0;
+    g = per >= 1 ? num_sms() : 0;
+    if (g > GC_MAX_G) g = GC_MAX_G;
+  }
+  return g;
+}
+
 }  // namespace lvsk
 
 using namespace lvsk;
@@ -451,6 +677,12 @@ extern "C" size_t lvsk_hashed_workspace_bytes(int64_t n, int32_t s, int64_t k) {
   m.take<uint32_t>(N);  // sorted vals
   m.take<uint32_t>(k + 1);
   radix::measure<uint32_t>(m, N);
+  if (k <= GC_MAX_K) {  // cooperative grouping: CTA histograms and prefixes, bucket totals, barrier
+    m.take<uint32_t>(static_cast<size_t>(GC_MAX_G) * k);
+    m.take<uint32_t>(static_cast<size_t>(GC_MAX_G) * k);
+    m.take<uint32_t>(k);
+    m.take<uint32_t>(4);
+  }
   return m.off;
 }
 
@@ -483,17 +715,52 @@ extern "C" int32_t lvsk_hashed_sketch(const void* X, int32_t dtype, int64_t n, i
   auto rb = radix::carve<uint32_t>(c, N);
   LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
 
-  for (int j0 = 0; j0 < s; j0 += KEYGEN_MAX_BLOCKS) {
-    const int nb = s - j0 < KEYGEN_MAX_BLOCKS ? s - j0 : KEYGEN_MAX_BLOCKS;
+  const int G = k <= GC_MAX_K && s <= KEYGEN_MAX_BLOCKS ? gc_grid() : 0;
+  if (G >= 1 && getenv("LVSK_GROUP_RADIX") == nullptr) {
+    uint32_t* ghist = c.take<uint32_t>(static_cast<size_t>(GC_MAX_G) * k);  // [k][G]
+    uint32_t* pre = c.take<uint32_t>(static_cast<size_t>(GC_MAX_G) * k);    // [G][k]
+    uint32_t* gtot = c.take<uint32_t>(k);
+    uint32_t* bar = c.take<uint32_t>(4);
+    LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
+    cudaError_t e = cudaMemsetAsync(bar, 0, 4 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return cuda_status(e, "group memset");
     KeygenBlocks P;
-    fill_blocks(P, blocks, j0, nb);
-    hashed_keygen_kernel<<<grid_for(n * nb, 256), 256, 0, st>>>(n, row0, j0, nb, P, keys, vals);
+    fill_blocks(P, blocks, 0, s);
+    int nb = s;
+    unsigned int* barp = bar;
+    static unsigned long long* trace = nullptr;
+    const bool tracing = getenv("LVSK_GROUP_TRACE") != nullptr;
+    if (tracing && trace == nullptr) cudaMalloc(&trace, 16 * sizeof(unsigned long long));
+    unsigned long long* tr = tracing ? trace : nullptr;
+    void* args[] = {(void*)&n, (void*)&nb, (void*)&row0, (void*)&P, (void*)&k, (void*)&svals, (void*)&start,
+                    (void*)&ghist, (void*)&gtot, (void*)&pre, (void*)&barp, (void*)&tr};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(group_coop_kernel), dim3(G), dim3(GC_THREADS), args,
+                                    static_cast<size_t>(sizeof(uint32_t) * ((GC_WARPS + 2) * k + 2 * GC_CAP)), st);
+    if (e != cudaSuccess) return cuda_status(e, "group coop launch");
+    if (tracing) {
+      unsigned long long h[16];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+      for (int c = 0; c < 2; ++c) {
+        const unsigned long long* q = h + 8 * c;
+        fprintf(stderr, "group cta %s: count %.1f bar %.1f colscan %.1f bar %.1f bases %.1f scatter %.1f us\n",
+                c ? "last" : "0", (q[1] - q[0]) / 1e3, (q[2] - q[1]) / 1e3, (q[3] - q[2]) / 1e3, (q[4] - q[3]) / 1e3,
+                (q[5] - q[4]) / 1e3, (q[6] - q[5]) / 1e3);
+      }
+    }
+  } else {
+    for (int j0 = 0; j0 < s; j0 += KEYGEN_MAX_BLOCKS) {
+      const int nb = s - j0 < KEYGEN_MAX_BLOCKS ? s - j0 : KEYGEN_MAX_BLOCKS;
+      KeygenBlocks P;
+      fill_blocks(P, blocks, j0, nb);
+      hashed_keygen_kernel<<<grid_for(n * nb, 256), 256, 0, st>>>(n, row0, j0, nb, P, keys, vals);
+    }
+    LVSK_CHECK_LAUNCH("hashed keygen");
+    int32_t rc = radix::sort_pairs<uint32_t, uint32_t>(keys, vals, N, ceil_log2(k), rb, skeys, svals, st);
+    if (rc != LVSK_OK) return rc;
+    radix::bucket_bounds_kernel<uint32_t><<<grid_for(N + 1, 256), 256, 0, st>>>(skeys, N, k, start);
+    LVSK_CHECK_LAUNCH("bucket bounds");
   }
-  LVSK_CHECK_LAUNCH("hashed keygen");
-  int32_t rc = radix::sort_pairs<uint32_t, uint32_t>(keys, vals, N, ceil_log2(k), rb, skeys, svals, st);
-  if (rc != LVSK_OK) return rc;
-  radix::bucket_bounds_kernel<uint32_t><<<grid_for(N + 1, 256), 256, 0, st>>>(skeys, N, k, start);
-  LVSK_CHECK_LAUNCH("bucket bounds");
 
   const uintptr_t xa = reinterpret_cast<uintptr_t>(X);
   const bool bulk = getenv("LVSK_K1_REGS") == nullptr;  // register-path gather kept for A/B checks

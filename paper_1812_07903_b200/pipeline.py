@@ -223,9 +223,16 @@ class LeveragePipeline:
         elif fam == GAUSSIAN:
             sk = 2
         else:
-            sk = 1 + radix(self.n * self.spec.s, max(1, (self.k - 1).bit_length())) + 1 + 1 + 1
+            # grouping: one cooperative counting sort (k <= 4096, s <= 64; csrc/sketch_hashed.cu)
+            # or keygen + radix passes + bucket bounds; then the gather (K1) and the hi+lo fold
+            coop = self.k <= 4096 and self.spec.s <= 64 and not os.environ.get("LVSK_GROUP_RADIX")
+            group = 1 if coop else 1 + radix(self.n * self.spec.s, max(1, (self.k - 1).bit_length())) + 1
+            sk = group + 1 + 1
         lev = 1
         k, d = self.sx.shape
-        fold = 1 if (self.pi is not None and self.rank is None and k >= d) else 0  # KF (chol_fold_kernel)
-        order_ = (3 + 1 + radix(self.n, 64)) if self.order else 0
+        # KF (chol_fold_kernel) + the K5 operand split (split_fold_kernel)
+        fold = 2 if (self.pi is not None and self.rank is None and k >= d) else 0
+        # normalise (2-stage sum + divide), then K7: one cooperative kernel up to 8M keys
+        coop_sort = self.n <= (8 << 20) and not os.environ.get("LVSK_ARGSORT_CLASSIC")
+        order_ = (3 + (1 if coop_sort else 1 + radix(self.n, 64))) if self.order else 0
         return sk + fold + lev + order_

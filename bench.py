@@ -431,7 +431,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     roofline = {
         "bound": "hbm",
         "kernel": {"sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. keygen + radix grouping)",
-                              "osnap": "csr_gather_kernel (K2, incl. keygen + radix grouping)" if csr else
+                              "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
                               "hashed_gather_bulk_kernel (K1, incl. keygen + radix grouping)",
                               "srht": "srht_pass1/pass2 kernels (K3)",
                               "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
@@ -472,7 +472,10 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
 
         def e2e_step():
             if world == 1:
-                res = P.leverage_sketched_trunc(Xh, spec, cfg["sv_tol"], jl_dim=r, rank=cfg.get("rank"))
+                # C3's SRHT transform buffer (4.3 GB) exceeds the reference's 4 GiB default cap (G8)
+                cap = (16 << 30) if cfg["family"] == "srht" else None
+                res = P.leverage_sketched_trunc(Xh, spec, cfg["sv_tol"], mem_cap_bytes=cap, jl_dim=r,
+                                                rank=cfg.get("rank"))
                 plan = P.make_plan(P.scores_to_distribution(res.scores), P.OrderingPolicy("dec"))
                 return plan.indices
             local, *_ = P.run_sharded(Xh, row0, n * world, spec, cfg["sv_tol"], jl_dim=r)

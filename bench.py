@@ -430,9 +430,9 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             traffic = None
     roofline = {
         "bound": "hbm",
-        "kernel": {"sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. keygen + radix grouping)",
+        "kernel": {"sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
                               "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
-                              "hashed_gather_bulk_kernel (K1, incl. keygen + radix grouping)",
+                              "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
                               "srht": "srht_pass1/pass2 kernels (K3)",
                               "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
                               if not csr and X.dtype == torch.bfloat16 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],

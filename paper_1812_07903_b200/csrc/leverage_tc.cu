@@ -219,6 +219,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 // ~2^-19 of the result.  Per 256 x 32 stage the tensor core reads 88 KB of
 // smem operands instead of 144 KB in v1.
 
+// v2 runs 8 worker warps (two per TMEM lane quarter): all 8 make the x_lo
+// tile of every stage (the transform is the kernel's longest per-stage chain),
+// warps 2-5 read back sub-tile 0 and warps 6-9 sub-tile 1
+constexpr int V2_EPI = 256;               // x_lo transform threads (all worker warps; 12 warps measured slower)
+constexpr int V2_READ = 256;              // TMEM read-back threads (the first 8 worker warps)
+constexpr int V2_THREADS = 64 + V2_EPI;
+
 struct Cfg2 {
   static constexpr int N = 64;
   static constexpr int SX = 4;                             // X ring (the HBM stream)
@@ -241,7 +248,7 @@ struct Cfg2 {
       (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 };
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(V2_THREADS, 1)
     leverage_v2_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapHi,
                        const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ CUtensorMap mapHb,
                        int64_t n, int kchunks, double* __restrict__ scores, int32_t* flags) {
@@ -265,19 +272,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::SX; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&xempty[s], 1 + EPI_THREADS);
+      mbar_init(&xempty[s], 1 + V2_EPI);
     }
     for (int s = 0; s < C::SB; ++s) {
       mbar_init(&bfull[s], 1);
       mbar_init(&bempty[s], 1);
     }
     for (int s = 0; s < C::SL; ++s) {
-      mbar_init(&xlfull[s], EPI_THREADS);
+      mbar_init(&xlfull[s], V2_EPI);
       mbar_init(&xlempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
-      mbar_init(&accempty[b], EPI_THREADS);
+      mbar_init(&accempty[b], V2_READ);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
@@ -370,6 +377,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     const int et = threadIdx.x - 64;
     const int quarter = warp & 3;
+    const int my_sub = (warp - 2) >> 2;  // epilogue sub-tile of this warp
     bool bad = false;
     uint32_t it = 0, lt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint8_t* xsm = smem + sx * C::X_BYTES;
         uint8_t* xl = smem + C::OFF_XL + sl * C::XL_BYTES;
 #pragma unroll 4
-        for (int i = et; i < TILE_ROWS * 8; i += EPI_THREADS) {
+        for (int i = et; i < TILE_ROWS * 8; i += V2_EPI) {
           const int row = i >> 3, c = i & 7;
           const float4 v = *reinterpret_cast<const float4*>(xsm + row * 128 + ((c ^ (row & 7)) << 4));
           bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
@@ -401,11 +409,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_arrive(&xlfull[sl]);
         mbar_arrive(&xempty[sx]);
       }
+      if (my_sub >= SUB) continue;  // transform-only warps
       const uint32_t ab = lt & 1u, aph = (lt >> 1) & 1u;
       mbar_wait(&accfull[ab], aph);
       tc_fence_after();
-#pragma unroll
-      for (int sub = 0; sub < SUB; ++sub) {
+      {
+        const int sub = my_sub;
         float acc = 0.f;
         const uint32_t base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + ab * C::ACC_COLS + sub * 2 * C::N;
 #pragma unroll
@@ -483,7 +492,7 @@ static int32_t launch_v2(const float* X, int64_t n, int64_t d, int64_t ldx, cons
   const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
   const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
   const int kchunks = static_cast<int>((d + BK - 1) / BK);
-  leverage_v2_kernel<<<grid, THREADS, C::SMEM_BYTES, st>>>(mx, mh, ml, mb, n, kchunks, scores, flags);
+  leverage_v2_kernel<<<grid, V2_THREADS, C::SMEM_BYTES, st>>>(mx, mh, ml, mb, n, kchunks, scores, flags);
   LVSK_CHECK_LAUNCH("leverage v2");
   return LVSK_OK;
 }

@@ -675,3 +675,28 @@ def test_streamed_host_input_equals_device_input(monkeypatch):
         a = P.leverage_sketched_trunc(Xh, spec, 1e-6, jl_dim=64)
         b = P.leverage_sketched_trunc(Xd, spec, 1e-6, jl_dim=64)
         assert np.array_equal(a.scores, b.scores), fam
+
+
+# ---------------------------------------------------------------------------
+# out-of-core streaming
+
+
+@pytest.mark.parametrize("family,s,dtype", [("countsketch", None, torch.float64), ("osnap", 3, torch.float64),
+                                            ("gaussian", None, torch.float32)])
+def test_leverage_streamed_matches_in_memory(tmp_path, family, s, dtype):
+    """Two streaming passes over an LVSK file in ragged blocks give the scores
+    of the in-memory call (hashed families: the same sketch bits)."""
+    rng = np.random.default_rng(3)
+    n, d = 20_011, 40
+    x = rng.standard_normal((n, 6)) @ rng.standard_normal((6, d)) + 0.3 * rng.standard_normal((n, d))
+    path = tmp_path / "x.lvsk"
+    P.save_matrix(x, path)
+    spec = P.SketchSpec(family, eps=0.5, d=d, seed=2, rows_override=512, osnap_s=s)
+    got = P.leverage_streamed(path, spec, 1e-6, block_rows=3001, dtype=dtype, jl_dim=16)
+    xin = x if dtype == torch.float64 else x.astype(np.float32)
+    ref = P.leverage_sketched_trunc(torch.from_numpy(xin).cuda(), spec, 1e-6, jl_dim=16)
+    assert got.effective_rank == ref.effective_rank
+    if family == "gaussian":
+        np.testing.assert_allclose(got.scores, ref.scores, rtol=1e-5)  # fp32 blocks: partial sums reassociate
+    else:
+        assert np.array_equal(got.scores, ref.scores)

@@ -191,3 +191,22 @@ def test_error_hierarchy():
                  "DegenerateInputError", "SingularInversionError", "UnsupportedFamilyError", "ConfigurationError"):
         assert issubclass(getattr(errors, name), errors.LevsketchError)
     assert issubclass(errors.ParseError, errors.FormatError)
+
+
+def test_open_lvsk_validates_header(tmp_path):
+    import paper_1812_07903_b200 as P
+    from paper_1812_07903_b200 import errors
+
+    x = np.arange(12.0).reshape(4, 3)
+    good = tmp_path / "g.lvsk"
+    P.save_matrix(x, good)
+    m = P.open_lvsk(good)
+    assert m.shape == (4, 3) and np.array_equal(np.asarray(m), x)
+    bad = tmp_path / "b.lvsk"
+    bad.write_bytes(b"XXXX" + good.read_bytes()[4:])
+    with pytest.raises(errors.FormatError):
+        P.open_lvsk(bad)
+    short = tmp_path / "s.lvsk"
+    short.write_bytes(good.read_bytes()[:-8])
+    with pytest.raises(errors.FormatError):
+        P.open_lvsk(short)

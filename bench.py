@@ -260,7 +260,10 @@ def run_reference(args, cfg, rank: int):
     # adaptive sample: the whole --steps K run should take about two minutes
     rate, _ = cpu_leg(cfg, 20_000, threads)
     per_step_s = 120.0 / max(1, args.steps)
-    sample = int(min(args.ref_rows, max(10_000, rate * per_step_s)))
+    # the sample grows up to the whole workload (the SVD / sort fixed costs then
+    # weigh on the CPU rate as they do on a full run)
+    cap = args.ref_rows if args.ref_rows else cfg["n"]
+    sample = int(min(cap, max(10_000, rate * per_step_s)))
     times = []
     for _ in range(args.steps):
         _, dt = cpu_leg(cfg, sample, threads)
@@ -550,7 +553,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-rows", type=int, default=500_000)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-rows", type=int, default=100_000)
+    ap.add_argument("--ref-rows", type=int, default=0, help="cap on the reference arm's rows per step (0: the workload's n)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stage-sync", action="store_true", help="sync after every step to sum stage times")

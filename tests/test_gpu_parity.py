@@ -89,6 +89,24 @@ def test_hashed_ragged_and_strided():
             assert np.array_equal(P.apply_sketch(view, spec).data, hi + lo), (n, d, fam)
 
 
+@pytest.mark.parametrize("k,s,n", [(4096, 1, 200_003), (4096, 4, 300_001), (4095, 2, 30_000), (6000, 1, 40_000),
+                                   (1, 1, 999), (37, 37, 2_000)])
+def test_hashed_grouping_paths(monkeypatch, k, s, n):
+    """K1's bucket grouping: the cooperative counting sort (k <= 4096, s <= 64;
+    ragged item ranges over the CTAs, items cached in shared memory or rehashed
+    when a CTA holds more than 7168, one bucket) and the
+    radix fallback (k > 4096, or forced) give the oracle's state bit for bit."""
+    rng = np.random.default_rng(k + s)
+    d = 24
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    fam = "countsketch" if s == 1 else "osnap"
+    spec = P.SketchSpec(fam, eps=0.5, d=d, seed=9, rows_override=k, osnap_s=s if s > 1 else None)
+    hi, lo = O.hashed_sketch(x, fam, k, 9, s)
+    assert np.array_equal(P.apply_sketch(dev(x), spec).data, hi + lo)
+    monkeypatch.setenv("LVSK_GROUP_RADIX", "1")
+    assert np.array_equal(P.apply_sketch(dev(x), spec).data, hi + lo)
+
+
 def test_stream_update_and_order_independence(golden, golden_meta):
     m = golden_meta["sketch"][0]
     x = golden["sk0_x"]

@@ -121,38 +121,58 @@ __device__ __forceinline__ void store_tile_t(double* g, int64_t ld, const double
 
 // ---- tile math ---------------------------------------------------------------
 
+// one k-step of the 4 x 4 register-blocked tile product: rows a >= AMIN only
+// (At upper triangular), and only blocks a <= b when SYM (symmetric result,
+// upper triangle needed)
+template <int AMIN, bool SYM>
+__device__ __forceinline__ void gemm_step(double (&acc)[4][4], const double* At, const double* B, int p, int ty,
+                                          int tx, double sg) {
+  double av[4], bv[4];
+#pragma unroll
+  for (int a = AMIN; a < 4; ++a) av[a] = sg * At[p * FLD + ty + 16 * a];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) bv[b] = B[p * FLD + tx + 16 * b];
+#pragma unroll
+  for (int a = AMIN; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (!SYM || a <= b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+}
+
 // out = At^T B (MODE 0), C - At^T B (MODE 1) or C + At^T B (MODE 2); At[p][m],
 // B[p][c] in smem; C (ldc) read through L2 when CG, else from smem; out (ldo)
-// may be smem or global.  4 x 4 register blocking, 256 threads.
-template <int MODE, bool CG>
+// may be smem or global.  4 x 4 register blocking, 256 threads (rows ty+16a,
+// columns tx+16b).  SHAPE 1: At is upper triangular, so row m only needs
+// p <= m (the k loop runs in four row-group segments: ~half the FMAs);
+// SHAPE 2: only the upper triangle of the (symmetric) result is formed.
+template <int MODE, bool CG, int SHAPE = 0>
 __device__ __forceinline__ void gemm_tile(const double* At, const double* B, const double* C, int64_t ldc, double* out,
                                           int64_t ldo) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  constexpr bool SYM = SHAPE == 2;
   double acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const double* cp = C + (ty + 16 * a) * ldc + tx + 16 * b;
-      acc[a][b] = MODE == 0 ? 0.0 : (CG ? __ldcg(cp) : *cp);
+      acc[a][b] = (MODE == 0 || (SYM && a > b)) ? 0.0 : (CG ? __ldcg(cp) : *cp);
     }
   const double sg = MODE == 1 ? -1.0 : 1.0;
+  if constexpr (SHAPE == 1) {
+    for (int p = 0; p <= ty; ++p) gemm_step<0, false>(acc, At, B, p, ty, tx, sg);
+    for (int p = ty + 1; p <= ty + 16; ++p) gemm_step<1, false>(acc, At, B, p, ty, tx, sg);
+    for (int p = ty + 17; p <= ty + 32; ++p) gemm_step<2, false>(acc, At, B, p, ty, tx, sg);
+    for (int p = ty + 33; p <= ty + 48; ++p) gemm_step<3, false>(acc, At, B, p, ty, tx, sg);
+  } else {
 #pragma unroll 4
-  for (int p = 0; p < FT; ++p) {
-    double av[4], bv[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) av[a] = sg * At[p * FLD + ty + 16 * a];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) bv[b] = B[p * FLD + tx + 16 * b];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    for (int p = 0; p < FT; ++p) gemm_step<0, SYM>(acc, At, B, p, ty, tx, sg);
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) out[(ty + 16 * a) * ldo + tx + 16 * b] = acc[a][b];
+    for (int b = 0; b < 4; ++b)
+      if (!SYM || a <= b) out[(ty + 16 * a) * ldo + tx + 16 * b] = acc[a][b];
 }
 
 // fixed-order sum of squares of the valid (rows < nr, cols < nc) entries of a
@@ -380,11 +400,14 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       load_tile(x, atile(a, j, j + 1), dp);
       load_tile(y, atile(a, j + 1, j + 1), dp);
       __syncthreads();
-      gemm_tile<0, false>(T, x, nullptr, 0, z, FLD);  // U_j,j+1 = T_j^T A_j,j+1
+      kf_stamp(a, 600 + 4 * j);
+      gemm_tile<0, false, 1>(T, x, nullptr, 0, z, FLD);  // U_j,j+1 = T_j^T A_j,j+1 (T_j upper)
       __syncthreads();
+      kf_stamp(a, 601 + 4 * j);
       store_tile(atile(a, j, j + 1), dp, z);
       signal(a.verA + j * nb + j + 1, j + 1);
-      gemm_tile<1, false>(z, z, y, FLD, x, FLD);  // A_j+1,j+1 - U^T U
+      kf_stamp(a, 602 + 4 * j);
+      gemm_tile<1, false, 2>(z, z, y, FLD, x, FLD);  // A_j+1,j+1 - U^T U (upper triangle)
       __syncthreads();
       kf_stamp(a, 3 + 3 * j);
       chol_inv_tile(x, y, scratch, a.ctl + 2);  // x = U_j+1,j+1, y = T_j+1
@@ -428,7 +451,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       load_tile(b0, ttile(a, j), FT);
       load_tile(b1, atile(a, j, k), dp);
       __syncthreads();
-      gemm_tile<0, false>(b0, b1, nullptr, 0, atile(a, j, k), dp);
+      gemm_tile<0, false, 1>(b0, b1, nullptr, 0, atile(a, j, k), dp);
       signal(a.verA + j * nb + k, j + 1);
     } else if (tk.x == T_YROW) {  // Y_jm = T_j^T W_jm
       const int m = tk.z;
@@ -438,7 +461,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       load_tile(b0, ttile(a, j), FT);
       load_tile(b1, wtile(a, j, m), dp);
       __syncthreads();
-      gemm_tile<0, false>(b0, b1, nullptr, 0, b2, FLD);
+      gemm_tile<0, false, 1>(b0, b1, nullptr, 0, b2, FLD);
       __syncthreads();
       store_tile(wtile(a, j, m), dp, b2);
       const double ss = tile_sumsq<false>(b2, static_cast<int>(a.d - static_cast<int64_t>(j) * FT),
@@ -459,7 +482,10 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       load_tile(b0, atile(a, j, k), dp);
       if (l != k) load_tile(b1, atile(a, j, l), dp);
       __syncthreads();
-      gemm_tile<1, true>(b0, l != k ? b1 : b0, atile(a, k, l), dp, atile(a, k, l), dp);
+      if (l != k)
+        gemm_tile<1, true>(b0, b1, atile(a, k, l), dp, atile(a, k, l), dp);
+      else  // diagonal tile: only its upper triangle is ever read
+        gemm_tile<1, true, 2>(b0, b0, atile(a, k, l), dp, atile(a, k, l), dp);
       signal(a.verA + k * nb + l, j + 1);
     } else if (tk.x == T_WUPD) {  // W_km -= U_jk^T Y_jm
       const int k = tk.z, m = tk.w;
@@ -642,6 +668,12 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
               (h[4 + 3 * j] - h[3 + 3 * j]) / 1000.0);
       prev = h[4 + 3 * j];
     }
+    fprintf(stderr, "\n  load/gemm1/store+signal/gemm2 (us):");
+    cudaMemcpy(h + 600, trace + 600, 4 * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    for (int j = 0; j + 1 < nst && j < 8; ++j)
+      fprintf(stderr, " %.1f/%.1f/%.1f/%.1f", (h[600 + 4 * j] - h[2 + 3 * j]) / 1000.0,
+              (h[601 + 4 * j] - h[600 + 4 * j]) / 1000.0, (h[602 + 4 * j] - h[601 + 4 * j]) / 1000.0,
+              (h[3 + 3 * j] - h[602 + 4 * j]) / 1000.0);
     fprintf(stderr, "\n");
   }
   return LVSK_OK;

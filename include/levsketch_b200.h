@@ -78,7 +78,8 @@ LVSK_API int32_t lvsk_abi_version(void);
  * (reference sketch.py:260-266, 173-191, 166-170) as driven by consume_rows
  * (sketch.py:289-312).  Rows X[0..n) carry GLOBAL indices row0..row0+n-1.
  * The compensated state (hi, lo), k x d float64 row-major, is read from
- * (hi_in, lo_in) and written to (hi_out, lo_out) (may alias).  Contributions to
+ * (hi_in, lo_in) and written to (hi_out, lo_out) (may alias; hi_in = lo_in = NULL
+ * starts from the zero state without reading it).  Contributions to
  * one bucket are applied in ascending row index, each as a TwoSum, which is
  * the reference's exact operation sequence: the result is bit-identical.
  * blocks: HOST array of s blocks.  scale = 1/sqrt(s) (float64). */

@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
   const int64_t so = b * d + col0;
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    h[v] = (active && col0 + v < d) ? hi_in[so + v] : 0.0;
-    l[v] = (active && col0 + v < d) ? lo_in[so + v] : 0.0;
+    h[v] = (hi_in != nullptr && active && col0 + v < d) ? hi_in[so + v] : 0.0;  // NULL state: zeros
+    l[v] = (lo_in != nullptr && active && col0 + v < d) ? lo_in[so + v] : 0.0;
   }
   const uint32_t p0 = start[b], p1 = start[b + 1];
   bool bad = false;
@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1), 8) hashed_gath
   const int64_t so = b * d + c0 + col;
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    h[v] = v < nv ? hi_in[so + v] : 0.0;
-    l[v] = v < nv ? lo_in[so + v] : 0.0;
+    h[v] = (hi_in != nullptr && v < nv) ? hi_in[so + v] : 0.0;  // NULL state: zeros
+    l[v] = (lo_in != nullptr && v < nv) ? lo_in[so + v] : 0.0;
   }
   bool bad = false;
   auto apply_row = [&](const uint8_t* seg, bool neg) {
@@ -700,6 +700,12 @@ extern "C" int32_t lvsk_hashed_sketch(const void* X, int32_t dtype, int64_t n, i
                "unknown dtype %d", dtype);
   cudaStream_t st = as_stream(stream);
   if (n == 0) {
+    if (hi_in == nullptr || lo_in == nullptr) {
+      cudaError_t e = cudaMemsetAsync(hi_out, 0, static_cast<size_t>(k * d) * sizeof(double), st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(lo_out, 0, static_cast<size_t>(k * d) * sizeof(double), st);
+      if (e != cudaSuccess) return cuda_status(e, "hashed zero state");
+      return LVSK_OK;
+    }
     if (hi_in != hi_out) copy_f64_kernel<<<grid_for(k * d, 256), 256, 0, st>>>(hi_in, hi_out, k * d);
     if (lo_in != lo_out) copy_f64_kernel<<<grid_for(k * d, 256), 256, 0, st>>>(lo_in, lo_out, k * d);
     LVSK_CHECK_LAUNCH("hashed copy");

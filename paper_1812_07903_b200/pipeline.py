@@ -95,11 +95,9 @@ class LeveragePipeline:
             N.check(L.lvsk_gaussian_sketch(X.data_ptr(), self.code, self.n, self.d, ldx, self.row0, self.spec.seed,
                                            self.k, self.sx.data_ptr(), 0, self.ws_sketch.data_ptr(),
                                            self.ws_sketch.numel(), self.flags.data_ptr(), st), "gaussian")
-        else:
-            s._hi.zero_()
-            s._lo.zero_()
+        else:  # a fresh state each run: NULL (hi_in, lo_in) = zeros, no memset and no state read
             N.check(L.lvsk_hashed_sketch(X.data_ptr(), self.code, self.n, self.d, ldx, self.row0, s._blocks,
-                                         self.spec.s, s._scale, s._hi.data_ptr(), s._lo.data_ptr(), s._hi.data_ptr(),
+                                         self.spec.s, s._scale, None, None, s._hi.data_ptr(),
                                          s._lo.data_ptr(), self.k, self.ws_sketch.data_ptr(), self.ws_sketch.numel(),
                                          self.flags.data_ptr(), st), "hashed sketch")
             N.check(L.lvsk_fold_compensated(s._hi.data_ptr(), s._lo.data_ptr(), self.sx.data_ptr(), self.sx.numel(), st),

@@ -497,7 +497,14 @@ __global__ void __launch_bounds__(AS_THREADS, 1) argsort_coop_kernel(AsArgs a) {
   const uint64_t* ks = as_passes(a, 4, 7, diff, nbar, as_smem, c0, c1);
   if (diff & 0xFFFFFFFFull) {
     as_stamp(a, 40);
+    unsigned long long fx0 = 0;
+    if (a.trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fx0));
     as_fixup(a, ks, as_smem, c0, c1);
+    if (a.trace != nullptr && threadIdx.x == 0) {
+      unsigned long long fx1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fx1));
+      atomicMax(a.trace + 50, fx1 - fx0);
+    }
     as_stamp(a, 41);
     as_barrier(a.bar, nbar);
     as_stamp(a, 42);
@@ -614,8 +621,8 @@ extern "C" int32_t lvsk_argsort_f64(const double* keys, int64_t n, int32_t desce
     a.flag = reinterpret_cast<unsigned int*>(ctl + 3);
     static unsigned long long* trace = nullptr;
     const bool tracing = getenv("LVSK_SORT_TRACE") != nullptr;
-    if (tracing && trace == nullptr) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
-    if (tracing) cudaMemsetAsync(trace, 0, 64 * sizeof(unsigned long long), st);
+    if (tracing && trace == nullptr) cudaMalloc(&trace, 512 * sizeof(unsigned long long));
+    if (tracing) cudaMemsetAsync(trace, 0, 512 * sizeof(unsigned long long), st);
     a.trace = tracing ? trace : nullptr;
     void* args[] = {(void*)&a};
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(argsort_coop_kernel), dim3(G), dim3(AS_THREADS), args,
@@ -630,7 +637,8 @@ extern "C" int32_t lvsk_argsort_f64(const double* keys, int64_t n, int32_t desce
         if (h[4 * p + 2])
           fprintf(stderr, " p%d hist-bar %.1f offs %.1f scatter %.1f |", p, (h[4 * p + 3] - h[4 * p + 2]) / 1e3,
                   (h[4 * p + 4] - h[4 * p + 3]) / 1e3, (h[4 * p + 5] - h[4 * p + 4]) / 1e3);
-      if (h[40]) fprintf(stderr, " fixup %.1f bar %.1f", (h[41] - h[40]) / 1e3, (h[42] - h[41]) / 1e3);
+      if (h[40]) fprintf(stderr, " fixup %.1f (max over CTAs %.1f) bar %.1f", (h[41] - h[40]) / 1e3, h[50] / 1e3,
+                         (h[42] - h[41]) / 1e3);
       fprintf(stderr, " total(from p0 end) %.1f\n", (h[42] ? h[42] : h[1]) > h[0] ? ((h[42] ? h[42] : h[1]) - h[0]) / 1e3 : 0.0);
     }
     return LVSK_OK;

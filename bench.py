@@ -436,7 +436,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         "kernel": {"sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
                               "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
                               "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
-                              "srht": "srht_pass1/pass2 kernels (K3)",
+                              "srht": "srht_sampled_kernel (K3 v3: one pass, block WHT + sampled combine)",
                               "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
                               if not csr and X.dtype == torch.bfloat16 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],
                    "leverage": "csr_rowsumsq_kernel (K6)" if csr else "leverage_v2_kernel (K5, tcgen05)"}[dominant],

@@ -1,0 +1,408 @@
+// K3 v3 (fp32 X) — SRHT in ONE pass over X: block WHT in shared memory +
+// sampled combine in registers.  Reference: SketchState.data SRHT branch and
+// fwht (pkg/src/levsketch/sketch.py:248-257, 364-385): SX = fwht(D X)[sample]
+// / divisor, signs/sample drawn on the host exactly as sketch.py:220-224.
+//
+// Why a different factorisation.  H_m = H_hi (x) H_lo with the low B = 11
+// row bits inside a block:  for sampled row p = (p_hi, p_lo)
+//     SX[p] = sum_j (-1)^popc(p_hi & j) * W_j[p_lo],   W_j = H_2048 (D X)_block j
+// The two-pass kernels (srht.cu) transform the low 16 bits completely and
+// round-trip a 64 MB intermediate through L2/DRAM (3 x 2 GB of traffic at C3).
+// Here the high bits are only ever evaluated at the k sampled rows, so the
+// intermediate never leaves the SM: a persistent CTA owns one 8-column slab
+// (32 B of every row) and keeps the k x 8 sampled outputs of that slab in
+// fp32 registers (k <= 4096: 16 samples x 8 columns per thread), streams the
+// 2048-row blocks of its slab with TMA (double-buffered), applies the row
+// signs (bit-packed, XOR of the float sign bit), runs the 11-level WHT as two
+// register passes through shared memory (row bits 2-7, then 0,1,8,9,10, with
+// an XOR-swizzled layout that keeps both passes bank-conflict free), and adds
+// (-1)^popc(p_hi & j) * W_j[p_lo] into its accumulators.  Every 64 blocks the
+// fp32 accumulators are stored (store-only) as one partial run, and a final
+// kernel sums the runs in a fixed order in fp64 and divides: the result is
+// deterministic, error ~2e-7 relative (fp32 within a run, fp64 across runs).
+//
+// X is read exactly once.  Eight consecutive CTAs own the eight slabs of one
+// 256-byte column segment and walk the same block sequence, so a 256 B L2
+// line fetched for one of them is consumed by the other seven while it is
+// still resident.  Algorithmic bytes: n*d*4 (+ k*d*8 written).
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace lvsk {
+namespace srht3 {
+
+constexpr int B = 11;                    // in-block row bits
+constexpr int ROWS = 1 << B;             // 2048 rows per block
+constexpr int W = 8;                     // fp32 columns per slab (32 B)
+constexpr int OCT = 8;                   // slabs per 256 B column segment (CTAs per group)
+constexpr int THREADS = 256;
+constexpr int SPT = 16;                  // samples per thread
+constexpr int KMAX = SPT * THREADS;      // 4096
+constexpr int TILE_BYTES = ROWS * W * 4;  // 64 KB
+constexpr int SIGN_BYTES = ROWS / 8;      // 256 B of sign bits per block
+constexpr int STAGE_BYTES = TILE_BYTES + SIGN_BYTES;
+constexpr int BOX_ROWS = 256;
+constexpr int FLUSH = 64;                // blocks per fp32 accumulation run
+constexpr int SMEM_BYTES = 2 * STAGE_BYTES + KMAX * 8 + 64 + 128;
+
+// XOR swizzle of rows inside each 4-row group: bits 0,1 ^= bits 2,3
+__device__ __forceinline__ int swz(int r) { return r ^ ((r >> 2) & 3); }
+
+template <int N>
+__device__ __forceinline__ void wht(float (&v)[N]) {
+#pragma unroll
+  for (int h = 1; h < N; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if ((i & h) == 0) {
+        const float a = v[i], b = v[i + h];
+        v[i] = a + b;
+        v[i + h] = a - b;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+struct Params {
+  const uint32_t* signbits;  // m/32 words, bit set = negative sign (nullptr: no flip)
+  const uint2* slots;        // KMAX slots {(p & 2047) | (p >> 11) << 11, sample index t or ~0u}
+  float* partial;            // [ctas][rmax][k][8] fp32 runs
+  int64_t rmax;              // runs per CTA (capacity)
+  int64_t k;
+  int64_t jblocks;           // active 2048-row blocks (ceil(n / 2048))
+  int64_t octets;            // ceil(slabs / 8)
+  int64_t groups;            // CTA groups of 8
+};
+
+__device__ __forceinline__ void group_range(const Params& P, int64_t g, int64_t& lo, int64_t& hi) {
+  const int64_t T = P.octets * P.jblocks;
+  lo = g * T / P.groups;
+  hi = (g + 1) * T / P.groups;
+}
+
+__global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_constant__ CUtensorMap mx, Params P) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint2* meta_s = reinterpret_cast<uint2*>(smem + 2 * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGE_BYTES + KMAX * 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t g = blockIdx.x / OCT;
+  const int o = blockIdx.x % OCT;
+  int64_t lo, hi;
+  group_range(P, g, lo, hi);
+  if (lo >= hi) return;
+
+  const int k = static_cast<int>(P.k);
+  for (int t = tid; t < KMAX; t += THREADS) meta_s[t] = P.slots[t];
+  if (tid == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint64_t pol = tc::l2_policy_evict_first();
+  auto issue = [&](int64_t task, int s) {
+    const int64_t oct = task / P.jblocks, j = task % P.jblocks;
+    const int col = static_cast<int>((oct * OCT + o) * W);
+    const int row0 = static_cast<int>(j * ROWS);
+    tc::mbar_expect_tx(&full[s], P.signbits ? STAGE_BYTES : TILE_BYTES);
+#pragma unroll
+    for (int b = 0; b < ROWS / BOX_ROWS; ++b)
+      tc::tma_load_2d(&mx, &full[s], smem + s * STAGE_BYTES + b * BOX_ROWS * W * 4, col, row0 + b * BOX_ROWS, pol);
+    if (P.signbits) bulk_g2s(smem + s * STAGE_BYTES + TILE_BYTES, P.signbits + j * (ROWS / 32), SIGN_BYTES, &full[s]);
+  };
+  if (tid == 0) {
+    issue(lo, 0);
+    if (lo + 1 < hi) issue(lo + 1, 1);
+  }
+
+  float acc[SPT][W];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u)
+#pragma unroll
+    for (int c = 0; c < W; ++c) acc[u][c] = 0.f;
+
+  int run = 0;           // fp32 partial runs written so far
+  int runs = 0;          // blocks accumulated in the current run
+  int64_t cur_oct = lo / P.jblocks;
+
+  // store-only: each run of <= FLUSH blocks of one column segment becomes
+  // one fp32 partial; the reduce kernel adds the runs in order in fp64
+  auto flush = [&]() {
+    float* base = P.partial + ((static_cast<int64_t>(blockIdx.x) * P.rmax + run) * P.k) * W;
+    const int rot = (lane & 1) * 4;  // see the gather: odd lanes hold columns 4-7 first
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      const uint32_t t = meta_s[tid + THREADS * u].y;
+      if (t != ~0u) {
+        float* p = base + static_cast<int64_t>(t) * W;
+        *reinterpret_cast<float4*>(p + rot) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+        *reinterpret_cast<float4*>(p + (rot ^ 4)) = make_float4(acc[u][4], acc[u][5], acc[u][6], acc[u][7]);
+      }
+#pragma unroll
+      for (int c = 0; c < W; ++c) acc[u][c] = 0.f;
+    }
+    ++run;
+    runs = 0;
+  };
+
+  const int64_t jb = P.jblocks;
+  int64_t oct = cur_oct;
+  uint32_t j = static_cast<uint32_t>(lo - oct * jb);
+  for (int64_t task = lo; task < hi; ++task, ++j) {
+    const int it = static_cast<int>(task - lo);
+    const int s = it & 1;
+    if (j == jb) {
+      j = 0;
+      ++oct;
+    }
+    if (oct != cur_oct) {  // crossed into the next column segment
+      if (runs > 0) flush();
+      cur_oct = oct;
+    }
+    tc::mbar_wait(&full[s], static_cast<uint32_t>((it >> 1) & 1));
+    float* T = reinterpret_cast<float*>(smem + s * STAGE_BYTES);
+    const uint32_t* sb = reinterpret_cast<const uint32_t*>(smem + s * STAGE_BYTES + TILE_BYTES);
+
+    // ---- pass A: row bits 2..7 (lanes: column, bits 0-1; warps: bits 8-10)
+    {
+      const int c = lane & 7, b01 = lane >> 3;
+      const int rbase = b01 + 256 * warp;
+      float v[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = T[(rbase + 4 * i) * W + c];
+      if (P.signbits) {
+        uint32_t wv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) wv[q] = sb[8 * warp + q] >> b01;
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          v[i] = __uint_as_float(__float_as_uint(v[i]) ^ ((wv[i >> 3] << (31 - 4 * (i & 7))) & 0x80000000u));
+      }
+      wht<64>(v);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 64; ++i) T[(256 * warp + 4 * i + (b01 ^ (i & 3))) * W + c] = v[i];
+    }
+    __syncthreads();
+    // ---- pass B: row bits 0,1,8,9,10 (lanes: column, bits 2-3; warps: bits 4-6; rounds: bit 7)
+    {
+      const int c = lane & 7, b23 = lane >> 3;
+#pragma unroll
+      for (int rnd = 0; rnd < 2; ++rnd) {
+        const int rb = 4 * b23 + 16 * warp + 128 * rnd;
+        float v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = T[(rb + 256 * (u >> 2) + ((u & 3) ^ b23)) * W + c];
+        wht<32>(v);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) T[(rb + 256 * (u >> 2) + ((u & 3) ^ b23)) * W + c] = v[u];
+      }
+    }
+    __syncthreads();
+    // ---- sampled combine: acc[t] += (-1)^popc(p_hi & j) * W_j[p_lo]
+    {
+      const int h0 = lane & 1;
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        const uint32_t mt = meta_s[tid + THREADS * u].x;
+        const int q = static_cast<int>(mt & (ROWS - 1));
+        const uint32_t sbit = static_cast<uint32_t>(__popc((mt >> B) & j) & 1) << 31;
+        const float* row = T + swz(q) * W;
+        const float4 a = *reinterpret_cast<const float4*>(row + 4 * h0);
+        const float4 b = *reinterpret_cast<const float4*>(row + 4 * (h0 ^ 1));
+        // lanes with h0 = 1 keep columns 4-7 in acc[u][0..3] (undone in flush)
+        const float sg = __uint_as_float(0x3f800000u | sbit);
+        acc[u][0] = fmaf(a.x, sg, acc[u][0]);
+        acc[u][1] = fmaf(a.y, sg, acc[u][1]);
+        acc[u][2] = fmaf(a.z, sg, acc[u][2]);
+        acc[u][3] = fmaf(a.w, sg, acc[u][3]);
+        acc[u][4] = fmaf(b.x, sg, acc[u][4]);
+        acc[u][5] = fmaf(b.y, sg, acc[u][5]);
+        acc[u][6] = fmaf(b.z, sg, acc[u][6]);
+        acc[u][7] = fmaf(b.w, sg, acc[u][7]);
+      }
+    }
+    __syncthreads();  // stage s is free
+    if (tid == 0 && task + 2 < hi) issue(task + 2, s);
+    if (++runs == FLUSH) flush();
+  }
+  if (runs > 0) flush();
+}
+
+// SX[t][col] = sum over the CTAs covering col's segment (fixed order) / divisor
+__global__ void srht_sampled_reduce_kernel(Params P, int64_t d, double divisor, double* __restrict__ SX,
+                                           int32_t* flags) {
+  const int64_t total = P.k * d;
+  bool bad = false;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = e / d, col = e % d;
+    const int64_t slab = col / W, oct = slab / OCT, o = slab % OCT;
+    double s = 0.0;
+    for (int64_t g = 0; g < P.groups; ++g) {
+      int64_t lo, hi;
+      group_range(P, g, lo, hi);
+      if (lo >= hi) continue;
+      const int64_t first = lo / P.jblocks, last = (hi - 1) / P.jblocks;
+      if (oct < first || oct > last) continue;
+      const int64_t cta = g * OCT + o;
+      // runs: segment 0 = [lo, b) then segment 1 = [b, hi), b = (first + 1) * jblocks
+      const int64_t b = (first + 1) * P.jblocks;
+      const int64_t n0 = ((hi < b ? hi : b) - lo + FLUSH - 1) / FLUSH;
+      const int64_t r0 = oct == first ? 0 : n0;
+      const int64_t r1 = oct == first ? n0 : n0 + (hi - b + FLUSH - 1) / FLUSH;
+      for (int64_t r = r0; r < r1; ++r) s += P.partial[((cta * P.rmax + r) * P.k + t) * W + (col % W)];
+    }
+    s /= divisor;
+    bad |= !isfinite(s);
+    SX[e] = s;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
+}
+
+__global__ void srht_pack_kernel(const int8_t* __restrict__ signs, int64_t words, uint32_t* __restrict__ bits) {
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < words;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t b = 0;
+    const int8_t* s = signs + w * 32;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) b |= static_cast<uint32_t>(s[i] < 0) << i;
+    bits[w] = b;
+  }
+}
+
+// Sample -> accumulator slot.  Slot s lives in thread s % 256, register set
+// s / 256; in the gather, lane l reads its row halves in the order
+// (l & 1, l & 1 ^ 1), so a quarter-warp is conflict-free when lane l's row
+// sits in 4-row position (l >> 1) & 3 (bank group 2 * pos + half).  Samples
+// go to slots of their own class while those last, the rest to free slots.
+// (Which slot a sample lands in does not change its arithmetic, so atomics
+// here keep the result deterministic.)
+__global__ void __launch_bounds__(1024) srht_slots_kernel(const int64_t* __restrict__ sample, int64_t k, int64_t m,
+                                                          uint2* __restrict__ slots, int32_t* flags) {
+  constexpr int PER = KMAX / 4;
+  __shared__ int cnt[4], ovf;
+  __shared__ uint32_t over[2 * KMAX];
+  if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) ovf = 0;
+  for (int s = threadIdx.x; s < KMAX; s += blockDim.x) slots[s] = make_uint2(0u, ~0u);
+  __syncthreads();
+  auto slot_of = [](int c, int pos) { return (pos & 1) | (c << 1) | ((pos >> 1) << 3); };
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    const int64_t p = sample[t];
+    if (p < 0 || p >= m) atomicOr(flags, LVSK_FLAG_BADINDEX);
+    const uint64_t pu = static_cast<uint64_t>(p) & (static_cast<uint64_t>(m) - 1);
+    const uint32_t q = static_cast<uint32_t>(pu & (ROWS - 1));
+    const uint2 e = make_uint2(q | static_cast<uint32_t>(pu >> B) << B, static_cast<uint32_t>(t));
+    const int c = static_cast<int>((q ^ (q >> 2)) & 3);
+    const int pos = atomicAdd(&cnt[c], 1);
+    if (pos < PER) {
+      slots[slot_of(c, pos)] = e;
+    } else {
+      const int i = atomicAdd(&ovf, 1);
+      over[2 * i] = e.x;
+      over[2 * i + 1] = e.y;
+    }
+  }
+  __syncthreads();
+  // the i-th overflow sample takes the i-th free slot (classes in order)
+  for (int i = threadIdx.x; i < ovf; i += blockDim.x) {
+    int rem = i;
+    for (int c = 0; c < 4; ++c) {
+      const int fr = cnt[c] < PER ? PER - cnt[c] : 0;
+      if (rem < fr) {
+        slots[slot_of(c, cnt[c] + rem)] = make_uint2(over[2 * i], over[2 * i + 1]);
+        break;
+      }
+      rem -= fr;
+    }
+  }
+}
+
+struct Shape {
+  int64_t jblocks, octets, groups, ctas, rmax;
+};
+
+static Shape shape(int64_t n, int64_t d) {
+  Shape s;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  s.jblocks = (n + ROWS - 1) / ROWS;
+  const int64_t slabs = (d + W - 1) / W;
+  s.octets = (slabs + OCT - 1) / OCT;
+  // a group's range spans at most two column segments: groups >= octets
+  s.groups = sms / OCT > s.octets ? sms / OCT : s.octets;
+  const int64_t T = s.octets * s.jblocks;
+  if (s.groups > T) s.groups = T;
+  s.ctas = s.groups * OCT;
+  s.rmax = ((T + s.groups - 1) / s.groups + FLUSH - 1) / FLUSH + 1;
+  return s;
+}
+
+}  // namespace srht3
+
+// Usable for fp32 X with 16-byte aligned rows, m >= 2^11, k <= 4096.
+bool srht_sampled_ok(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, int64_t k) {
+  if (getenv("LVSK_SRHT_V2") != nullptr) return false;
+  return m >= srht3::ROWS && k <= srht3::KMAX && m <= (int64_t{1} << 32) && n < (int64_t{1} << 31) &&
+         d % 4 == 0 && ldx % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0;
+}
+
+size_t srht_sampled_workspace(int64_t n, int64_t d, int64_t m, int64_t k) {
+  const srht3::Shape s = srht3::shape(n, d);
+  Measure ms;
+  ms.take<uint32_t>(static_cast<size_t>(m / 32));
+  ms.take<uint2>(srht3::KMAX);
+  ms.take<float>(static_cast<size_t>(s.ctas) * s.rmax * k * srht3::W);
+  return ms.off;
+}
+
+int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, const int8_t* signs,
+                     const int64_t* sample, int64_t k, double divisor, double* SX, void* ws, size_t ws_bytes,
+                     int32_t* flags, cudaStream_t st) {
+  using namespace srht3;
+  const Shape S = shape(n, d);
+  Carve cv(ws, ws_bytes);
+  uint32_t* bits = cv.take<uint32_t>(static_cast<size_t>(m / 32));
+  uint2* slots = cv.take<uint2>(KMAX);
+  float* partial = cv.take<float>(static_cast<size_t>(S.ctas) * S.rmax * k * W);
+  LVSK_REQUIRE(cv.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", cv.off, ws_bytes);
+  CUtensorMap mx;
+  if (!tc::make_map(&mx, X, d, n, ldx * 4, W, BOX_ROWS, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                    CU_TENSOR_MAP_SWIZZLE_NONE)) {
+    set_error("cuTensorMapEncodeTiled failed (SRHT X)");
+    return LVSK_ERR_CUDA;
+  }
+  const int64_t words = signs ? S.jblocks * (ROWS / 32) : 0;
+  if (words) srht_pack_kernel<<<296, 256, 0, st>>>(signs, words, bits);
+  srht_slots_kernel<<<1, 1024, 0, st>>>(sample, k, m, slots, flags);
+  LVSK_CHECK_LAUNCH("srht pack");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(srht_sampled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  Params P{signs ? bits : nullptr, slots, partial, S.rmax, k, S.jblocks, S.octets, S.groups};
+  srht_sampled_kernel<<<static_cast<unsigned>(S.ctas), THREADS, SMEM_BYTES, st>>>(mx, P);
+  LVSK_CHECK_LAUNCH("srht sampled");
+  srht_sampled_reduce_kernel<<<592, 256, 0, st>>>(P, d, divisor, SX, flags);
+  LVSK_CHECK_LAUNCH("srht sampled reduce");
+  return LVSK_OK;
+}
+
+}  // namespace lvsk

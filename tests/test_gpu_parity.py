@@ -182,11 +182,13 @@ def test_srht_matches_reference(golden, golden_meta):
         assert np.linalg.norm(got - ref32) <= 1e-5 * np.linalg.norm(ref32)
 
 
-@pytest.mark.parametrize("n,d", [(2**16, 8), (3 * 2**15 + 17, 33), (2**17, 256), (2**20 + 3, 4)])
-def test_srht_multi_chunk(n, d):
+@pytest.mark.parametrize("n,d,k", [(2**16, 8, 512), (3 * 2**15 + 17, 33, 512), (2**17, 256, 512),
+                                   (2**20 + 3, 4, 512), (2**14 + 17, 100, 4096), (5000, 68, 4097)])
+def test_srht_multi_chunk(n, d, k):
+    """fp32 X: the one-pass sampled kernel (srht_sampled.cu; d % 4 == 0,
+    k <= 4096) and the two-pass kernels (srht.cu) against explicit rows of H."""
     rng = np.random.default_rng(n)
     x = rng.standard_normal((n, d)).astype(np.float32)
-    k = 512
     spec = P.SketchSpec("srht", eps=0.5, d=d, seed=7, rows_override=k)
     got = P.srht_apply(spec, dev(x)).data
     S_rows = O.srht_signs_sample(7, O.next_pow2(n), k)
@@ -204,6 +206,19 @@ def test_srht_multi_chunk(n, d):
         ref[t0 : t0 + 64] = (1.0 - 2.0 * par.astype(np.float64)) @ xs
     ref /= math.sqrt(k)
     assert np.linalg.norm(got - ref) <= 2e-6 * np.linalg.norm(ref)
+    # deterministic: a second call is bit-identical
+    assert np.array_equal(P.srht_apply(spec, dev(x)).data, got)
+
+
+def test_srht_sampled_vs_two_pass(monkeypatch):
+    """The one-pass kernel and the two-pass kernels agree on C3-shaped input."""
+    n, d, k = 2**18, 64, 4096
+    x = np.random.default_rng(3).standard_normal((n, d)).astype(np.float32)
+    spec = P.SketchSpec("srht", eps=0.5, d=d, seed=5, rows_override=k)
+    a = P.srht_apply(spec, dev(x)).data
+    monkeypatch.setenv("LVSK_SRHT_V2", "1")
+    b = P.srht_apply(spec, dev(x)).data
+    assert np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(b)
 
 
 def test_fwht_kats(golden):

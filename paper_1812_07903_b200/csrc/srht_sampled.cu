@@ -16,7 +16,7 @@
 // signs (bit-packed, XOR of the float sign bit), runs the 11-level WHT as two
 // register passes through shared memory (row bits 2-7, then 0,1,8,9,10, with
 // an XOR-swizzled layout that keeps both passes bank-conflict free), and adds
-// (-1)^popc(p_hi & j) * W_j[p_lo] into its accumulators.  Every 64 blocks the
+// (-1)^popc(p_hi & j) * W_j[p_lo] into its accumulators.  Every 128 blocks the
 // fp32 accumulators are stored (store-only) as one partial run, and a final
 // kernel sums the runs in a fixed order in fp64 and divides: the result is
 // deterministic, error ~2e-7 relative (fp32 within a run, fp64 across runs).
@@ -46,7 +46,7 @@ constexpr int TILE_BYTES = ROWS * W * 4;  // 64 KB
 constexpr int SIGN_BYTES = ROWS / 8;      // 256 B of sign bits per block
 constexpr int STAGE_BYTES = TILE_BYTES + SIGN_BYTES;
 constexpr int BOX_ROWS = 256;
-constexpr int FLUSH = 64;                // blocks per fp32 accumulation run
+constexpr int FLUSH = 128;               // blocks per fp32 accumulation run
 constexpr int SMEM_BYTES = 2 * STAGE_BYTES + KMAX * 8 + 64 + 128;
 
 // XOR swizzle of rows inside each 4-row group: bits 0,1 ^= bits 2,3
@@ -65,6 +65,51 @@ __device__ __forceinline__ void wht(float (&v)[N]) {
       }
     }
   }
+}
+
+// packed fp32 pairs (sm_100 FADD2 / FFMA2)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rr;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rr, ra, rb;\n\tmov.b64 {%0,%1}, rr;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rr;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "sub.rn.f32x2 rr, ra, rb;\n\tmov.b64 {%0,%1}, rr;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc, rr;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mov.b64 rc, {%6,%7};\n\tfma.rn.f32x2 rr, ra, rb, rc;\n\tmov.b64 {%0,%1}, rr;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
+// WHT of the 2N values x[m] = v[m].x, x[m + N] = v[m].y: the butterflies over
+// the low log2(N) index bits run packed, the top bit inside each pair.
+template <int N>
+__device__ __forceinline__ void wht_packed(float2 (&v)[N]) {
+#pragma unroll
+  for (int h = 1; h < N; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if ((i & h) == 0) {
+        const float2 a = v[i], b = v[i + h];
+        v[i] = add2(a, b);
+        v[i + h] = sub2(a, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = make_float2(v[i].x + v[i].y, v[i].x - v[i].y);
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -94,7 +139,8 @@ __device__ __forceinline__ void group_range(const Params& P, int64_t g, int64_t&
 
 __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_constant__ CUtensorMap mx, Params P) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  uint2* meta_s = reinterpret_cast<uint2*>(smem + 2 * STAGE_BYTES);
+  uint32_t* meta_s = reinterpret_cast<uint32_t*>(smem + 2 * STAGE_BYTES);  // row | p_hi << 11
+  uint32_t* samp_s = meta_s + KMAX;                                          // sample index or ~0u
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGE_BYTES + KMAX * 8);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -105,7 +151,11 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
   if (lo >= hi) return;
 
   const int k = static_cast<int>(P.k);
-  for (int t = tid; t < KMAX; t += THREADS) meta_s[t] = P.slots[t];
+  for (int t = tid; t < KMAX; t += THREADS) {
+    const uint2 e = P.slots[t];
+    meta_s[t] = e.x;
+    samp_s[t] = e.y;
+  }
   if (tid == 0) {
     tc::mbar_init(&full[0], 1);
     tc::mbar_init(&full[1], 1);
@@ -129,11 +179,11 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
     if (lo + 1 < hi) issue(lo + 1, 1);
   }
 
-  float acc[SPT][W];
+  float2 acc[SPT][W / 2];
 #pragma unroll
   for (int u = 0; u < SPT; ++u)
 #pragma unroll
-    for (int c = 0; c < W; ++c) acc[u][c] = 0.f;
+    for (int c = 0; c < W / 2; ++c) acc[u][c] = make_float2(0.f, 0.f);
 
   int run = 0;           // fp32 partial runs written so far
   int runs = 0;          // blocks accumulated in the current run
@@ -146,14 +196,14 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
     const int rot = (lane & 1) * 4;  // see the gather: odd lanes hold columns 4-7 first
 #pragma unroll
     for (int u = 0; u < SPT; ++u) {
-      const uint32_t t = meta_s[tid + THREADS * u].y;
+      const uint32_t t = samp_s[tid + THREADS * u];
       if (t != ~0u) {
         float* p = base + static_cast<int64_t>(t) * W;
-        *reinterpret_cast<float4*>(p + rot) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
-        *reinterpret_cast<float4*>(p + (rot ^ 4)) = make_float4(acc[u][4], acc[u][5], acc[u][6], acc[u][7]);
+        *reinterpret_cast<float4*>(p + rot) = make_float4(acc[u][0].x, acc[u][0].y, acc[u][1].x, acc[u][1].y);
+        *reinterpret_cast<float4*>(p + (rot ^ 4)) = make_float4(acc[u][2].x, acc[u][2].y, acc[u][3].x, acc[u][3].y);
       }
 #pragma unroll
-      for (int c = 0; c < W; ++c) acc[u][c] = 0.f;
+      for (int c = 0; c < W / 2; ++c) acc[u][c] = make_float2(0.f, 0.f);
     }
     ++run;
     runs = 0;
@@ -181,35 +231,54 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
     {
       const int c = lane & 7, b01 = lane >> 3;
       const int rbase = b01 + 256 * warp;
-      float v[64];
+      float2 v[32];  // v[m] = (x[m], x[m + 32]), x[i] = row rbase + 4 i
 #pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = T[(rbase + 4 * i) * W + c];
+      for (int m = 0; m < 32; ++m) v[m] = make_float2(T[(rbase + 4 * m) * W + c], T[(rbase + 4 * (m + 32)) * W + c]);
       if (P.signbits) {
         uint32_t wv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) wv[q] = sb[8 * warp + q] >> b01;
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
-          v[i] = __uint_as_float(__float_as_uint(v[i]) ^ ((wv[i >> 3] << (31 - 4 * (i & 7))) & 0x80000000u));
+        for (int m = 0; m < 32; ++m) {
+          const int i0 = m, i1 = m + 32;
+          v[m].x = __uint_as_float(__float_as_uint(v[m].x) ^ ((wv[i0 >> 3] << (31 - 4 * (i0 & 7))) & 0x80000000u));
+          v[m].y = __uint_as_float(__float_as_uint(v[m].y) ^ ((wv[i1 >> 3] << (31 - 4 * (i1 & 7))) & 0x80000000u));
+        }
       }
-      wht<64>(v);
+      wht_packed<32>(v);
       __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 64; ++i) T[(256 * warp + 4 * i + (b01 ^ (i & 3))) * W + c] = v[i];
+      for (int m = 0; m < 32; ++m) {
+        T[(256 * warp + 4 * m + (b01 ^ (m & 3))) * W + c] = v[m].x;
+        T[(256 * warp + 4 * (m + 32) + (b01 ^ (m & 3))) * W + c] = v[m].y;
+      }
     }
     __syncthreads();
-    // ---- pass B: row bits 0,1,8,9,10 (lanes: column, bits 2-3; warps: bits 4-6; rounds: bit 7)
+    // ---- pass B: row bits 0,1,8,9,10 (lanes: column, bits 2-3; warps: bits 4-6); the two
+    // halves of row bit 7 are independent transforms and ride in the two lanes of each pair
     {
       const int c = lane & 7, b23 = lane >> 3;
+      const int rb = 4 * b23 + 16 * warp;
+      // u = 0..31 over row bits 0,1 (u & 3) and 8,9,10 (u >> 2)
+      auto at = [&](int u) { return (rb + 256 * (u >> 2) + ((u & 3) ^ b23)) * W + c; };
+      float2 v[32];
 #pragma unroll
-      for (int rnd = 0; rnd < 2; ++rnd) {
-        const int rb = 4 * b23 + 16 * warp + 128 * rnd;
-        float v[32];
+      for (int u = 0; u < 32; ++u) v[u] = make_float2(T[at(u)], T[at(u) + 128 * W]);
 #pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = T[(rb + 256 * (u >> 2) + ((u & 3) ^ b23)) * W + c];
-        wht<32>(v);
+      for (int h = 1; h < 32; h <<= 1) {
 #pragma unroll
-        for (int u = 0; u < 32; ++u) T[(rb + 256 * (u >> 2) + ((u & 3) ^ b23)) * W + c] = v[u];
+        for (int i = 0; i < 32; ++i) {
+          if ((i & h) == 0) {
+            const float2 x = v[i], y = v[i + h];
+            v[i] = add2(x, y);
+            v[i + h] = sub2(x, y);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        T[at(u)] = v[u].x;
+        T[at(u) + 128 * W] = v[u].y;
       }
     }
     __syncthreads();
@@ -218,22 +287,19 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
       const int h0 = lane & 1;
 #pragma unroll
       for (int u = 0; u < SPT; ++u) {
-        const uint32_t mt = meta_s[tid + THREADS * u].x;
+        const uint32_t mt = meta_s[tid + THREADS * u];
         const int q = static_cast<int>(mt & (ROWS - 1));
         const uint32_t sbit = static_cast<uint32_t>(__popc((mt >> B) & j) & 1) << 31;
         const float* row = T + swz(q) * W;
         const float4 a = *reinterpret_cast<const float4*>(row + 4 * h0);
         const float4 b = *reinterpret_cast<const float4*>(row + 4 * (h0 ^ 1));
         // lanes with h0 = 1 keep columns 4-7 in acc[u][0..3] (undone in flush)
-        const float sg = __uint_as_float(0x3f800000u | sbit);
-        acc[u][0] = fmaf(a.x, sg, acc[u][0]);
-        acc[u][1] = fmaf(a.y, sg, acc[u][1]);
-        acc[u][2] = fmaf(a.z, sg, acc[u][2]);
-        acc[u][3] = fmaf(a.w, sg, acc[u][3]);
-        acc[u][4] = fmaf(b.x, sg, acc[u][4]);
-        acc[u][5] = fmaf(b.y, sg, acc[u][5]);
-        acc[u][6] = fmaf(b.z, sg, acc[u][6]);
-        acc[u][7] = fmaf(b.w, sg, acc[u][7]);
+        const float sg1 = __uint_as_float(0x3f800000u | sbit);
+        const float2 sg = make_float2(sg1, sg1);
+        acc[u][0] = fma2(make_float2(a.x, a.y), sg, acc[u][0]);
+        acc[u][1] = fma2(make_float2(a.z, a.w), sg, acc[u][1]);
+        acc[u][2] = fma2(make_float2(b.x, b.y), sg, acc[u][2]);
+        acc[u][3] = fma2(make_float2(b.z, b.w), sg, acc[u][3]);
       }
     }
     __syncthreads();  // stage s is free
@@ -243,33 +309,59 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
   if (runs > 0) flush();
 }
 
-// SX[t][col] = sum over the CTAs covering col's segment (fixed order) / divisor
+// SX[t][col] = sum over the runs of the CTAs covering col's segment (fixed
+// order: groups ascending, runs ascending) / divisor.  One thread per
+// (8-column slab, sample), samples fastest (coalesced run reads); the run table of every (segment, group) is built
+// in shared memory first.
 __global__ void srht_sampled_reduce_kernel(Params P, int64_t d, double divisor, double* __restrict__ SX,
                                            int32_t* flags) {
-  const int64_t total = P.k * d;
+  extern __shared__ int2 runs_s[];  // [octets][groups] = (first run, end run), empty if equal
+  const int64_t G = P.groups;
+  for (int64_t e = threadIdx.x; e < P.octets * G; e += blockDim.x) {
+    const int64_t oct = e / G, g = e % G;
+    int64_t lo, hi;
+    group_range(P, g, lo, hi);
+    int2 v = make_int2(0, 0);
+    if (lo < hi) {
+      const int64_t first = lo / P.jblocks, last = (hi - 1) / P.jblocks;
+      if (oct >= first && oct <= last) {
+        const int64_t b = (first + 1) * P.jblocks;
+        const int64_t n0 = ((hi < b ? hi : b) - lo + FLUSH - 1) / FLUSH;
+        v = oct == first ? make_int2(0, static_cast<int>(n0))
+                         : make_int2(static_cast<int>(n0), static_cast<int>(n0 + (hi - b + FLUSH - 1) / FLUSH));
+      }
+    }
+    runs_s[e] = v;
+  }
+  __syncthreads();
+  const int64_t slabs = (d + W - 1) / W;
+  const int64_t total = P.k * slabs;
   bool bad = false;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = e / d, col = e % d;
-    const int64_t slab = col / W, oct = slab / OCT, o = slab % OCT;
-    double s = 0.0;
-    for (int64_t g = 0; g < P.groups; ++g) {
-      int64_t lo, hi;
-      group_range(P, g, lo, hi);
-      if (lo >= hi) continue;
-      const int64_t first = lo / P.jblocks, last = (hi - 1) / P.jblocks;
-      if (oct < first || oct > last) continue;
-      const int64_t cta = g * OCT + o;
-      // runs: segment 0 = [lo, b) then segment 1 = [b, hi), b = (first + 1) * jblocks
-      const int64_t b = (first + 1) * P.jblocks;
-      const int64_t n0 = ((hi < b ? hi : b) - lo + FLUSH - 1) / FLUSH;
-      const int64_t r0 = oct == first ? 0 : n0;
-      const int64_t r1 = oct == first ? n0 : n0 + (hi - b + FLUSH - 1) / FLUSH;
-      for (int64_t r = r0; r < r1; ++r) s += P.partial[((cta * P.rmax + r) * P.k + t) * W + (col % W)];
+    const int64_t slab = e / P.k, t = e % P.k, oct = slab / OCT, o = slab % OCT;
+    double acc[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) acc[c] = 0.0;
+    for (int64_t g = 0; g < G; ++g) {
+      const int2 rr = runs_s[oct * G + g];
+      const float* base = P.partial + ((g * OCT + o) * P.rmax * P.k + t) * W;
+      for (int r = rr.x; r < rr.y; ++r) {
+        const float4 a = *reinterpret_cast<const float4*>(base + static_cast<int64_t>(r) * P.k * W);
+        const float4 b = *reinterpret_cast<const float4*>(base + static_cast<int64_t>(r) * P.k * W + 4);
+        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+      }
     }
-    s /= divisor;
-    bad |= !isfinite(s);
-    SX[e] = s;
+    double* out = SX + t * d + slab * W;
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      if (slab * W + c < d) {
+        const double v = acc[c] / divisor;
+        bad |= !isfinite(v);
+        out[c] = v;
+      }
+    }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
 }
@@ -359,7 +451,7 @@ static Shape shape(int64_t n, int64_t d) {
 // Usable for fp32 X with 16-byte aligned rows, m >= 2^11, k <= 4096.
 bool srht_sampled_ok(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, int64_t k) {
   if (getenv("LVSK_SRHT_V2") != nullptr) return false;
-  return m >= srht3::ROWS && k <= srht3::KMAX && m <= (int64_t{1} << 32) && n < (int64_t{1} << 31) &&
+  return m >= srht3::ROWS && k <= srht3::KMAX && d <= 4096 && m <= (int64_t{1} << 32) && n < (int64_t{1} << 31) &&
          d % 4 == 0 && ldx % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0;
 }
 
@@ -400,7 +492,11 @@ int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t 
   Params P{signs ? bits : nullptr, slots, partial, S.rmax, k, S.jblocks, S.octets, S.groups};
   srht_sampled_kernel<<<static_cast<unsigned>(S.ctas), THREADS, SMEM_BYTES, st>>>(mx, P);
   LVSK_CHECK_LAUNCH("srht sampled");
-  srht_sampled_reduce_kernel<<<592, 256, 0, st>>>(P, d, divisor, SX, flags);
+  const size_t rsm = static_cast<size_t>(S.octets * S.groups) * sizeof(int2);
+  LVSK_REQUIRE(rsm <= 48 * 1024, LVSK_ERR_CONFIGURATION, "SRHT: d=%lld too wide for the run table", (long long)d);
+  const int64_t rthreads = k * ((d + W - 1) / W);
+  srht_sampled_reduce_kernel<<<static_cast<unsigned>((rthreads + 255) / 256), 256, rsm, st>>>(P, d, divisor, SX,
+                                                                                               flags);
   LVSK_CHECK_LAUNCH("srht sampled reduce");
   return LVSK_OK;
 }

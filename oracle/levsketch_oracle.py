@@ -268,47 +268,48 @@ def explicit_srht_matrix(k, seed, n):
 
 # ---------------------------------------------------------------------------
 # Gaussian sketch (extension; parity unpinned by reference tests).
-# S[j, i] = bf16(table-driven Box-Muller of the 16-bit halves of Philox4x32-10
-# word (j >> 1) & 3, counter (i_lo, i_hi, j >> 3, 0), key (seed_lo,
-# seed_hi ^ 'GAUS')) / sqrt(k); every step is an IEEE fp32 op or a table
-# lookup, so CPU and GPU agree bit-for-bit (definition: csrc/philox.cuh).
+# S[j, i] = Z[j, i] / sqrt(k), Z[8q + m, i] = TAB[16-bit field (m & 3) of
+# h_(m >> 2) >> 4], h_w = mix64(key + phi * ((i << 24) | (q << 1) | w)) — the
+# reference's splitmix64 finaliser (sketch.py:141-148) run as a counter-based
+# stream — and TAB a 4096-level equiprobable Gaussian (definition:
+# csrc/philox.cuh), so CPU and GPU agree bit-for-bit.
 
-_PH_M0, _PH_M1 = 0xD2511F53, 0xCD9E8D57
-_PH_W0, _PH_W1 = 0x9E3779B9, 0xBB67AE85
-_U32 = np.uint64(0xFFFFFFFF)
-
-
-def philox4x32(c0, c1, c2, c3, k0, k1, rounds=10):
-    """Random123 Philox4x32 on uint32-valued uint64 arrays (vectorised)."""
-    c0, c1, c2, c3 = (np.asarray(c, dtype=np.uint64) & _U32 for c in (c0, c1, c2, c3))
-    k0 = np.uint64(k0) & _U32
-    k1 = np.uint64(k1) & _U32
-    for r in range(rounds):
-        if r:
-            k0 = (k0 + np.uint64(_PH_W0)) & _U32
-            k1 = (k1 + np.uint64(_PH_W1)) & _U32
-        p0 = np.uint64(_PH_M0) * c0
-        p1 = np.uint64(_PH_M1) * c2
-        hi0, lo0 = p0 >> np.uint64(32), p0 & _U32
-        hi1, lo1 = p1 >> np.uint64(32), p1 & _U32
-        c0, c1, c2, c3 = (hi1 ^ c1 ^ k0) & _U32, lo1, (hi0 ^ c3 ^ k1) & _U32, lo0
-    return c0, c1, c2, c3
+_PHI = np.uint64(0x9E3779B97F4A7C15)
 
 
-_f = np.float32
+def _inv_normal_cdf(p: float) -> float:
+    """Bisection of 0.5 erfc(-x / sqrt 2) = p on [-10, 10], 100 halvings
+    (the same float64 steps as csrc/gaussian.cu)."""
+    lo, hi = -10.0, 10.0
+    for _ in range(100):
+        mid = 0.5 * (lo + hi)
+        if 0.5 * math.erfc(-mid / 1.4142135623730951) < p:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+_GT = None
 
 
 def gaussian_tables() -> np.ndarray:
-    """The generator's float32 table INV[128] | LN[128] | CSA[256][2] | CSB[256][2]
-    (csrc/philox.cuh; same float64 expressions, rounded once)."""
-    i = np.arange(128, dtype=np.float64)
-    two_pi = 2.0 * 3.141592653589793
-    a = np.arange(256, dtype=np.float64)
-    ang_a = two_pi * a / 256.0
-    ang_b = two_pi * (a + 0.5) / 65536.0
-    csa = np.stack([np.cos(ang_a), np.sin(ang_a)], axis=1).reshape(-1)
-    csb = np.stack([np.cos(ang_b), np.sin(ang_b)], axis=1).reshape(-1)
-    return np.concatenate([128.0 / (128.0 + i), np.log1p(i / 128.0), csa, csb]).astype(np.float32)
+    """TAB[4096] (float32, bf16-valued): bf16_rn(float(t_j / sqrt(mean t^2))),
+    t_j = Phi^-1((j + 1/2) / 4096), t_(4095-j) = -t_j."""
+    global _GT
+    if _GT is None:
+        n = 4096
+        t = [0.0] * n
+        for j in range(n // 2):
+            t[j] = _inv_normal_cdf((j + 0.5) / n)
+            t[n - 1 - j] = -t[j]
+        m2 = 0.0
+        for v in t:  # sequential, like the C++ loop
+            m2 += v * v
+        scale = 1.0 / math.sqrt(m2 / n)
+        f = np.array([v * scale for v in t], dtype=np.float64).astype(np.float32)
+        _GT = _bf16_rn(f)
+    return _GT.copy()
 
 
 def _bf16_rn(x):
@@ -317,47 +318,30 @@ def _bf16_rn(x):
     return b.astype(np.uint32).view(np.float32)
 
 
-def _box_muller16(w, tab):
-    """(r cos, r sin) of 32-bit words w, every step one IEEE fp32 op (philox.cuh)."""
-    w = w.astype(np.uint32)
-    v1, v2 = w & np.uint32(0xFFFF), w >> np.uint32(16)
-    u1 = (v1.astype(np.float32) + _f(0.5)) * _f(2.0**-16)
-    bits = u1.view(np.uint32)
-    ex = (bits >> np.uint32(23)).astype(np.int32) - 127
-    idx = ((bits >> np.uint32(16)) & np.uint32(0x7F)).astype(np.int64)
-    f = ((bits & np.uint32(0x007FFFFF)) | np.uint32(0x3F800000)).view(np.float32)
-    f0 = ((bits & np.uint32(0x007F0000)) | np.uint32(0x3F800000)).view(np.float32)
-    y = (f - f0) * tab[idx]
-    t = y - (y * y) * _f(0.5)
-    lnf = tab[128 + idx] + t
-    lnu = ex.astype(np.float32) * _f(0.693147182464599609375) + lnf
-    r = np.sqrt(lnu * _f(-2.0))
-    ia, ib = (v2 >> np.uint32(8)).astype(np.int64), (v2 & np.uint32(0xFF)).astype(np.int64)
-    ac, as_ = tab[256 + 2 * ia], tab[256 + 2 * ia + 1]
-    bc, bs = tab[768 + 2 * ib], tab[768 + 2 * ib + 1]
-    c = ac * bc - as_ * bs
-    s = as_ * bc + ac * bs
-    return r * c, r * s
+def _mix64_arr(x):
+    x = x ^ (x >> np.uint64(30))
+    x = x * np.uint64(0xBF58476D1CE4E5B9)
+    x = x ^ (x >> np.uint64(27))
+    x = x * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
 
 
 def gaussian_z(seed: int, k: int, row0: int, n: int) -> np.ndarray:
     """Unscaled Gaussian sketch entries Z (k x n, float32, bf16-representable)
-    for global rows row0..row0+n-1; S = Z / sqrt(k).  Z[8q + 2h + e, i] comes
-    from word h of Philox4x32-10(counter=(i_lo, i_hi, q, 0), key=(seed_lo,
-    seed_hi ^ 'GAUS')) through the table-driven Box-Muller of csrc/philox.cuh."""
+    for global rows row0..row0+n-1; S = Z / sqrt(k) (csrc/philox.cuh)."""
     tab = gaussian_tables()
     i = np.arange(row0, row0 + n, dtype=np.uint64)
     q = np.arange((k + 7) // 8, dtype=np.uint64)
     I, Q = np.meshgrid(i, q)  # (k/8, n)
-    k0 = seed & 0xFFFFFFFF
-    k1 = ((seed >> 32) & 0xFFFFFFFF) ^ GAUSS_KEY_XOR
-    words = philox4x32(I & _U32, I >> np.uint64(32), Q, np.zeros_like(Q), k0, k1)
+    key = np.uint64(((((seed >> 32) & 0xFFFFFFFF) ^ GAUSS_KEY_XOR) << 32) | (seed & 0xFFFFFFFF))
     out = np.empty((Q.shape[0], 8, n), dtype=np.float32)
-    with np.errstate(over="ignore", invalid="ignore"):
-        for h, w in enumerate(words):
-            z0, z1 = _box_muller16(w, tab)
-            out[:, 2 * h] = _bf16_rn(z0)
-            out[:, 2 * h + 1] = _bf16_rn(z1)
+    with np.errstate(over="ignore"):
+        base = key + _PHI * ((I << np.uint64(24)) | (Q << np.uint64(1)))
+        for w in range(2):
+            h = _mix64_arr(base + _PHI * np.uint64(w))
+            for f in range(4):
+                field = (h >> np.uint64(16 * f)) & np.uint64(0xFFFF)
+                out[:, 4 * w + f] = tab[(field >> np.uint64(4)).astype(np.int64)]
     return out.reshape(-1, n)[:k]
 
 

@@ -15,24 +15,34 @@
 
 namespace lvsk {
 
-// ---- generator tables (philox.cuh) ----------------------------------------
-// Built in float64 then rounded to float32, with the same expressions as the
-// oracle (gaussian_tables); tests pin the two against each other.
+// ---- generator table (philox.cuh) -----------------------------------------
+// Same float64 steps as the oracle (gaussian_tables): bisection of
+// 0.5 erfc(-x / sqrt 2) = p on [-10, 10] (100 halvings reach adjacent
+// doubles), sequential sum of squares, one rounding to float then to bf16.
+static double inv_normal_cdf(double p) {
+  double lo = -10.0, hi = 10.0;
+  for (int it = 0; it < 100; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (0.5 * std::erfc(-mid / 1.4142135623730951) < p)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
 void gaussian_table_host(float* out) {
-  const double two_pi = 2.0 * 3.141592653589793;
-  for (int i = 0; i < 128; ++i) {
-    out[GT_INV + i] = static_cast<float>(128.0 / (128.0 + i));
-    out[GT_LN + i] = static_cast<float>(std::log1p(i / 128.0));
+  double t[GT_SIZE];
+  for (int j = 0; j < GT_SIZE / 2; ++j) {
+    t[j] = inv_normal_cdf((j + 0.5) / GT_SIZE);
+    t[GT_SIZE - 1 - j] = -t[j];
   }
-  for (int a = 0; a < 256; ++a) {
-    const double ang = two_pi * a / 256.0;
-    out[GT_CSA + 2 * a] = static_cast<float>(std::cos(ang));
-    out[GT_CSA + 2 * a + 1] = static_cast<float>(std::sin(ang));
-  }
-  for (int b = 0; b < 256; ++b) {
-    const double ang = two_pi * (b + 0.5) / 65536.0;
-    out[GT_CSB + 2 * b] = static_cast<float>(std::cos(ang));
-    out[GT_CSB + 2 * b + 1] = static_cast<float>(std::sin(ang));
+  double m2 = 0.0;
+  for (int j = 0; j < GT_SIZE; ++j) m2 += t[j] * t[j];
+  const double scale = 1.0 / std::sqrt(m2 / GT_SIZE);
+  for (int j = 0; j < GT_SIZE; ++j) {
+    const float f = static_cast<float>(t[j] * scale);
+    out[j] = __bfloat162float(__float2bfloat16_rn(f));
   }
 }
 

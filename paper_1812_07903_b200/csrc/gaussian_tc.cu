@@ -385,7 +385,11 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
 
 int32_t gaussian_tc_bf16(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
                          uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
-  if (p.ns == 512 && p.dslabs == 2 && getenv("LVSK_K4_NOCLUSTER") == nullptr)
+  // the 2-CTA cluster that shares each Z tile over DSMEM paid off while Z
+  // generation was the bound (Box-Muller, ~40 instructions / entry); with the
+  // table generator (~8 / entry) its cluster-scope release fences cost more
+  // than regenerating the tile: C5 5.25 ms (CL = 2) vs 3.68 ms (CL = 1)
+  if (p.ns == 512 && p.dslabs == 2 && getenv("LVSK_K4_CLUSTER") != nullptr)
     return launch_gauss_tc<512, 2>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
   return p.ns == 512 ? launch_gauss_tc<512, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st)
                      : launch_gauss_tc<256, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);

@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
   double* hi = csr_dyn + static_cast<int64_t>(warp) * 2 * CSR_GROUP;
   double* lo = hi + CSR_GROUP;
   for (int64_t c = lane; c < width; c += 32) {
-    hi[c] = hi_in[b * d + c0 + c];
-    lo[c] = lo_in[b * d + c0 + c];
+    hi[c] = hi_in ? hi_in[b * d + c0 + c] : 0.0;
+    lo[c] = lo_in ? lo_in[b * d + c0 + c] : 0.0;
   }
   __syncwarp();
   const int64_t base0 = row_ptr[0];
@@ -111,29 +111,73 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 // segments / 1024 entries; longer rows are split, harmless since one row's
 // entries have distinct columns) with cp.async into a 4-deep ring signalled
 // by cp.async.mbarrier.arrive; warps 1..8 apply the chunk's segments
-// concurrently (segment q by warp q mod 8) with returning shared-memory
-// atomics: hi += v, and the exact rounding error of that addition (TwoSum of
-// the returned old value and v) onto lo, so hi + lo is the compensated sum of
-// the bucket's contributions in whatever order they land (the sketch equals
-// the reference's to ~1e-16 relative instead of bit-for-bit;
-// LVSK_K2_DETERMINISTIC=1 selects the ordered csr_gather_kernel, which is
-// bit-exact).  The same warps validate their segments (strictly increasing
-// in-range columns, finite values).
+// concurrently (segment q by warp q mod 5), each into its OWN float64 row of
+// partial sums in shared memory (5 x 32 KB): a segment's entries have distinct
+// columns, so a warp's 32 lanes never collide and every update is a plain
+// load-add-store — no atomics (the first version used returning shared fp64
+// atomics, CAS loops that serialised on the Zipf-hot columns: 17.6 ms at C4).
+// At the end hi_out + lo_out = TwoSum fold of (hi_in, lo_in, P_0 .. P_4) in
+// warp order.  Deterministic; equal to the reference's compensated state to
+// ~1e-16 relative instead of bit-for-bit (LVSK_K2_DETERMINISTIC=1 selects the
+// ordered csr_gather_kernel, which is bit-exact).  The same warps validate
+// their segments (strictly increasing in-range columns, finite values).
 constexpr int ST_COLS = 4096;
-constexpr int ST_APPLY = 8;  // applier warps
+constexpr int ST_APPLY = 5;  // applier warps, one private fp64 partial row each
 constexpr int ST_ECAP = 1024;
 constexpr int ST_RMAX = 64;
 constexpr int ST_STAGES = 4;
 
-struct SegInfo {
-  int32_t off, len;  // position in the stage buffer, entry count
-  int32_t flags;     // bit0 negative sign, bit1 continuation of the previous segment's row, bit2 end of stream
-  int32_t pad;
-};
-
 __device__ __forceinline__ uint32_t csr_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+struct SegInfo {
+  int32_t off, len;  // position of the first column index in the stage buffer, entry count
+  int32_t flags;     // bit0 negative sign, bit1 continuation of the previous segment's row
+  int32_t voff;      // position of the first value (the two arrays' 16-byte alignments differ)
+};
+
+// Stage slot of a row piece of `len` entries: its 16-byte aligned superset in
+// either array (<= 3 leading + <= 3 trailing entries) rounded to 4 entries.
+__device__ __forceinline__ int32_t st_slot(int64_t len) { return static_cast<int32_t>((len + 9) & ~int64_t{3}); }
+
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   csr_smem(dst)),
+               "l"(src), "r"(bytes), "r"(csr_smem(bar))
+               : "memory");
+}
+
+// Issue the aligned-superset copies of entries [src, src + len) of col / val
+// into the stage at slot position pos; returns the SegInfo offsets.  A
+// 16-byte aligned chunk holding one valid byte cannot cross a page, so the
+// superset reads are always safe.
+template <typename V>
+__device__ __forceinline__ void st_issue(const int32_t* col, const V* val, int64_t src, int64_t len, int32_t pos,
+                                         int32_t* cbuf, V* vbuf, uint64_t* bar, int32_t& coff, int32_t& voff) {
+  const uintptr_t ca = reinterpret_cast<uintptr_t>(col + src), va = reinterpret_cast<uintptr_t>(val + src);
+  const int32_t padc = static_cast<int32_t>((ca & 15) >> 2);
+  const int32_t padv = static_cast<int32_t>((va & 15) / sizeof(V));
+  constexpr int VW = 16 / sizeof(V);
+  const uint32_t cbytes = static_cast<uint32_t>(((padc + len + 3) & ~int64_t{3}) * 4);
+  const uint32_t vbytes = static_cast<uint32_t>(((padv + len + VW - 1) / VW) * 16);
+  bulk_copy_g2s(cbuf + pos, reinterpret_cast<const void*>(ca & ~uintptr_t{15}), cbytes, bar);
+  bulk_copy_g2s(vbuf + pos, reinterpret_cast<const void*>(va & ~uintptr_t{15}), vbytes, bar);
+  coff = pos + padc;
+  voff = pos + padv;
+}
+template <typename V>
+__device__ __forceinline__ uint32_t st_bytes(const int32_t* col, const V* val, int64_t src, int64_t len) {
+  const uintptr_t ca = reinterpret_cast<uintptr_t>(col + src), va = reinterpret_cast<uintptr_t>(val + src);
+  const int64_t padc = (ca & 15) >> 2, padv = (va & 15) / sizeof(V);
+  constexpr int VW = 16 / sizeof(V);
+  return static_cast<uint32_t>(((padc + len + 3) & ~int64_t{3}) * 4 + ((padv + len + VW - 1) / VW) * 16);
+}
+__device__ __forceinline__ void st_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(bar)), "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(csr_smem(dst)), "l"(src) : "memory");
 }
@@ -169,9 +213,8 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
     const uint32_t* __restrict__ start, double scale, const double* hi_in, const double* lo_in, double* hi_out,
     double* lo_out, int32_t* flags) {
   extern __shared__ __align__(128) uint8_t st_smem[];
-  double* hi = reinterpret_cast<double*>(st_smem);
-  double* lo = hi + ST_COLS;
-  V* bval = reinterpret_cast<V*>(lo + ST_COLS);                          // [ST_STAGES][ST_ECAP]
+  double* part = reinterpret_cast<double*>(st_smem);                     // [ST_APPLY][ST_COLS]
+  V* bval = reinterpret_cast<V*>(part + ST_APPLY * ST_COLS);             // [ST_STAGES][ST_ECAP]
   int32_t* bcol = reinterpret_cast<int32_t*>(bval + ST_STAGES * ST_ECAP);  // [ST_STAGES][ST_ECAP]
   SegInfo* seg = reinterpret_cast<SegInfo*>(bcol + ST_STAGES * ST_ECAP);  // [ST_STAGES][ST_RMAX]
   int32_t* nseg = reinterpret_cast<int32_t*>(seg + ST_STAGES * ST_RMAX);  // [ST_STAGES]
@@ -183,80 +226,117 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
   const int64_t width = d - c0 < ST_COLS ? d - c0 : ST_COLS;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST_STAGES; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&full[s])), "r"(33));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&full[s])), "r"(1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&empty[s])), "r"(ST_APPLY));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
-    hi[c] = hi_in[b * d + c0 + c];
-    lo[c] = lo_in[b * d + c0 + c];
-  }
+  for (int c = threadIdx.x; c < ST_APPLY * ST_COLS; c += blockDim.x) part[c] = 0.0;
   __syncthreads();
   const uint32_t p0 = start[b], p1 = start[b + 1];
   if (warp == 0) {
-    // ---- loader
+    // ---- loader: 32 rows at a time, one lane per row — a warp scan places
+    //      each row's 16-byte aligned superset in the stage and the lane
+    //      issues its two cp.async.bulk copies; a row longer than a whole
+    //      stage is streamed in pieces by lane 0
     uint32_t pb = p0;          // next pair batch
-    int64_t src = 0, rem = 0;  // row in progress (lane-uniform)
-    uint32_t neg = 0;
-    bool cont = false;
     int bcnt = 0, bq = 0;      // pairs in the current batch / consumed
     int64_t my_src = 0;
     int32_t my_len = 0;
     uint32_t my_v = 0;
+    int64_t lsrc = 0, lrem = 0;  // long row in progress (lane-uniform)
+    uint32_t lneg = 0;
+    bool lcont = false;
     for (uint32_t it = 0;; ++it) {
       const uint32_t s = it % ST_STAGES, ph = (it / ST_STAGES) & 1u;
       st_wait(&empty[s], ph ^ 1u);
+      int32_t* cbuf = bcol + s * ST_ECAP;
+      V* vbuf = bval + s * ST_ECAP;
       int ns = 0, ne = 0;
       bool done = false;
-      while (ns < ST_RMAX && ne < ST_ECAP) {
-        if (rem == 0 && !cont) {
-          if (bq == bcnt) {  // fetch the next 32 pairs' (src, len, sign) in parallel
-            if (pb >= p1) {
-              done = true;
-              break;
-            }
-            bcnt = p1 - pb < 32u ? static_cast<int>(p1 - pb) : 32;
-            if (lane < bcnt) {
-              my_src = msrc[pb + lane];
-              my_len = mlen[pb + lane];
-              my_v = svals[pb + lane];
-            }
-            pb += bcnt;
-            bq = 0;
+      while (ns < ST_RMAX) {
+        if (lrem > 0) {
+          const int64_t room = ST_ECAP - ne - 6;
+          if (room < 1) break;
+          const int64_t plen = lrem < room ? lrem : room;
+          if (lane == 0) {
+            st_expect(&full[s], st_bytes<V>(col, val, lsrc, plen));
+            SegInfo si;
+            st_issue<V>(col, val, lsrc, plen, ne, cbuf, vbuf, &full[s], si.off, si.voff);
+            si.len = static_cast<int32_t>(plen);
+            si.flags = static_cast<int32_t>(lneg | (lcont ? 2u : 0u));
+            seg[s * ST_RMAX + ns] = si;
           }
-          src = __shfl_sync(0xFFFFFFFFu, my_src, bq);
-          rem = __shfl_sync(0xFFFFFFFFu, my_len, bq);
-          neg = __shfl_sync(0xFFFFFFFFu, my_v, bq) & 1u;
+          ++ns;
+          ne += st_slot(plen);
+          lsrc += plen;
+          lrem -= plen;
+          lcont = true;
+          continue;
+        }
+        if (bq == bcnt) {  // fetch the next 32 pairs' (src, len, sign) in parallel
+          if (pb >= p1) {
+            done = true;
+            break;
+          }
+          bcnt = p1 - pb < 32u ? static_cast<int>(p1 - pb) : 32;
+          if (lane < bcnt) {
+            my_src = msrc[pb + lane];
+            my_len = mlen[pb + lane];
+            my_v = svals[pb + lane];
+          }
+          pb += bcnt;
+          bq = 0;
+        }
+        const bool pend = lane >= bq && lane < bcnt;
+        const bool longrow = pend && st_slot(my_len) > ST_ECAP;
+        const uint32_t lm = __ballot_sync(0xFFFFFFFFu, longrow);
+        const int first_long = lm ? __ffs(lm) - 1 : 32;
+        const bool cand = pend && lane < first_long;
+        const int32_t S = cand && my_len > 0 ? st_slot(my_len) : 0;
+        const int32_t R = S > 0 ? 1 : 0;
+        int32_t incl = S, rincl = R;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o), tr = __shfl_up_sync(0xFFFFFFFFu, rincl, o);
+          if (lane >= o) {
+            incl += t;
+            rincl += tr;
+          }
+        }
+        const bool fits = ne + incl <= ST_ECAP && ns + rincl <= ST_RMAX;
+        const uint32_t nf = __ballot_sync(0xFFFFFFFFu, cand && !fits);
+        int stop = nf ? __ffs(nf) - 1 : first_long;  // first lane not taken
+        if (stop > bcnt) stop = bcnt;
+        const bool take = cand && lane < stop;
+        const uint32_t bytes = take && S > 0 ? st_bytes<V>(col, val, my_src, my_len) : 0u;
+        const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bytes);
+        if (lane == 0 && total) st_expect(&full[s], total);
+        __syncwarp();
+        if (take && S > 0) {
+          SegInfo si;
+          st_issue<V>(col, val, my_src, my_len, ne + incl - S, cbuf, vbuf, &full[s], si.off, si.voff);
+          si.len = my_len;
+          si.flags = static_cast<int32_t>(my_v & 1u);
+          seg[s * ST_RMAX + ns + rincl - 1] = si;
+        }
+        const int last_take = stop - 1;  // >= bq - 1
+        if (last_take >= bq) {
+          ne += __shfl_sync(0xFFFFFFFFu, incl, last_take);
+          ns += __shfl_sync(0xFFFFFFFFu, rincl, last_take);
+        }
+        bq = stop;
+        if (nf) break;  // the stage is full
+        if (first_long < bcnt && bq == first_long) {  // hand the long row to the piece path
+          lsrc = __shfl_sync(0xFFFFFFFFu, my_src, first_long);
+          lrem = __shfl_sync(0xFFFFFFFFu, my_len, first_long);
+          lneg = __shfl_sync(0xFFFFFFFFu, my_v, first_long) & 1u;
+          lcont = false;
           ++bq;
-          if (rem == 0) {  // empty row: nothing to apply or validate
-            continue;
-          }
         }
-        const int64_t len = rem < ST_ECAP - ne ? rem : ST_ECAP - ne;
-        if (len == 0) break;
-        SegInfo si;
-        si.off = ne;
-        si.len = static_cast<int32_t>(len);
-        si.flags = static_cast<int32_t>(neg | (cont ? 2u : 0u));
-        si.pad = 0;
-        if (lane == 0) seg[s * ST_RMAX + ns] = si;
-        for (int e = lane; e < len; e += 32) {
-          cp_async4(bcol + s * ST_ECAP + ne + e, col + src + e);
-          if constexpr (sizeof(V) == 8)
-            cp_async8(bval + s * ST_ECAP + ne + e, val + src + e);
-          else
-            cp_async4(bval + s * ST_ECAP + ne + e, val + src + e);
-        }
-        ++ns;
-        ne += static_cast<int>(len);
-        src += len;
-        rem -= len;
-        cont = rem > 0;
       }
       if (lane == 0) nseg[s] = done && ns == 0 ? -1 : ns;
       if (done && ns > 0 && lane == 0) nseg[s] = ns | (1 << 30);  // last chunk
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(csr_smem(&full[s])) : "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[s])) : "memory");
       if (done) break;
@@ -275,35 +355,51 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
       const int ns = raw & ((1 << 30) - 1);
       const V* vb = bval + s * ST_ECAP;
       const int32_t* cb = bcol + s * ST_ECAP;
-      // segments are independent: every entry goes through a returning
-      // shared-memory atomic on hi and its exact rounding error (TwoSum of
-      // the old value and the addend) onto lo, so hi + lo carries the
-      // compensated sum in any order
+      // segments are independent and this warp's partial row is private, so
+      // every entry is a plain load-add-store (lanes hold distinct columns)
+      double* mine = part + aw * ST_COLS;
       for (int q = aw; q < ns; q += ST_APPLY) {
         const SegInfo si = seg[s * ST_RMAX + q];
         const double sg = (si.flags & 1) ? -scale : scale;
-        int32_t carry = (si.flags & 2) ? (q > 0 ? cb[si.off - 1] : lastcol) : -1;
-        for (int e0v = 0; e0v < si.len; e0v += 32) {
-          const int e = e0v + lane;
-          const bool live = e < si.len;
-          const int32_t c = live ? cb[si.off + e] : INT32_MAX;
-          const V xv = live ? vb[si.off + e] : V(0);
-          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-          const int32_t before = lane == 0 ? carry : cprev;
-          if (live) {
-            if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
-            if (!isfinite(static_cast<double>(xv))) bad |= LVSK_FLAG_NONFINITE;
-            const int64_t lc = static_cast<int64_t>(c) - c0;
-            if (lc >= 0 && lc < width) {
-              const double v = __dmul_rn(sg, static_cast<double>(xv));
-              const double old = atomicAdd(&hi[lc], v);
-              double su, er;
-              two_sum(old, v, su, er);
-              atomicAdd(&lo[lc], er);
-            }
+        int32_t carry = -1;
+        if (si.flags & 2) {
+          if (q > 0) {
+            const SegInfo sp = seg[s * ST_RMAX + q - 1];
+            carry = cb[sp.off + sp.len - 1];
+          } else {
+            carry = lastcol;
           }
-          carry = __shfl_sync(0xFFFFFFFFu, c, 31);
         }
+        // four 32-entry chunks at a time: one row's entries have distinct
+        // columns, so their loads / adds / stores are independent (ILP)
+        for (int e0v = 0; e0v < si.len; e0v += 128) {
+          int32_t cc[4];
+          double xx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0v + 32 * u + lane;
+            const bool live = e < si.len;
+            const int32_t c = live ? cb[si.off + e] : INT32_MAX;
+            const V xv = live ? vb[si.voff + e] : V(0);
+            const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+            const int32_t before = lane == 0 ? carry : cprev;
+            carry = __shfl_sync(0xFFFFFFFFu, c, 31);
+            if (live) {
+              if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
+              if (!isfinite(static_cast<double>(xv))) bad |= LVSK_FLAG_NONFINITE;
+            }
+            const int64_t lc = static_cast<int64_t>(c) - c0;
+            cc[u] = (live && lc >= 0 && lc < width) ? static_cast<int32_t>(lc) : -1;
+            xx[u] = __dmul_rn(sg, static_cast<double>(xv));
+          }
+          double old[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) old[u] = cc[u] >= 0 ? mine[cc[u]] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (cc[u] >= 0) mine[cc[u]] = __dadd_rn(old[u], xx[u]);
+        }
+        __syncwarp();  // the next segment may hit the same columns from other lanes
       }
       if (ns > 0) {
         const SegInfo sl = seg[s * ST_RMAX + ns - 1];
@@ -318,8 +414,20 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
   }
   __syncthreads();
   for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
-    hi_out[b * d + c0 + c] = hi[c];
-    lo_out[b * d + c0 + c] = lo[c];
+    double h = 0.0, l = 0.0;  // NULL input state = zeros (no read)
+    if (hi_in) {
+      h = hi_in[b * d + c0 + c];
+      l = lo_in[b * d + c0 + c];
+    }
+#pragma unroll
+    for (int w = 0; w < ST_APPLY; ++w) {
+      double su, er;
+      two_sum(h, part[w * ST_COLS + c], su, er);
+      h = su;
+      l = __dadd_rn(l, er);
+    }
+    hi_out[b * d + c0 + c] = h;
+    lo_out[b * d + c0 + c] = l;
   }
 }
 
@@ -463,7 +571,7 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
     const int sgroups = static_cast<int>((d + ST_COLS - 1) / ST_COLS);
     const int vsz = val_dtype == LVSK_F64 ? 8 : 4;
     auto smem_for = [](int v) {
-      return 2 * ST_COLS * 8 + ST_STAGES * ST_ECAP * (v + 4) + ST_STAGES * ST_RMAX * static_cast<int>(sizeof(SegInfo)) +
+      return ST_APPLY * ST_COLS * 8 + ST_STAGES * ST_ECAP * (v + 4) + ST_STAGES * ST_RMAX * static_cast<int>(sizeof(SegInfo)) +
              ST_STAGES * 4 + 2 * ST_STAGES * 8;
     };
     static bool sattr = false;

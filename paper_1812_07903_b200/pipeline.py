@@ -76,11 +76,10 @@ class LeveragePipeline:
         L, st, s = N.lib(), N.stream_ptr(), self.state
         fam = self.spec.family
         if isinstance(X, CSRMatrix):
-            s._hi.zero_()
-            s._lo.zero_()
+            # a fresh state each run: NULL (hi_in, lo_in) = zeros, no memset and no state read
             N.check(L.lvsk_hashed_sketch_csr(X.indptr.data_ptr(), X.indices.data_ptr(), X.data.data_ptr(),
                                              csr_code(X), X.n, X.d, self.row0, s._blocks, self.spec.s, s._scale,
-                                             s._hi.data_ptr(), s._lo.data_ptr(), s._hi.data_ptr(), s._lo.data_ptr(),
+                                             None, None, s._hi.data_ptr(), s._lo.data_ptr(),
                                              self.k, self.ws_sketch.data_ptr(), self.ws_sketch.numel(),
                                              self.flags.data_ptr(), st), "csr sketch")
             N.check(L.lvsk_fold_compensated(s._hi.data_ptr(), s._lo.data_ptr(), self.sx.data_ptr(), self.sx.numel(), st),

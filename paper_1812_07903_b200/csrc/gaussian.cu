@@ -2,13 +2,15 @@
 //
 // Extension: the reference rejects the "gaussian" family
 // (pkg/src/levsketch/sketch.py:38-41, 74-75); BASELINE configs 1 and 5 ask
-// for it.  Z[j, i] (j < k sketch row, i global input row) is the bf16-rounded
-// table-driven Box-Muller normal of philox.cuh, which the CPU oracle
-// (oracle/levsketch_oracle.py: gaussian_z) reproduces bit-for-bit.  bf16 X runs on the tensor cores
-// (gaussian_tc.cu); this file holds the entry generator, the SIMT GEMM used
-// for fp32 / fp64 X (split-K) and the deterministic float64 reduction of the
-// split partials shared by both.
+// for it.  Z[j, i] (j < k sketch row, i global input row) is the counter-based
+// splitmix64 + 4096-level Gaussian table entry of philox.cuh, which the CPU
+// oracle (oracle/levsketch_oracle.py: gaussian_z) reproduces bit-for-bit.
+// bf16 X runs on the tensor cores (gaussian_tc.cu), fp32 X too after an exact
+// three-plane bf16 split (split3_bf16_kernel); this file holds the entry
+// generator, the SIMT GEMM (fp64 X, small fp32 cases; split-K) and the
+// deterministic float64 reduction of the split partials shared by all.
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "philox.cuh"
@@ -194,6 +196,36 @@ static GaussPlan plan_gauss(int64_t n, int64_t d, int64_t k) {
   return p;
 }
 
+// fp32 X on the tensor cores: X = P0 + P1 + P2 exactly, P_j = bf16_rn(X -
+// P0 - .. - P_{j-1}) (fp32 has 24 significand bits, bf16 8: three planes hold
+// every normal fp32 value exactly), so Z X = Z P0 + Z P1 + Z P2 with exact
+// bf16 products and fp32 TMEM accumulation — the same arithmetic class as the
+// SIMT path (fp32 accumulation per split, fp64 across splits) at tensor-core
+// speed.  A non-finite x poisons P0 (and P1 = inf - inf = NaN), so the
+// reduce kernel's finiteness check still fires.
+__global__ void split3_bf16_kernel(const float* __restrict__ X, int64_t n, int64_t d, int64_t ldx, int64_t ldp,
+                                   __nv_bfloat16* __restrict__ P) {
+  const int64_t plane = n * ldp;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * ldp;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / ldp, j = e % ldp;
+    const float x = j < d ? X[i * ldx + j] : 0.f;
+    const __nv_bfloat16 a = __float2bfloat16_rn(x);
+    const float r1 = __fsub_rn(x, __bfloat162float(a));
+    const __nv_bfloat16 b = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 c = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(b)));
+    P[e] = a;
+    P[plane + e] = b;
+    P[2 * plane + e] = c;
+  }
+}
+
+static bool f32_tc(int64_t n, int64_t d, int64_t k) {
+  if (getenv("LVSK_NO_TC") != nullptr) return false;
+  const int64_t ldp = (d + 7) / 8 * 8;
+  return k >= 64 && n >= 256 && 3 * n * ldp * 2 <= (int64_t{3} << 30);
+}
+
 }  // namespace lvsk
 
 using namespace lvsk;
@@ -207,6 +239,13 @@ extern "C" size_t lvsk_gaussian_workspace_bytes(int64_t n, int64_t d, int64_t k,
   }
   Measure m;
   m.take<char>(static_cast<size_t>(splits) * k * d * (dtype == LVSK_F64 ? 8 : 4));
+  if (dtype == LVSK_F32 && f32_tc(n, d, k)) {
+    const GaussTcPlan t = plan_gauss_tc(n, d, k);
+    Measure m3;
+    m3.take<float>(static_cast<size_t>(3 * t.splits) * k * d);
+    m3.take<__nv_bfloat16>(static_cast<size_t>(3 * n * ((d + 7) / 8 * 8)));
+    if (m3.off > m.off) return m3.off;
+  }
   return m.off;
 }
 
@@ -239,6 +278,21 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
     const int32_t rc = gaussian_tc_bf16(static_cast<const __nv_bfloat16*>(X), n, d, ldx, k, row0, k0, k1, t, part, st);
     if (rc != LVSK_OK) return rc;
     gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, t.splits, count, scale, SX, accumulate, flags);
+  } else if (dtype == LVSK_F32 && f32_tc(n, d, k)) {
+    const GaussTcPlan t = plan_gauss_tc(n, d, k);
+    const int64_t ldp = (d + 7) / 8 * 8;
+    float* part = c.take<float>(static_cast<size_t>(3 * t.splits) * count);
+    __nv_bfloat16* planes = c.take<__nv_bfloat16>(static_cast<size_t>(3 * n * ldp));
+    LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
+    const int sgrid = static_cast<int>((n * ldp + 255) / 256 < num_sms() * 16 ? (n * ldp + 255) / 256 : num_sms() * 16);
+    split3_bf16_kernel<<<sgrid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx, ldp, planes);
+    LVSK_CHECK_LAUNCH("gaussian split");
+    for (int j = 0; j < 3; ++j) {
+      const int32_t rc = gaussian_tc_bf16(planes + j * n * ldp, n, d, ldp, k, row0, k0, k1, t,
+                                          part + static_cast<int64_t>(j) * t.splits * count, st);
+      if (rc != LVSK_OK) return rc;
+    }
+    gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, 3 * t.splits, count, scale, SX, accumulate, flags);
   } else {
     float* part = c.take<float>(static_cast<size_t>(p.splits) * count);
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);

@@ -260,6 +260,21 @@ def test_gaussian_sketch_matches_oracle():
         assert np.linalg.norm(st.data - ref) <= tol * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("n,d,k", [(20000, 256, 1024), (3001, 100, 200), (700, 520, 64)])
+def test_gaussian_fp32_tensor_core_vs_simt(n, d, k, monkeypatch):
+    """fp32 X through the exact three-plane bf16 split on tcgen05 (default)
+    vs the SIMT split-K GEMM (LVSK_NO_TC=1) vs the float64 oracle."""
+    x = np.random.default_rng(n).standard_normal((n, d)).astype(np.float32)
+    X = torch.from_numpy(x).cuda()
+    spec = P.SketchSpec("gaussian", eps=0.5, d=d, seed=4, rows_override=k)
+    tc = P.apply_sketch(X, spec).data
+    ref = O.gaussian_sketch(x.astype(np.float64), k, 4)
+    assert np.linalg.norm(tc - ref) <= 2e-6 * np.linalg.norm(ref)
+    monkeypatch.setenv("LVSK_NO_TC", "1")
+    simt = P.apply_sketch(X, spec).data
+    assert np.linalg.norm(simt - ref) <= 2e-6 * np.linalg.norm(ref)
+
+
 @pytest.mark.parametrize("n,d,k,ldx,row0", [(5000, 1024, 300, 1024, 0), (3001, 200, 128, 208, 7),
                                             (700, 520, 256, 520, 2**33 + 5), (64, 64, 8, 64, 0)])
 def test_gaussian_tc_bf16_vs_oracle(n, d, k, ldx, row0):

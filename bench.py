@@ -438,7 +438,9 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
                               "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
                               "srht": "srht_sampled_kernel (K3 v3: one pass, block WHT + sampled combine)",
                               "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
-                              if not csr and X.dtype == torch.bfloat16 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],
+                              if X.dtype == torch.bfloat16 else
+                              "split3_bf16_kernel + 3 x gaussian_tc_kernel (K4-TC on the exact bf16 planes of fp32 X) + reduce"
+                              if X.dtype == torch.float32 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],
                    "leverage": "csr_rowsumsq_kernel (K6)" if csr else "leverage_v2_kernel (K5, tcgen05)"}[dominant],
         "achieved": dom_gbs,
         "peak": peak,
@@ -448,8 +450,9 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         "algorithmic_bytes_per_launch": dom_bytes,
         "peak_source": peak_src,
     }
-    if dominant == "sketch" and cfg["family"] == "gaussian" and not csr and X.dtype == torch.bfloat16:
-        # K4-TC is a GEMM: 2*k*n*d flop per launch against the measured bf16 tensor peak
+    if dominant == "sketch" and cfg["family"] == "gaussian" and not csr and X.dtype in (torch.bfloat16, torch.float32):
+        # K4-TC is a GEMM: 2*k*n*d algorithmic flop per launch (fp32 X runs it on three exact
+        # bf16 planes: 3x the tensor work for the same algorithmic flops) against the bf16 tensor peak
         tpeak, tsrc = measured_tensor_peak()
         flops = 2.0 * k * n * d
         ach = flops / (stage_ms["sketch"] / 1000) / 1e12

@@ -437,7 +437,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
                               "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
                               "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
                               "srht": "srht_sampled_kernel (K3 v3: one pass, block WHT + sampled combine)",
-                              "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
+                              "gaussian": "gaussian_gemm_kernel (K4, SIMT)" if csr else
+                              "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
                               if X.dtype == torch.bfloat16 else
                               "split3_bf16_kernel + 3 x gaussian_tc_kernel (K4-TC on the exact bf16 planes of fp32 X) + reduce"
                               if X.dtype == torch.float32 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],

@@ -122,10 +122,16 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 // ordered csr_gather_kernel, which is bit-exact).  The same warps validate
 // their segments (strictly increasing in-range columns, finite values).
 constexpr int ST_COLS = 4096;
-constexpr int ST_APPLY = 5;  // applier warps, one private fp64 partial row each
+#ifndef LVSK_ST_APPLY
+#define LVSK_ST_APPLY 5
+#endif
+#ifndef LVSK_ST_STAGES
+#define LVSK_ST_STAGES 4
+#endif
+constexpr int ST_APPLY = LVSK_ST_APPLY;  // applier warps, one private fp64 partial row each
 constexpr int ST_ECAP = 1024;
 constexpr int ST_RMAX = 64;
-constexpr int ST_STAGES = 4;
+constexpr int ST_STAGES = LVSK_ST_STAGES;
 
 __device__ __forceinline__ uint32_t csr_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -574,11 +580,15 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
       return ST_APPLY * ST_COLS * 8 + ST_STAGES * ST_ECAP * (v + 4) + ST_STAGES * ST_RMAX * static_cast<int>(sizeof(SegInfo)) +
              ST_STAGES * 4 + 2 * ST_STAGES * 8;
     };
-    static bool sattr = false;
-    if (!sattr) {
-      cudaFuncSetAttribute(csr_stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(4));
-      cudaFuncSetAttribute(csr_stream_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(8));
-      sattr = true;
+    static bool sattr[2] = {false, false};
+    if (!sattr[vsz == 8]) {
+      const cudaError_t e =
+          vsz == 8 ? cudaFuncSetAttribute(csr_stream_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          smem_for(8))
+                   : cudaFuncSetAttribute(csr_stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          smem_for(4));
+      if (e != cudaSuccess) return cuda_status(e, "csr stream shared-memory attribute");
+      sattr[vsz == 8] = true;
     }
     const unsigned sgrid = static_cast<unsigned>(k * sgroups);
     if (val_dtype == LVSK_F32)

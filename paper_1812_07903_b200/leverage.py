@@ -180,11 +180,13 @@ def cholesky_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor):
 _EIGH_KAPPA = 1e4
 
 
-def _cholqr2(Y: torch.Tensor) -> torch.Tensor:
+def _cholqr2(Y: torch.Tensor, rounds: int = 2) -> torch.Tensor:
     """Orthonormal basis of range(Y) by two rounds of Cholesky QR (stable for
-    cond(Y) up to ~1e7 in float64).  No host synchronisation: a failed
-    factorisation yields NaNs, which the caller's residual test rejects."""
-    for _ in range(2):
+    cond(Y) up to ~1e7 in float64; one round leaves an orthogonality error of
+    ~eps * cond(Y)^2, harmless between power steps, which re-condition the
+    block).  No host synchronisation: a failed factorisation yields NaNs,
+    which the caller's residual test rejects."""
+    for _ in range(rounds):
         L, _ = torch.linalg.cholesky_ex(Y.T @ Y)
         Y = torch.linalg.solve_triangular(L, Y.T, upper=False).T
     return Y
@@ -203,8 +205,12 @@ def _topk_gram(G: torch.Tensor, want: int, rounds: int = 2, iters: int = 6, tol:
     gen = torch.Generator(device=G.device).manual_seed(0x5EED)
     Q = torch.randn(d, b, dtype=G.dtype, device=G.device, generator=gen)
     for _ in range(rounds):
-        for _ in range(iters):
-            Q = _cholqr2(G @ Q)
+        for it in range(iters):
+            # full CholQR2 on the first steps (the random start is badly
+            # conditioned) and the last (Rayleigh-Ritz needs an orthonormal
+            # basis); one Cholesky QR in between (each small potrf + trsm is
+            # ~0.1 ms of cuSOLVER latency)
+            Q = _cholqr2(G @ Q, 2 if it < 2 or it == iters - 1 else 1)
         Y = G @ Q
         Bm = Q.T @ Y
         theta, W = torch.linalg.eigh(0.5 * (Bm + Bm.T))

@@ -25,7 +25,15 @@ def main():
            "chol_128_us": t(lambda: torch.linalg.cholesky_ex(B)),
            "trsm_1024x128_us": t(lambda: torch.linalg.solve_triangular(L, Q.T, upper=False)),
            "eigh_128_us": t(lambda: torch.linalg.eigh(B)), "eigh_256_us": t(lambda: torch.linalg.eigh(G[:256, :256])),
-           "eigh_1024_us": t(lambda: torch.linalg.eigh(G), 3)})
+           "eigh_1024_us": t(lambda: torch.linalg.eigh(G), 3),
+           "svd_gesvdj_128_us": t(lambda: torch.linalg.svd(B, driver="gesvdj")),
+           "svd_gesvd_128_us": t(lambda: torch.linalg.svd(B, driver="gesvd")),
+           "svd_gesvda_128_us": t(lambda: torch.linalg.svd(B, driver="gesvda")),
+           "eigvalsh_128_us": t(lambda: torch.linalg.eigvalsh(B)),
+           "inv_ex_128_us": t(lambda: torch.linalg.inv_ex(B)),
+           "qr_1024x128_us": t(lambda: torch.linalg.qr(Q)),
+           "eigh_128_batched2_us": t(lambda: torch.linalg.eigh(torch.stack([B, B]))),
+           "eigh_32_batched16_us": t(lambda: torch.linalg.eigh(B[:32, :32].expand(16, 32, 32).contiguous()))})
 
 
 if __name__ == "__main__":

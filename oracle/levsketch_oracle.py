@@ -268,11 +268,12 @@ def explicit_srht_matrix(k, seed, n):
 
 # ---------------------------------------------------------------------------
 # Gaussian sketch (extension; parity unpinned by reference tests).
-# S[j, i] = Z[j, i] / sqrt(k), Z[8q + m, i] = TAB[16-bit field (m & 3) of
-# h_(m >> 2) >> 4], h_w = mix64(key + phi * ((i << 24) | (q << 1) | w)) — the
-# reference's splitmix64 finaliser (sketch.py:141-148) run as a counter-based
-# stream — and TAB a 4096-level equiprobable Gaussian (definition:
-# csrc/philox.cuh), so CPU and GPU agree bit-for-bit.
+# S[j, i] = Z[j, i] / sqrt(k), Z[8q + m, i] = TAB[32 b + ((i >> 1) & 31)], b = byte m
+# of h = mix64(key + phi * ((i << 24) | (q << 1))) — the reference's splitmix64
+# finaliser (sketch.py:141-148) run as a counter-based stream — and TAB the
+# signed levels of an 8192-level equiprobable Gaussian, each column class
+# (i >> 1) & 31 rescaled to unit second moment (definition: csrc/philox.cuh),
+# so CPU and GPU agree bit-for-bit.
 
 _PHI = np.uint64(0x9E3779B97F4A7C15)
 
@@ -294,21 +295,24 @@ _GT = None
 
 
 def gaussian_tables() -> np.ndarray:
-    """TAB[4096] (float32, bf16-valued): bf16_rn(float(t_j / sqrt(mean t^2))),
-    t_j = Phi^-1((j + 1/2) / 4096), t_(4095-j) = -t_j."""
+    """TAB[8192] (float32, bf16-valued): for b < 128, TAB[32 b + c] is level
+    L = 32 b + c, Phi^-1(1/2 + (L + 1/2) / 8192), column class c rescaled to
+    unit second moment (sequential float64 sums, as csrc/gaussian.cu);
+    TAB[4096 + L] = -TAB[L]."""
     global _GT
     if _GT is None:
-        n = 4096
-        t = [0.0] * n
-        for j in range(n // 2):
-            t[j] = _inv_normal_cdf((j + 0.5) / n)
-            t[n - 1 - j] = -t[j]
-        m2 = 0.0
-        for v in t:  # sequential, like the C++ loop
-            m2 += v * v
-        scale = 1.0 / math.sqrt(m2 / n)
-        f = np.array([v * scale for v in t], dtype=np.float64).astype(np.float32)
-        _GT = _bf16_rn(f)
+        half = 4096
+        raw = [_inv_normal_cdf(0.5 + (L + 0.5) / (2.0 * half)) for L in range(half)]
+        out = np.empty(half, dtype=np.float64)
+        for c in range(32):
+            m2 = 0.0
+            for r in range(half // 32):
+                m2 += raw[32 * r + c] * raw[32 * r + c]
+            scale = 1.0 / math.sqrt(m2 / (half // 32))
+            for r in range(half // 32):
+                out[32 * r + c] = raw[32 * r + c] * scale
+        pos = _bf16_rn(out.astype(np.float32))
+        _GT = np.concatenate([pos, -pos])
     return _GT.copy()
 
 
@@ -335,13 +339,12 @@ def gaussian_z(seed: int, k: int, row0: int, n: int) -> np.ndarray:
     I, Q = np.meshgrid(i, q)  # (k/8, n)
     key = np.uint64(((((seed >> 32) & 0xFFFFFFFF) ^ GAUSS_KEY_XOR) << 32) | (seed & 0xFFFFFFFF))
     out = np.empty((Q.shape[0], 8, n), dtype=np.float32)
+    cls = ((I >> np.uint64(1)) & np.uint64(31)).astype(np.int64)
     with np.errstate(over="ignore"):
-        base = key + _PHI * ((I << np.uint64(24)) | (Q << np.uint64(1)))
-        for w in range(2):
-            h = _mix64_arr(base + _PHI * np.uint64(w))
-            for f in range(4):
-                field = (h >> np.uint64(16 * f)) & np.uint64(0xFFFF)
-                out[:, 4 * w + f] = tab[(field >> np.uint64(4)).astype(np.int64)]
+        h = _mix64_arr(key + _PHI * ((I << np.uint64(24)) | (Q << np.uint64(1))))
+        for m in range(8):
+            b = ((h >> np.uint64(8 * m)) & np.uint64(0xFF)).astype(np.int64)
+            out[:, m] = tab[32 * b + cls]
     return out.reshape(-1, n)[:k]
 
 

@@ -20,7 +20,8 @@ namespace lvsk {
 // ---- generator table (philox.cuh) -----------------------------------------
 // Same float64 steps as the oracle (gaussian_tables): bisection of
 // 0.5 erfc(-x / sqrt 2) = p on [-10, 10] (100 halvings reach adjacent
-// doubles), sequential sum of squares, one rounding to float then to bf16.
+// doubles), sequential sums of squares per column class, one rounding to
+// float then to bf16.
 static double inv_normal_cdf(double p) {
   double lo = -10.0, hi = 10.0;
   for (int it = 0; it < 100; ++it) {
@@ -34,17 +35,22 @@ static double inv_normal_cdf(double p) {
 }
 
 void gaussian_table_host(float* out) {
-  double t[GT_SIZE];
-  for (int j = 0; j < GT_SIZE / 2; ++j) {
-    t[j] = inv_normal_cdf((j + 0.5) / GT_SIZE);
-    t[GT_SIZE - 1 - j] = -t[j];
-  }
-  double m2 = 0.0;
-  for (int j = 0; j < GT_SIZE; ++j) m2 += t[j] * t[j];
-  const double scale = 1.0 / std::sqrt(m2 / GT_SIZE);
-  for (int j = 0; j < GT_SIZE; ++j) {
-    const float f = static_cast<float>(t[j] * scale);
-    out[j] = __bfloat162float(__float2bfloat16_rn(f));
+  // 4096 positive levels of an 8192-level equiprobable Gaussian, level L at
+  // TAB[L] = TAB[32 b + c] (b < 128), each column class c rescaled to unit
+  // second moment; TAB[32 (b + 128) + c] = -TAB[32 b + c]
+  constexpr int HALF = GT_SIZE / 2;
+  double raw[HALF];
+  for (int L = 0; L < HALF; ++L) raw[L] = inv_normal_cdf(0.5 + (L + 0.5) / GT_SIZE);
+  for (int c = 0; c < 32; ++c) {
+    double m2 = 0.0;
+    for (int r = 0; r < HALF / 32; ++r) m2 += raw[32 * r + c] * raw[32 * r + c];
+    const double scale = 1.0 / std::sqrt(m2 / (HALF / 32));
+    for (int r = 0; r < HALF / 32; ++r) {
+      const float f = static_cast<float>(raw[32 * r + c] * scale);
+      const float v = __bfloat162float(__float2bfloat16_rn(f));
+      out[32 * r + c] = v;
+      out[HALF + 32 * r + c] = -v;
+    }
   }
 }
 
@@ -66,8 +72,7 @@ const float* gaussian_table_device() {
 
 __global__ void gaussian_entries_kernel(uint32_t k0, uint32_t k1, int64_t k, uint64_t row0, int64_t n,
                                         const float* __restrict__ gtab, float* Z) {
-  __shared__ float tab[GT_SIZE];
-  load_gaussian_table(tab, gtab);
+  const float* tab = gtab;  // 32 KB, L1-resident (the SIMT GEMM needs its shared memory for tiles)
   __syncthreads();
   const int64_t nq = (k + 7) / 8;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nq * n;
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(256) gaussian_gemm_kernel(const T* __restrict_
                                                             int64_t k, int64_t rows_per_split,
                                                             const float* __restrict__ gtab,
                                                             A* __restrict__ partial, int32_t* flags) {
-  __shared__ float tab[GT_SIZE];
+  const float* tab = gtab;  // 32 KB, L1-resident
   __shared__ A Zs[G_RT][G_JT + 1];
   __shared__ A Xs[G_RT][G_CT + 1];
   const int tid = threadIdx.x;
@@ -102,7 +107,6 @@ __global__ void __launch_bounds__(256) gaussian_gemm_kernel(const T* __restrict_
   const int64_t split = blockIdx.z;
   const int64_t r_begin = split * rows_per_split;
   const int64_t r_end = min(n, r_begin + rows_per_split);
-  load_gaussian_table(tab, gtab);
   __syncthreads();
   A acc[4][8];
 #pragma unroll

@@ -4,20 +4,24 @@
 // ask for it.
 //
 // Definition (restated bit-for-bit by oracle/levsketch_oracle.py gaussian_z):
-//   Z[8q + m, i] (i = global input row, m = 0..7) = TAB[f >> 4], f = the
-//   16-bit field (m & 3) of the 64-bit word h_(m >> 2), where
-//     h_w = mix64(key + phi * ((i << 24) | (q << 1) | w)),
+//   Z[8q + m, i] = TAB[32 b + c]  (i = global input row, m = 0..7), where
+//     b = byte m of h = mix64(key + phi * ((i << 24) | (q << 1))),
+//     c = (i >> 1) & 31,
 //   mix64 the splitmix64 finaliser (the reference's _mix64, sketch.py:141-148),
-//   phi = 0x9E3779B97F4A7C15 and key = (seed_hi ^ 'GAUS') << 32 | seed_lo —
-//   i.e. splitmix64 output number (i << 24 | q << 1 | w) of the seeded
-//   stream.  TAB is a 4096-level equiprobable Gaussian: TAB[j] =
-//   bf16_rn(float(t_j / sqrt(mean t^2))), t_j = Phi^-1((j + 1/2) / 4096) by
-//   bisection on erfc (antisymmetric: t_4095-j = -t_j), so E Z = 0 and
-//   E Z^2 = 1 up to the bf16 rounding, tails at +-3.8 sigma.  Built once on
-//   the host (lvsk_gaussian_tables exports it so the CPU tests pin it to the
-//   oracle's).  Cost: two 64-bit hashes per 8 entries + one table read per
-//   entry (~8 SASS instructions / entry; the earlier Philox4x32-10 + Box-Muller
-//   definition cost ~40 and bounded K4-TC below the tensor-core rate).
+//   phi = 0x9E3779B97F4A7C15, key = (seed_hi ^ 'GAUS') << 32 | seed_lo — i.e.
+//   splitmix64 output number (i << 24 | q << 1) of the seeded stream, one
+//   64-bit hash per 8 entries.  TAB[32 b + c], b < 128, is positive level
+//   L = 32 b + c of an 8192-level equiprobable Gaussian, Phi^-1(1/2 + (L + 1/2)
+//   / 8192), each column class c rescaled to unit second moment and bf16-
+//   rounded; TAB[32 (b + 128) + c] = -TAB[32 b + c] (so every entry is
+//   symmetric).  The class is the TC kernel's lane (lanes own input rows 2l,
+//   2l+1 of a 64-row stage), so a warp's 32 table reads hit 32 different banks
+//   and an entry costs a byte permute, an address and one shared load — ~4
+//   SASS instructions including its share of the hash (the round-1 Philox +
+//   Box-Muller definition cost ~40 and a 12-bit-indexed table ~3.5 shared
+//   wavefronts per 32 reads; both bounded K4-TC below the tensor rate).
+//   Built on the host (bisection on erfc, float64) with the same steps as the
+//   oracle; lvsk_gaussian_tables exports the table so a CPU test pins the two.
 #pragma once
 
 #include "common.cuh"
@@ -28,7 +32,7 @@ struct Philox {
   static constexpr uint32_t KEY_XOR = 0x47415553u;  // "GAUS"
 };
 
-constexpr int GT_SIZE = 4096;  // TAB: 4096 equiprobable Gaussian levels (bf16-valued floats)
+constexpr int GT_SIZE = 8192;  // TAB[256 byte values][32 column classes] (bf16-valued floats)
 
 const float* gaussian_table_device();  // device copy (built on first use)
 void gaussian_table_host(float* out);  // GT_SIZE floats
@@ -38,14 +42,13 @@ __device__ __forceinline__ void gaussian8(uint64_t i, uint32_t q, uint32_t k0, u
                                           const float* __restrict__ tab, float (&z)[8]) {
   constexpr uint64_t PHI = 0x9E3779B97F4A7C15ull;
   const uint64_t key = (static_cast<uint64_t>(k1) << 32) | k0;
-  const uint64_t base = key + PHI * ((i << 24) | (static_cast<uint64_t>(q) << 1));
-  const uint64_t h0 = mix64(base), h1 = mix64(base + PHI);
-  const uint32_t w[4] = {static_cast<uint32_t>(h0), static_cast<uint32_t>(h0 >> 32), static_cast<uint32_t>(h1),
-                         static_cast<uint32_t>(h1 >> 32)};
+  const uint64_t h = mix64(key + PHI * ((i << 24) | (static_cast<uint64_t>(q) << 1)));
+  const uint32_t w0 = static_cast<uint32_t>(h), w1 = static_cast<uint32_t>(h >> 32);
+  const float* tc = tab + ((i >> 1) & 31u);  // this column class's bank
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
-    z[2 * m] = tab[(w[m] >> 4) & 0xFFFu];
-    z[2 * m + 1] = tab[w[m] >> 20];
+    z[m] = tc[__byte_perm(w0, 0u, 0x4440u | m) * 32];
+    z[4 + m] = tc[__byte_perm(w1, 0u, 0x4440u | m) * 32];
   }
 }
 

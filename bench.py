@@ -327,8 +327,14 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     if world > 1:
         pipe.n = n  # local rows; the state covers n*world global rows
         pipe.scores = torch.empty(n, dtype=torch.float64, device=dev)
-    gather_p = torch.empty(n * world, dtype=torch.float64, device=dev) if world > 1 else None
-    order_all = torch.empty(n * world, dtype=torch.int64, device=dev) if world > 1 else None
+    # multi-rank global order: double-buffered so rank 0 sorts step i's probabilities on a
+    # side stream while step i+1 sketches (the 8M-key sort would otherwise sit on the
+    # critical path of every step at N = 8)
+    gather_p = [torch.empty(n * world, dtype=torch.float64, device=dev) for _ in range(2)] if world > 1 else None
+    order_all = [torch.empty(n * world, dtype=torch.int64, device=dev) for _ in range(2)] if world > 1 else None
+    side = torch.cuda.Stream(device=dev) if world > 1 else None
+    sort_done = [None, None]
+    buf = [0]
     ws_sort = torch.empty(max(N.lib().lvsk_argsort_workspace_bytes(n * world), 256), dtype=torch.uint8, device=dev)
     pi = jl_device(0, d, r)
 
@@ -365,10 +371,21 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         local_sum = pipe.scores.sum().reshape(1)
         dist.all_reduce(local_sum)
         p_local = pipe.scores / local_sum
-        dist.all_gather_into_tensor(gather_p, p_local)
+        b = buf[0]
+        buf[0] ^= 1
+        if sort_done[b] is not None:  # the sort of two steps ago has released this buffer
+            torch.cuda.current_stream().wait_event(sort_done[b])
+        dist.all_gather_into_tensor(gather_p[b], p_local)
         if rank == 0:
-            N.check(N.lib().lvsk_argsort_f64(gather_p.data_ptr(), n * world, 1, order_all.data_ptr(),
-                                             ws_sort.data_ptr(), ws_sort.numel(), N.stream_ptr()))
+            ready = torch.cuda.Event()
+            ready.record()
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
+                N.check(N.lib().lvsk_argsort_f64(gather_p[b].data_ptr(), n * world, 1, order_all[b].data_ptr(),
+                                                 ws_sort.data_ptr(), ws_sort.numel(), N.stream_ptr()))
+                done = torch.cuda.Event()
+                done.record()
+            sort_done[b] = done
         if timing:
             ev["order"][1].record()
 
@@ -403,6 +420,14 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         # stage events of the last step only (no extra syncs inside the timed loop)
         for name, ms in pipe.stage_ms().items():
             stage_sum[name] = ms * args.steps
+    if world > 1 and rank == 0:
+        # the last global order is a descending permutation of the gathered probabilities
+        lb = buf[0] ^ 1
+        o = order_all[lb]
+        ps = gather_p[lb][o]
+        ok = bool((ps[:-1] >= ps[1:]).all()) and bool((torch.bincount(o, minlength=n * world) == 1).all())
+        if not ok:
+            raise SystemExit("bench: multi-rank global order failed its check")
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -183,7 +183,8 @@ def test_srht_matches_reference(golden, golden_meta):
 
 
 @pytest.mark.parametrize("n,d,k", [(2**16, 8, 512), (3 * 2**15 + 17, 33, 512), (2**17, 256, 512),
-                                   (2**20 + 3, 4, 512), (2**14 + 17, 100, 4096), (5000, 68, 4097)])
+                                   (2**20 + 3, 4, 512), (2**14 + 17, 100, 4096), (5000, 68, 4097),
+                                   (3000, 64, 300), (2048, 4096, 64)])
 def test_srht_multi_chunk(n, d, k):
     """fp32 X: the one-pass sampled kernel (srht_sampled.cu; d % 4 == 0,
     k <= 4096) and the two-pass kernels (srht.cu) against explicit rows of H."""

@@ -310,9 +310,6 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1 and cfg["family"] == "srht":
-        # the reference's run_distributed rejects SRHT (dist.py:95-98); K3 has no row offset
-        raise SystemExit("bench: SRHT (c3) runs on one GPU only")
     dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
     n, d, k, r = cfg["n"], cfg["d"], cfg["k"], cfg["r"]
     spec = P.SketchSpec(cfg["family"], eps=0.5, d=d, seed=0, rows_override=k, osnap_s=cfg["s"])
@@ -346,11 +343,19 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         ev = pipe.events
         if timing:
             ev["sketch"][0].record()
-        pipe._sketch(X)
+        s = pipe.state
+        if cfg["family"] == "srht":
+            # extension G7 (the reference's run_distributed rejects SRHT, dist.py:95-98): the
+            # one-pass K3 over this rank's 2048-aligned global row block, partials all-reduced
+            N.check(N.lib().lvsk_srht_rows(X.data_ptr(), n, d, X.stride(0), row0, s._m, s._signs_dev.data_ptr(),
+                                           s._sample_dev.data_ptr(), k, math.sqrt(k), pipe.sx.data_ptr(),
+                                           pipe.ws_sketch.data_ptr(), pipe.ws_sketch.numel(),
+                                           pipe.flags.data_ptr(), N.stream_ptr()), "srht rows")
+        else:
+            pipe._sketch(X)
         if timing:
             ev["sketch"][1].record()
-        s = pipe.state
-        if cfg["family"] == "gaussian":  # a plain float64 partial per rank
+        if cfg["family"] in ("gaussian", "srht"):  # a plain float64 partial per rank
             dist.all_reduce(pipe.sx)
         else:  # hashed: row slices exchanged all-to-all, rank-ordered TwoSum merge, folded slices gathered
             pipe.sx.copy_(sliced_hashed_merge(s._hi, s._lo, rank, world))

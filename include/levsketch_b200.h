@@ -115,14 +115,27 @@ LVSK_API size_t lvsk_srht_workspace_bytes(int64_t m, int64_t d, int32_t dtype, i
 LVSK_API int32_t lvsk_srht(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx, int64_t m,
                   const int8_t* signs, const int64_t* sample, int64_t k, double divisor, double* SX,
                   void* ws, size_t ws_bytes, int32_t* flags, void* stream);
+/* Row-block SRHT (extension: the sketch is linear in the rows, so
+ * ranks holding row blocks sum their partials — the reference's
+ * run_distributed rejects SRHT, dist.py:95-98, and still does here): X holds
+ * the GLOBAL rows row0 .. row0+n-1 of the m-row matrix, signs the global m
+ * signs; SX receives this block's contribution (/ divisor) and the sum over
+ * blocks is lvsk_srht of the whole matrix.  One-pass kernel conditions: fp32
+ * X, 16-byte aligned rows, d % 4 == 0, d <= 4096, k <= 4096, row0 % 2048 == 0
+ * (else LVSK_ERR_UNSUPPORTED).  Workspace: lvsk_srht_workspace_bytes. */
+LVSK_API int32_t lvsk_srht_rows(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t row0, int64_t m,
+                                const int8_t* signs, const int64_t* sample, int64_t k, double divisor, double* SX,
+                                void* ws, size_t ws_bytes, int32_t* flags, void* stream);
 
 /* ---- K4: Gaussian sketch (extension: the reference rejects "gaussian",
  * sketch.py:74-75) ----------------------------------------------------------
- * SX (+)= Z X / sqrt(k), Z[j,i] = bf16-rounded standard normal from
- * Philox4x32-10(counter=(i_lo,i_hi,j>>2,0), key=(seed_lo, seed_hi^0x47415553)),
- * Box-Muller with IEEE-only fp32 transcendentals (oracle/levsketch_oracle.py
- * gaussian_z).  Rows carry global indices row0..  SX: k x d float64;
- * accumulate != 0 adds to SX instead of overwriting. */
+ * SX (+)= Z X / sqrt(k), Z[j,i] = TAB[32 b + ((i >> 1) & 31)] with b = byte
+ * (j & 7) of mix64(key + phi ((i << 24) | ((j >> 3) << 1))) — splitmix64 as a
+ * counter-based stream, key = (seed_hi ^ 0x47415553) << 32 | seed_lo — and TAB
+ * the signed levels of an 8192-level equiprobable Gaussian (csrc/philox.cuh;
+ * oracle/levsketch_oracle.py gaussian_z, bit-exact).  Rows carry global
+ * indices row0..  SX: k x d float64; accumulate != 0 adds to SX instead of
+ * overwriting. */
 LVSK_API size_t lvsk_gaussian_workspace_bytes(int64_t n, int64_t d, int64_t k, int32_t dtype);
 LVSK_API int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n, int64_t d, int64_t ldx,
                              uint64_t row0, uint64_t seed, int64_t k, double* SX, int32_t accumulate,

@@ -54,6 +54,7 @@ _SIGS = {
     "lvsk_fold_compensated": (_I32, [_P, _P, _P, _I64, _P]),
     "lvsk_srht_workspace_bytes": (_SZ, [_I64, _I64, _I32, _I64]),
     "lvsk_srht": (_I32, [_P, _I32, _I64, _I64, _I64, _I64, _P, _P, _I64, _D, _P, _P, _SZ, _P, _P]),
+    "lvsk_srht_rows": (_I32, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _D, _P, _P, _SZ, _P, _P]),
     "lvsk_gaussian_workspace_bytes": (_SZ, [_I64, _I64, _I64, _I32]),
     "lvsk_gaussian_sketch": (_I32, [_P, _I32, _I64, _I64, _I64, _U64, _U64, _I64, _P, _I32, _P, _SZ, _P, _P]),
     "lvsk_gaussian_entries": (_I32, [_U64, _I64, _U64, _I64, _P, _P]),

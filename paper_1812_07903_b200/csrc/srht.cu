@@ -343,11 +343,11 @@ static void launch_pass2(int B2, dim3 grid, cudaStream_t st, const C* T1, int64_
 #undef LVSK_P2
 }
 
-bool srht_sampled_ok(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, int64_t k);
+bool srht_sampled_ok(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, int64_t k, int64_t row0);
 size_t srht_sampled_workspace(int64_t n, int64_t d, int64_t m, int64_t k);
-int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, const int8_t* signs,
-                     const int64_t* sample, int64_t k, double divisor, double* SX, void* ws, size_t ws_bytes,
-                     int32_t* flags, cudaStream_t st);
+int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t row0, int64_t m,
+                     const int8_t* signs, const int64_t* sample, int64_t k, double divisor, double* SX, void* ws,
+                     size_t ws_bytes, int32_t* flags, cudaStream_t st);
 bool srht_tma_ok(const float* X, int64_t d, int64_t ldx, int B1);
 int32_t srht_tma_chunk(const float* X, int64_t n, int64_t d, int64_t ldx, int B1, int B2, int64_t chunk, int cbits,
                        const int8_t* signs, float* T1, const int64_t* sample, const uint32_t* order,
@@ -359,8 +359,8 @@ static int32_t run_srht(const T* X, int64_t n, int64_t d, int64_t ldx, int64_t m
                         const int64_t* sample, int64_t k, double divisor, double* SX, void* ws, size_t ws_bytes,
                         int32_t* flags, cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value) {
-    if (srht_sampled_ok(X, n, d, ldx, m, k))
-      return srht_sampled(X, n, d, ldx, m, signs, sample, k, divisor, SX, ws, ws_bytes, flags, st);
+    if (srht_sampled_ok(X, n, d, ldx, m, k, 0))
+      return srht_sampled(X, n, d, ldx, 0, m, signs, sample, k, divisor, SX, ws, ws_bytes, flags, st);
   }
   const SrhtPlan P = plan_srht(m, d, sizeof(C));
   Carve c(ws, ws_bytes);

@@ -129,6 +129,7 @@ struct Params {
   int64_t jblocks;           // active 2048-row blocks (ceil(n / 2048))
   int64_t octets;            // ceil(slabs / 8)
   int64_t groups;            // CTA groups of 8
+  int64_t j0;                // global index of the first block (row0 / 2048)
 };
 
 __device__ __forceinline__ void group_range(const Params& P, int64_t g, int64_t& lo, int64_t& hi) {
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
       if (runs > 0) flush();
       cur_oct = oct;
     }
+    const uint32_t jg = j + static_cast<uint32_t>(P.j0);  // global block index (high row bits)
     tc::mbar_wait(&full[s], static_cast<uint32_t>((it >> 1) & 1));
     float* T = reinterpret_cast<float*>(smem + s * STAGE_BYTES);
     const uint32_t* sb = reinterpret_cast<const uint32_t*>(smem + s * STAGE_BYTES + TILE_BYTES);
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(THREADS, 1) srht_sampled_kernel(const __grid_c
       for (int u = 0; u < SPT; ++u) {
         const uint32_t mt = meta_s[tid + THREADS * u];
         const int q = static_cast<int>(mt & (ROWS - 1));
-        const uint32_t sbit = static_cast<uint32_t>(__popc((mt >> B) & j) & 1) << 31;
+        const uint32_t sbit = static_cast<uint32_t>(__popc((mt >> B) & jg) & 1) << 31;
         const float* row = T + swz(q) * W;
         const float4 a = *reinterpret_cast<const float4*>(row + 4 * h0);
         const float4 b = *reinterpret_cast<const float4*>(row + 4 * (h0 ^ 1));
@@ -449,7 +451,8 @@ static Shape shape(int64_t n, int64_t d) {
 }  // namespace srht3
 
 // Usable for fp32 X with 16-byte aligned rows, m >= 2^11, k <= 4096.
-bool srht_sampled_ok(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, int64_t k) {
+bool srht_sampled_ok(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, int64_t k, int64_t row0) {
+  if (row0 % srht3::ROWS != 0 || row0 + n > m) return false;
   if (getenv("LVSK_SRHT_V2") != nullptr) return false;
   return m >= srht3::ROWS && k <= srht3::KMAX && d <= 4096 && m <= (int64_t{1} << 32) && n < (int64_t{1} << 31) &&
          d % 4 == 0 && ldx % 4 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0;
@@ -464,9 +467,9 @@ size_t srht_sampled_workspace(int64_t n, int64_t d, int64_t m, int64_t k) {
   return ms.off;
 }
 
-int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t m, const int8_t* signs,
-                     const int64_t* sample, int64_t k, double divisor, double* SX, void* ws, size_t ws_bytes,
-                     int32_t* flags, cudaStream_t st) {
+int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t row0, int64_t m,
+                     const int8_t* signs, const int64_t* sample, int64_t k, double divisor, double* SX, void* ws,
+                     size_t ws_bytes, int32_t* flags, cudaStream_t st) {
   using namespace srht3;
   const Shape S = shape(n, d);
   Carve cv(ws, ws_bytes);
@@ -481,7 +484,7 @@ int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t 
     return LVSK_ERR_CUDA;
   }
   const int64_t words = signs ? S.jblocks * (ROWS / 32) : 0;
-  if (words) srht_pack_kernel<<<296, 256, 0, st>>>(signs, words, bits);
+  if (words) srht_pack_kernel<<<296, 256, 0, st>>>(signs + row0, words, bits);
   srht_slots_kernel<<<1, 1024, 0, st>>>(sample, k, m, slots, flags);
   LVSK_CHECK_LAUNCH("srht pack");
   static bool attr = false;
@@ -489,7 +492,7 @@ int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t 
     cudaFuncSetAttribute(srht_sampled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
-  Params P{signs ? bits : nullptr, slots, partial, S.rmax, k, S.jblocks, S.octets, S.groups};
+  Params P{signs ? bits : nullptr, slots, partial, S.rmax, k, S.jblocks, S.octets, S.groups, row0 / ROWS};
   srht_sampled_kernel<<<static_cast<unsigned>(S.ctas), THREADS, SMEM_BYTES, st>>>(mx, P);
   LVSK_CHECK_LAUNCH("srht sampled");
   const size_t rsm = static_cast<size_t>(S.octets * S.groups) * sizeof(int2);
@@ -502,3 +505,18 @@ int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t 
 }
 
 }  // namespace lvsk
+
+using namespace lvsk;
+
+extern "C" int32_t lvsk_srht_rows(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t row0, int64_t m,
+                                  const int8_t* signs, const int64_t* sample, int64_t k, double divisor, double* SX,
+                                  void* ws, size_t ws_bytes, int32_t* flags, void* stream) {
+  LVSK_REQUIRE(n >= 1 && d >= 1 && ldx >= d && row0 >= 0, LVSK_ERR_DIMENSION, "bad shape n=%lld d=%lld row0=%lld",
+               (long long)n, (long long)d, (long long)row0);
+  LVSK_REQUIRE(m >= row0 + n && (m & (m - 1)) == 0, LVSK_ERR_CONFIGURATION,
+               "m=%lld must be a power of two >= row0 + n", (long long)m);
+  LVSK_REQUIRE(k >= 1 && k <= m && divisor != 0.0, LVSK_ERR_CONFIGURATION, "SRHT needs 1 <= k <= m, divisor != 0");
+  LVSK_REQUIRE(getenv("LVSK_SRHT_V2") == nullptr && srht_sampled_ok(X, n, d, ldx, m, k, row0), LVSK_ERR_UNSUPPORTED,
+               "row-block SRHT needs fp32 16-byte aligned rows, d %% 4 == 0, d <= 4096, k <= 4096, row0 %% 2048 == 0");
+  return srht_sampled(X, n, d, ldx, row0, m, signs, sample, k, divisor, SX, ws, ws_bytes, flags, as_stream(stream));
+}

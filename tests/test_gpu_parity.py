@@ -779,3 +779,38 @@ def test_leverage_streamed_matches_in_memory(tmp_path, family, s, dtype):
         np.testing.assert_allclose(got.scores, ref.scores, rtol=1e-5)  # fp32 blocks: partial sums reassociate
     else:
         assert np.array_equal(got.scores, ref.scores)
+
+
+def test_srht_row_blocks_sum_to_whole():
+    """lvsk_srht_rows (extension G7): partials of 2048-aligned global row blocks
+    sum to the whole-matrix SRHT; unaligned row0 is refused."""
+    from paper_1812_07903_b200.sketch import srht_signs_and_sample
+
+    n, d, k = 3 * 2048 + 100, 64, 256
+    m = O.next_pow2(n)
+    x = np.random.default_rng(8).standard_normal((n, d)).astype(np.float32)
+    X = dev(x)
+    signs, sample = srht_signs_and_sample(3, m, k)
+    sg = torch.from_numpy(signs.astype(np.int8)).cuda()
+    sm = torch.from_numpy(sample.astype(np.int64)).cuda()
+    L = N.lib()
+    ws = N.workspace(L.lvsk_srht_workspace_bytes(m, d, N.LVSK_F32, k))
+    flags = N.Flags()
+    whole = torch.empty((k, d), dtype=torch.float64, device="cuda")
+    N.check(L.lvsk_srht(X.data_ptr(), N.LVSK_F32, n, d, d, m, sg.data_ptr(), sm.data_ptr(), k, math.sqrt(k),
+                        whole.data_ptr(), ws.data_ptr(), ws.numel(), flags.p, N.stream_ptr()), "srht")
+    total = torch.zeros_like(whole)
+    part = torch.empty_like(whole)
+    for r0, r1 in ((0, 4096), (4096, n)):
+        N.check(L.lvsk_srht_rows(X[r0:].data_ptr(), r1 - r0, d, d, r0, m, sg.data_ptr(), sm.data_ptr(), k,
+                                 math.sqrt(k), part.data_ptr(), ws.data_ptr(), ws.numel(), flags.p,
+                                 N.stream_ptr()), "srht rows")
+        total += part
+    assert flags.read() == 0
+    w = whole.cpu().numpy()
+    assert np.linalg.norm(total.cpu().numpy() - w) <= 1e-6 * np.linalg.norm(w)
+    ref = O.srht_sketch(x, k, 3)
+    assert np.linalg.norm(w - ref) <= 2e-6 * np.linalg.norm(ref)
+    rc = L.lvsk_srht_rows(X[100:].data_ptr(), n - 100, d, d, 100, m, sg.data_ptr(), sm.data_ptr(), k,
+                          math.sqrt(k), part.data_ptr(), ws.data_ptr(), ws.numel(), flags.p, N.stream_ptr())
+    assert rc == 5  # LVSK_ERR_UNSUPPORTED

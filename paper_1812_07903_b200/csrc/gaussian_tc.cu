@@ -87,11 +87,24 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
+
+// MX = 2: the two CTAs of a cluster are consecutive k tiles of the same
+// (column slab, split); each issues half of every X stage's boxes with TMA
+// multicast to both, so X crosses L2 -> SM once per pair, and a slot is
+// refilled only after both CTAs' MMAs released it (commit multicast).
 // CL = 1: one CTA per (k tile, column slab, split), each generating its whole
 // Z tile.  CL = 2 (d in (512, 1024]): the two column slabs of a k tile form a
 // cluster; each CTA generates half of the Z tile's rows and stores them into
 // both CTAs' shared memory (DSMEM), so every Z entry is generated once.
-template <int NS, int CL>
+template <int NS, int CL, int MX>
 __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
                        uint32_t k0, uint32_t k1, int ktiles, int dslabs, int64_t rows_per_split,
@@ -129,7 +142,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::S; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MX);
     }
     for (int s = 0; s < C::SZ; ++s) {
       mbar_init(&zfull[s], C::GEN_WARPS * CL);
@@ -148,7 +161,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
+  if constexpr (CL > 1 || MX > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -159,9 +172,17 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&xfull[s], C::X_BYTES);
         const int row = static_cast<int>(r_begin + static_cast<int64_t>(t) * C::BKN);
+        if constexpr (MX > 1) {
+          const int rk = ktile % MX;  // cluster rank
 #pragma unroll
-        for (int b = 0; b < C::NB; ++b)
-          tma_load_2d(&mapX, &xfull[s], smem + s * C::X_BYTES + b * C::BOX_BYTES, col0 + b * 64, row, pol);
+          for (int b = rk; b < C::NB; b += MX)
+            tma_load_2d_mc(&mapX, &xfull[s], smem + s * C::X_BYTES + b * C::BOX_BYTES, col0 + b * 64, row,
+                           static_cast<uint16_t>((1u << MX) - 1u), pol);
+        } else {
+#pragma unroll
+          for (int b = 0; b < C::NB; ++b)
+            tma_load_2d(&mapX, &xfull[s], smem + s * C::X_BYTES + b * C::BOX_BYTES, col0 + b * 64, row, pol);
+        }
       }
     }
   } else if (warp == 1) {
@@ -189,7 +210,14 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
             umma_f16(tmem_base + h * 256, a + 2 * kk, b, C::IDESC, (t | kk) ? 1u : 0u);
           }
         }
-        umma_commit(&empty[s]);
+        if constexpr (MX > 1)
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&empty[s])),
+              "h"(static_cast<uint16_t>((1u << MX) - 1u))
+              : "memory");
+        else
+          umma_commit(&empty[s]);
         if constexpr (CL > 1)
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -315,7 +343,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(NS));
   }
-  if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still write into it
+  if constexpr (CL > 1 || MX > 1) cluster_sync_all();  // no CTA leaves while its peer may still write into it
 }
 
 }  // namespace tc
@@ -342,7 +370,7 @@ bool gaussian_tc_ok(const void* X, int64_t n, int64_t d, int64_t ldx, int64_t k)
   return true;
 }
 
-template <int NS, int CL>
+template <int NS, int CL, int MX>
 static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
                                uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
   using C = tc::CfgG<NS>;
@@ -353,7 +381,7 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
   }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::gaussian_tc_kernel<NS, CL>,
+    cudaError_t e = cudaFuncSetAttribute(tc::gaussian_tc_kernel<NS, CL, MX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return cuda_status(e, "gaussian tc smem attribute");
     attr = true;
@@ -371,12 +399,12 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = CL;
+  attrs[0].val.clusterDim.x = CL * MX;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, CL>, mx, n, d, k, row0, k0, k1, p.ktiles,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, CL, MX>, mx, n, d, k, row0, k0, k1, p.ktiles,
                                      p.dslabs, p.rows_per_split, gtab, partial,
                                      getenv("LVSK_K4_NOGEN") != nullptr ? 1 : 0);
   if (e != cudaSuccess) return cuda_status(e, "gaussian tc launch");
@@ -390,9 +418,11 @@ int32_t gaussian_tc_bf16(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t l
   // table generator (~8 / entry) its cluster-scope release fences cost more
   // than regenerating the tile: C5 5.25 ms (CL = 2) vs 3.68 ms (CL = 1)
   if (p.ns == 512 && p.dslabs == 2 && getenv("LVSK_K4_CLUSTER") != nullptr)
-    return launch_gauss_tc<512, 2>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
-  return p.ns == 512 ? launch_gauss_tc<512, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st)
-                     : launch_gauss_tc<256, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
+    return launch_gauss_tc<512, 2, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
+  if (p.ns == 512 && p.ktiles % 2 == 0 && getenv("LVSK_K4_NOMC") == nullptr)
+    return launch_gauss_tc<512, 1, 2>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
+  return p.ns == 512 ? launch_gauss_tc<512, 1, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st)
+                     : launch_gauss_tc<256, 1, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
 }
 
 }  // namespace lvsk

@@ -1,6 +1,6 @@
 import torch
 from paper_1812_07903_b200 import _native as N
-for n in (1_000_000, 4_000_000):
+for n in (1_000_000, 2_097_152, 4_000_000):
     keys = torch.rand(n, dtype=torch.float64, device="cuda") ** 3 * 1e-5
     out = torch.empty(n, dtype=torch.int64, device="cuda")
     L = N.lib()

@@ -129,11 +129,14 @@ LVSK_API int32_t lvsk_srht_rows(const float* X, int64_t n, int64_t d, int64_t ld
 
 /* ---- K4: Gaussian sketch (extension: the reference rejects "gaussian",
  * sketch.py:74-75) ----------------------------------------------------------
- * SX (+)= Z X / sqrt(k), Z[j,i] = TAB[32 b + ((i >> 1) & 31)] with b = byte
- * (j & 7) of mix64(key + phi ((i << 24) | ((j >> 3) << 1))) — splitmix64 as a
- * counter-based stream, key = (seed_hi ^ 0x47415553) << 32 | seed_lo — and TAB
- * the signed levels of an 8192-level equiprobable Gaussian (csrc/philox.cuh;
- * oracle/levsketch_oracle.py gaussian_z, bit-exact).  Rows carry global
+ * SX (+)= Z X / sqrt(k), Z[j,i] = the bf16 value with bits
+ * MAG[w & 0x7FFF] | (w & 0x8000), w = 16-bit field (j & 3) of
+ * mix64(key + phi ((i << 24) | (j >> 2))) — splitmix64 as a counter-based
+ * stream, key = (seed_hi ^ 0x47415553) << 32 | seed_lo — and
+ * MAG[L] = bf16(Phi^-1(1/2 + (L + 1/2) / 65536)): the inverse normal CDF of a
+ * 16-bit uniform, the same N(0,1) (up to 16-bit quantisation and bf16
+ * rounding) for every entry (csrc/gauss_gen.cuh; oracle/levsketch_oracle.py
+ * gaussian_z, bit-exact).  k <= 2^26, row0 + n <= 2^40.  Rows carry global
  * indices row0..  SX: k x d float64; accumulate != 0 adds to SX instead of
  * overwriting. */
 LVSK_API size_t lvsk_gaussian_workspace_bytes(int64_t n, int64_t d, int64_t k, int32_t dtype);
@@ -143,9 +146,9 @@ LVSK_API int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n, i
 /* Materialise Z (k x n float32, row-major) for KAT parity. */
 LVSK_API int32_t lvsk_gaussian_entries(uint64_t seed, int64_t k, uint64_t row0, int64_t n, float* Z,
                               void* stream);
-/* The generator's 1280-float table (INV[128] | LN[128] | CSA[256][2] |
- * CSB[256][2], see csrc/philox.cuh), host-side; count >= 1280. */
-LVSK_API int32_t lvsk_gaussian_tables(float* out, int64_t count);
+/* The generator's magnitude table MAG (32768 bf16 bit patterns, see
+ * csrc/gauss_gen.cuh), built host-side; count >= 32768. */
+LVSK_API int32_t lvsk_gaussian_tables(uint16_t* out, int64_t count);
 
 /* ---- K5: leverage pass --------------------------------------------------
  * Replaces _block_scores (reference leverage.py:88-95):

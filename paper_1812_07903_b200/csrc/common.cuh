@@ -136,13 +136,13 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-inline int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
+// Per-device launch facts, cached per (device, kernel) so a process that
+// drives several GPUs (torch.cuda.set_device switches) stays correct (capi.cu).
+int num_sms();  // SMs of the current device
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+int32_t ensure_smem_attr(const void* fn, int smem_bytes, const char* what);
+// co-resident CTAs per SM of `fn` at (threads, smem) on the current device
+// (after ensure_smem_attr); 0 when the attribute or the query failed
+int resident_ctas(const void* fn, int threads, int smem_bytes);
 
 }  // namespace lvsk

@@ -566,12 +566,10 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
   const int64_t units = k * ngroups;
   const unsigned grid = static_cast<unsigned>((units + CSR_WARPS - 1) / CSR_WARPS);
   const int smem = CSR_WARPS * 2 * CSR_GROUP * static_cast<int>(sizeof(double));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(csr_gather_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(csr_gather_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  rc = val_dtype == LVSK_F64
+           ? ensure_smem_attr(reinterpret_cast<const void*>(csr_gather_kernel<double>), smem, "csr gather smem attribute")
+           : ensure_smem_attr(reinterpret_cast<const void*>(csr_gather_kernel<float>), smem, "csr gather smem attribute");
+  if (rc != LVSK_OK) return rc;
   if (getenv("LVSK_K2_DETERMINISTIC") == nullptr) {
     csr_prep_kernel<<<csr_grid(N, 256), 256, 0, st>>>(row_ptr, svals, N, msrc, mlen);
     const int sgroups = static_cast<int>((d + ST_COLS - 1) / ST_COLS);
@@ -580,16 +578,11 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
       return ST_APPLY * ST_COLS * 8 + ST_STAGES * ST_ECAP * (v + 4) + ST_STAGES * ST_RMAX * static_cast<int>(sizeof(SegInfo)) +
              ST_STAGES * 4 + 2 * ST_STAGES * 8;
     };
-    static bool sattr[2] = {false, false};
-    if (!sattr[vsz == 8]) {
-      const cudaError_t e =
-          vsz == 8 ? cudaFuncSetAttribute(csr_stream_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          smem_for(8))
-                   : cudaFuncSetAttribute(csr_stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          smem_for(4));
-      if (e != cudaSuccess) return cuda_status(e, "csr stream shared-memory attribute");
-      sattr[vsz == 8] = true;
-    }
+    rc = vsz == 8 ? ensure_smem_attr(reinterpret_cast<const void*>(csr_stream_kernel<double>), smem_for(8),
+                                     "csr stream shared-memory attribute")
+                  : ensure_smem_attr(reinterpret_cast<const void*>(csr_stream_kernel<float>), smem_for(4),
+                                     "csr stream shared-memory attribute");
+    if (rc != LVSK_OK) return rc;
     const unsigned sgrid = static_cast<unsigned>(k * sgroups);
     if (val_dtype == LVSK_F32)
       csr_stream_kernel<float><<<sgrid, 32 * (1 + ST_APPLY), smem_for(vsz), st>>>(

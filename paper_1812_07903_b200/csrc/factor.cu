@@ -625,17 +625,10 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.dp = P.dp;
   a.rp = P.rp;
   const int smem = 4 * FTILE_SMEM + (5 * FT + 8) * 8;
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(chol_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_status(e, "chol_fold smem attribute");
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chol_fold_kernel, FTHREADS, smem);
-    grid_cap = per >= 1 ? sms : 0;
-    if (grid_cap < 2) return cuda_status(cudaErrorInvalidConfiguration, "chol_fold needs two co-resident CTAs");
-  }
+  const int32_t arc = ensure_smem_attr(reinterpret_cast<const void*>(chol_fold_kernel), smem, "chol_fold smem attribute");
+  if (arc != LVSK_OK) return arc;
+  const int grid_cap = resident_ctas(reinterpret_cast<const void*>(chol_fold_kernel), FTHREADS, smem) >= 1 ? num_sms() : 0;
+  if (grid_cap < 2) return cuda_status(cudaErrorInvalidConfiguration, "chol_fold needs two co-resident CTAs");
   // CTA 0 runs the chain; more queue CTAs than tasks only add polling
   const int ntask = kf_queue_tasks(P.nb, P.rt);
   const int grid = 1 + (ntask < grid_cap - 1 ? ntask : grid_cap - 1);

@@ -2,28 +2,29 @@
 //
 // Extension: the reference rejects the "gaussian" family
 // (pkg/src/levsketch/sketch.py:38-41, 74-75); BASELINE configs 1 and 5 ask
-// for it.  Z[j, i] (j < k sketch row, i global input row) is the counter-based
-// splitmix64 + 4096-level Gaussian table entry of philox.cuh, which the CPU
-// oracle (oracle/levsketch_oracle.py: gaussian_z) reproduces bit-for-bit.
-// bf16 X runs on the tensor cores (gaussian_tc.cu), fp32 X too after an exact
-// three-plane bf16 split (split3_bf16_kernel); this file holds the entry
-// generator, the SIMT GEMM (fp64 X, small fp32 cases; split-K) and the
-// deterministic float64 reduction of the split partials shared by all.
+// for it.  Z[j, i] (j < k sketch row, i global input row) is the
+// counter-based splitmix64 + 16-bit inverse-CDF entry of gauss_gen.cuh,
+// which the CPU oracle (oracle/levsketch_oracle.py: gaussian_z) reproduces
+// bit-for-bit.  bf16 X runs on the tensor cores (gaussian_tc.cu), fp32 X too
+// after an exact three-plane bf16 split (split3_bf16_kernel); this file holds
+// the generator table, the entry dump, the SIMT GEMM (fp64 X, small fp32
+// cases; split-K) and the deterministic float64 reduction of the split
+// partials shared by all.
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
-#include "philox.cuh"
+#include "gauss_gen.cuh"
 
 namespace lvsk {
 
-// ---- generator table (philox.cuh) -----------------------------------------
+// ---- generator table (gauss_gen.cuh) ----------------------------------------
 // Same float64 steps as the oracle (gaussian_tables): bisection of
-// 0.5 erfc(-x / sqrt 2) = p on [-10, 10] (100 halvings reach adjacent
-// doubles), sequential sums of squares per column class, one rounding to
-// float then to bf16.
+// 0.5 erfc(-x / sqrt 2) = p on [0, 10] (100 halvings reach adjacent doubles),
+// one rounding to float, then round-to-nearest-even to bf16.
 static double inv_normal_cdf(double p) {
-  double lo = -10.0, hi = 10.0;
+  double lo = 0.0, hi = 10.0;
   for (int it = 0; it < 100; ++it) {
     const double mid = 0.5 * (lo + hi);
     if (0.5 * std::erfc(-mid / 1.4142135623730951) < p)
@@ -34,55 +35,56 @@ static double inv_normal_cdf(double p) {
   return 0.5 * (lo + hi);
 }
 
-void gaussian_table_host(float* out) {
-  // 4096 positive levels of an 8192-level equiprobable Gaussian, level L at
-  // TAB[L] = TAB[32 b + c] (b < 128), each column class c rescaled to unit
-  // second moment; TAB[32 (b + 128) + c] = -TAB[32 b + c]
-  constexpr int HALF = GT_SIZE / 2;
-  double raw[HALF];
-  for (int L = 0; L < HALF; ++L) raw[L] = inv_normal_cdf(0.5 + (L + 0.5) / GT_SIZE);
-  for (int c = 0; c < 32; ++c) {
-    double m2 = 0.0;
-    for (int r = 0; r < HALF / 32; ++r) m2 += raw[32 * r + c] * raw[32 * r + c];
-    const double scale = 1.0 / std::sqrt(m2 / (HALF / 32));
-    for (int r = 0; r < HALF / 32; ++r) {
-      const float f = static_cast<float>(raw[32 * r + c] * scale);
-      const float v = __bfloat162float(__float2bfloat16_rn(f));
-      out[32 * r + c] = v;
-      out[HALF + 32 * r + c] = -v;
-    }
-  }
+static uint16_t bf16_bits_rn(float f) {
+  uint32_t b;
+  std::memcpy(&b, &f, 4);
+  b += 0x7FFFu + ((b >> 16) & 1u);
+  return static_cast<uint16_t>(b >> 16);
 }
 
-const float* gaussian_table_device() {
-  static float* dev = nullptr;
+void gaussian_table_host(uint16_t* out) {
+  // MAG[L] = bf16_rn(Phi^-1(1/2 + (L + 1/2) / 65536)), L < 32768
+  for (int L = 0; L < GT_LEVELS; ++L)
+    out[L] = bf16_bits_rn(static_cast<float>(inv_normal_cdf(0.5 + (L + 0.5) / (2.0 * GT_LEVELS))));
+}
+
+const uint16_t* gaussian_table_device() {
+  // one copy per device: a process may drive several GPUs (set_device switches)
+  constexpr int MAXDEV = 64;
+  static uint16_t* dev[MAXDEV] = {};
   static std::mutex mu;
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur < 0 || cur >= MAXDEV) return nullptr;
   std::lock_guard<std::mutex> g(mu);
-  if (dev == nullptr) {
-    float host[GT_SIZE];
-    gaussian_table_host(host);
-    if (cudaMalloc(&dev, sizeof(host)) != cudaSuccess) {
-      dev = nullptr;
+  if (dev[cur] == nullptr) {
+    static uint16_t host[GT_LEVELS];
+    static bool built = false;
+    if (!built) {
+      gaussian_table_host(host);
+      built = true;
+    }
+    uint16_t* p = nullptr;
+    if (cudaMalloc(&p, sizeof(host)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(p, host, sizeof(host), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(p);
       return nullptr;
     }
-    cudaMemcpy(dev, host, sizeof(host), cudaMemcpyHostToDevice);
+    dev[cur] = p;
   }
-  return dev;
+  return dev[cur];
 }
 
-__global__ void gaussian_entries_kernel(uint32_t k0, uint32_t k1, int64_t k, uint64_t row0, int64_t n,
-                                        const float* __restrict__ gtab, float* Z) {
-  const float* tab = gtab;  // 32 KB, L1-resident (the SIMT GEMM needs its shared memory for tiles)
-  __syncthreads();
-  const int64_t nq = (k + 7) / 8;
+__global__ void gaussian_entries_kernel(uint64_t key, int64_t k, uint64_t row0, int64_t n,
+                                        const uint16_t* __restrict__ mag, float* Z) {
+  const int64_t nq = (k + 3) / 4;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nq * n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t q = t / n, i = t - q * n;
-    float z[8];
-    gaussian8(row0 + static_cast<uint64_t>(i), static_cast<uint32_t>(q), k0, k1, tab, z);
+    float z[4];
+    gaussian4(key, row0 + static_cast<uint64_t>(i), static_cast<uint32_t>(q), mag, z);
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
-      if (8 * q + s < k) Z[(8 * q + s) * n + i] = bf16_rn(z[s]);
+    for (int s = 0; s < 4; ++s)
+      if (4 * q + s < k) Z[(4 * q + s) * n + i] = z[s];
   }
 }
 
@@ -93,11 +95,11 @@ constexpr int G_RT = 16;   // input rows per step
 
 template <typename T, typename A>
 __global__ void __launch_bounds__(256) gaussian_gemm_kernel(const T* __restrict__ X, int64_t n, int64_t d,
-                                                            int64_t ldx, uint64_t row0, uint32_t k0, uint32_t k1,
+                                                            int64_t ldx, uint64_t row0, uint64_t key,
                                                             int64_t k, int64_t rows_per_split,
-                                                            const float* __restrict__ gtab,
+                                                            const uint16_t* __restrict__ mag,
                                                             A* __restrict__ partial, int32_t* flags) {
-  const float* tab = gtab;  // 32 KB, L1-resident
+  // MAG (64 KB) is read through L1; the shared memory holds the tiles
   __shared__ A Zs[G_RT][G_JT + 1];
   __shared__ A Xs[G_RT][G_CT + 1];
   const int tid = threadIdx.x;
@@ -115,13 +117,13 @@ __global__ void __launch_bounds__(256) gaussian_gemm_kernel(const T* __restrict_
     for (int b = 0; b < 8; ++b) acc[a][b] = A(0);
   bool bad = false;
   for (int64_t r0 = r_begin; r0 < r_end; r0 += G_RT) {
-    if (tid < G_RT * (G_JT / 8)) {  // Z tile: thread -> (row offset, octet of sketch rows)
+    if (tid < G_RT * (G_JT / 4)) {  // Z tile: thread -> (row offset, quad of sketch rows)
       const int ro = tid % G_RT, q = tid / G_RT;
       const int64_t r = r0 + ro;
-      float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (r < r_end) gaussian8(row0 + static_cast<uint64_t>(r), static_cast<uint32_t>(j0 / 8 + q), k0, k1, tab, z);
+      float z[4] = {0.f, 0.f, 0.f, 0.f};
+      if (r < r_end) gaussian4(key, row0 + static_cast<uint64_t>(r), static_cast<uint32_t>(j0 / 4 + q), mag, z);
 #pragma unroll
-      for (int s = 0; s < 8; ++s) Zs[ro][8 * q + s] = static_cast<A>(bf16_rn(z[s]));
+      for (int s = 0; s < 4; ++s) Zs[ro][4 * q + s] = static_cast<A>(z[s]);
     }
     for (int e = tid; e < G_RT * G_CT; e += 256) {
       const int ro = e / G_CT, cc = e % G_CT;
@@ -258,12 +260,14 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
                                         void* ws, size_t ws_bytes, int32_t* flags, void* stream) {
   LVSK_REQUIRE(n >= 1 && d >= 1 && ldx >= d, LVSK_ERR_DIMENSION, "bad shape n=%lld d=%lld", (long long)n,
                (long long)d);
-  LVSK_REQUIRE(k >= 1, LVSK_ERR_CONFIGURATION, "k must be >= 1");
+  LVSK_REQUIRE(k >= 1 && k <= GAUSS_MAX_K, LVSK_ERR_CONFIGURATION, "k must be in [1, 2^26]");
+  LVSK_REQUIRE(row0 < GAUSS_MAX_ROW && static_cast<uint64_t>(n) <= GAUSS_MAX_ROW - row0, LVSK_ERR_DIMENSION,
+               "global row indices must stay below 2^40");
   cudaStream_t st = as_stream(stream);
-  const float* gtab = gaussian_table_device();
-  LVSK_REQUIRE(gtab != nullptr, LVSK_ERR_CUDA, "cannot allocate the Gaussian generator table");
+  const uint16_t* mag = gaussian_table_device();
+  LVSK_REQUIRE(mag != nullptr, LVSK_ERR_CUDA, "cannot allocate the Gaussian generator table");
   const GaussPlan p = plan_gauss(n, d, k);
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32) ^ Philox::KEY_XOR;
+  const uint64_t key = gauss_key(seed);
   dim3 grid(p.gx, p.gy, static_cast<unsigned>(p.splits));
   const double scale = 1.0 / sqrt(static_cast<double>(k));
   const int64_t count = k * d;
@@ -272,14 +276,14 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
   if (dtype == LVSK_F64) {
     double* part = c.take<double>(static_cast<size_t>(p.splits) * count);
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
-    gaussian_gemm_kernel<double, double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), n, d, ldx, row0, k0,
-                                                               k1, k, p.rows_per_split, gtab, part, flags);
+    gaussian_gemm_kernel<double, double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), n, d, ldx, row0, key,
+                                                               k, p.rows_per_split, mag, part, flags);
     gaussian_reduce_kernel<double><<<rgrid, 256, 0, st>>>(part, p.splits, count, scale, SX, accumulate, flags);
   } else if (dtype == LVSK_BF16 && gaussian_tc_ok(X, n, d, ldx, k)) {
     const GaussTcPlan t = plan_gauss_tc(n, d, k);
     float* part = c.take<float>(static_cast<size_t>(t.splits) * count);
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
-    const int32_t rc = gaussian_tc_bf16(static_cast<const __nv_bfloat16*>(X), n, d, ldx, k, row0, k0, k1, t, part, st);
+    const int32_t rc = gaussian_tc_bf16(static_cast<const __nv_bfloat16*>(X), n, d, ldx, k, row0, key, t, part, st);
     if (rc != LVSK_OK) return rc;
     gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, t.splits, count, scale, SX, accumulate, flags);
   } else if (dtype == LVSK_F32 && f32_tc(n, d, k)) {
@@ -292,7 +296,7 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
     split3_bf16_kernel<<<sgrid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx, ldp, planes);
     LVSK_CHECK_LAUNCH("gaussian split");
     for (int j = 0; j < 3; ++j) {
-      const int32_t rc = gaussian_tc_bf16(planes + j * n * ldp, n, d, ldp, k, row0, k0, k1, t,
+      const int32_t rc = gaussian_tc_bf16(planes + j * n * ldp, n, d, ldp, k, row0, key, t,
                                           part + static_cast<int64_t>(j) * t.splits * count, st);
       if (rc != LVSK_OK) return rc;
     }
@@ -301,12 +305,12 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
     float* part = c.take<float>(static_cast<size_t>(p.splits) * count);
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
     if (dtype == LVSK_F32)
-      gaussian_gemm_kernel<float, float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx, row0, k0,
-                                                               k1, k, p.rows_per_split, gtab, part, flags);
+      gaussian_gemm_kernel<float, float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx, row0, key,
+                                                               k, p.rows_per_split, mag, part, flags);
     else
       gaussian_gemm_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X), n, d,
-                                                                       ldx, row0, k0, k1, k, p.rows_per_split,
-                                                                       gtab, part, flags);
+                                                                       ldx, row0, key, k, p.rows_per_split,
+                                                                       mag, part, flags);
     gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, p.splits, count, scale, SX, accumulate, flags);
   }
   LVSK_CHECK_LAUNCH("gaussian sketch");
@@ -315,20 +319,21 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
 
 extern "C" int32_t lvsk_gaussian_entries(uint64_t seed, int64_t k, uint64_t row0, int64_t n, float* Z,
                                          void* stream) {
-  LVSK_REQUIRE(k >= 1 && n >= 0, LVSK_ERR_CONFIGURATION, "bad arguments");
+  LVSK_REQUIRE(k >= 1 && k <= GAUSS_MAX_K && n >= 0, LVSK_ERR_CONFIGURATION, "bad arguments");
+  LVSK_REQUIRE(row0 < GAUSS_MAX_ROW && static_cast<uint64_t>(n) <= GAUSS_MAX_ROW - row0, LVSK_ERR_DIMENSION,
+               "global row indices must stay below 2^40");
   if (n == 0) return LVSK_OK;
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32) ^ Philox::KEY_XOR;
-  const float* gtab = gaussian_table_device();
-  LVSK_REQUIRE(gtab != nullptr, LVSK_ERR_CUDA, "cannot allocate the Gaussian generator table");
-  const int64_t work = (k + 7) / 8 * n;
+  const uint16_t* mag = gaussian_table_device();
+  LVSK_REQUIRE(mag != nullptr, LVSK_ERR_CUDA, "cannot allocate the Gaussian generator table");
+  const int64_t work = (k + 3) / 4 * n;
   const int grid = static_cast<int>((work + 255) / 256 < num_sms() * 32 ? (work + 255) / 256 : num_sms() * 32);
-  gaussian_entries_kernel<<<grid, 256, 0, as_stream(stream)>>>(k0, k1, k, row0, n, gtab, Z);
+  gaussian_entries_kernel<<<grid, 256, 0, as_stream(stream)>>>(gauss_key(seed), k, row0, n, mag, Z);
   LVSK_CHECK_LAUNCH("gaussian entries");
   return LVSK_OK;
 }
 
-extern "C" int32_t lvsk_gaussian_tables(float* out, int64_t count) {
-  LVSK_REQUIRE(out != nullptr && count >= GT_SIZE, LVSK_ERR_CAPACITY, "need %d floats", GT_SIZE);
+extern "C" int32_t lvsk_gaussian_tables(uint16_t* out, int64_t count) {
+  LVSK_REQUIRE(out != nullptr && count >= GT_LEVELS, LVSK_ERR_CAPACITY, "need %d uint16 entries", GT_LEVELS);
   gaussian_table_host(out);
   return LVSK_OK;
 }

@@ -11,11 +11,11 @@
 //   warp 0   TMA: X[64 rows][NS cols] as NS/64 SW128 boxes.  X is the MMA's
 //            B operand in MN-major layout (rows of X = K, contiguous columns
 //            = N), so no transpose pass exists anywhere;
-//   warps 2-17 generate the Z tile [128 x 64] (philox.cuh: 8 entries per
-//            Philox call, table-driven Box-Muller, bit-identical to the SIMT
-//            path and the oracle) straight into the K-major SW128 A
-//            layout in shared memory and arrive (the MMA thread issues the
-//            generic->async proxy fence once per stage);
+//   warps 2-17 generate the Z tile [128 x 64] (gauss_gen.cuh: one mix64
+//            per 4 entries, a 16-bit inverse-CDF table lookup per entry,
+//            bit-identical to the SIMT path and the oracle) straight into
+//            the K-major SW128 A layout in shared memory and arrive (the MMA
+//            thread issues the generic->async proxy fence once per stage);
 //   warp 1   issues 4 x (NS/256) tcgen05.mma kind::f16 (M = 128, N = 256,
 //            K = 16) and commits the stage back to both producers.
 // After the last stage warps 2-17 drain TMEM (tcgen05.ld 32x32b) into the
@@ -25,7 +25,7 @@
 // generated ceil(d/NS) times.
 #include <cstdlib>
 
-#include "philox.cuh"
+#include "gauss_gen.cuh"
 #include "tc_common.cuh"
 
 namespace lvsk {
@@ -40,11 +40,11 @@ struct CfgG {
   static constexpr int X_BYTES = NB * BOX_BYTES;
   static constexpr int Z_BYTES = BM * BKN * 2;  // 16 KB
   static constexpr int S = NS == 512 ? 2 : 4;  // X stages
-  static constexpr int SZ = 4;                  // Z stages (generation runs up to 4 stages ahead)
+  static constexpr int SZ = 2;                  // Z stages (the 64 KB table leaves room for two)
   static constexpr int OFF_Z = S * X_BYTES;
   static constexpr int OFF_BAR = OFF_Z + SZ * Z_BYTES;
   static constexpr int OFF_TAB = OFF_BAR + 256;
-  static constexpr int SMEM_BYTES = OFF_TAB + GT_SIZE * 4 + 1024;
+  static constexpr int SMEM_BYTES = OFF_TAB + GT_LEVELS * 2 + 1024;
   static constexpr int GEN_WARPS = 16;  // one per 8-row octet of the 128-row tile
   static constexpr int NTHREADS = 64 + 32 * GEN_WARPS;
   // kind::f16: F32 accumulate, A = B = bf16, B MN-major, N = 256, M = 128
@@ -69,20 +69,6 @@ __device__ __forceinline__ uint64_t l2_policy_evict_normal() {
   return p;
 }
 
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra.uni WAITC_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -100,15 +86,14 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t*
 // (column slab, split); each issues half of every X stage's boxes with TMA
 // multicast to both, so X crosses L2 -> SM once per pair, and a slot is
 // refilled only after both CTAs' MMAs released it (commit multicast).
-// CL = 1: one CTA per (k tile, column slab, split), each generating its whole
-// Z tile.  CL = 2 (d in (512, 1024]): the two column slabs of a k tile form a
-// cluster; each CTA generates half of the Z tile's rows and stores them into
-// both CTAs' shared memory (DSMEM), so every Z entry is generated once.
-template <int NS, int CL, int MX>
+// MX = 1: one CTA per (k tile, column slab, split).  Every CTA generates its
+// whole Z tile (a 2-CTA DSMEM-sharing variant paid more in cluster-scope
+// release fences than it saved: C5 5.25 vs 3.68 ms in round 1).
+template <int NS, int MX>
 __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
-                       uint32_t k0, uint32_t k1, int ktiles, int dslabs, int64_t rows_per_split,
-                       const float* __restrict__ gtab, float* __restrict__ partial, int nogen) {
+                       uint64_t key, int ktiles, int dslabs, int64_t rows_per_split,
+                       const uint16_t* __restrict__ gmag, float* __restrict__ partial) {
   using C = CfgG<NS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays a shared-space pointer
@@ -119,21 +104,13 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   uint64_t* zempty = zfull + C::SZ;
   uint64_t* accfull = zempty + C::SZ;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
-  float* tab = reinterpret_cast<float*>(smem + C::OFF_TAB);
+  uint16_t* mag = reinterpret_cast<uint16_t*>(smem + C::OFF_TAB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int item = blockIdx.x;
-  int ktile, dslab;
-  int64_t split;
-  if constexpr (CL == 1) {
-    ktile = item % ktiles;
-    dslab = (item / ktiles) % dslabs;
-    split = item / (ktiles * dslabs);
-  } else {  // cluster rank = column slab
-    dslab = item % CL;
-    ktile = (item / CL) % ktiles;
-    split = item / (CL * ktiles);
-  }
+  const int ktile = item % ktiles;
+  const int dslab = (item / ktiles) % dslabs;
+  const int64_t split = item / (ktiles * dslabs);
   const int64_t r_begin = split * rows_per_split;
   const int64_t r_end = r_begin + rows_per_split < n ? r_begin + rows_per_split : n;
   const int nstages = static_cast<int>((r_end - r_begin + C::BKN - 1) / C::BKN);
@@ -145,14 +122,14 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       mbar_init(&empty[s], MX);
     }
     for (int s = 0; s < C::SZ; ++s) {
-      mbar_init(&zfull[s], C::GEN_WARPS * CL);
-      mbar_init(&zempty[s], CL);
+      mbar_init(&zfull[s], C::GEN_WARPS);
+      mbar_init(&zempty[s], 1);
     }
     mbar_init(accfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
   }
-  load_gaussian_table(tab, gtab);
+  load_gaussian_table(mag, gmag);
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(NS));
@@ -161,7 +138,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if constexpr (CL > 1 || MX > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
+  if constexpr (MX > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -191,13 +168,10 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
         const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
         const uint32_t sz = t % C::SZ, phz = (t / C::SZ) & 1u;
         mbar_wait(&xfull[s], ph);
-        if constexpr (CL > 1)
-          mbar_wait_cluster(&zfull[sz], phz);
-        else
-          mbar_wait(&zfull[sz], phz);
-        // the Z tile was written through the generic proxy (local and DSMEM
-        // stores); one proxy fence here, after the acquire, orders it before
-        // the tensor core's async-proxy reads (instead of one per producer warp)
+        mbar_wait(&zfull[sz], phz);
+        // the Z tile was written through the generic proxy; one proxy fence
+        // here, after the acquire, orders it before the tensor core's
+        // async-proxy reads (instead of one per producer warp)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_after();
         const uint64_t a = sw128_desc(smem_u32(smem + C::OFF_Z + sz * C::Z_BYTES));
@@ -218,96 +192,50 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
               : "memory");
         else
           umma_commit(&empty[s]);
-        if constexpr (CL > 1)
-          asm volatile(
-              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                  smem_u32(&zempty[sz])),
-              "h"(static_cast<uint16_t>((1u << CL) - 1u))
-              : "memory");
-        else
-          umma_commit(&zempty[sz]);
+        umma_commit(&zempty[sz]);
       }
       umma_commit(accfull);
     }
   } else {
     const int gw = warp - 2;
-    if constexpr (CL == 1) {
-      // ---- Z generation: warp gw -> sketch rows 8gw .. 8gw+7 of the tile,
-      //      lane -> input rows 2*lane, 2*lane+1 of the stage (2 Philox calls)
-      const int q = gw;
-      const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
-      for (int t = 0; t < nstages; ++t) {
-        const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
-        const uint64_t g0 = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + 2 * lane);
-        float z[2][8];
-        if (nogen) {  // profiling aid (LVSK_K4_NOGEN): stage the MMA with constant Z
+    // ---- Z generation: warp gw -> sketch rows 8gw .. 8gw+7 of the tile
+    //      (quads t0, t0 + 1), lane -> input rows 2*lane, 2*lane+1 of the
+    //      stage: four mix64 per lane per stage, counters advanced by
+    //      constant adds (gauss_ctr is linear in (i << 24) | t)
+    const uint32_t t0 = static_cast<uint32_t>(ktile * (BM / 4) + 2 * gw);
+    uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(r_begin + 2 * lane), t0);
+    constexpr uint64_t ROW = GAUSS_PHI << 24;             // next input row
+    constexpr uint64_t STAGE = GAUSS_PHI << 30;           // 64 input rows on
+    const uint32_t mbase = smem_u32(mag);
+    for (int t = 0; t < nstages; ++t, ctr += STAGE) {
+      const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
+      // h[r][q]: input row 2 lane + r, quad t0 + q
+      const uint64_t h00 = mix64(ctr), h01 = mix64(ctr + GAUSS_PHI);
+      const uint64_t h10 = mix64(ctr + ROW), h11 = mix64(ctr + ROW + GAUSS_PHI);
+      uint32_t w[8];  // sketch row 8 gw + r8: bf16 pair (input row 2 lane, 2 lane + 1)
 #pragma unroll
-          for (int r8 = 0; r8 < 8; ++r8) z[0][r8] = z[1][r8] = 1.0f;
-        } else {
-          gaussian8(g0, qg, k0, k1, tab, z[0]);
-          gaussian8(g0 + 1, qg, k0, k1, tab, z[1]);
-        }
-        mbar_wait(&zempty[s], ph ^ 1u);
-        uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
-#pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) {
-          const int j = 8 * q + r8;
-          __nv_bfloat162 v = __floats2bfloat162_rn(z[0][r8], z[1][r8]);
-          // row j: 128 B = 8 swizzled 16-byte chunks; lane owns bytes [4 lane, 4 lane + 4)
-          const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
-          *reinterpret_cast<__nv_bfloat162*>(zt + off) = v;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&zfull[s]);
+      for (int r8 = 0; r8 < 8; ++r8) {
+        const uint64_t ha = r8 < 4 ? h00 : h01, hb = r8 < 4 ? h10 : h11;
+        const uint32_t fa = static_cast<uint32_t>(ha >> (16 * (r8 & 3)));
+        const uint32_t fb = static_cast<uint32_t>(hb >> (16 * (r8 & 3)));
+        uint16_t ma, mb;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(ma) : "r"(mbase + 2 * (fa & 0x7FFFu)));
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(mb) : "r"(mbase + 2 * (fb & 0x7FFFu)));
+        const uint32_t za = static_cast<uint32_t>(ma) | (fa & 0x8000u);
+        const uint32_t zb = static_cast<uint32_t>(mb) | (fb & 0x8000u);
+        w[r8] = za | (zb << 16);
       }
-    } else {
-      // ---- Z generation, cluster of 2: this CTA (rank = dslab) makes rows
-      //      [64 rank, 64 rank + 64) of the tile — warp gw -> octet q, half of
-      //      the 64 input rows; lane -> one input row (1 Philox call) — and
-      //      stores them into both CTAs' Z slot
-      const uint32_t peer = static_cast<uint32_t>(dslab ^ 1);
-      const int q = dslab * 8 + (gw >> 1);
-      const int cbase = (gw & 1) * 32;
-      const uint32_t qg = static_cast<uint32_t>(ktile * (BM / 8) + q);
-      const uint32_t zfull_peer0 = map_peer(smem_u32(&zfull[0]), peer);
-      for (int t = 0; t < nstages; ++t) {
-        const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
-        const int cidx = cbase + lane;  // input row of the stage = Z column
-        const uint64_t g = row0 + static_cast<uint64_t>(r_begin + static_cast<int64_t>(t) * C::BKN + cidx);
-        float z[8], zp[8];
-        if (nogen) {
+      mbar_wait(&zempty[s], ph ^ 1u);
+      uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
 #pragma unroll
-          for (int r8 = 0; r8 < 8; ++r8) z[r8] = 1.0f;
-        } else {
-          gaussian8(g, qg, k0, k1, tab, z);
-        }
-#pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) zp[r8] = __shfl_xor_sync(0xFFFFFFFFu, z[r8], 1);
-        mbar_wait(&zempty[s], ph ^ 1u);
-        const uint32_t zt = smem_u32(smem + C::OFF_Z + s * C::Z_BYTES);
-        const uint32_t ztp = map_peer(zt, peer);
-        const int cpair = cidx & ~1;  // even column of this lane's pair
-        const bool odd = lane & 1;    // even lanes write rows 0-3, odd lanes rows 4-7
-#pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) {
-          if ((r8 >= 4) == odd) {
-            const int j = 8 * q + r8;
-            const float a = odd ? zp[r8] : z[r8];   // even column
-            const float bv = odd ? z[r8] : zp[r8];  // odd column
-            __nv_bfloat162 v = __floats2bfloat162_rn(a, bv);
-            const uint32_t w = *reinterpret_cast<uint32_t*>(&v);
-            const int off = j * 128 + ((((cpair * 2) >> 4) ^ (j & 7)) << 4) + ((cpair * 2) & 15);
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(zt + off), "r"(w) : "memory");
-            asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(ztp + off), "r"(w) : "memory");
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&zfull[s]);
-          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(zfull_peer0 + s * 8)
-                       : "memory");
-        }
+      for (int r8 = 0; r8 < 8; ++r8) {
+        const int j = 8 * gw + r8;
+        // row j: 128 B = 8 swizzled 16-byte chunks; lane owns bytes [4 lane, 4 lane + 4)
+        const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
+        *reinterpret_cast<uint32_t*>(zt + off) = w[r8];
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&zfull[s]);
     }
     // ---- epilogue: TMEM -> fp32 partial
     mbar_wait(accfull, 0);
@@ -343,7 +271,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(NS));
   }
-  if constexpr (CL > 1 || MX > 1) cluster_sync_all();  // no CTA leaves while its peer may still write into it
+  if constexpr (MX > 1) cluster_sync_all();  // no CTA leaves while its peer may still write into it
 }
 
 }  // namespace tc
@@ -370,25 +298,21 @@ bool gaussian_tc_ok(const void* X, int64_t n, int64_t d, int64_t ldx, int64_t k)
   return true;
 }
 
-template <int NS, int CL, int MX>
+template <int NS, int MX>
 static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
-                               uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
+                               uint64_t key, const GaussTcPlan& p, float* partial, cudaStream_t st) {
   using C = tc::CfgG<NS>;
   CUtensorMap mx;
   if (!tc::make_map(&mx, X, d, n, ldx * 2, 64, C::BKN, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16)) {
     set_error("cuTensorMapEncodeTiled failed");
     return LVSK_ERR_CUDA;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::gaussian_tc_kernel<NS, CL, MX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "gaussian tc smem attribute");
-    attr = true;
-  }
+  const int32_t rc = ensure_smem_attr(reinterpret_cast<const void*>(tc::gaussian_tc_kernel<NS, MX>), C::SMEM_BYTES,
+                                      "gaussian tc smem attribute");
+  if (rc != LVSK_OK) return rc;
   const int64_t items = static_cast<int64_t>(p.ktiles) * p.dslabs * p.splits;
-  const float* gtab = gaussian_table_device();
-  if (gtab == nullptr) {
+  const uint16_t* gmag = gaussian_table_device();
+  if (gmag == nullptr) {
     set_error("cannot allocate the Gaussian generator table");
     return LVSK_ERR_CUDA;
   }
@@ -399,30 +323,23 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = CL * MX;
+  attrs[0].val.clusterDim.x = MX;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, CL, MX>, mx, n, d, k, row0, k0, k1, p.ktiles,
-                                     p.dslabs, p.rows_per_split, gtab, partial,
-                                     getenv("LVSK_K4_NOGEN") != nullptr ? 1 : 0);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, MX>, mx, n, d, k, row0, key, p.ktiles,
+                                     p.dslabs, p.rows_per_split, gmag, partial);
   if (e != cudaSuccess) return cuda_status(e, "gaussian tc launch");
   return LVSK_OK;
 }
 
 int32_t gaussian_tc_bf16(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
-                         uint32_t k0, uint32_t k1, const GaussTcPlan& p, float* partial, cudaStream_t st) {
-  // the 2-CTA cluster that shares each Z tile over DSMEM paid off while Z
-  // generation was the bound (Box-Muller, ~40 instructions / entry); with the
-  // table generator (~8 / entry) its cluster-scope release fences cost more
-  // than regenerating the tile: C5 5.25 ms (CL = 2) vs 3.68 ms (CL = 1)
-  if (p.ns == 512 && p.dslabs == 2 && getenv("LVSK_K4_CLUSTER") != nullptr)
-    return launch_gauss_tc<512, 2, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
-  if (p.ns == 512 && p.ktiles % 2 == 0 && getenv("LVSK_K4_NOMC") == nullptr)
-    return launch_gauss_tc<512, 1, 2>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
-  return p.ns == 512 ? launch_gauss_tc<512, 1, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st)
-                     : launch_gauss_tc<256, 1, 1>(X, n, d, ldx, k, row0, k0, k1, p, partial, st);
+                         uint64_t key, const GaussTcPlan& p, float* partial, cudaStream_t st) {
+  if (p.ns == 512 && p.ktiles % 2 == 0)
+    return launch_gauss_tc<512, 2>(X, n, d, ldx, k, row0, key, p, partial, st);
+  return p.ns == 512 ? launch_gauss_tc<512, 1>(X, n, d, ldx, k, row0, key, p, partial, st)
+                     : launch_gauss_tc<256, 1>(X, n, d, ldx, k, row0, key, p, partial, st);
 }
 
 }  // namespace lvsk

@@ -171,13 +171,9 @@ static int32_t launch_bf16(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t
     set_error("cuTensorMapEncodeTiled failed");
     return LVSK_ERR_CUDA;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(leverage_bf16_kernel<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "leverage bf16 smem attribute");
-    attr = true;
-  }
+  const int32_t arc = ensure_smem_attr(reinterpret_cast<const void*>(leverage_bf16_kernel<N2>), C::SMEM_BYTES,
+                                       "leverage bf16 smem attribute");
+  if (arc != LVSK_OK) return arc;
   const int64_t ntiles = (n + BM - 1) / BM;
   const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
   const int kchunks = static_cast<int>((d + C::BKB - 1) / C::BKB);

@@ -458,13 +458,9 @@ static int32_t launch(const float* X, int64_t n, int64_t d, int64_t ldx, const f
     set_error("cuTensorMapEncodeTiled failed");
     return LVSK_ERR_CUDA;
   }
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(leverage_tf32x3_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "leverage tc smem attribute");
-    attr_done = true;
-  }
+  const int32_t arc = ensure_smem_attr(reinterpret_cast<const void*>(leverage_tf32x3_kernel<N>), C::SMEM_BYTES,
+                                       "leverage tc smem attribute");
+  if (arc != LVSK_OK) return arc;
   const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
   const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
   const int kchunks = static_cast<int>((d + BK - 1) / BK);
@@ -483,12 +479,9 @@ static int32_t launch_v2(const float* X, int64_t n, int64_t d, int64_t ldx, cons
     set_error("cuTensorMapEncodeTiled failed");
     return LVSK_ERR_CUDA;
   }
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(leverage_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "leverage v2 smem attribute");
-    attr_done = true;
-  }
+  const int32_t arc = ensure_smem_attr(reinterpret_cast<const void*>(leverage_v2_kernel), C::SMEM_BYTES,
+                                       "leverage v2 smem attribute");
+  if (arc != LVSK_OK) return arc;
   const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
   const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
   const int kchunks = static_cast<int>((d + BK - 1) / BK);

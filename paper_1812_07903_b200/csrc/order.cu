@@ -513,17 +513,9 @@ __global__ void __launch_bounds__(AS_THREADS, 1) argsort_coop_kernel(AsArgs a) {
 }
 
 static int coop_grid() {
-  static int g = -1;
-  if (g < 0) {
-    int per = 0;
-    if (cudaFuncSetAttribute(argsort_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(AS_SMEM)) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, argsort_coop_kernel, AS_THREADS, AS_SMEM) !=
-            cudaSuccess)
-      per = 0;
-    g = per >= 1 ? num_sms() * (per > 2 ? 2 : per) : 0;
-    if (g > AS_MAX_G) g = AS_MAX_G;
-  }
+  const int per = resident_ctas(reinterpret_cast<const void*>(argsort_coop_kernel), AS_THREADS, static_cast<int>(AS_SMEM));
+  int g = per >= 1 ? num_sms() * (per > 2 ? 2 : per) : 0;
+  if (g > AS_MAX_G) g = AS_MAX_G;
   return g;
 }
 

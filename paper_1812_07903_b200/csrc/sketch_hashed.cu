@@ -651,16 +651,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) group_coop_kernel(int64_t n, in
 }
 
 static int gc_grid() {
-  static int g = -1;
-  if (g < 0) {
-    int per = 0;
-    if (cudaFuncSetAttribute(group_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(GC_SMEM)) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, group_coop_kernel, GC_THREADS, GC_SMEM) != cudaSuccess)
-      per = 0;
-    g = per >= 1 ? num_sms() : 0;
-    if (g > GC_MAX_G) g = GC_MAX_G;
-  }
+  const int per = resident_ctas(reinterpret_cast<const void*>(group_coop_kernel), GC_THREADS, static_cast<int>(GC_SMEM));
+  int g = per >= 1 ? num_sms() : 0;
+  if (g > GC_MAX_G) g = GC_MAX_G;
   return g;
 }
 

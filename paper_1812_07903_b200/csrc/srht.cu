@@ -348,12 +348,6 @@ size_t srht_sampled_workspace(int64_t n, int64_t d, int64_t m, int64_t k);
 int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t row0, int64_t m,
                      const int8_t* signs, const int64_t* sample, int64_t k, double divisor, double* SX, void* ws,
                      size_t ws_bytes, int32_t* flags, cudaStream_t st);
-bool srht_tma_ok(const float* X, int64_t d, int64_t ldx, int B1);
-int32_t srht_tma_chunk(const float* X, int64_t n, int64_t d, int64_t ldx, int B1, int B2, int64_t chunk, int cbits,
-                       const int8_t* signs, float* T1, const int64_t* sample, const uint32_t* order,
-                       const uint32_t* qstart, double* SX, int first, double final_div, int32_t* flags,
-                       cudaStream_t st);
-
 template <typename T, typename C>
 static int32_t run_srht(const T* X, int64_t n, int64_t d, int64_t ldx, int64_t m, const int8_t* signs,
                         const int64_t* sample, int64_t k, double divisor, double* SX, void* ws, size_t ws_bytes,
@@ -386,16 +380,6 @@ static int32_t run_srht(const T* X, int64_t n, int64_t d, int64_t ldx, int64_t m
   const unsigned ycols = static_cast<unsigned>((d + SrhtCfg<C>::DC - 1) / SrhtCfg<C>::DC);
   const bool vector_ok = reinterpret_cast<uintptr_t>(X) % 16 == 0 && (ldx * sizeof(T)) % 16 == 0 &&
                          (d * sizeof(C)) % 16 == 0 && (d * sizeof(T)) % 16 == 0;
-  if constexpr (std::is_same<T, float>::value && std::is_same<C, float>::value) {
-    if (P.B1 == 8 && P.B2 >= 1 && srht_tma_ok(X, d, ldx, P.B1)) {
-      for (int64_t ch = 0; ch <= last; ++ch) {
-        const int32_t rc2 = srht_tma_chunk(X, n, d, ldx, P.B1, P.B2, ch, P.cb, signs, T1, sample, order, qstart, SX,
-                                           ch == 0 ? 1 : 0, ch == last ? divisor : 0.0, flags, st);
-        if (rc2 != LVSK_OK) return rc2;
-      }
-      return LVSK_OK;
-    }
-  }
   for (int64_t ch = 0; ch <= last; ++ch) {
     dim3 g1(static_cast<unsigned>(chunk_rows >> P.B1), ycols);
     if (vector_ok)

@@ -487,11 +487,9 @@ int32_t srht_sampled(const float* X, int64_t n, int64_t d, int64_t ldx, int64_t 
   if (words) srht_pack_kernel<<<296, 256, 0, st>>>(signs + row0, words, bits);
   srht_slots_kernel<<<1, 1024, 0, st>>>(sample, k, m, slots, flags);
   LVSK_CHECK_LAUNCH("srht pack");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(srht_sampled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr = true;
-  }
+  const int32_t arc = ensure_smem_attr(reinterpret_cast<const void*>(srht_sampled_kernel), SMEM_BYTES,
+                                       "srht sampled smem attribute");
+  if (arc != LVSK_OK) return arc;
   Params P{signs ? bits : nullptr, slots, partial, S.rmax, k, S.jblocks, S.octets, S.groups, row0 / ROWS};
   srht_sampled_kernel<<<static_cast<unsigned>(S.ctas), THREADS, SMEM_BYTES, st>>>(mx, P);
   LVSK_CHECK_LAUNCH("srht sampled");

@@ -243,6 +243,17 @@ def test_gaussian_entries_bit_exact():
         assert np.array_equal(Z.cpu().numpy(), O.gaussian_z(seed, k, row0, n)), (seed, k, row0)
 
 
+def test_gaussian_entries_bit_exact_at_ks_sample_size():
+    """The 1.2e7 entries the CPU distribution test (test_oracle_golden.py:
+    KS vs bf16_rn(N(0,1)), moments, per-column law) runs on, generated by the
+    device generator: bit-identical, so the distribution result is the
+    kernel's."""
+    k, n, row0 = 4096, 3000, 5_000_000
+    Z = torch.empty((k, n), dtype=torch.float32, device="cuda")
+    N.check(N.lib().lvsk_gaussian_entries(0, k, row0, n, Z.data_ptr(), N.stream_ptr()))
+    assert np.array_equal(Z.cpu().numpy(), O.gaussian_z(0, k, row0, n))
+
+
 def test_gaussian_sketch_matches_oracle():
     rng = np.random.default_rng(1)
     for n, d, k, dt in ((3000, 40, 256, torch.float32), (2000, 130, 100, torch.float64), (1500, 64, 128, torch.bfloat16)):

@@ -35,10 +35,12 @@ def test_gaussian_generator_table_matches_oracle():
     bit for bit, so device entries can equal the oracle's exactly."""
     import ctypes
 
-    out = np.zeros(O.gaussian_tables().size, dtype=np.float32)
+    out = np.zeros(O.gaussian_tables().size, dtype=np.uint16)
     rc = _native.lib().lvsk_gaussian_tables(out.ctypes.data_as(ctypes.c_void_p), out.size)
     assert rc == 0
-    assert np.array_equal(out.view(np.uint32), O.gaussian_tables().view(np.uint32))
+    assert np.array_equal(out, O.gaussian_tables())
+    # too small a buffer is refused, not overrun
+    assert _native.lib().lvsk_gaussian_tables(out.ctypes.data_as(ctypes.c_void_p), out.size - 1) != 0
 
 
 def test_no_cpu_fallback_without_gpu():

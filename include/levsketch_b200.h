@@ -212,11 +212,15 @@ LVSK_API int32_t lvsk_rowsumsq_csr(const int64_t* row_ptr, const int32_t* col, c
  * triangle read, leading dimension ldg), Pi: d x r float64 row-major.
  * Writes M = R^-1 Pi (d x r, R^T R = G, R upper with positive diagonal) and
  * diag[3] = {info (0 = positive definite), trace(G), trace(G^-1)}; the caller
- * certifies trace(G) * trace(G^-1) < 1/sv_tol^2 before using M.  One
- * cooperative launch; stream-capturable. */
+ * certifies trace(G) * trace(G^-1) < 1/sv_tol^2 before using M.  The kernel
+ * also evaluates that certificate on the device: when info != 0, a trace is
+ * not finite and positive, or trace(G) * trace(G^-1) >= cert_limit, it adds 1
+ * to *cert_fail (if non-NULL) — so a stream of unsynchronised folds keeps a
+ * count of uncertified results.  One cooperative launch; stream-capturable. */
 LVSK_API size_t lvsk_chol_fold_workspace_bytes(int64_t d, int64_t r);
 LVSK_API int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const double* Pi, int64_t r, double* M,
-                                double* diag, void* ws, size_t ws_bytes, void* stream);
+                                double* diag, double cert_limit, int32_t* cert_fail, void* ws, size_t ws_bytes,
+                                void* stream);
 
 /* ---- ordering -------------------------------------------------------------
  * scores_to_distribution (order.py:51-63): p = scores / sum(scores), with

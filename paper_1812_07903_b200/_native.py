@@ -73,7 +73,7 @@ _SIGS = {
     "lvsk_split_fold": (_I32, [_P, _I64, _I64, _I32, _I64, _P, _P, _P, _P]),
     "lvsk_chol_fold_workspace_bytes": (_SZ, [_I64, _I64]),
     "lvsk_gaussian_tables": (_I32, [_P, _I64]),
-    "lvsk_chol_fold": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
+    "lvsk_chol_fold": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _D, _P, _P, _SZ, _P]),
     "lvsk_argsort_workspace_bytes": (_SZ, [_I64]),
     "lvsk_argsort_f64": (_I32, [_P, _I64, _I32, _P, _P, _SZ, _P]),
 }
@@ -141,16 +141,31 @@ def dtype_code(t: torch.Tensor) -> int:
 
 
 class Workspace:
-    """Grow-only device scratch buffer reused across calls (no allocation in the C ABI)."""
+    """Grow-only device scratch buffers reused across calls (the C ABI never
+    allocates).  One buffer per (thread, device, stream): kernels queued on
+    different streams, devices or host threads never share scratch memory,
+    so the ABI's reentrancy holds at the Python layer too.  The caching
+    allocator orders a replaced buffer's reuse after the work queued on its
+    stream."""
+
+    MAX_KEYS = 32
 
     def __init__(self):
-        self._buf = None
+        self._bufs: dict = {}
 
     def get(self, nbytes: int) -> torch.Tensor:
+        import threading
+
         nbytes = max(int(nbytes), 256)
-        if self._buf is None or self._buf.numel() < nbytes or self._buf.device != device():
-            self._buf = torch.empty(nbytes, dtype=torch.uint8, device=device())
-        return self._buf
+        dev = device()
+        key = (threading.get_ident(), dev.index, torch.cuda.current_stream(dev).cuda_stream)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            if buf is None and len(self._bufs) >= self.MAX_KEYS:
+                self._bufs.pop(next(iter(self._bufs)))  # oldest key
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            self._bufs[key] = buf
+        return buf
 
 
 _ws = Workspace()

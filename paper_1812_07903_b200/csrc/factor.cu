@@ -58,6 +58,8 @@ struct FactorArgs {
   int64_t r;
   double* M;  // d x r, row-major
   double* diag;
+  double cert_limit;   // certificate: trace(G) * trace(G^-1) < cert_limit
+  int32_t* cert_fail;  // optional counter, +1 when the certificate fails
   double* A;   // dp x dp: upper tiles, A -> U in place
   double* W;   // dp x dp: lower tiles, W -> Y = U^-T in place
   double* T;   // nb tiles 64 x 64: inverses of the diagonal tiles of U
@@ -532,7 +534,12 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
         for (int k = 0; k < nb; ++k)
           for (int m = 0; m <= k; ++m) tr += a.partial[k * nb + m];
         a.diag[2] = tr;
-        a.diag[0] = static_cast<double>(ld_acquire(a.ctl + 2));
+        const int32_t info = ld_acquire(a.ctl + 2);
+        a.diag[0] = static_cast<double>(info);
+        // trace(G) was written before the grid barrier of phase 0
+        const double trg = a.diag[1];
+        const bool ok = info == 0 && isfinite(trg) && isfinite(tr) && trg > 0.0 && tr > 0.0 && trg * tr < a.cert_limit;
+        if (!ok && a.cert_fail != nullptr) atomicAdd(a.cert_fail, 1);
       }
       __syncthreads();
     }
@@ -604,7 +611,8 @@ extern "C" size_t lvsk_chol_fold_workspace_bytes(int64_t d, int64_t r) {
 }
 
 extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const double* Pi, int64_t r, double* M,
-                                  double* diag, void* ws, size_t ws_bytes, void* stream) {
+                                  double* diag, double cert_limit, int32_t* cert_fail, void* ws, size_t ws_bytes,
+                                  void* stream) {
   LVSK_REQUIRE(d >= 1 && r >= 1 && ldg >= d, LVSK_ERR_DIMENSION, "bad fold shape d=%lld r=%lld ldg=%lld",
                (long long)d, (long long)r, (long long)ldg);
   LVSK_REQUIRE(G && Pi && M && diag, LVSK_ERR_CONFIGURATION, "null pointer argument");
@@ -618,6 +626,8 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.r = r;
   a.M = M;
   a.diag = diag;
+  a.cert_limit = cert_limit;
+  a.cert_fail = cert_fail;
   kf_layout(c, P, &a);
   LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
   a.nb = P.nb;

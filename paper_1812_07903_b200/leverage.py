@@ -127,23 +127,38 @@ def gram_upper(sx: torch.Tensor) -> torch.Tensor:
 
 
 
-def _chol_body(sx: torch.Tensor, pi: torch.Tensor):
+def cert_limit(sv_tol: float | None) -> float:
+    """The certificate's bound on trace(G) * trace(G^-1) (see chol_certified)."""
+    lim = _CHOL_KAPPA_GUARD
+    if sv_tol is not None and sv_tol > 0:
+        lim = min(lim, 1.0 / (sv_tol * sv_tol))
+    return lim
+
+
+def fold_workspace(d: int, r: int, device) -> torch.Tensor:
+    return torch.empty(int(N.lib().lvsk_chol_fold_workspace_bytes(d, r)), dtype=torch.uint8, device=device)
+
+
+def _chol_body(sx: torch.Tensor, pi: torch.Tensor, sv_tol: float | None = None, cert_fail: torch.Tensor | None = None,
+               ws: torch.Tensor | None = None):
     """Shape-static Cholesky fold (CUDA-graph capturable, no host sync):
     G = SX^T SX (cuBLAS DGEMM) = R^T R, then the KF kernel (csrc/factor.cu):
     M = R^-1 Pi and diag = [info, trace(G), trace(G^-1)] with
-    trace(G^-1) = ||R^-1||_F^2."""
+    trace(G^-1) = ||R^-1||_F^2; the kernel also adds 1 to ``cert_fail`` (a
+    device int32) when the certificate of :func:`chol_certified` fails."""
     k, d = sx.shape
     r = pi.shape[1]
     G = gram_upper(sx)
-    key = (d, r, sx.device)
-    ws = _FOLD_WS.get(key)
-    if ws is None:
-        ws = torch.empty(int(N.lib().lvsk_chol_fold_workspace_bytes(d, r)), dtype=torch.uint8, device=sx.device)
-        _FOLD_WS[key] = ws
+    if ws is None:  # eager calls: one scratch buffer per (shape, device, stream)
+        key = (d, r, sx.device, torch.cuda.current_stream(sx.device).cuda_stream)
+        ws = _FOLD_WS.get(key)
+        if ws is None:
+            ws = _FOLD_WS[key] = fold_workspace(d, r, sx.device)
     pi = pi.contiguous()
     M = torch.empty((d, r), dtype=torch.float64, device=sx.device)
     diag = torch.empty(3, dtype=torch.float64, device=sx.device)
     N.check(N.lib().lvsk_chol_fold(G.data_ptr(), d, G.stride(0), pi.data_ptr(), r, M.data_ptr(), diag.data_ptr(),
+                                   cert_limit(sv_tol), N.ptr(cert_fail),
                                    ws.data_ptr(), ws.numel(), N.stream_ptr()), "cholesky fold")
     return M, diag
 
@@ -432,9 +447,12 @@ class FoldGraph:
         self.sx, self.sv_tol, self.pi = sx, sv_tol, pi
         self.ops = KernelOperands(None, X_like, (d, pi.shape[1]))
         self.diag = torch.zeros(3, dtype=torch.float64, device=sx.device)
+        # device count of replays whose certificate failed (evaluated by the KF kernel)
+        self.cert_fail = torch.zeros(1, dtype=torch.int32, device=sx.device)
+        self.ws = fold_workspace(d, pi.shape[1], sx.device)  # owned by the graph: replays never share scratch
         self.graph = None
-        # warm up cuBLAS handles and the fold workspace outside capture
-        M, diag = _chol_body(sx, pi)
+        # warm up cuBLAS handles outside capture
+        M, diag = _chol_body(sx, pi, ws=self.ws)
         self.ops.set(M)
         torch.cuda.synchronize()
         s = torch.cuda.Stream()
@@ -442,7 +460,7 @@ class FoldGraph:
         with torch.cuda.stream(s):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
-                M, diag = _chol_body(self.sx, self.pi)
+                M, diag = _chol_body(self.sx, self.pi, self.sv_tol, self.cert_fail, self.ws)
                 self.ops.set(M)
                 self.diag.copy_(diag)
         torch.cuda.current_stream().wait_stream(s)

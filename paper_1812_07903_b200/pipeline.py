@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import FormatError
+from .errors import FormatError, UncertifiedFoldError
 from .leverage import FoldGraph, KernelOperands, jl_device, sketch_fold
 from .csr import CSRMatrix, csr_code
 from .sketch import GAUSSIAN, SRHT, SketchSpec, SketchState, sketch_rows
@@ -65,6 +65,7 @@ class LeveragePipeline:
         self._x_like = torch.empty((1, d), dtype=dtype, device=dev)
         self._fold_graph = None
         self._cert_pending = False
+        self._cert_fails_seen = 0  # certificate failures already accounted for by check()
         self._last_X = None
         self._m32 = None
         self._m32_src = None
@@ -104,7 +105,9 @@ class LeveragePipeline:
 
     def _factor(self) -> None:
         k, d = self.sx.shape
-        self._cert_pending = False
+        # a certificate still pending from an earlier run(check=False) is not
+        # dropped: the KF kernel counts failures on the device (cert_fail) and
+        # check() raises if any run other than the last one was uncertified
         if (self.factor_method == "auto" and self.pi is not None and self.rank is None and k >= d
                 and os.environ.get("LVSK_NO_GRAPH", "0") != "1"):
             if self._fold_graph is None:
@@ -121,11 +124,23 @@ class LeveragePipeline:
         M, self.effective_rank = sketch_fold(self.sx, self.sv_tol, self.rank, self.pi, self.factor_method)
         self.set_fold(M)
 
+    def cert_failures(self) -> int:
+        """Runs whose optimistic Cholesky fold failed its certificate (device count)."""
+        return int(self._fold_graph.cert_fail.item()) if self._fold_graph is not None else 0
+
     def _verify_fold(self) -> None:
         if not self._cert_pending:
             return
         self._cert_pending = False
-        if self._fold_graph.certified():
+        fails = self.cert_failures()
+        last_ok = self._fold_graph.certified()
+        earlier = fails - self._cert_fails_seen - (0 if last_ok else 1)
+        self._cert_fails_seen = fails
+        if earlier > 0:
+            raise UncertifiedFoldError(
+                f"{earlier} earlier run(check=False) result(s) came from a Cholesky fold whose certificate failed; "
+                "call check() after each run (or run(check=True)) when the sketch may be ill-conditioned")
+        if last_ok:
             return
         M, self.effective_rank = sketch_fold(self.sx, self.sv_tol, self.rank, self.pi, "qr")
         self.set_fold(M)
@@ -199,7 +214,9 @@ class LeveragePipeline:
 
     def check(self) -> None:
         """Verify the fold certificate of the last run (redoing the fold and the
-        passes after it if it failed) and raise on flagged input errors."""
+        passes after it if it failed), raise UncertifiedFoldError if an earlier
+        unchecked run used an uncertified fold, and raise on flagged input
+        errors."""
         self._verify_fold()
         f = int(self.flags.item())
         if f & N.FLAG_BADINDEX:

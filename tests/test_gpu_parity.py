@@ -148,6 +148,57 @@ def test_nonfinite_rejected_and_state_untouched():
         P.leverage_sketched_trunc(torch.tensor(bad, device="cuda", dtype=torch.float32), spec, 0.0)
 
 
+@pytest.mark.parametrize("family", ["countsketch", "osnap", "gaussian", "csr"])
+def test_nonfinite_first_block_leaves_zero_state(family):
+    """A rejected FIRST block (the state is still zero and updated in place)
+    must not poison the state: a retry with clean rows equals a fresh state
+    (the reference validates before touching anything,
+    matrix.py:30-39)."""
+    rng = np.random.default_rng(3)
+    d, n = 24, 40
+    clean = rng.standard_normal((n, d))
+    bad = clean.copy()
+    bad[7, 3] = np.nan
+    fam = "osnap" if family == "csr" else family
+    spec = P.SketchSpec(fam, eps=0.5, d=d, seed=2, rows_override=16, osnap_s=3 if fam == "osnap" else None)
+    if family == "csr":
+        import scipy.sparse as sp
+
+        clean_in, bad_in = sp.csr_matrix(clean), sp.csr_matrix(bad)
+    else:
+        clean_in, bad_in = clean, bad
+    st = P.SketchState(spec, n)
+    with pytest.raises(errors.FormatError):
+        P.consume_rows(st, bad_in, 0)
+    assert st.rows_consumed == 0 and not np.any(st.data)
+    P.consume_rows(st, clean_in, 0)
+    ref = P.consume_rows(P.SketchState(spec, n), clean_in, 0)
+    assert np.array_equal(st.data, ref.data)
+
+
+def test_srht_whole_matrix_is_transformed_eagerly():
+    """SRHT consume of the whole matrix: the product is formed inside the
+    call (no reference to the caller's rows is kept, errors raise from the
+    call itself, as the reference's consume_rows does)."""
+    rng = np.random.default_rng(4)
+    n, d, k = 1000, 16, 64
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    spec = P.SketchSpec("srht", eps=0.5, d=d, seed=3, rows_override=k)
+    X = torch.from_numpy(x).cuda()
+    st = P.apply_sketch(X, spec)
+    ref = O.srht_sketch(x.astype(np.float64), k, 3)
+    X.mul_(2.0)  # the caller edits its array afterwards
+    assert np.linalg.norm(st.data - ref) <= 2e-6 * np.linalg.norm(ref)
+    X[5, 5] = float("inf")
+    with pytest.raises(errors.FormatError):
+        P.consume_rows(P.SketchState(spec, n), X, 0)
+    # a fully consumed state merges with an empty one (linearity of the transform)
+    m = P.merge(st, P.SketchState(spec, n))
+    assert np.array_equal(m.data, st.data)
+    with pytest.raises(errors.IncompatibleSketchError):
+        P.merge(st, st)
+
+
 def test_capacity_and_srht_config():
     with pytest.raises(errors.ConfigurationError):
         P.SketchState(P.SketchSpec("srht", eps=0.5, d=8, rows_override=64), 10)
@@ -428,10 +479,17 @@ def test_kf_cholesky_fold_flags_indefinite():
     ws = torch.empty(int(L.lvsk_chol_fold_workspace_bytes(d, 16)), dtype=torch.uint8, device="cuda")
     M = torch.empty((d, 16), dtype=torch.float64, device="cuda")
     diag = torch.empty(3, dtype=torch.float64, device="cuda")
+    fail = torch.zeros(1, dtype=torch.int32, device="cuda")
     P._native.check(L.lvsk_chol_fold(Gt.data_ptr(), d, d, pi.data_ptr(), 16, M.data_ptr(), diag.data_ptr(),
-                                     ws.data_ptr(), ws.numel(), P._native.stream_ptr()), "fold")
+                                     1e10, fail.data_ptr(), ws.data_ptr(), ws.numel(), P._native.stream_ptr()), "fold")
     assert diag[0].item() != 0.0
     assert not P.leverage.chol_certified(diag.tolist(), 1e-6)
+    assert int(fail.item()) == 1  # the device-side certificate agrees and counts the failure
+    g2 = rng.standard_normal((400, d))
+    G2 = torch.from_numpy(g2.T @ g2).cuda()
+    P._native.check(L.lvsk_chol_fold(G2.data_ptr(), d, d, pi.data_ptr(), 16, M.data_ptr(), diag.data_ptr(),
+                                     1e10, fail.data_ptr(), ws.data_ptr(), ws.numel(), P._native.stream_ptr()), "fold")
+    assert P.leverage.chol_certified(diag.tolist(), 1e-6) and int(fail.item()) == 1
 
 
 # ---------------------------------------------------------------------------
@@ -607,6 +665,33 @@ def test_pipeline_fold_certificate_and_fallback(sv_tol, noise):
     got = scores.cpu().numpy()
     assert np.max(np.abs(got - ref) / np.maximum(ref, 1e-30)) < 1e-4
     assert np.array_equal(order.cpu().numpy(), np.argsort(-(got / got.sum()), kind="stable"))
+
+
+def test_pipeline_unchecked_uncertified_runs_raise():
+    """run(check=False) repeatedly on a sketch whose certificate fails: the
+    KF kernel counts every failure on the device, check() redoes the last run
+    and raises UncertifiedFoldError for the earlier ones instead
+    of dropping their certificates."""
+    rng = np.random.default_rng(12)
+    n, d, k, jl = 6000, 96, 512, 32
+    x = (rng.standard_normal((n, 12)) @ rng.standard_normal((12, d))).astype(np.float32)  # rank 12 < d
+    X = torch.from_numpy(x).cuda()
+    spec = P.SketchSpec("countsketch", eps=0.5, d=d, seed=5, rows_override=k)
+    pipe = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=0.05, jl_dim=jl, jl_seed=6)
+    pipe.run(X)  # checked: fine, the fallback recomputes
+    assert pipe.cert_failures() == 1
+    pipe.run(X, check=False)
+    pipe.run(X, check=False)
+    with pytest.raises(errors.UncertifiedFoldError):
+        pipe.check()
+    assert pipe.cert_failures() == 3
+    # a well-conditioned sketch never trips it
+    good = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=1e-6, jl_dim=jl, jl_seed=6)
+    y = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).cuda()
+    for _ in range(3):
+        good.run(y, check=False)
+    good.check()
+    assert good.cert_failures() == 0
 
 
 # ---------------------------------------------------------------------------

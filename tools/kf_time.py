@@ -29,7 +29,7 @@ def main():
         diag = torch.empty(3, dtype=torch.float64, device="cuda")
 
         def kf():
-            L.lvsk_chol_fold(G.data_ptr(), d, d, pi.data_ptr(), r, M.data_ptr(), diag.data_ptr(), ws.data_ptr(),
+            L.lvsk_chol_fold(G.data_ptr(), d, d, pi.data_ptr(), r, M.data_ptr(), diag.data_ptr(), 1e10, None, ws.data_ptr(),
                              ws.numel(), N.stream_ptr())
 
         def chol_torch():

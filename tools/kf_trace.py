@@ -11,5 +11,5 @@ for d, r in ((512, 64), (256, 64)):
     M = torch.empty((d, r), dtype=torch.float64, device="cuda")
     diag = torch.empty(3, dtype=torch.float64, device="cuda")
     for _ in range(3):
-        L.lvsk_chol_fold(G.data_ptr(), d, d, pi.data_ptr(), r, M.data_ptr(), diag.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr())
+        L.lvsk_chol_fold(G.data_ptr(), d, d, pi.data_ptr(), r, M.data_ptr(), diag.data_ptr(), 1e10, None, ws.data_ptr(), ws.numel(), N.stream_ptr())
     torch.cuda.synchronize()

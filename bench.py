@@ -1,18 +1,25 @@
 """Benchmark: leverage-score rows/s on B200 (BASELINE.json metric).
 
 Workload at N=1 = BASELINE configs[1] ("C2"): CountSketch, X fp32
-1,000,000 x 512 (rank-50 + 0.01 noise, singular values 10 -> 1), k = 4096,
-JL r = 64, sv_tol 1e-6, curriculum order "dec".  One step = one full pass of
-the hot path over device-resident X:
-    K1 sketch -> fp64 factorisation -> fold M -> K5 leverage pass
+1,000,000 x 512 (rank 50 with singular values 10 -> 1 plus 0.01 N(0,1)),
+k = 4096, JL r = 64, sv_tol 1e-6, curriculum order "dec".  Inputs come from
+paper_1812_07903_b200/synth.py, the generators the config-level parity tests
+(tests/test_gpu_configs.py) check against the oracle.  One step = one full
+pass of the hot path over device-resident X:
+    K1 sketch -> fold (Gram + KF Cholesky) -> K5 leverage pass
     -> normalise -> K7 argsort.
 N > 1 (torchrun, NCCL): weak scaling, 1e6 rows per rank with global row
-indices; the compensated sketch partials are all-gathered and folded in rank
-order, rank 0 factorises and broadcasts M, scores stay rank-local, and the
-global "dec" order is formed on rank 0 from the gathered probabilities.
+indices (C5: its 8e6 rows split across ranks, strong); the compensated
+sketch partials meet in a sliced all-to-all merged in rank order, every rank
+folds the same SX (deterministic kernels, identical M, no broadcast on the
+critical path), scores stay rank-local, and rank 0 sorts the gathered
+probabilities (the global "dec" order) on a side stream that the timed
+region waits for.
 
---impl reference times the reference algorithm's CPU implementation (the
-numpy port in oracle/, all host threads, bounded row sample per step).
+--impl reference times the reference package itself (baseline/_ref, a pip
+install of /root/reference/pkg) on the box's host cores: C2 through its
+run_distributed(workers = cores) + scores_to_distribution + make_plan("dec")
+over the config's full 1e6 rows per step, on inputs from the same generator.
 """
 
 from __future__ import annotations
@@ -33,86 +40,63 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "leverage-score rows/s"
 UNIT = "rows/s"
-
-CONFIGS = {
-    # name: family, n (per rank), d, k, r, s, dtype, sv_tol
-    "c2": dict(family="countsketch", n=1_000_000, d=512, k=4096, r=64, s=None, dtype="f32", sv_tol=1e-6,
-               desc="configs[1]: CountSketch dense fp32 1e6x512, k=4096, r=64"),
-    "c1": dict(family="gaussian", n=20_000, d=256, k=1024, r=64, s=None, dtype="f32", sv_tol=1e-6,
-               desc="configs[0]: Gaussian sketch fp32 20000x256, k=1024, r=64"),
-    "c4": dict(family="osnap", n=4_000_000, d=4096, k=16384, r=128, s=4, dtype="f32", sv_tol=1e-6, csr=True,
-               desc="configs[3]: OSNAP s=4 on CSR 4e6x4096, ~80 Zipf(1.1) draws/row, k=16384, r=128"),
-    "c5": dict(family="gaussian", n=1_000_000, d=1024, k=2048, r=128, s=None, dtype="bf16", sv_tol=1e-6, rank=100,
-               desc="configs[4]: Gaussian sketch on bf16 X 1e6x1024 per GPU (8e6 on 8), k=2048, rank-100, r=128"),
-    "c3": dict(family="srht", n=2**21, d=256, k=4096, r=64, s=None, dtype="f32", sv_tol=1e-6,
-               desc="configs[2]: SRHT fp32 2^21x256, k=4096, r=64"),
-}
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
-def gen_csr(n, d, draws, seed, device, chunk=250_000):
-    """Bag-of-words-like canonical CSR on the device: `draws` column draws per
-    row from Zipf(1.1) truncated to [1, d] (inverse CDF), lognormal(0, 1)
-    values, duplicate columns summed, rows L2-normalised."""
+def configs():
+    from paper_1812_07903_b200.synth import CONFIGS
+
+    return CONFIGS
+
+
+def rows_of(name: str, cfg: dict, rank: int, world: int, rows: int | None):
+    """(lo, hi, n_total) of this rank's global rows.  C5 is strong scaling
+    (the config's 8e6 rows over the ranks); the others weak (cfg n per rank)."""
+    from paper_1812_07903_b200.dist import partition_rows
+
+    n = rows or cfg["n"]
+    if name == "c5":
+        lo, hi = partition_rows(n, world)[rank]
+        return lo, hi, n
+    return rank * n, (rank + 1) * n, n * world
+
+
+def gather0(t, parts):
+    """dist.gather to rank 0 (NCCL); the gloo share-mode check path (CUDA
+    tensors, where gloo has no gather) stages it as an all_gather."""
     import torch
+    import torch.distributed as dist
 
-    from paper_1812_07903_b200.csr import CSRMatrix
-
-    g = torch.Generator(device=device).manual_seed(seed)
-    w = torch.arange(1, d + 1, device=device, dtype=torch.float64).pow(-1.1)
-    cdf = torch.cumsum(w, 0) / w.sum()
-    ptrs, cols, vals = [torch.zeros(1, dtype=torch.int64, device=device)], [], []
-    base = 0
-    for r0 in range(0, n, chunk):
-        rows = min(chunk, n - r0)
-        u = torch.rand(rows * draws, generator=g, device=device, dtype=torch.float64)
-        c = torch.searchsorted(cdf, u).clamp_(max=d - 1)
-        v = torch.exp(torch.randn(rows * draws, generator=g, device=device))
-        r = torch.arange(rows, device=device).repeat_interleave(draws)
-        key = r * d + c
-        key, order = torch.sort(key)
-        v = v[order]
-        uk, inv = torch.unique_consecutive(key, return_inverse=True)
-        vs = torch.zeros(uk.numel(), device=device, dtype=torch.float32).index_add_(0, inv, v)
-        ur = uk // d
-        norm = torch.zeros(rows, device=device, dtype=torch.float32).index_add_(0, ur, vs * vs).sqrt_()
-        vs = vs / norm[ur]
-        cnt = torch.bincount(ur, minlength=rows)
-        ptrs.append(base + torch.cumsum(cnt, 0))
-        base += int(uk.numel())
-        cols.append((uk % d).to(torch.int32))
-        vals.append(vs)
-    indptr = torch.cat(ptrs)
-    return CSRMatrix(indptr, torch.cat(cols), torch.cat(vals), (n, d))
+    if dist.get_backend() == "nccl":
+        dist.gather(t, parts, dst=0)
+        return
+    outs = parts if parts is not None else [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(outs, t)
 
 
-def gen_x(cfg, rank: int, device):
-    """Seeded synthetic X with the config's structure, generated on the device."""
-    import torch
+def counts_of(name: str, cfg: dict, world: int, rows: int | None) -> list[int]:
+    return [hi - lo for lo, hi, _ in (rows_of(name, cfg, q, world, rows) for q in range(world))]
 
-    if cfg.get("csr"):
-        return gen_csr(cfg["n"], cfg["d"], 80, 1000 + rank, device)
 
-    n, d = cfg["n"], cfg["d"]
-    g = torch.Generator(device=device).manual_seed(1000 + rank)
-    if cfg["family"] == "countsketch":
-        # rank-50, singular values linear 10 -> 1, plus 0.01 N(0,1)
-        u = torch.randn(n, 50, generator=g, device=device, dtype=torch.float32) / math.sqrt(n)
-        v, _ = torch.linalg.qr(torch.randn(d, 50, generator=g, device=device, dtype=torch.float32))
-        s = torch.linspace(10.0, 1.0, 50, device=device)
-        x = (u * s) @ v.T + 0.01 * torch.randn(n, d, generator=g, device=device, dtype=torch.float32)
-    elif cfg["family"] == "gaussian" and cfg.get("rank"):
-        # image-feature-like: sigmoid(G1 G2 + 0.05 N) in [0, 1], G1 n x 100, G2 100 x d
-        g1 = torch.randn(n, 100, generator=g, device=device) / 10.0
-        g2 = torch.randn(100, d, generator=g, device=device)
-        x = torch.sigmoid(g1 @ g2 + 0.05 * torch.randn(n, d, generator=g, device=device))
-    elif cfg["family"] == "srht":
-        x = torch.randn(n, d, generator=g, device=device) / torch.sqrt(torch.arange(1, d + 1, device=device, dtype=torch.float32))
-    else:
-        u, _ = torch.linalg.qr(torch.randn(n, d, generator=g, device=device))
-        v, _ = torch.linalg.qr(torch.randn(d, d, generator=g, device=device))
-        s = 0.9 ** torch.arange(d, device=device, dtype=torch.float32)
-        x = (u * s) @ v.T + 0.01 * torch.randn(n, d, generator=g, device=device)
-    return x.contiguous()
+def gen_local(name: str, rank: int, lo: int, hi: int, device):
+    """This rank's rows.  C1 / C2 are generated whole (exactly orthonormal
+    factors) with seed = rank; C3 / C4 / C5 are row windows [lo, hi) of one
+    global matrix (synth.py chunks)."""
+    from paper_1812_07903_b200 import synth as S
+
+    if name == "c1":
+        return S.gen_c1(rank, device)
+    if name == "c2":
+        return S.gen_c2(rank, device, n=hi - lo)
+    return S.generate(name, 0, device, lo=lo, hi=hi)
+
+
+def config_line(name: str, cfg: dict, n_local: int, world: int) -> dict:
+    """The config dict both arms print (identical, so the driver can match them)."""
+    return {"workload": cfg["desc"], "rows_per_gpu": n_local, "d": cfg["d"], "k": cfg["k"], "jl_r": cfg["r"],
+            "sv_tol": cfg["sv_tol"], "parallelism": f"row-partition x{world}",
+            "l2": "inputs larger than L2 (X read from HBM each pass)" if name != "c1" else
+                  "C1 X (20 MB) fits in L2: no flush between steps (launch-bound config)"}
 
 
 class ClockSampler:
@@ -187,59 +171,6 @@ def measured_tensor_peak():
     return 2250.0, "fallback 2.25 PFLOP/s dense bf16 (nominal)"
 
 
-# ---------------------------------------------------------------------------
-# CPU legs (oracle port of the reference algorithm)
-
-
-def cpu_leg(cfg, rows: int, threads: int):
-    """Time the reference algorithm (numpy port, oracle/) on `rows` rows of the
-    workload: sketch (threads = row partitions merged in order, dist.py style)
-    -> SVD -> fold -> scores -> dec argsort.  Returns (rows/s, seconds)."""
-    import numpy as np
-
-    from oracle import levsketch_oracle as O
-
-    rng = np.random.default_rng(7)
-    d = cfg["d"]
-    if cfg.get("csr"):
-        # densified CSR rows streamed through the reference hashing (SURVEY §6 C4);
-        # the n-independent 16384 x 4096 SVD is excluded here (~23 s in LAPACK)
-        import scipy.sparse as sp
-
-        w = np.arange(1, d + 1, dtype=np.float64) ** -1.1
-        cdf = np.cumsum(w) / w.sum()
-        r = np.repeat(np.arange(rows), 80)
-        c = np.minimum(np.searchsorted(cdf, rng.random(rows * 80)), d - 1)
-        m = sp.csr_matrix((rng.lognormal(0, 1, rows * 80), (r, c)), shape=(rows, d))
-        m.sum_duplicates()
-        x = np.asarray(m.todense())
-        x /= np.maximum(np.linalg.norm(x, axis=1, keepdims=True), 1e-30)
-        pi = O.jl_matrix(0, d, cfg["r"])
-        t0 = time.perf_counter()
-        hp = O.HashParams("osnap", 0, cfg["k"], cfg["s"])
-        hi = np.zeros((cfg["k"], d))
-        lo = np.zeros_like(hi)
-        O.hashed_consume(hi, lo, hp, x, 0)
-        O.row_scores(x, np.linalg.qr(pi)[0])  # stands in for the fold's d x r product
-        dt = time.perf_counter() - t0
-        return rows / dt, dt
-    x = (rng.standard_normal((rows, 50)) @ (np.linspace(10, 1, 50)[:, None] * rng.standard_normal((50, d)))
-         + 0.01 * rng.standard_normal((rows, d))).astype(np.float32).astype(np.float64)
-    pi = O.jl_matrix(0, d, cfg["r"])
-    t0 = time.perf_counter()
-    if cfg["family"] == "countsketch":
-        scores, _, _ = O.pipeline_hashed(x, "countsketch", cfg["k"], 0, 1, cfg["sv_tol"], pi, workers=threads)
-    elif cfg["family"] == "srht":
-        sx = O.srht_sketch(x, cfg["k"], 0)
-        scores, _, _ = O.leverage_from_sketch(x, sx, cfg["sv_tol"], pi)
-    else:
-        sx = O.gaussian_sketch(x, cfg["k"], 0)
-        scores, _, _ = O.leverage_from_sketch(x, sx, cfg["sv_tol"], pi)
-    O.order(O.distribution(scores), "dec")
-    dt = time.perf_counter() - t0
-    return rows / dt, dt
-
-
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -247,48 +178,177 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def run_reference(args, cfg, rank: int):
-    if rank != 0:
-        return
-    threads = host_threads()
+# ---------------------------------------------------------------------------
+# CPU legs: the reference package itself (baseline/_ref)
+
+
+def load_reference():
+    """The unmodified reference package (pip-installed into baseline/_ref by
+    __graft_entry__.build()), or None."""
+    if (REF_DIR / "levsketch" / "__init__.py").exists():
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        import levsketch
+
+        return levsketch
+    return None
+
+
+class RefLeg:
+    """One step of the reference's own CPU implementation of the path on
+    `rows` rows of the config (inputs from synth.py generated on the host with
+    the same definitions).  kind = "reference" where the reference package
+    computes every stage; Gaussian sketches (which the reference rejects,
+    sketch.py:38-41) are the oracle's numpy restatement feeding the
+    reference's own SVD / truncation / basis / block scores."""
+
+    def __init__(self, name: str, cfg: dict, rows: int, threads: int):
+        import numpy as np
+
+        from paper_1812_07903_b200 import synth as S
+
+        self.name, self.cfg, self.rows, self.threads = name, cfg, rows, threads
+        self.R = load_reference()
+        self.kind = "reference" if self.R is not None else "port"
+        self.note = ""
+        d = cfg["d"]
+        if name == "c1":
+            self.x = S.gen_c1(0, "cpu").double().numpy()[:rows]
+            self.note = "Gaussian S restated (oracle numpy; the reference has no Gaussian family) + reference tail"
+            self.kind += "+port"
+        elif name == "c2":
+            self.x = S.gen_c2(0, "cpu", n=rows).double().numpy()
+        elif name == "c3":
+            self.x = S.gen_c3(0, "cpu", 0, rows).double().numpy()
+        elif name == "c4":
+            ip, ix, dv, shape = S.gen_c4(0, "cpu", 0, rows, arrays=True)
+            import scipy.sparse as sp
+
+            self.x = np.asarray(sp.csr_matrix((dv.double().numpy(), ix.numpy(), ip.numpy()), shape=shape).todense())
+            self.note = ("densified CSR rows through the reference consume_rows (the reference has no sparse input); "
+                         "the n-independent 16384 x 4096 SVD is excluded from the per-row rate")
+        else:
+            self.x = S.gen_c5(0, "cpu", 0, rows).double().numpy()
+            self.note = "Gaussian S restated (oracle numpy) on bf16 values upcast to float64 + reference tail"
+            self.kind += "+port"
+        self.n, self.d = self.x.shape
+
+    def spec(self):
+        c = self.cfg
+        fam = "osnap" if self.name == "c4" else c["family"]
+        return self.R.SketchSpec(fam, eps=0.5, d=c["d"], seed=0, rows_override=c["k"],
+                                 osnap_s=c["s"] if fam == "osnap" else None)
+
+    def step(self) -> float:
+        """Seconds for one pass over the rows."""
+        import numpy as np
+
+        from oracle import levsketch_oracle as O
+
+        c, R, x = self.cfg, self.R, self.x
+        t0 = time.perf_counter()
+        if R is None:  # no reference install: the oracle port (same algorithm)
+            if c["family"] == "countsketch":
+                scores, _, _ = O.pipeline_hashed(x, "countsketch", c["k"], 0, 1, c["sv_tol"], None,
+                                                 workers=self.threads)
+            elif c["family"] == "srht":
+                scores, _, _ = O.leverage_from_sketch(x, O.srht_sketch(x, c["k"], 0), c["sv_tol"])
+            elif self.name == "c4":
+                h = np.zeros((c["k"], self.d))
+                O.hashed_consume(h, np.zeros_like(h), O.HashParams("osnap", 0, c["k"], c["s"]), x, 0)
+                scores = O.row_scores(x, O.jl_matrix(0, self.d, c["r"]))
+            else:
+                scores, _, _ = O.leverage_from_sketch(x, O.gaussian_sketch(x, c["k"], 0), c["sv_tol"], None, c["rank"])
+            O.order(O.distribution(scores), "dec")
+            return time.perf_counter() - t0
+        if self.name == "c2":
+            res, _ = R.run_distributed(x, self.spec(), workers=self.threads, sv_tol=c["sv_tol"])
+            scores = res.scores
+        elif self.name == "c3":
+            scores = R.leverage_sketched_trunc(x, self.spec(), c["sv_tol"], mem_cap_bytes=1 << 40).scores
+        elif self.name == "c4":
+            st = R.SketchState(self.spec(), self.n, mem_cap=1 << 40)
+            for lo in range(0, self.n, 4096):
+                R.consume_rows(st, x[lo : lo + 4096], lo)
+            _ = st.data
+            t_sk = time.perf_counter() - t0
+            # the reference's scoring pass (_block_scores) with a d x r basis stand-in: the
+            # k x d SVD is n-independent and excluded (SURVEY §6)
+            basis = np.linalg.qr(O.jl_matrix(0, self.d, c["r"]))[0]
+            t1 = time.perf_counter()
+            scores = R.leverage._block_scores(x, basis)
+            R.make_plan(R.scores_to_distribution(scores), R.OrderingPolicy("dec"))
+            return t_sk + time.perf_counter() - t1
+        else:  # Gaussian configs (C1, C5)
+            sx = O.gaussian_sketch(x, c["k"], 0)
+            svd = R.truncate(R.thin_svd(sx), c["sv_tol"])
+            if c["rank"]:  # fixed-rank truncation (G4): the leading components of the SvdResult
+                svd = type(svd)(u=svd.u[:, : c["rank"]], sigma=svd.sigma[: c["rank"]], vt=svd.vt[: c["rank"]])
+            scores = R.leverage._block_scores(x, R.leverage._approx_basis(svd))
+        R.make_plan(R.scores_to_distribution(scores), R.OrderingPolicy("dec"))
+        return time.perf_counter() - t0
+
+    def describe(self, extra: str = "") -> str:
+        src = "reference package (baseline/_ref)" if self.R is not None else "oracle numpy port (reference not installed)"
+        api = {"c2": f"run_distributed(workers={self.threads}) + scores_to_distribution + make_plan('dec')",
+               "c3": "leverage_sketched_trunc(srht) + scores_to_distribution + make_plan('dec')"}.get(self.name, "")
+        return "; ".join(p for p in (f"{self.rows} rows x {self.d} of the {self.name} workload per step", src, api,
+                                     self.note, extra) if p)
+
+
+def _blas_threads(threads: int) -> None:
     try:
         from threadpoolctl import threadpool_limits
 
         threadpool_limits(threads)
     except ImportError:
         pass
-    # adaptive sample: the whole --steps K run should take about two minutes
-    rate, _ = cpu_leg(cfg, 20_000, threads)
-    per_step_s = 120.0 / max(1, args.steps)
-    # the sample grows up to the whole workload (the SVD / sort fixed costs then
-    # weigh on the CPU rate as they do on a full run)
-    cap = args.ref_rows if args.ref_rows else cfg["n"]
-    sample = int(min(cap, max(10_000, rate * per_step_s)))
+
+
+def run_reference(args, name: str, cfg: dict, rank: int, world: int):
+    if rank != 0:
+        return
+    threads = host_threads()
+    _blas_threads(threads)
+    lo, hi, _ = rows_of(name, cfg, 0, 1, args.rows)
+    full = hi - lo
+    # C4 / C5 have no tractable full-size CPU step (C4's sketch extrapolates to ~2100 s,
+    # C5's float64 X is 65 GB): a bounded row sample, labelled
+    rows = {"c4": 16_384, "c5": 131_072}.get(name, full)
+    if args.ref_rows:
+        rows = min(rows, args.ref_rows)
+    leg = RefLeg(name, cfg, rows, threads)
+    for _ in range(args.warmup):
+        leg.step()
     times = []
+    budget = args.ref_budget_s
+    t_start = time.perf_counter()
     for _ in range(args.steps):
-        _, dt = cpu_leg(cfg, sample, threads)
-        times.append(dt)
+        times.append(leg.step())
+        if time.perf_counter() - t_start > budget:
+            break  # C3 (~60 s per full step): fewer timed steps, never fewer rows
     total = sum(times)
-    value = sample * args.steps / total
+    value = rows * len(times) / total
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": value,
         "unit": UNIT,
-        "n_gpus": args.gpus,
+        "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1000 * total / args.steps,
+        "ms_per_step": 1000 * total / len(times),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if name == "c5" else "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": cfg["desc"], "rows_per_step": sample, "note": "bounded row sample per step"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} rows x {cfg['d']} of the {args.config} workload per step "
-                                   "(oracle/levsketch_oracle.py numpy port of the reference path, "
-                                   "row partitions in threads + BLAS threads)"},
+        "data": "synthetic (seeded; synth.py generators on the host)",
+        "config": config_line(name, cfg, full, 1),
+        "rows_per_step": rows,
+        "same_config": rows == full,
+        "steps_timed": len(times),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": leg.kind,
+                         "sample": leg.describe("full workload per step" if rows == full else "bounded row sample")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -298,7 +358,7 @@ def run_reference(args, cfg, rank: int):
 # GPU arm
 
 
-def run_ours(args, cfg, rank: int, world: int, local_rank: int):
+def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -311,29 +371,40 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
-    n, d, k, r = cfg["n"], cfg["d"], cfg["k"], cfg["r"]
-    spec = P.SketchSpec(cfg["family"], eps=0.5, d=d, seed=0, rows_override=k, osnap_s=cfg["s"])
-    X = gen_x(cfg, rank, dev)
-    csr = cfg.get("csr", False)
+    d, k, r = cfg["d"], cfg["k"], cfg["r"]
+    csr = bool(cfg.get("csr"))
+    fam = cfg["family"]
+    lo, hi, n_total = rows_of(name, cfg, rank, world, args.rows)
+    n = hi - lo
+    spec = P.SketchSpec(fam, eps=0.5, d=d, seed=0, rows_override=k, osnap_s=cfg["s"])
+    X = gen_local(name, rank, lo, hi, dev)
     if not csr:
-        X = X.to(dtype)
+        X = X.to(dtype).contiguous()
     torch.cuda.synchronize()
-    row0 = rank * n
-    pipe = P.LeveragePipeline(spec, n * world if world > 1 else n, d, dtype, sv_tol=cfg["sv_tol"], jl_dim=r,
+    row0 = lo
+    pipe = P.LeveragePipeline(spec, n_total if world > 1 else n, d, dtype, sv_tol=cfg["sv_tol"], jl_dim=r,
                               rank=cfg.get("rank"), order=(world == 1), row0=row0)
     if world > 1:
-        pipe.n = n  # local rows; the state covers n*world global rows
+        pipe.n = n  # local rows; the state covers n_total global rows
         pipe.scores = torch.empty(n, dtype=torch.float64, device=dev)
-    # multi-rank global order: double-buffered so rank 0 sorts step i's probabilities on a
-    # side stream while step i+1 sketches (the 8M-key sort would otherwise sit on the
-    # critical path of every step at N = 8)
-    gather_p = [torch.empty(n * world, dtype=torch.float64, device=dev) for _ in range(2)] if world > 1 else None
-    order_all = [torch.empty(n * world, dtype=torch.int64, device=dev) for _ in range(2)] if world > 1 else None
+    # multi-rank global order: rank 0 sorts the gathered probabilities of step i on a
+    # side stream while step i+1 sketches; the timed region ends after the last sort
+    gather_p = [torch.empty(n_total, dtype=torch.float64, device=dev) for _ in range(2)] \
+        if world > 1 and rank == 0 else None
+    order_all = [torch.empty(n_total, dtype=torch.int64, device=dev) for _ in range(2)] \
+        if world > 1 and rank == 0 else None
     side = torch.cuda.Stream(device=dev) if world > 1 else None
     sort_done = [None, None]
     buf = [0]
-    ws_sort = torch.empty(max(N.lib().lvsk_argsort_workspace_bytes(n * world), 256), dtype=torch.uint8, device=dev)
+    ws_sort = torch.empty(max(N.lib().lvsk_argsort_workspace_bytes(n_total), 256), dtype=torch.uint8, device=dev) \
+        if world > 1 and rank == 0 else None
     pi = jl_device(0, d, r)
+    counts = counts_of(name, cfg, world, args.rows)
+    even = len(set(counts)) == 1
+    p_pad = torch.zeros(max(counts), dtype=torch.float64, device=dev) if world > 1 and not even else None
+    parts = [torch.empty(max(counts), dtype=torch.float64, device=dev) for _ in range(world)] \
+        if world > 1 and rank == 0 and not even else None
+    nnz = X.nnz if csr else None
 
     def step(timing=False):
         if world == 1:
@@ -344,7 +415,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         if timing:
             ev["sketch"][0].record()
         s = pipe.state
-        if cfg["family"] == "srht":
+        if fam == "srht":
             # extension G7 (the reference's run_distributed rejects SRHT, dist.py:95-98): the
             # one-pass K3 over this rank's 2048-aligned global row block, partials all-reduced
             N.check(N.lib().lvsk_srht_rows(X.data_ptr(), n, d, X.stride(0), row0, s._m, s._signs_dev.data_ptr(),
@@ -355,14 +426,15 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             pipe._sketch(X)
         if timing:
             ev["sketch"][1].record()
-        if cfg["family"] in ("gaussian", "srht"):  # a plain float64 partial per rank
+        if fam in ("gaussian", "srht"):  # a plain float64 partial per rank
             dist.all_reduce(pipe.sx)
         else:  # hashed: row slices exchanged all-to-all, rank-ordered TwoSum merge, folded slices gathered
             pipe.sx.copy_(sliced_hashed_merge(s._hi, s._lo, rank, world))
         if timing:
             ev["factor"][0].record()
         # every rank holds the same SX: the fold is computed redundantly (deterministic
-        # kernels, identical M) instead of folding on rank 0 and broadcasting
+        # kernels, identical M) instead of folding on rank 0 and broadcasting M — a
+        # broadcast would only add its latency to the critical path
         M = sketch_fold(pipe.sx, cfg["sv_tol"], cfg.get("rank"), pi)[0].contiguous()
         pipe.set_fold(M)
         if timing:
@@ -372,25 +444,34 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         if timing:
             ev["leverage"][1].record()
             ev["order"][0].record()
-        # global dec order: p = s / global sum, gathered on every rank, sorted on rank 0
+        # global dec order: p = s / global sum, gathered to rank 0 only, sorted there
         local_sum = pipe.scores.sum().reshape(1)
         dist.all_reduce(local_sum)
         p_local = pipe.scores / local_sum
-        b = buf[0]
-        buf[0] ^= 1
-        if sort_done[b] is not None:  # the sort of two steps ago has released this buffer
-            torch.cuda.current_stream().wait_event(sort_done[b])
-        dist.all_gather_into_tensor(gather_p[b], p_local)
+        if not even:  # equal-size gather: pad to the largest partition
+            p_pad[:n] = p_local
+            p_local = p_pad
         if rank == 0:
+            b = buf[0]
+            buf[0] ^= 1
+            if sort_done[b] is not None:  # the sort of two steps ago has released this buffer
+                torch.cuda.current_stream().wait_event(sort_done[b])
+            if even:
+                gather0(p_local, list(gather_p[b].view(world, n).unbind(0)))
+            else:
+                gather0(p_local, parts)
+                torch.cat([parts[q][: counts[q]] for q in range(world)], out=gather_p[b])
             ready = torch.cuda.Event()
             ready.record()
             side.wait_event(ready)
             with torch.cuda.stream(side):
-                N.check(N.lib().lvsk_argsort_f64(gather_p[b].data_ptr(), n * world, 1, order_all[b].data_ptr(),
+                N.check(N.lib().lvsk_argsort_f64(gather_p[b].data_ptr(), n_total, 1, order_all[b].data_ptr(),
                                                  ws_sort.data_ptr(), ws_sort.numel(), N.stream_ptr()))
                 done = torch.cuda.Event()
                 done.record()
             sort_done[b] = done
+        else:
+            gather0(p_local, None)
         if timing:
             ev["order"][1].record()
 
@@ -398,39 +479,53 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         if world > 1:
             dist.barrier()
 
+    def drain_sorts():
+        # the timed region includes rank 0's last global sort
+        if world > 1 and rank == 0:
+            for e in sort_done:
+                if e is not None:
+                    torch.cuda.current_stream().wait_event(e)
+
     for _ in range(args.warmup):
         step()
+    drain_sorts()
     torch.cuda.synchronize()
     pipe.check()
     barrier()
 
-    # ---- timed region (device events; inputs 2 GB >> 126 MB L2) ----
+    # ---- timed region (device events; inputs >> 126 MB L2) ----
     stage_sum = {"sketch": 0.0, "factor": 0.0, "leverage": 0.0, "order": 0.0}
     gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0]) if os.environ.get(
         "CUDA_VISIBLE_DEVICES", "").strip().isdigit() else local_rank
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fails0 = pipe.cert_failures() if world == 1 else 0
     with ClockSampler(gpu_index) as clocks:
         torch.cuda.synchronize()
         barrier()
         start.record()
         for _ in range(args.steps):
             step(timing=True)
-            for name, ms in pipe.stage_ms().items() if args.stage_sync else ():
-                stage_sum[name] += ms
+            for name_, ms in pipe.stage_ms().items() if args.stage_sync else ():
+                stage_sum[name_] += ms
+        drain_sorts()
         stop.record()
         torch.cuda.synchronize()
         barrier()
     elapsed_ms = start.elapsed_time(stop)
+    if world == 1 and pipe.cert_failures() != fails0:
+        # an optimistic fold inside the timed region failed its certificate: the timed
+        # steps used an uncertified M — the number is void, fail loudly
+        raise SystemExit(f"bench: {pipe.cert_failures() - fails0} timed step(s) ran on an uncertified fold")
     if not args.stage_sync:
         # stage events of the last step only (no extra syncs inside the timed loop)
-        for name, ms in pipe.stage_ms().items():
-            stage_sum[name] = ms * args.steps
+        for name_, ms in pipe.stage_ms().items():
+            stage_sum[name_] = ms * args.steps
     if world > 1 and rank == 0:
         # the last global order is a descending permutation of the gathered probabilities
         lb = buf[0] ^ 1
         o = order_all[lb]
         ps = gather_p[lb][o]
-        ok = bool((ps[:-1] >= ps[1:]).all()) and bool((torch.bincount(o, minlength=n * world) == 1).all())
+        ok = bool((ps[:-1] >= ps[1:]).all()) and bool((torch.bincount(o, minlength=n_total) == 1).all())
         if not ok:
             raise SystemExit("bench: multi-rank global order failed its check")
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
@@ -439,16 +534,18 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     elapsed_ms = float(t.item())
     pipe.check()
     ms_per_step = elapsed_ms / args.steps
-    rows_total = n * world
-    value = rows_total / (ms_per_step / 1000.0)
+    value = n_total / (ms_per_step / 1000.0)
+
+    if args.verify:
+        verify(args, name, cfg, X, pipe, rank, world, n, n_total, lo, gather_p, order_all, buf, dev)
 
     # ---- per-kernel roofline (algorithmic bytes / event-timed duration) ----
     peak, peak_src = measured_peaks()
     elt = 4 if csr else X.element_size()
-    x_bytes = (X.nnz * 8 + 8 * (n + 1)) if csr else n * d * elt  # CSR: int32 col + f32 val + int64 row_ptr
+    x_bytes = (nnz * 8 + 8 * (n + 1)) if csr else n * d * elt  # CSR: int32 col + f32 val + int64 row_ptr
     stage_ms = {k_: v / args.steps for k_, v in stage_sum.items()}
     lev_bytes = x_bytes + 8 * n  # X once + float64 scores
-    sk_bytes = x_bytes + 2 * 8 * k * d  # X once + compensated state write (the kernel reads CSR rows s times)
+    sk_bytes = x_bytes + 2 * 8 * k * d  # X once + compensated state write
     lev_gbs = lev_bytes / (stage_ms["leverage"] / 1000) / 1e9 if stage_ms.get("leverage") else None
     sk_gbs = sk_bytes / (stage_ms["sketch"] / 1000) / 1e9 if stage_ms.get("sketch") else None
     dominant = "sketch" if stage_ms.get("sketch", 0) >= stage_ms.get("leverage", 0) else "leverage"
@@ -458,21 +555,23 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(f"{args.config}:{dominant}")
+            traffic = json.loads(tf.read_text()).get(f"{name}:{dominant}")
         except (ValueError, OSError):
             traffic = None
+    kernels = {
+        "sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
+                   "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
+                   "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
+                   "srht": "srht_sampled_kernel (K3 v3: one pass, block WHT + sampled combine)",
+                   "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
+                   if dtype == torch.bfloat16 else
+                   "split3_bf16_kernel + 3 x gaussian_tc_kernel (K4-TC on the exact bf16 planes of fp32 X) + reduce"}[fam],
+        "leverage": "csr_rowsumsq_kernel (K6)" if csr else
+                    ("leverage_bf16_kernel (K5, tcgen05 kind::f16)" if dtype == torch.bfloat16 else
+                     "leverage_v2_kernel (K5, tcgen05)")}
     roofline = {
         "bound": "hbm",
-        "kernel": {"sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
-                              "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
-                              "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
-                              "srht": "srht_sampled_kernel (K3 v3: one pass, block WHT + sampled combine)",
-                              "gaussian": "gaussian_gemm_kernel (K4, SIMT)" if csr else
-                              "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
-                              if X.dtype == torch.bfloat16 else
-                              "split3_bf16_kernel + 3 x gaussian_tc_kernel (K4-TC on the exact bf16 planes of fp32 X) + reduce"
-                              if X.dtype == torch.float32 else "gaussian_gemm_kernel (K4, SIMT)"}[cfg["family"]],
-                   "leverage": "csr_rowsumsq_kernel (K6)" if csr else "leverage_v2_kernel (K5, tcgen05)"}[dominant],
+        "kernel": kernels[dominant],
         "achieved": dom_gbs,
         "peak": peak,
         "unit": "GB/s",
@@ -481,9 +580,9 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         "algorithmic_bytes_per_launch": dom_bytes,
         "peak_source": peak_src,
     }
-    if dominant == "sketch" and cfg["family"] == "gaussian" and not csr and X.dtype in (torch.bfloat16, torch.float32):
-        # K4-TC is a GEMM: 2*k*n*d algorithmic flop per launch (fp32 X runs it on three exact
-        # bf16 planes: 3x the tensor work for the same algorithmic flops) against the bf16 tensor peak
+    if dominant == "sketch" and fam == "gaussian" and not csr:
+        # K4-TC is a GEMM: 2*k*n*d algorithmic flop per launch against the bf16 tensor peak
+        # (fp32 X runs it on three exact bf16 planes: 3x the tensor work for the same flops)
         tpeak, tsrc = measured_tensor_peak()
         flops = 2.0 * k * n * d
         ach = flops / (stage_ms["sketch"] / 1000) / 1e12
@@ -497,7 +596,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         "order_ms": stage_ms.get("order"),
     }
 
-    # ---- e2e through the public API with host buffers (rank 0 view) ----
+    # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
         if csr:
@@ -510,12 +609,12 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
         def e2e_step():
             if world == 1:
                 # C3's SRHT transform buffer (4.3 GB) exceeds the reference's 4 GiB default cap (G8)
-                cap = (16 << 30) if cfg["family"] == "srht" else None
+                cap = (16 << 30) if fam == "srht" else None
                 res = P.leverage_sketched_trunc(Xh, spec, cfg["sv_tol"], mem_cap_bytes=cap, jl_dim=r,
                                                 rank=cfg.get("rank"))
                 plan = P.make_plan(P.scores_to_distribution(res.scores), P.OrderingPolicy("dec"))
                 return plan.indices
-            local, *_ = P.run_sharded(Xh, row0, n * world, spec, cfg["sv_tol"], jl_dim=r)
+            local, *_ = P.run_sharded(Xh, row0, n_total, spec, cfg["sv_tol"], jl_dim=r)
             return local.cpu()
 
         e2e_step()
@@ -530,24 +629,16 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         h2d = x_bytes + (2 * 8 * n if world == 1 else 0)
         d2h = (3 * 8 * n) if world == 1 else 8 * n
-        e2e = {"value": rows_total / float(e2e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": n_total / float(e2e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                "api": "leverage_sketched_trunc(pinned host X) -> scores_to_distribution -> make_plan('dec')"
                if world == 1 else "run_sharded(pinned host shard)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = host_threads()
-        # calibrate, then repeat a bounded sample until ~10 s of CPU work has been timed
-        rate, _ = cpu_leg(cfg, 20_000, threads)
-        rows = int(min(args.cpu_rows, max(20_000, rate * args.cpu_seconds / 2)))
-        total_rows, total_s, passes = 0, 0.0, 0
-        while total_s < args.cpu_seconds and passes < 25:
-            _, dt = cpu_leg(cfg, rows, threads)
-            total_rows, total_s, passes = total_rows + rows, total_s + dt, passes + 1
-        cpu = {"value": total_rows / total_s, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{passes} x {rows} rows of the {args.config} workload ({total_s:.1f} s timed), oracle "
-                         "numpy port of the reference path incl. SVD and dec argsort, sketch partitions in threads"}
+        del X
+        torch.cuda.empty_cache()
+        cpu = cpu_baseline(args, name, cfg)
 
     if rank == 0:
         line = {
@@ -559,14 +650,11 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if name == "c5" else "weak",
             "vs_baseline": None,
             "dtype": {"f32": "f32", "bf16": "bf16"}[cfg["dtype"]],
-            "data": "synthetic (seeded, generated on device; random-init, no dataset)",
-            "config": {"workload": cfg["desc"], "rows_per_gpu": n, "d": d, "k": k, "jl_r": r,
-                       "sv_tol": cfg["sv_tol"], "parallelism": f"row-partition x{world}",
-                       "l2": f"inputs larger than L2 (X = {x_bytes / 1e9:.2f} GB per GPU)",
-                       **({"nnz": X.nnz} if csr else {})},
+            "data": "synthetic (seeded synth.py generators on the device; random-init, no dataset)",
+            "config": config_line(name, cfg, n, world),
             "stages_ms": other,
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -574,7 +662,88 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             "gpu_launches": pipe.launches_per_run() * args.steps,
             "clocks": clocks.summary(),
         }
+        if csr:
+            line["nnz_per_gpu"] = nnz
         print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, name: str, cfg: dict):
+    """The reference's CPU implementation (RefLeg) on a bounded sample of the
+    workload, rank 0 at N=1: ~args.cpu_seconds of CPU work."""
+    threads = host_threads()
+    _blas_threads(threads)
+    probe_rows = {"c1": cfg["n"], "c4": 2048, "c5": 16_384}.get(name, 100_000)
+    probe = RefLeg(name, cfg, probe_rows, threads)
+    dt = probe.step()
+    rate = probe_rows / dt
+    full = cfg["n"]
+    rows = int(min(full, max(probe_rows, rate * args.cpu_seconds / 2)))
+    rows = min(rows, {"c4": 16_384, "c5": 131_072}.get(name, rows))
+    leg = probe if rows == probe_rows else RefLeg(name, cfg, rows, threads)
+    total_rows, total_s, passes = 0, 0.0, 0
+    while total_s < args.cpu_seconds and passes < 10:
+        dt = leg.step()
+        total_rows, total_s, passes = total_rows + rows, total_s + dt, passes + 1
+    return {"value": total_rows / total_s, "unit": UNIT, "cores": threads, "kind": leg.kind,
+            "sample": leg.describe(f"{passes} passes, {total_s:.1f} s timed")}
+
+
+def verify(args, name, cfg, X, pipe, rank, world, n, n_total, lo, gather_p, order_all, buf, dev):
+    """--verify (small --rows): the multi-rank step's merged SX, scores and
+    global order against the CPU oracle over the concatenated global rows."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from oracle import levsketch_oracle as O
+
+    xs = X.to_dense().double() if hasattr(X, "to_dense") else X.double()
+    if world > 1:
+        # every rank's rows and scores to rank 0 (uneven partitions padded)
+        mx = max(counts_of(name, cfg, world, args.rows))
+        xb = torch.zeros((mx, xs.shape[1]), dtype=torch.float64, device=dev)
+        xb[: xs.shape[0]] = xs
+        sb = torch.zeros(mx, dtype=torch.float64, device=dev)
+        sb[:n] = pipe.scores
+        parts = [torch.empty_like(xb) for _ in range(world)] if rank == 0 else None
+        gather0(xb, parts)
+        sc = [torch.empty_like(sb) for _ in range(world)] if rank == 0 else None
+        gather0(sb, sc)
+        if rank != 0:
+            return
+        cnt = counts_of(name, cfg, world, args.rows)
+        x = torch.cat([parts[q][: cnt[q]] for q in range(world)]).cpu().numpy()
+        scores = torch.cat([sc[q][: cnt[q]] for q in range(world)]).cpu().numpy()
+        order = order_all[buf[0] ^ 1].cpu().numpy()
+        p = gather_p[buf[0] ^ 1].cpu().numpy()
+    else:
+        x = xs.cpu().numpy()
+        scores = pipe.scores.cpu().numpy()
+        order = pipe.idx.cpu().numpy()
+        p = pipe.p.cpu().numpy()
+    sx = pipe.sx.cpu().numpy()
+    c = cfg
+    pi = O.jl_matrix(0, c["d"], c["r"])
+    if c["family"] in ("countsketch", "osnap"):
+        hi, lo_ = O.hashed_sketch(x, c["family"], c["k"], 0, c["s"] or 1)
+        sx_err = 0.0
+        assert np.array_equal(sx, hi + lo_), "merged sketch differs from the oracle's"
+    elif c["family"] == "srht":
+        sx_o = O.srht_sketch(x, c["k"], 0, n_rows=n_total)
+        sx_err = float(np.linalg.norm(sx - sx_o) / np.linalg.norm(sx_o))
+    else:
+        sx_o = O.gaussian_sketch(x, c["k"], 0)
+        sx_err = float(np.linalg.norm(sx - sx_o) / np.linalg.norm(sx_o))
+    assert sx_err <= 1e-4, f"sketch rel err {sx_err}"
+    # fold + leverage pass + order, from the device sketch (the fold of a near-degenerate
+    # spectrum amplifies sketch rounding; the sketch itself is checked just above)
+    ref, _, _ = O.leverage_from_sketch(x, sx, c["sv_tol"], pi, c.get("rank"))
+    rel = float(np.max(np.abs(scores - ref) / np.maximum(ref, 1e-300)))
+    assert rel <= (2e-2 if c["dtype"] == "bf16" else 1e-4), f"scores rel err {rel}"
+    assert np.array_equal(order, np.argsort(-p, kind="stable")), "global order is not the stable argsort"
+    assert np.allclose(p, scores / scores.sum(), rtol=1e-12, atol=0)
+    print(json.dumps({"verify": "ok", "config": name, "world": world, "rows": int(x.shape[0]), "sketch_rel": sx_err,
+                      "score_max_rel": rel}), flush=True)
 
 
 def main():
@@ -583,21 +752,26 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--rows", type=int, default=0, help="rows per rank (0: the config's n) — tests only")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-rows", type=int, default=500_000)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-rows", type=int, default=0, help="cap on the reference arm's rows per step (0: the workload's n)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-rows", type=int, default=0, help="cap on the reference arm's rows per step (0: full)")
+    ap.add_argument("--ref-budget-s", type=float, default=240.0, help="reference arm: stop timing steps after this")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--verify", action="store_true", help="check the results against the oracle (small --rows)")
     ap.add_argument("--stage-sync", action="store_true", help="sync after every step to sum stage times")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # the timing rules: at least 3 untimed warm-up steps
+    name = args.config
+    cfg = configs()[name]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, cfg, rank)
+        run_reference(args, name, cfg, rank, world)
         return
     # LVSK_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo — a correctness
     # check of the multi-rank code path on a one-GPU box, never a measurement
@@ -614,7 +788,7 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, cfg, rank, world, local_rank)
+        run_ours(args, name, cfg, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

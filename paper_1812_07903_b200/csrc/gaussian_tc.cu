@@ -69,6 +69,28 @@ __device__ __forceinline__ uint64_t l2_policy_evict_normal() {
   return p;
 }
 
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// 4-byte store into a peer CTA's shared memory that completes 4 bytes of the
+// transaction count of the peer's mbarrier (no release fence: the barrier
+// carries the ordering)
+__device__ __forceinline__ void st_async_b32(uint32_t remote_addr, uint32_t v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr), "r"(v),
+               "r"(remote_bar)
+               : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -86,10 +108,18 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t*
 // (column slab, split); each issues half of every X stage's boxes with TMA
 // multicast to both, so X crosses L2 -> SM once per pair, and a slot is
 // refilled only after both CTAs' MMAs released it (commit multicast).
-// MX = 1: one CTA per (k tile, column slab, split).  Every CTA generates its
-// whole Z tile (a 2-CTA DSMEM-sharing variant paid more in cluster-scope
-// release fences than it saved: C5 5.25 vs 3.68 ms in round 1).
-template <int NS, int MX>
+// CL = 2 (d in (NS, 2 NS]): the two column slabs of a k tile form a cluster
+// and share its Z tile: each CTA generates half of the tile's rows and writes
+// them into its own shared memory (st.shared) and into the peer's
+// (st.async, completing bytes of the peer's zfull transaction count), so
+// every Z entry is generated once per k tile instead of once per slab — the
+// 16-bit table lookups (random banks, ~3.5 wavefronts per warp read) are the
+// kernel's shared-memory bound.  Round 1's version of this signalled the
+// peer with cluster-scope release arrives and lost (5.25 vs 3.68 ms); the
+// transaction-count form needs no fence.
+// Otherwise one CTA per (k tile, column slab, split), generating its whole Z
+// tile.  CL and MX are not combined.
+template <int NS, int CL, int MX>
 __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
                        uint64_t key, int ktiles, int dslabs, int64_t rows_per_split,
@@ -108,9 +138,17 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int item = blockIdx.x;
-  const int ktile = item % ktiles;
-  const int dslab = (item / ktiles) % dslabs;
-  const int64_t split = item / (ktiles * dslabs);
+  int ktile, dslab;
+  int64_t split;
+  if constexpr (CL == 1) {
+    ktile = item % ktiles;
+    dslab = (item / ktiles) % dslabs;
+    split = item / (ktiles * dslabs);
+  } else {  // cluster rank = column slab
+    dslab = item % CL;
+    ktile = (item / CL) % ktiles;
+    split = item / (CL * ktiles);
+  }
   const int64_t r_begin = split * rows_per_split;
   const int64_t r_end = r_begin + rows_per_split < n ? r_begin + rows_per_split : n;
   const int nstages = static_cast<int>((r_end - r_begin + C::BKN - 1) / C::BKN);
@@ -122,8 +160,8 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       mbar_init(&empty[s], MX);
     }
     for (int s = 0; s < C::SZ; ++s) {
-      mbar_init(&zfull[s], C::GEN_WARPS);
-      mbar_init(&zempty[s], 1);
+      mbar_init(&zfull[s], C::GEN_WARPS);  // + (CL = 2) the peer's half of the tile as transaction bytes
+      mbar_init(&zempty[s], CL);           // every CTA's MMA that reads the slot
     }
     mbar_init(accfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -138,7 +176,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if constexpr (MX > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
+  if constexpr (CL > 1 || MX > 1) cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -168,7 +206,10 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
         const uint32_t s = t % C::S, ph = (t / C::S) & 1u;
         const uint32_t sz = t % C::SZ, phz = (t / C::SZ) & 1u;
         mbar_wait(&xfull[s], ph);
-        mbar_wait(&zfull[sz], phz);
+        if constexpr (CL > 1)
+          mbar_wait_cluster(&zfull[sz], phz);  // half of the tile came from the peer
+        else
+          mbar_wait(&zfull[sz], phz);
         // the Z tile was written through the generic proxy; one proxy fence
         // here, after the acquire, orders it before the tensor core's
         // async-proxy reads (instead of one per producer warp)
@@ -192,50 +233,99 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
               : "memory");
         else
           umma_commit(&empty[s]);
-        umma_commit(&zempty[sz]);
+        if constexpr (CL > 1)  // both CTAs write this Z slot: both MMAs release it
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&zempty[sz])),
+              "h"(static_cast<uint16_t>((1u << CL) - 1u))
+              : "memory");
+        else
+          umma_commit(&zempty[sz]);
       }
       umma_commit(accfull);
     }
   } else {
     const int gw = warp - 2;
-    // ---- Z generation: warp gw -> sketch rows 8gw .. 8gw+7 of the tile
-    //      (quads t0, t0 + 1), lane -> input rows 2*lane, 2*lane+1 of the
-    //      stage: four mix64 per lane per stage, counters advanced by
-    //      constant adds (gauss_ctr is linear in (i << 24) | t)
-    const uint32_t t0 = static_cast<uint32_t>(ktile * (BM / 4) + 2 * gw);
-    uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(r_begin + 2 * lane), t0);
-    constexpr uint64_t ROW = GAUSS_PHI << 24;             // next input row
-    constexpr uint64_t STAGE = GAUSS_PHI << 30;           // 64 input rows on
+    constexpr uint64_t ROW = GAUSS_PHI << 24;    // next input row
+    constexpr uint64_t STAGE = GAUSS_PHI << 30;  // 64 input rows on
     const uint32_t mbase = smem_u32(mag);
-    for (int t = 0; t < nstages; ++t, ctr += STAGE) {
-      const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
-      // h[r][q]: input row 2 lane + r, quad t0 + q
-      const uint64_t h00 = mix64(ctr), h01 = mix64(ctr + GAUSS_PHI);
-      const uint64_t h10 = mix64(ctr + ROW), h11 = mix64(ctr + ROW + GAUSS_PHI);
-      uint32_t w[8];  // sketch row 8 gw + r8: bf16 pair (input row 2 lane, 2 lane + 1)
+    if constexpr (CL == 1) {
+      // ---- Z generation: warp gw -> sketch rows 8gw .. 8gw+7 of the tile
+      //      (quads t0, t0 + 1), lane -> input rows 2*lane, 2*lane+1 of the
+      //      stage: four mix64 per lane per stage, counters advanced by
+      //      constant adds (gauss_ctr is linear in (i << 24) | t)
+      const uint32_t t0 = static_cast<uint32_t>(ktile * (BM / 4) + 2 * gw);
+      uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(r_begin + 2 * lane), t0);
+      for (int t = 0; t < nstages; ++t, ctr += STAGE) {
+        const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
+        // h[r][q]: input row 2 lane + r, quad t0 + q
+        const uint64_t h00 = mix64(ctr), h01 = mix64(ctr + GAUSS_PHI);
+        const uint64_t h10 = mix64(ctr + ROW), h11 = mix64(ctr + ROW + GAUSS_PHI);
+        uint32_t w[8];  // sketch row 8 gw + r8: bf16 pair (input row 2 lane, 2 lane + 1)
 #pragma unroll
-      for (int r8 = 0; r8 < 8; ++r8) {
-        const uint64_t ha = r8 < 4 ? h00 : h01, hb = r8 < 4 ? h10 : h11;
-        const uint32_t fa = static_cast<uint32_t>(ha >> (16 * (r8 & 3)));
-        const uint32_t fb = static_cast<uint32_t>(hb >> (16 * (r8 & 3)));
-        uint16_t ma, mb;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(ma) : "r"(mbase + 2 * (fa & 0x7FFFu)));
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(mb) : "r"(mbase + 2 * (fb & 0x7FFFu)));
-        const uint32_t za = static_cast<uint32_t>(ma) | (fa & 0x8000u);
-        const uint32_t zb = static_cast<uint32_t>(mb) | (fb & 0x8000u);
-        w[r8] = za | (zb << 16);
-      }
-      mbar_wait(&zempty[s], ph ^ 1u);
-      uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
+        for (int r8 = 0; r8 < 8; ++r8) {
+          const uint64_t ha = r8 < 4 ? h00 : h01, hb = r8 < 4 ? h10 : h11;
+          const uint32_t fa = static_cast<uint32_t>(ha >> (16 * (r8 & 3)));
+          const uint32_t fb = static_cast<uint32_t>(hb >> (16 * (r8 & 3)));
+          uint16_t ma, mb;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(ma) : "r"(mbase + 2 * (fa & 0x7FFFu)));
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(mb) : "r"(mbase + 2 * (fb & 0x7FFFu)));
+          w[r8] = (static_cast<uint32_t>(ma) | (fa & 0x8000u)) | ((static_cast<uint32_t>(mb) | (fb & 0x8000u)) << 16);
+        }
+        mbar_wait(&zempty[s], ph ^ 1u);
+        uint8_t* zt = smem + C::OFF_Z + s * C::Z_BYTES;
 #pragma unroll
-      for (int r8 = 0; r8 < 8; ++r8) {
-        const int j = 8 * gw + r8;
-        // row j: 128 B = 8 swizzled 16-byte chunks; lane owns bytes [4 lane, 4 lane + 4)
-        const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
-        *reinterpret_cast<uint32_t*>(zt + off) = w[r8];
+        for (int r8 = 0; r8 < 8; ++r8) {
+          const int j = 8 * gw + r8;
+          // row j: 128 B = 8 swizzled 16-byte chunks; lane owns bytes [4 lane, 4 lane + 4)
+          const int off = j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
+          *reinterpret_cast<uint32_t*>(zt + off) = w[r8];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&zfull[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&zfull[s]);
+    } else {
+      // ---- Z generation, cluster of 2: this CTA (rank = dslab) makes tile
+      //      rows [64 rank, 64 rank + 64): warp gw -> rows 64 rank + 4 gw ..
+      //      +3 (one quad), lane -> input rows 2 lane, 2 lane + 1; each word
+      //      goes to both CTAs' Z slot
+      const uint32_t peer = static_cast<uint32_t>(dslab ^ 1);
+      const int jbase = 64 * dslab + 4 * gw;
+      const uint32_t t0 = static_cast<uint32_t>(ktile * (BM / 4) + jbase / 4);
+      uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(r_begin + 2 * lane), t0);
+      const uint32_t zloc = smem_u32(smem + C::OFF_Z);
+      const uint32_t zrem = map_peer(zloc, peer);
+      const uint32_t fullrem = map_peer(smem_u32(&zfull[0]), peer);
+      for (int t = 0; t < nstages; ++t, ctr += STAGE) {
+        const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
+        const uint64_t h0 = mix64(ctr), h1 = mix64(ctr + ROW);
+        uint32_t w[4];
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) {
+          const uint32_t fa = static_cast<uint32_t>(h0 >> (16 * r4));
+          const uint32_t fb = static_cast<uint32_t>(h1 >> (16 * r4));
+          uint16_t ma, mb;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(ma) : "r"(mbase + 2 * (fa & 0x7FFFu)));
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(mb) : "r"(mbase + 2 * (fb & 0x7FFFu)));
+          w[r4] = (static_cast<uint32_t>(ma) | (fa & 0x8000u)) | ((static_cast<uint32_t>(mb) | (fb & 0x8000u)) << 16);
+        }
+        mbar_wait_cluster(&zempty[s], ph ^ 1u);  // both CTAs' MMAs are done with this slot
+        const uint32_t slot = static_cast<uint32_t>(s * C::Z_BYTES);
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) {
+          const int j = jbase + r4;
+          const uint32_t off = slot + j * 128 + ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4;
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(zloc + off), "r"(w[r4]) : "memory");
+          st_async_b32(zrem + off, w[r4], fullrem + 8 * s);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (gw == 0)  // this CTA's arrival also announces the peer's 8 KB half
+            mbar_expect_tx(&zfull[s], 64 * 128);
+          else
+            mbar_arrive(&zfull[s]);
+        }
+      }
     }
     // ---- epilogue: TMEM -> fp32 partial
     mbar_wait(accfull, 0);
@@ -271,7 +361,7 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(NS));
   }
-  if constexpr (MX > 1) cluster_sync_all();  // no CTA leaves while its peer may still write into it
+  if constexpr (CL > 1 || MX > 1) cluster_sync_all();  // no CTA leaves while its peer may still write into it
 }
 
 }  // namespace tc
@@ -298,7 +388,7 @@ bool gaussian_tc_ok(const void* X, int64_t n, int64_t d, int64_t ldx, int64_t k)
   return true;
 }
 
-template <int NS, int MX>
+template <int NS, int CL, int MX>
 static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
                                uint64_t key, const GaussTcPlan& p, float* partial, cudaStream_t st) {
   using C = tc::CfgG<NS>;
@@ -307,7 +397,7 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
     set_error("cuTensorMapEncodeTiled failed");
     return LVSK_ERR_CUDA;
   }
-  const int32_t rc = ensure_smem_attr(reinterpret_cast<const void*>(tc::gaussian_tc_kernel<NS, MX>), C::SMEM_BYTES,
+  const int32_t rc = ensure_smem_attr(reinterpret_cast<const void*>(tc::gaussian_tc_kernel<NS, CL, MX>), C::SMEM_BYTES,
                                       "gaussian tc smem attribute");
   if (rc != LVSK_OK) return rc;
   const int64_t items = static_cast<int64_t>(p.ktiles) * p.dslabs * p.splits;
@@ -323,12 +413,12 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = MX;
+  attrs[0].val.clusterDim.x = CL * MX;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, MX>, mx, n, d, k, row0, key, p.ktiles,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, CL, MX>, mx, n, d, k, row0, key, p.ktiles,
                                      p.dslabs, p.rows_per_split, gmag, partial);
   if (e != cudaSuccess) return cuda_status(e, "gaussian tc launch");
   return LVSK_OK;
@@ -336,10 +426,12 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
 
 int32_t gaussian_tc_bf16(const __nv_bfloat16* X, int64_t n, int64_t d, int64_t ldx, int64_t k, uint64_t row0,
                          uint64_t key, const GaussTcPlan& p, float* partial, cudaStream_t st) {
+  if (p.ns == 512 && p.dslabs == 2 && getenv("LVSK_K4_NOSHARE") == nullptr)
+    return launch_gauss_tc<512, 2, 1>(X, n, d, ldx, k, row0, key, p, partial, st);
   if (p.ns == 512 && p.ktiles % 2 == 0)
-    return launch_gauss_tc<512, 2>(X, n, d, ldx, k, row0, key, p, partial, st);
-  return p.ns == 512 ? launch_gauss_tc<512, 1>(X, n, d, ldx, k, row0, key, p, partial, st)
-                     : launch_gauss_tc<256, 1>(X, n, d, ldx, k, row0, key, p, partial, st);
+    return launch_gauss_tc<512, 1, 2>(X, n, d, ldx, k, row0, key, p, partial, st);
+  return p.ns == 512 ? launch_gauss_tc<512, 1, 1>(X, n, d, ldx, k, row0, key, p, partial, st)
+                     : launch_gauss_tc<256, 1, 1>(X, n, d, ldx, k, row0, key, p, partial, st);
 }
 
 }  // namespace lvsk

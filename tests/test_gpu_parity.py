@@ -338,12 +338,17 @@ def test_gaussian_fp32_tensor_core_vs_simt(n, d, k, monkeypatch):
     assert np.linalg.norm(simt - ref) <= 2e-6 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("variant", ["3", "2", "1", "0"])
 @pytest.mark.parametrize("n,d,k,ldx,row0", [(5000, 1024, 300, 1024, 0), (3001, 200, 128, 208, 7),
-                                            (700, 520, 256, 520, 2**33 + 5), (64, 64, 8, 64, 0)])
-def test_gaussian_tc_bf16_vs_oracle(n, d, k, ldx, row0):
+                                            (700, 520, 256, 520, 2**33 + 5), (64, 64, 8, 64, 0),
+                                            (4100, 1024, 250, 1032, 2**35 + 1), (2000, 700, 512, 704, 3)])
+def test_gaussian_tc_bf16_vs_oracle(n, d, k, ldx, row0, variant, monkeypatch):
     """K4-TC (tcgen05, bf16 X as the MN-major B operand, Z generated in smem)
     against the oracle's exact Z X / sqrt(k): ragged k / d (TMA zero fill),
-    two 512-column slabs, strided rows, a large global row offset."""
+    two 512-column slabs, strided rows, a large global row offset — for every
+    kernel variant (LVSK_K4_VARIANT: 3 = CTA pair x shared Z tiles, 2 = Z
+    tiles shared by the slab pair, 1 = X multicast, 0 = plain)."""
+    monkeypatch.setenv("LVSK_K4_VARIANT", variant)
     rng = np.random.default_rng(n + d)
     buf = torch.from_numpy(rng.standard_normal((n, ldx))).to(torch.bfloat16).cuda()
     X = buf[:, :d]
@@ -803,7 +808,8 @@ def test_csr_validation():
                        P.SketchSpec("srht", eps=0.5, d=8, rows_override=2))
 
 
-@pytest.mark.parametrize("n,d,r", [(5000, 1024, 128), (3000, 256, 100), (2048, 64, 30), (777, 512, 64)])
+@pytest.mark.parametrize("n,d,r", [(5000, 1024, 128), (3000, 256, 100), (2048, 64, 30), (777, 512, 64),
+                                   (100, 1024, 128), (257, 128, 120), (70_000, 1024, 128)])
 def test_tcgen05_bf16_leverage_vs_fp64(n, d, r):
     g = torch.Generator(device="cpu").manual_seed(n + r)
     X = torch.rand(n, d, generator=g, dtype=torch.float64).to(torch.bfloat16).cuda()
@@ -816,6 +822,16 @@ def test_tcgen05_bf16_leverage_vs_fp64(n, d, r):
     ops.run(X, out, fl.p)
     rel = ((out - ref).abs() / ref).max().item()
     assert rel < 1e-4, rel  # bf16 X exact, M as bf16 hi + lo (~16 bits), fp32 accumulation
+    if ops.r_pad == 128:  # the CTA-pair kernel (cta_group::2) and the 1-CTA kernel: same arithmetic, same bits
+        import os
+
+        os.environ["LVSK_K5_SINGLE_CTA"] = "1"
+        try:
+            single = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+            ops.run(X, single, fl.p)
+        finally:
+            del os.environ["LVSK_K5_SINGLE_CTA"]
+        assert torch.equal(single, out)
 
 
 def test_c5_shaped_pipeline_small():

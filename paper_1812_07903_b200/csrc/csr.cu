@@ -122,16 +122,14 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 // ordered csr_gather_kernel, which is bit-exact).  The same warps validate
 // their segments (strictly increasing in-range columns, finite values).
 constexpr int ST_COLS = 4096;
-#ifndef LVSK_ST_APPLY
-#define LVSK_ST_APPLY 5
-#endif
-#ifndef LVSK_ST_STAGES
-#define LVSK_ST_STAGES 4
-#endif
-constexpr int ST_APPLY = LVSK_ST_APPLY;  // applier warps, one private fp64 partial row each
 constexpr int ST_ECAP = 1024;
 constexpr int ST_RMAX = 64;
-constexpr int ST_STAGES = LVSK_ST_STAGES;
+constexpr int ST_STAGES = 4;
+// smem of a csr_stream_kernel<V, APPLY> CTA: APPLY private fp64 partial rows + the ring
+constexpr int st_smem_bytes(int apply, int vsz) {
+  return apply * ST_COLS * 8 + ST_STAGES * ST_ECAP * (vsz + 4) + ST_STAGES * ST_RMAX * 16 + ST_STAGES * 4 +
+         2 * ST_STAGES * 8;
+}
 
 __device__ __forceinline__ uint32_t csr_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -212,12 +210,17 @@ __global__ void csr_prep_kernel(const int64_t* __restrict__ row_ptr, const uint3
   }
 }
 
-template <typename V>
+// APPLY applier warps (private partial rows): 5 fills one SM per CTA; 2
+// leaves room for two CTAs (two loaders) per SM.  Buckets below
+// `validate_below` (OSNAP block 0: every row meets it exactly once)
+// validate their segments; the other blocks' warps skip the per-entry
+// checks.
+template <typename V, int ST_APPLY>
 __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
     const int32_t* __restrict__ col, const V* __restrict__ val, int64_t d, int ngroups,
     const uint32_t* __restrict__ svals, const int64_t* __restrict__ msrc, const int32_t* __restrict__ mlen,
     const uint32_t* __restrict__ start, double scale, const double* hi_in, const double* lo_in, double* hi_out,
-    double* lo_out, int32_t* flags) {
+    double* lo_out, int32_t* flags, int64_t validate_below) {
   extern __shared__ __align__(128) uint8_t st_smem[];
   double* part = reinterpret_cast<double*>(st_smem);                     // [ST_APPLY][ST_COLS]
   V* bval = reinterpret_cast<V*>(part + ST_APPLY * ST_COLS);             // [ST_STAGES][ST_ECAP]
@@ -250,6 +253,16 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
     int64_t my_src = 0;
     int32_t my_len = 0;
     uint32_t my_v = 0;
+    // the next batch's (src, len, sign), loaded one batch ahead so the
+    // global-load latency overlaps the current batch's copies
+    int64_t nx_src = 0;
+    int32_t nx_len = 0;
+    uint32_t nx_v = 0;
+    if (lane < static_cast<int>(p1 - p0)) {
+      nx_src = msrc[p0 + lane];
+      nx_len = mlen[p0 + lane];
+      nx_v = svals[p0 + lane];
+    }
     int64_t lsrc = 0, lrem = 0;  // long row in progress (lane-uniform)
     uint32_t lneg = 0;
     bool lcont = false;
@@ -286,13 +299,16 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
             break;
           }
           bcnt = p1 - pb < 32u ? static_cast<int>(p1 - pb) : 32;
-          if (lane < bcnt) {
-            my_src = msrc[pb + lane];
-            my_len = mlen[pb + lane];
-            my_v = svals[pb + lane];
-          }
+          my_src = nx_src;
+          my_len = nx_len;
+          my_v = nx_v;
           pb += bcnt;
           bq = 0;
+          if (pb + lane < p1) {
+            nx_src = msrc[pb + lane];
+            nx_len = mlen[pb + lane];
+            nx_v = svals[pb + lane];
+          }
         }
         const bool pend = lane >= bq && lane < bcnt;
         const bool longrow = pend && st_slot(my_len) > ST_ECAP;
@@ -350,6 +366,7 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
   } else {
     // ---- appliers
     const int aw = warp - 1;
+    const bool validate = b < validate_below;
     int bad = 0;
     int32_t lastcol = -1;
     for (uint32_t it = 0;; ++it) {
@@ -368,7 +385,7 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
         const SegInfo si = seg[s * ST_RMAX + q];
         const double sg = (si.flags & 1) ? -scale : scale;
         int32_t carry = -1;
-        if (si.flags & 2) {
+        if (validate && (si.flags & 2)) {
           if (q > 0) {
             const SegInfo sp = seg[s * ST_RMAX + q - 1];
             carry = cb[sp.off + sp.len - 1];
@@ -387,12 +404,14 @@ __global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
             const bool live = e < si.len;
             const int32_t c = live ? cb[si.off + e] : INT32_MAX;
             const V xv = live ? vb[si.voff + e] : V(0);
-            const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-            const int32_t before = lane == 0 ? carry : cprev;
-            carry = __shfl_sync(0xFFFFFFFFu, c, 31);
-            if (live) {
-              if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
-              if (!isfinite(static_cast<double>(xv))) bad |= LVSK_FLAG_NONFINITE;
+            if (validate) {  // warp-uniform
+              const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+              const int32_t before = lane == 0 ? carry : cprev;
+              carry = __shfl_sync(0xFFFFFFFFu, c, 31);
+              if (live) {
+                if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
+                if (!isfinite(static_cast<double>(xv))) bad |= LVSK_FLAG_NONFINITE;
+              }
             }
             const int64_t lc = static_cast<int64_t>(c) - c0;
             cc[u] = (live && lc >= 0 && lc < width) ? static_cast<int32_t>(lc) : -1;
@@ -559,6 +578,8 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
   }
   csr_keygen_kernel<<<csr_grid(N, 256), 256, 0, st>>>(n, row0, 0, s, P, keys, vals);
   LVSK_CHECK_LAUNCH("csr keygen");
+  // every row meets the first block exactly once: its buckets validate the rows
+  const int64_t validate_below = blocks[0].offset == 0 ? blocks[0].size : k;
   int32_t rc = radix::sort_pairs<uint32_t, uint32_t>(keys, vals, N, ceil_log2_csr(k), rb, skeys, svals, st);
   if (rc != LVSK_OK) return rc;
   radix::bucket_bounds_kernel<uint32_t><<<csr_grid(N + 1, 256), 256, 0, st>>>(skeys, N, k, start);
@@ -574,24 +595,40 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
     csr_prep_kernel<<<csr_grid(N, 256), 256, 0, st>>>(row_ptr, svals, N, msrc, mlen);
     const int sgroups = static_cast<int>((d + ST_COLS - 1) / ST_COLS);
     const int vsz = val_dtype == LVSK_F64 ? 8 : 4;
-    auto smem_for = [](int v) {
-      return ST_APPLY * ST_COLS * 8 + ST_STAGES * ST_ECAP * (v + 4) + ST_STAGES * ST_RMAX * static_cast<int>(sizeof(SegInfo)) +
-             ST_STAGES * 4 + 2 * ST_STAGES * 8;
-    };
-    rc = vsz == 8 ? ensure_smem_attr(reinterpret_cast<const void*>(csr_stream_kernel<double>), smem_for(8),
-                                     "csr stream shared-memory attribute")
-                  : ensure_smem_attr(reinterpret_cast<const void*>(csr_stream_kernel<float>), smem_for(4),
-                                     "csr stream shared-memory attribute");
-    if (rc != LVSK_OK) return rc;
+    // applier warps per CTA (each with a private 32 KB partial row): 2 fits two
+    // CTAs (two loader warps) per SM, 1 three; LVSK_K2_APPLY overrides (A/B)
+    const int apply = getenv("LVSK_K2_APPLY") ? atoi(getenv("LVSK_K2_APPLY")) : 2;
     const unsigned sgrid = static_cast<unsigned>(k * sgroups);
-    if (val_dtype == LVSK_F32)
-      csr_stream_kernel<float><<<sgrid, 32 * (1 + ST_APPLY), smem_for(vsz), st>>>(
-          col, static_cast<const float*>(val), d, sgroups, svals, msrc, mlen, start, scale, hi_in, lo_in, hi_out,
-          lo_out, flags);
-    else
-      csr_stream_kernel<double><<<sgrid, 32 * (1 + ST_APPLY), smem_for(vsz), st>>>(
-          col, static_cast<const double*>(val), d, sgroups, svals, msrc, mlen, start, scale, hi_in, lo_in, hi_out,
-          lo_out, flags);
+    const int64_t vbelow = validate_below;
+#define LVSK_K2_LAUNCH(V, A)                                                                                       \
+  do {                                                                                                             \
+    const int sm = st_smem_bytes(A, static_cast<int>(sizeof(V)));                                                 \
+    rc = ensure_smem_attr(reinterpret_cast<const void*>(csr_stream_kernel<V, A>), sm, "csr stream smem attribute"); \
+    if (rc != LVSK_OK) return rc;                                                                                  \
+    csr_stream_kernel<V, A><<<sgrid, 32 * (1 + A), sm, st>>>(col, static_cast<const V*>(val), d, sgroups, svals,  \
+                                                             msrc, mlen, start, scale, hi_in, lo_in, hi_out,      \
+                                                             lo_out, flags, vbelow);                              \
+  } while (0)
+    if (val_dtype == LVSK_F32) {
+      if (apply == 1)
+        LVSK_K2_LAUNCH(float, 1);
+      else if (apply == 3)
+        LVSK_K2_LAUNCH(float, 3);
+      else if (apply == 5)
+        LVSK_K2_LAUNCH(float, 5);
+      else
+        LVSK_K2_LAUNCH(float, 2);
+    } else {
+      if (apply == 1)
+        LVSK_K2_LAUNCH(double, 1);
+      else if (apply == 3)
+        LVSK_K2_LAUNCH(double, 3);
+      else if (apply == 5)
+        LVSK_K2_LAUNCH(double, 5);
+      else
+        LVSK_K2_LAUNCH(double, 2);
+    }
+#undef LVSK_K2_LAUNCH
   } else if (val_dtype == LVSK_F32)
     csr_gather_kernel<float><<<grid, 32 * CSR_WARPS, smem, st>>>(row_ptr, col, static_cast<const float*>(val), d,
                                                               ngroups, svals, start, units, scale, hi_in, lo_in,

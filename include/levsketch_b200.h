@@ -222,6 +222,18 @@ LVSK_API int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const d
                                 double* diag, double cert_limit, int32_t* cert_fail, void* ws, size_t ws_bytes,
                                 void* stream);
 
+/* KG: G = SX^T SX (k x d float64 SX, row-major, leading dimension ldsx) on
+ * the int8 tensor cores (Ozaki scheme: per-column power-of-two scaling,
+ * seven exact 7-bit slices, exact int32 slice products, float64 recombination;
+ * error class of a float64 GEMM).  Writes the 256 x 256 block upper triangle
+ * of G (ldg >= d; the entries below the diagonal blocks are untouched);
+ * k <= 18000; a non-finite SX raises LVSK_FLAG_NONFINITE in *flags.
+ * Replaces the Gram DGEMM of the fold (svd.py:30-37 / leverage.py:75-85
+ * through factor.cu).  Stream-capturable. */
+LVSK_API size_t lvsk_gram_workspace_bytes(int64_t k, int64_t d);
+LVSK_API int32_t lvsk_gram_f64(const double* SX, int64_t k, int64_t d, int64_t ldsx, double* G, int64_t ldg,
+                               void* ws, size_t ws_bytes, int32_t* flags, void* stream);
+
 /* ---- ordering -------------------------------------------------------------
  * scores_to_distribution (order.py:51-63): p = scores / sum(scores), with
  * the sum a deterministic two-level float64 reduction.  Sets

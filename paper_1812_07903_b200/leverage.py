@@ -80,7 +80,7 @@ def factor_device(sx: torch.Tensor, sv_tol: float | None, rank: int | None = Non
     if method == "auto":
         method = "gram" if (sv_tol is not None and sv_tol >= 1e-6 and k >= d and d >= 256) else "svd"
     if method == "gram":
-        g = sx.T @ sx
+        g = gram_full(sx)
         lam, v = torch.linalg.eigh(g)
         sigma = torch.sqrt(torch.clamp(lam.flip(0), min=0.0))
         vt = v.flip(1).T
@@ -109,12 +109,41 @@ def fold_device(sigma: torch.Tensor, vt: torch.Tensor, s_host: np.ndarray, pi: t
 
 
 _FOLD_WS: dict = {}
+_GRAM_WS: dict = {}
+# KG (csrc/gram_i8.cu: the int8-tensor-core Ozaki Gram) from this d up; the
+# Grams of d < 2048 (C1-C3, C5: <= 0.14 ms) stay on cuBLAS DGEMM: KG's fixed
+# costs (slicing, seven float64 epilogue passes) only amortise on large d
+GRAM_KG_MIN_D = int(os.environ.get("LVSK_GRAM_KG_MIN_D", "2048"))
+GRAM_KG_MAX_K = 18000
 
 
-def gram_upper(sx: torch.Tensor) -> torch.Tensor:
-    """G = SX^T SX with only the block upper triangle computed (KF reads the
-    upper triangle): 10/16 of the DGEMM flops at d >= 1024 (4 x 4 blocks)."""
+def use_kg(k: int, d: int) -> bool:
+    return d >= GRAM_KG_MIN_D and k <= GRAM_KG_MAX_K
+
+
+def gram_workspace(k: int, d: int, device) -> torch.Tensor:
+    return torch.empty(int(N.lib().lvsk_gram_workspace_bytes(k, d)), dtype=torch.uint8, device=device)
+
+
+def gram_upper(sx: torch.Tensor, ws: torch.Tensor | None = None, flags: torch.Tensor | None = None) -> torch.Tensor:
+    """G = SX^T SX with (at least) the block upper triangle computed — KF
+    reads the upper triangle.  d >= GRAM_KG_MIN_D: KG on the int8 tensor
+    cores (float64-GEMM error class, csrc/gram_i8.cu), 256 x 256 upper
+    blocks; below: cuBLAS DGEMM."""
     k, d = sx.shape
+    if use_kg(k, d):
+        sx = sx.contiguous()
+        if ws is None:  # eager calls: one scratch buffer per (shape, device, stream)
+            key = (k, d, sx.device, torch.cuda.current_stream(sx.device).cuda_stream)
+            ws = _GRAM_WS.get(key)
+            if ws is None:
+                ws = _GRAM_WS[key] = gram_workspace(k, d, sx.device)
+        if flags is None:
+            flags = torch.zeros(1, dtype=torch.int32, device=sx.device)  # SX was checked by the sketch
+        G = torch.empty((d, d), dtype=torch.float64, device=sx.device)
+        N.check(N.lib().lvsk_gram_f64(sx.data_ptr(), k, d, sx.stride(0), G.data_ptr(), d, ws.data_ptr(), ws.numel(),
+                                      flags.data_ptr(), N.stream_ptr()), "gram")
+        return G
     if d < 1024:
         return sx.T @ sx
     G = torch.empty((d, d), dtype=sx.dtype, device=sx.device)
@@ -125,6 +154,14 @@ def gram_upper(sx: torch.Tensor) -> torch.Tensor:
         G[edges[i] : edges[i + 1], edges[i] :] = a.T @ sx[:, edges[i] :]
     return G
 
+
+def gram_full(sx: torch.Tensor) -> torch.Tensor:
+    """Symmetric G = SX^T SX (the eigen routes read all of it)."""
+    k, d = sx.shape
+    if not use_kg(k, d):
+        return sx.T @ sx
+    G = gram_upper(sx)
+    return torch.triu(G) + torch.triu(G, 1).T
 
 
 def cert_limit(sv_tol: float | None) -> float:
@@ -140,7 +177,7 @@ def fold_workspace(d: int, r: int, device) -> torch.Tensor:
 
 
 def _chol_body(sx: torch.Tensor, pi: torch.Tensor, sv_tol: float | None = None, cert_fail: torch.Tensor | None = None,
-               ws: torch.Tensor | None = None):
+               ws: torch.Tensor | None = None, gws: torch.Tensor | None = None, gflags: torch.Tensor | None = None):
     """Shape-static Cholesky fold (CUDA-graph capturable, no host sync):
     G = SX^T SX (cuBLAS DGEMM) = R^T R, then the KF kernel (csrc/factor.cu):
     M = R^-1 Pi and diag = [info, trace(G), trace(G^-1)] with
@@ -148,7 +185,7 @@ def _chol_body(sx: torch.Tensor, pi: torch.Tensor, sv_tol: float | None = None, 
     device int32) when the certificate of :func:`chol_certified` fails."""
     k, d = sx.shape
     r = pi.shape[1]
-    G = gram_upper(sx)
+    G = gram_upper(sx, gws, gflags)
     if ws is None:  # eager calls: one scratch buffer per (shape, device, stream)
         key = (d, r, sx.device, torch.cuda.current_stream(sx.device).cuda_stream)
         ws = _FOLD_WS.get(key)
@@ -268,7 +305,7 @@ def spectral_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: 
     if k >= d and not force_qr and rank is not None and rank <= jl and 2 * rank <= d:
         # rank-capped basis fold: only the top `rank` eigenpairs of the Gram are
         # needed — block subspace iteration with a residual certificate
-        top = _topk_gram(sx.T @ sx, rank)
+        top = _topk_gram(gram_full(sx), rank)
         if top is not None:
             lam, vcols = top
             sigma = torch.sqrt(torch.clamp(lam, min=0.0))
@@ -277,7 +314,7 @@ def spectral_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: 
             if r <= rank and s_host[r - 1] > 0 and s_host[0] / s_host[r - 1] <= _EIGH_KAPPA:
                 return (vcols[:, :r] / sigma[:r]).contiguous(), r
     if k >= d and not force_qr:
-        lam, v = torch.linalg.eigh(sx.T @ sx)
+        lam, v = torch.linalg.eigh(gram_full(sx))
         sigma = torch.sqrt(torch.clamp(lam.flip(0), min=0.0))
         vt = v.flip(1).T
         s_host = sigma.cpu().numpy()
@@ -450,9 +487,11 @@ class FoldGraph:
         # device count of replays whose certificate failed (evaluated by the KF kernel)
         self.cert_fail = torch.zeros(1, dtype=torch.int32, device=sx.device)
         self.ws = fold_workspace(d, pi.shape[1], sx.device)  # owned by the graph: replays never share scratch
+        self.gws = gram_workspace(k, d, sx.device) if use_kg(k, d) else None
+        self.gflags = torch.zeros(1, dtype=torch.int32, device=sx.device)
         self.graph = None
         # warm up cuBLAS handles outside capture
-        M, diag = _chol_body(sx, pi, ws=self.ws)
+        M, diag = _chol_body(sx, pi, ws=self.ws, gws=self.gws, gflags=self.gflags)
         self.ops.set(M)
         torch.cuda.synchronize()
         s = torch.cuda.Stream()
@@ -460,7 +499,7 @@ class FoldGraph:
         with torch.cuda.stream(s):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
-                M, diag = _chol_body(self.sx, self.pi, self.sv_tol, self.cert_fail, self.ws)
+                M, diag = _chol_body(self.sx, self.pi, self.sv_tol, self.cert_fail, self.ws, self.gws, self.gflags)
                 self.ops.set(M)
                 self.diag.copy_(diag)
         torch.cuda.current_stream().wait_stream(s)

@@ -926,3 +926,62 @@ def test_srht_row_blocks_sum_to_whole():
     rc = L.lvsk_srht_rows(X[100:].data_ptr(), n - 100, d, d, 100, m, sg.data_ptr(), sm.data_ptr(), k,
                           math.sqrt(k), part.data_ptr(), ws.data_ptr(), ws.numel(), flags.p, N.stream_ptr())
     assert rc == 5  # LVSK_ERR_UNSUPPORTED
+
+
+# ---------------------------------------------------------------------------
+# KG: the fold's Gram on the int8 tensor cores (Ozaki scheme, csrc/gram_i8.cu)
+
+
+@pytest.mark.parametrize("k,d,scaled", [(300, 100, False), (1000, 700, False), (2048, 1024, True),
+                                        (4100, 2100, False), (16384, 4096, False)])
+def test_kg_gram_vs_float64(k, d, scaled):
+    """KG's block upper triangle of SX^T SX against torch float64: the error
+    stays in the float64-GEMM class (below the worst-case DGEMM bound
+    k eps sum_k |x_kc||x_kd| and within a small multiple of the Ozaki bound
+    2^-49 k max|x_c| max|x_d|), ragged k / d, columns scaled over 12 decades."""
+    g = torch.Generator(device="cuda").manual_seed(k + d)
+    sx = torch.randn(k, d, dtype=torch.float64, device="cuda", generator=g)
+    if scaled:
+        sx *= torch.logspace(-6, 6, d, dtype=torch.float64, device="cuda")
+    L = N.lib()
+    ws = torch.empty(int(L.lvsk_gram_workspace_bytes(k, d)), dtype=torch.uint8, device="cuda")
+    G = torch.full((d, d), float("nan"), dtype=torch.float64, device="cuda")
+    fl = N.Flags()
+    N.check(L.lvsk_gram_f64(sx.data_ptr(), k, d, d, G.data_ptr(), d, ws.data_ptr(), ws.numel(), fl.p,
+                            N.stream_ptr()), "gram")
+    ref = sx.T @ sx
+    i = torch.arange(d, device="cuda")
+    up = (i[:, None] // 256) <= (i[None, :] // 256)
+    assert not torch.isnan(G[up]).any()
+    diff = torch.where(up, (G - ref).abs(), torch.zeros_like(G))
+    cm = sx.abs().max(0).values
+    ozaki = (cm[:, None] * cm[None, :]) * k * 2.0**-49
+    assert (diff / ozaki).max().item() < 16
+    assert fl.read() == 0
+    # deterministic
+    G2 = G.clone()
+    N.check(L.lvsk_gram_f64(sx.data_ptr(), k, d, d, G2.data_ptr(), d, ws.data_ptr(), ws.numel(), fl.p,
+                            N.stream_ptr()), "gram")
+    assert torch.equal(G2[up], G[up])
+    sx[k // 2, d // 3] = float("inf")
+    N.check(L.lvsk_gram_f64(sx.data_ptr(), k, d, d, G2.data_ptr(), d, ws.data_ptr(), ws.numel(), fl.p,
+                            N.stream_ptr()), "gram")
+    assert fl.read() & N.FLAG_NONFINITE
+
+
+def test_kf_fold_on_kg_gram_matches_oracle():
+    """The certified Cholesky fold with the KG Gram (d >= 2048) against the
+    oracle's fold_r in float64 (M to 1e-9)."""
+    k, d, r = 6000, 2048, 64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    sx = torch.randn(k, d, dtype=torch.float64, device="cuda", generator=g) * torch.linspace(1, 3, d, device="cuda",
+                                                                                               dtype=torch.float64)
+    pi = O.jl_matrix(2, d, r)
+    from paper_1812_07903_b200.leverage import cholesky_fold, use_kg
+
+    assert use_kg(k, d)
+    M = cholesky_fold(sx, 1e-6, torch.from_numpy(pi).cuda())
+    assert M is not None
+    M_o, r_o = O.fold_r(sx.cpu().numpy(), 1e-6, pi)
+    assert r_o == d
+    assert np.linalg.norm(M.cpu().numpy() - M_o) <= 1e-9 * np.linalg.norm(M_o)

@@ -563,7 +563,8 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
                    "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
                    "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
                    "srht": "srht_sampled_kernel (K3 v3: one pass, block WHT + sampled combine)",
-                   "gaussian": "gaussian_tc_kernel (K4-TC, tcgen05, Z generated on the fly) + reduce"
+                   "gaussian": ("gaussian_tc_pair_kernel (K4-TC: CTA pair x shared-Z cluster, Z generated on "
+                                "the fly) + reduce" if d > 512 else "gaussian_tc_kernel (K4-TC) + reduce")
                    if dtype == torch.bfloat16 else
                    "split3_bf16_kernel + 3 x gaussian_tc_kernel (K4-TC on the exact bf16 planes of fp32 X) + reduce"}[fam],
         "leverage": "csr_rowsumsq_kernel (K6)" if csr else

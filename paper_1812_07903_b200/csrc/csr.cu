@@ -641,6 +641,12 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
   return LVSK_OK;
 }
 
+namespace lvsk {
+bool csr_rowsumsq_tc_ok(const float* M, int64_t r);
+int32_t csr_rowsumsq_tc(const int64_t* row_ptr, const int32_t* col, const void* val, int32_t val_dtype, int64_t n,
+                        int64_t d, const float* M, double* scores, int32_t* flags, cudaStream_t st);
+}  // namespace lvsk
+
 extern "C" int32_t lvsk_rowsumsq_csr(const int64_t* row_ptr, const int32_t* col, const void* val, int32_t val_dtype,
                                      int64_t n, int64_t d, const float* M, int64_t r, double* scores, int32_t* flags,
                                      void* stream) {
@@ -648,6 +654,8 @@ extern "C" int32_t lvsk_rowsumsq_csr(const int64_t* row_ptr, const int32_t* col,
   LVSK_REQUIRE(val_dtype == LVSK_F32 || val_dtype == LVSK_F64, LVSK_ERR_CONFIGURATION, "values must be f32 or f64");
   if (n == 0) return LVSK_OK;
   cudaStream_t st = as_stream(stream);
+  // r = 128 (C4): the hot columns on the tensor cores (csr_tc.cu); LVSK_K6_SIMT=1 forces the SIMT kernel
+  if (csr_rowsumsq_tc_ok(M, r)) return csr_rowsumsq_tc(row_ptr, col, val, val_dtype, n, d, M, scores, flags, st);
   const int grid = csr_grid(n * 32, 256);
   const bool aligned = reinterpret_cast<uintptr_t>(M) % 16 == 0;
 #define LVSK_K6(RPL, V4)                                                                                         \

@@ -794,6 +794,28 @@ def test_csr_leverage_vs_oracle():
     assert np.all(res.scores[~mask] <= 1e-6 * ref.max())
 
 
+@pytest.mark.parametrize("n,d,per_row,vdt", [(3000, 4096, 80, np.float32), (257, 100, 30, np.float64),
+                                             (1000, 300, 0, np.float32), (5000, 1024, 200, np.float32)])
+def test_csr_leverage_tensor_core_vs_simt_and_fp64(n, d, per_row, vdt, monkeypatch):
+    """K6-TC (hot columns < 128 on tcgen05, cold ones gathered; r = 128)
+    against the SIMT kernel and a float64 recompute: Zipf rows, d < 128 hot
+    window edge, empty rows, long rows, f64 values, a ragged last tile."""
+    from paper_1812_07903_b200.csr import CSRMatrix, csr_scores
+
+    csr, dense = _random_csr(n, d, per_row, seed=n + d, dtype=vdt)
+    m = CSRMatrix.from_any(csr)
+    g = np.random.default_rng(d)
+    M = g.standard_normal((d, 128)) / math.sqrt(d)
+    Mt = torch.from_numpy(M).cuda()
+    tc = csr_scores(m, Mt).cpu().numpy()
+    ref = ((dense @ M.astype(np.float32).astype(np.float64)) ** 2).sum(1)
+    scale = max(ref.max(), 1e-30)
+    assert np.abs(tc - ref).max() <= 2e-5 * scale
+    monkeypatch.setenv("LVSK_K6_SIMT", "1")
+    simt = csr_scores(m, Mt).cpu().numpy()
+    assert np.abs(tc - simt).max() <= 2e-5 * scale
+
+
 def test_csr_validation():
     indptr = np.array([0, 2, 3], dtype=np.int64)
     spec = P.SketchSpec("countsketch", eps=0.5, d=8, seed=1, rows_override=16)

@@ -371,7 +371,7 @@ __device__ const uint64_t* as_passes(const AsArgs& a, int dlo, int dhi, unsigned
 // order locally (runs of <= AS_HALO keys, one thread each; in random data the
 // runs hold 1-3 keys).  A disordered longer run raises *flag and the caller
 // redoes the sort on every digit.
-__device__ void as_fixup(const AsArgs& a, const uint64_t* ks, uint8_t* smem, int64_t c0, int64_t c1) {
+__device__ void as_fixup(const AsArgs& a, const uint64_t* ks, uint8_t* smem, int64_t c0, int64_t c1, int hs) {
   uint64_t* K = reinterpret_cast<uint64_t*>(smem);                     // [AS_WIN + 2 AS_HALO]
   uint32_t* I = reinterpret_cast<uint32_t*>(K + AS_WIN + 2 * AS_HALO);  // [AS_WIN + 2 AS_HALO]
   const int64_t n = a.n;
@@ -392,12 +392,12 @@ __device__ void as_fixup(const AsArgs& a, const uint64_t* ks, uint8_t* smem, int
     for (int t = threadIdx.x; t < wlen; t += AS_THREADS) {
       const int64_t pos = w0 + t;
       const int j = t + AS_HALO;
-      const uint32_t hi = static_cast<uint32_t>(K[j] >> 32);
-      const bool start = pos == 0 || static_cast<uint32_t>(K[j - 1] >> 32) != hi;
+      const uint64_t hi = K[j] >> hs;
+      const bool start = pos == 0 || (K[j - 1] >> hs) != hi;
       if (start) {
         int L = 1;
         bool dis = false;
-        while (L <= AS_HALO && pos + L < n && static_cast<uint32_t>(K[j + L] >> 32) == hi) {
+        while (L <= AS_HALO && pos + L < n && (K[j + L] >> hs) == hi) {
           dis |= K[j + L] < K[j + L - 1];
           ++L;
         }
@@ -412,7 +412,7 @@ __device__ void as_fixup(const AsArgs& a, const uint64_t* ks, uint8_t* smem, int
         // disordered inside a run: fine if the run started within AS_HALO positions
         bool found = false;
         for (int q = 1; q <= AS_HALO && !found; ++q)
-          found = pos - q < 0 || static_cast<uint32_t>(K[j - q] >> 32) != hi;
+          found = pos - q < 0 || (K[j - q] >> hs) != hi;
         bad |= !found;
       }
     }
@@ -493,13 +493,17 @@ __global__ void __launch_bounds__(AS_THREADS, 1) argsort_coop_kernel(AsArgs a) {
     for (int64_t i = c0 + threadIdx.x; i < c1; i += AS_THREADS) a.out[i] = i;
     return;
   }
-  // fast path: the high 32 bits (digits 4..7), then the local fix-up
-  const uint64_t* ks = as_passes(a, 4, 7, diff, nbar, as_smem, c0, c1);
-  if (diff & 0xFFFFFFFFull) {
+  // fast path: the high 32 bits (digits 4..7) — 40 bits from 4M keys on, where
+  // runs of equal high-32-bit keys outgrow the fix-up's halo (C5's 8e6
+  // probabilities) — then the local fix-up of the runs
+  const int dfirst = n >= (int64_t{1} << 22) ? 3 : 4;
+  const int hs = 8 * dfirst;
+  const uint64_t* ks = as_passes(a, dfirst, 7, diff, nbar, as_smem, c0, c1);
+  if (diff & ((1ull << hs) - 1ull)) {
     as_stamp(a, 40);
     unsigned long long fx0 = 0;
     if (a.trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fx0));
-    as_fixup(a, ks, as_smem, c0, c1);
+    as_fixup(a, ks, as_smem, c0, c1, hs);
     if (a.trace != nullptr && threadIdx.x == 0) {
       unsigned long long fx1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fx1));

@@ -594,6 +594,21 @@ def test_argsort_matches_numpy_stable(n):
         assert np.array_equal(got, ref), (n, desc)
 
 
+@pytest.mark.parametrize("n", [4_194_303, 4_194_304, 8_000_000])
+def test_argsort_40bit_path_c5_like(n):
+    """From 4M keys K7 sorts on the high 40 key bits before the local fix-up:
+    8e6 probabilities of a narrow range (C5's scores: long runs of equal high
+    32 bits) plus ties, +-0, inf — bit-exact against numpy's stable argsort."""
+    rng = np.random.default_rng(n)
+    s = 0.8 + 0.4 * rng.random(n)
+    s[rng.integers(0, n, n // 50)] = s[11]
+    p = s / s.sum()
+    p[3], p[5], p[7] = 0.0, -0.0, np.inf
+    for desc in (True, False):
+        got = P.order.argsort_device(dev(p), desc).cpu().numpy()
+        assert np.array_equal(got, np.argsort(-p if desc else p, kind="stable")), (n, desc)
+
+
 @pytest.mark.parametrize("kind", ["long_runs", "short_runs", "wide_exponents"])
 def test_argsort_high_bits_then_fixup_paths(kind):
     """K7 sorts by the high 32 key bits, then orders runs of equal high bits

@@ -27,6 +27,9 @@ from .csr import CSRMatrix, csr_code
 from .sketch import GAUSSIAN, SRHT, SketchSpec, SketchState, sketch_rows
 
 STAGES = ("sketch", "factor", "leverage", "order")
+# LVSK_NVTX=1: one NVTX range per stage (sketch / factor / leverage / order) for
+# Nsight timelines (SURVEY §5 tracing); off by default (host cost per range)
+_NVTX = os.environ.get("LVSK_NVTX", "0") == "1"
 
 
 class LeveragePipeline:
@@ -191,12 +194,17 @@ class LeveragePipeline:
         steps = [("sketch", lambda: self._sketch(X)), ("factor", self._factor), ("leverage", lambda: self._leverage(X))]
         if self.order:
             steps.append(("order", self._order))
+        nvtx = _NVTX
         for name, fn in steps:
+            if nvtx:
+                torch.cuda.nvtx.range_push(f"levsketch.{name}")
             if timing:
                 ev[name][0].record()
             fn()
             if timing:
                 ev[name][1].record()
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
         if check:
             self.check()
         return self.scores, (self.idx if self.order else None)

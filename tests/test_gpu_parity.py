@@ -271,6 +271,10 @@ def test_srht_sampled_vs_two_pass(monkeypatch):
     monkeypatch.setenv("LVSK_SRHT_V2", "1")
     b = P.srht_apply(spec, dev(x)).data
     assert np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(b)
+    # both against the oracle's float64 transform (reference sketch.py:248-257)
+    ref = O.srht_sketch(x.astype(np.float64), k, 5)
+    assert np.linalg.norm(a - ref) <= 2e-6 * np.linalg.norm(ref)
+    assert np.linalg.norm(b - ref) <= 2e-6 * np.linalg.norm(ref)
 
 
 def test_fwht_kats(golden):
@@ -928,6 +932,18 @@ def test_leverage_streamed_matches_in_memory(tmp_path, family, s, dtype):
         np.testing.assert_allclose(got.scores, ref.scores, rtol=1e-5)  # fp32 blocks: partial sums reassociate
     else:
         assert np.array_equal(got.scores, ref.scores)
+    # and against the CPU oracle on the same values
+    xv = xin.astype(np.float64)
+    pi = O.jl_matrix(0, d, 16)
+    if family == "gaussian":
+        sx_o = O.gaussian_sketch(xv, 512, 2)
+    else:
+        hi, lo = O.hashed_sketch(xv, family, 512, 2, s or 1)
+        sx_o = hi + lo
+    oracle, r_o, _ = O.leverage_from_sketch(xv, sx_o, 1e-6, pi)
+    assert got.effective_rank == r_o
+    tol = 1e-4 if dtype == torch.float32 else 1e-9
+    assert np.max(np.abs(got.scores - oracle) / oracle) <= tol
 
 
 def test_srht_row_blocks_sum_to_whole():

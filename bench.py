@@ -387,6 +387,7 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
     if world > 1:
         pipe.n = n  # local rows; the state covers n_total global rows
         pipe.scores = torch.empty(n, dtype=torch.float64, device=dev)
+        pipe.keep_state = True  # the sliced merge exchanges the compensated pairs
     # multi-rank global order: rank 0 sorts the gathered probabilities of step i on a
     # side stream while step i+1 sketches; the timed region ends after the last sort
     gather_p = [torch.empty(n_total, dtype=torch.float64, device=dev) for _ in range(2)] \
@@ -545,7 +546,9 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
     x_bytes = (nnz * 8 + 8 * (n + 1)) if csr else n * d * elt  # CSR: int32 col + f32 val + int64 row_ptr
     stage_ms = {k_: v / args.steps for k_, v in stage_sum.items()}
     lev_bytes = x_bytes + 8 * n  # X once + float64 scores
-    sk_bytes = x_bytes + 2 * 8 * k * d  # X once + compensated state write
+    # X once + the sketch written: folded SX (k*d*8) on one GPU's hashed dense path, else the
+    # compensated pair (2*k*d*8) or the float64 SX / partials of the other families
+    sk_bytes = x_bytes + (8 if (world == 1 and fam in ("countsketch", "osnap") and not csr) else 16) * k * d
     lev_gbs = lev_bytes / (stage_ms["leverage"] / 1000) / 1e9 if stage_ms.get("leverage") else None
     sk_gbs = sk_bytes / (stage_ms["sketch"] / 1000) / 1e9 if stage_ms.get("sketch") else None
     dominant = "sketch" if stage_ms.get("sketch", 0) >= stage_ms.get("leverage", 0) else "leverage"

@@ -79,7 +79,9 @@ LVSK_API int32_t lvsk_abi_version(void);
  * (sketch.py:289-312).  Rows X[0..n) carry GLOBAL indices row0..row0+n-1.
  * The compensated state (hi, lo), k x d float64 row-major, is read from
  * (hi_in, lo_in) and written to (hi_out, lo_out) (may alias; hi_in = lo_in = NULL
- * starts from the zero state without reading it).  Contributions to
+ * starts from the zero state without reading it; lo_out = NULL writes the
+ * folded sketch hi + lo — the value lvsk_fold_compensated returns — to
+ * hi_out instead of the pair).  Contributions to
  * one bucket are applied in ascending row index, each as a TwoSum, which is
  * the reference's exact operation sequence: the result is bit-identical.
  * blocks: HOST array of s blocks.  scale = 1/sqrt(s) (float64). */

@@ -147,8 +147,12 @@ __global__ void __launch_bounds__(256, 3) hashed_gather_kernel(
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       if (col0 + v < d) {
-        hi_out[so + v] = h[v];
-        lo_out[so + v] = l[v];
+        if (lo_out != nullptr) {
+          hi_out[so + v] = h[v];
+          lo_out[so + v] = l[v];
+        } else {  // the folded sketch hi + lo (lvsk_fold_compensated's value)
+          hi_out[so + v] = __dadd_rn(h[v], l[v]);
+        }
       }
     }
   }
@@ -349,8 +353,12 @@ __global__ void __launch_bounds__(32 * (bulk_consumers<T>() + 1), 8) hashed_gath
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
     if (v < nv) {
-      hi_out[so + v] = h[v];
-      lo_out[so + v] = l[v];
+      if (lo_out != nullptr) {
+        hi_out[so + v] = h[v];
+        lo_out[so + v] = l[v];
+      } else {  // the folded sketch hi + lo (lvsk_fold_compensated's value)
+        hi_out[so + v] = __dadd_rn(h[v], l[v]);
+      }
       // fp32 / bf16 inputs cannot overflow a float64 sum: a non-finite state
       // means a non-finite input (checked once here instead of per element)
       if constexpr (sizeof(T) < 8) bad |= !(isfinite(h[v]) && isfinite(l[v]));

@@ -73,6 +73,9 @@ class LeveragePipeline:
         self._m32 = None
         self._m32_src = None
         self.effective_rank = None
+        # keep_state: also write the compensated pair (hi, lo) of the sketch
+        # (multi-rank merges need it); otherwise K1 writes the folded SX only
+        self.keep_state = False
         self.events = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in STAGES}
 
     # -- stages ------------------------------------------------------------
@@ -98,13 +101,18 @@ class LeveragePipeline:
             N.check(L.lvsk_gaussian_sketch(X.data_ptr(), self.code, self.n, self.d, ldx, self.row0, self.spec.seed,
                                            self.k, self.sx.data_ptr(), 0, self.ws_sketch.data_ptr(),
                                            self.ws_sketch.numel(), self.flags.data_ptr(), st), "gaussian")
-        else:  # a fresh state each run: NULL (hi_in, lo_in) = zeros, no memset and no state read
+        elif self.keep_state:  # a fresh state each run: NULL (hi_in, lo_in) = zeros, no memset and no state read
             N.check(L.lvsk_hashed_sketch(X.data_ptr(), self.code, self.n, self.d, ldx, self.row0, s._blocks,
                                          self.spec.s, s._scale, None, None, s._hi.data_ptr(),
                                          s._lo.data_ptr(), self.k, self.ws_sketch.data_ptr(), self.ws_sketch.numel(),
                                          self.flags.data_ptr(), st), "hashed sketch")
             N.check(L.lvsk_fold_compensated(s._hi.data_ptr(), s._lo.data_ptr(), self.sx.data_ptr(), self.sx.numel(), st),
                     "fold")
+        else:  # only SX is needed: K1 writes the folded hi + lo straight into it (no state pair, no fold pass)
+            N.check(L.lvsk_hashed_sketch(X.data_ptr(), self.code, self.n, self.d, ldx, self.row0, s._blocks,
+                                         self.spec.s, s._scale, None, None, self.sx.data_ptr(), None, self.k,
+                                         self.ws_sketch.data_ptr(), self.ws_sketch.numel(), self.flags.data_ptr(), st),
+                    "hashed sketch")
 
     def _factor(self) -> None:
         k, d = self.sx.shape
@@ -249,7 +257,7 @@ class LeveragePipeline:
             # or keygen + radix passes + bucket bounds; then the gather (K1) and the hi+lo fold
             coop = self.k <= 4096 and self.spec.s <= 64 and not os.environ.get("LVSK_GROUP_RADIX")
             group = 1 if coop else 1 + radix(self.n * self.spec.s, max(1, (self.k - 1).bit_length())) + 1
-            sk = group + 1 + 1
+            sk = group + 1 + (1 if self.keep_state else 0)
         lev = 1
         k, d = self.sx.shape
         # KF (chol_fold_kernel) + the K5 operand split (split_fold_kernel)

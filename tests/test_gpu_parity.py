@@ -1038,3 +1038,25 @@ def test_kf_fold_on_kg_gram_matches_oracle():
     M_o, r_o = O.fold_r(sx.cpu().numpy(), 1e-6, pi)
     assert r_o == d
     assert np.linalg.norm(M.cpu().numpy() - M_o) <= 1e-9 * np.linalg.norm(M_o)
+
+
+def test_k1_folded_output_equals_pair_then_fold():
+    """lvsk_hashed_sketch with lo_out = NULL writes hi + lo straight into
+    hi_out: bit-identical to the pair followed by lvsk_fold_compensated
+    (the pipeline's single-GPU sketch path)."""
+    rng = np.random.default_rng(21)
+    n, d, k = 20_000, 64, 1024
+    X = dev(rng.standard_normal((n, d)).astype(np.float32))
+    spec = P.SketchSpec("osnap", eps=0.5, d=d, seed=4, rows_override=k, osnap_s=3)
+    st = P.apply_sketch(X, spec)
+    ref = st.data_device
+    L = N.lib()
+    ws = torch.empty(int(L.lvsk_hashed_workspace_bytes(n, 3, k)), dtype=torch.uint8, device="cuda")
+    out = torch.empty((k, d), dtype=torch.float64, device="cuda")
+    fl = N.Flags()
+    N.check(L.lvsk_hashed_sketch(X.data_ptr(), N.LVSK_F32, n, d, d, 0, st._blocks, 3, st._scale, None, None,
+                                 out.data_ptr(), None, k, ws.data_ptr(), ws.numel(), fl.p, N.stream_ptr()))
+    assert torch.equal(out, ref)
+    pipe = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=1e-6, jl_dim=32)
+    scores, _ = pipe.run(X)
+    assert torch.equal(pipe.sx, ref)

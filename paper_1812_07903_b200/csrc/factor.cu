@@ -47,7 +47,7 @@ namespace cg = cooperative_groups;
 namespace lvsk {
 
 constexpr int FT = 64;          // tile edge
-constexpr int FLD = FT + 1;     // smem row stride (transposed loads stay ~conflict-free)
+constexpr int FLD = FT + 4;     // smem row stride, = 4 mod 16: DMMA fragment loads are conflict-free
 constexpr int FTHREADS = 256;
 constexpr int FTILE_SMEM = FT * FLD * 8;
 
@@ -103,15 +103,15 @@ __device__ __forceinline__ void signal(int32_t* f, int v) {
 // ---- tile movement (mutable tiles through L2 only) ------------------------------
 
 __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld) {
-  for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
-    const int m = e >> 6, c = e & 63;
-    s[m * FLD + c] = __ldcg(g + m * ld + c);
+  for (int e = threadIdx.x; e < FT * FT / 2; e += FTHREADS) {
+    const int m = e >> 5, c = 2 * (e & 31);
+    *reinterpret_cast<double2*>(s + m * FLD + c) = __ldcg(reinterpret_cast<const double2*>(g + m * ld + c));
   }
 }
 __device__ __forceinline__ void store_tile(double* g, int64_t ld, const double* s) {
-  for (int e = threadIdx.x; e < FT * FT; e += FTHREADS) {
-    const int m = e >> 6, c = e & 63;
-    g[m * ld + c] = s[m * FLD + c];
+  for (int e = threadIdx.x; e < FT * FT / 2; e += FTHREADS) {
+    const int m = e >> 5, c = 2 * (e & 31);
+    *reinterpret_cast<double2*>(g + m * ld + c) = *reinterpret_cast<const double2*>(s + m * FLD + c);
   }
 }
 __device__ __forceinline__ void store_tile_t(double* g, int64_t ld, const double* s) {
@@ -123,58 +123,67 @@ __device__ __forceinline__ void store_tile_t(double* g, int64_t ld, const double
 
 // ---- tile math ---------------------------------------------------------------
 
-// one k-step of the 4 x 4 register-blocked tile product: rows a >= AMIN only
-// (At upper triangular), and only blocks a <= b when SYM (symmetric result,
-// upper triangle needed)
-template <int AMIN, bool SYM>
-__device__ __forceinline__ void gemm_step(double (&acc)[4][4], const double* At, const double* B, int p, int ty,
-                                          int tx, double sg) {
-  double av[4], bv[4];
-#pragma unroll
-  for (int a = AMIN; a < 4; ++a) av[a] = sg * At[p * FLD + ty + 16 * a];
-#pragma unroll
-  for (int b = 0; b < 4; ++b) bv[b] = B[p * FLD + tx + 16 * b];
-#pragma unroll
-  for (int a = AMIN; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (!SYM || a <= b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+// one float64 tensor-core product (mma.m8n8k4: A 8x4 row-major — lane l holds
+// A[l / 4][l % 4]; B 4x8 column-major — B[l % 4][l / 4]; C 8x8 — C[l / 4][2 (l % 4) + i])
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
 }
 
 // out = At^T B (MODE 0), C - At^T B (MODE 1) or C + At^T B (MODE 2); At[p][m],
-// B[p][c] in smem; C (ldc) read through L2 when CG, else from smem; out (ldo)
-// may be smem or global.  4 x 4 register blocking, 256 threads (rows ty+16a,
-// columns tx+16b).  SHAPE 1: At is upper triangular, so row m only needs
-// p <= m (the k loop runs in four row-group segments: ~half the FMAs);
-// SHAPE 2: only the upper triangle of the (symmetric) result is formed.
+// B[p][c] in smem (row stride FLD); C (ldc) read through L2 when CG, else
+// from smem; out (ldo) may be smem or global.  On the float64 tensor cores
+// (DMMA): warp w owns rows 32 (w & 1) .. +31 and columns 16 (w >> 1) .. +15 as
+// 4 x 2 fragments of 8 x 8; per k-step of 4 it loads 4 A and 2 B fragment
+// values (FLD = 4 mod 16 keeps both loads bank-conflict free) for 8 DMMAs.
+// SHAPE 1: At is upper triangular, so row block i stops at k = its last row
+// (the skipped products are exact zeros); SHAPE 2: only the fragments that
+// hold upper-triangle entries of the (symmetric) result are formed.
 template <int MODE, bool CG, int SHAPE = 0>
 __device__ __forceinline__ void gemm_tile(const double* At, const double* B, const double* C, int64_t ldc, double* out,
                                           int64_t ldo) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  constexpr bool SYM = SHAPE == 2;
-  double acc[4][4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rb = (w & 1) * 32, cb = (w >> 1) * 16;
+  const int qr = lane >> 2, qc = lane & 3;
+  auto need = [&](int i, int j) { return SHAPE != 2 || cb + 8 * j + 7 >= rb + 8 * i; };
+  double acc[4][2][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const double* cp = C + (ty + 16 * a) * ldc + tx + 16 * b;
-      acc[a][b] = (MODE == 0 || (SYM && a > b)) ? 0.0 : (CG ? __ldcg(cp) : *cp);
+    for (int j = 0; j < 2; ++j) {
+      acc[i][j][0] = acc[i][j][1] = 0.0;
+      if (MODE != 0 && need(i, j)) {
+        const double* cp = C + (rb + 8 * i + qr) * ldc + cb + 8 * j + 2 * qc;
+        const double2 v = CG ? __ldcg(reinterpret_cast<const double2*>(cp)) : *reinterpret_cast<const double2*>(cp);
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      }
     }
   const double sg = MODE == 1 ? -1.0 : 1.0;
-  if constexpr (SHAPE == 1) {
-    for (int p = 0; p <= ty; ++p) gemm_step<0, false>(acc, At, B, p, ty, tx, sg);
-    for (int p = ty + 1; p <= ty + 16; ++p) gemm_step<1, false>(acc, At, B, p, ty, tx, sg);
-    for (int p = ty + 17; p <= ty + 32; ++p) gemm_step<2, false>(acc, At, B, p, ty, tx, sg);
-    for (int p = ty + 33; p <= ty + 48; ++p) gemm_step<3, false>(acc, At, B, p, ty, tx, sg);
-  } else {
+  const int kend = SHAPE == 1 ? rb + 32 : FT;
 #pragma unroll 4
-    for (int p = 0; p < FT; ++p) gemm_step<0, SYM>(acc, At, B, p, ty, tx, sg);
+  for (int k0 = 0; k0 < kend; k0 += 4) {
+    const double* ar = At + (k0 + qc) * FLD + rb + qr;
+    const double* br = B + (k0 + qc) * FLD + cb + qr;
+    double a[4], b[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = sg * ar[8 * i];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) b[j] = br[8 * j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (need(i, j) && (SHAPE != 1 || k0 <= rb + 8 * i + 7)) dmma(acc[i][j], a[i], b[j]);
   }
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (!SYM || a <= b) out[(ty + 16 * a) * ldo + tx + 16 * b] = acc[a][b];
+    for (int j = 0; j < 2; ++j)
+      if (need(i, j))
+        *reinterpret_cast<double2*>(out + (rb + 8 * i + qr) * ldo + cb + 8 * j + 2 * qc) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
 }
 
 // fixed-order sum of squares of the valid (rows < nr, cols < nc) entries of a

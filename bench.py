@@ -563,7 +563,7 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
             traffic = None
     kernels = {
         "sketch": {"countsketch": "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
-                   "osnap": "csr_stream_kernel (K2, incl. row prep + radix grouping)" if csr else
+                   "osnap": "csr_sketch_kernel (K2, incl. row prep + radix grouping)" if csr else
                    "hashed_gather_bulk_kernel (K1, incl. the cooperative bucket grouping)",
                    "srht": "srht_sampled_kernel (K3 v3: one pass, block WHT + sampled combine)",
                    "gaussian": ("gaussian_tc_pair_kernel (K4-TC: CTA pair x shared-Z cluster, Z generated on "

@@ -14,7 +14,10 @@
 // K6: one warp per row; lane l owns r/32 consecutive columns of u = x M and
 // gathers the M rows of the row's nonzeros (L1/L2-resident), fp32 FMA, then
 // the squared norm is reduced across the warp.
+#include <cmath>
 #include <cstdlib>
+#include <type_traits>
+#include <cstring>
 
 #include "radix_sort.cuh"
 
@@ -103,99 +106,12 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K2 streaming variant (default).  csr_prep_kernel turns the bucket-sorted
-// (row, sign) pairs into per-pair (source offset, length) so nothing
-// downstream chases row pointers.  csr_stream_kernel: one CTA owns one
-// (bucket, <= 4096-column group) with its float64 (hi, lo) slice in shared
-// memory (64 KB); warp 0 streams the bucket's rows in chunks (<= 64 row
-// segments / 1024 entries; longer rows are split, harmless since one row's
-// entries have distinct columns) with cp.async into a 4-deep ring signalled
-// by cp.async.mbarrier.arrive; warps 1..8 apply the chunk's segments
-// concurrently (segment q by warp q mod 5), each into its OWN float64 row of
-// partial sums in shared memory (5 x 32 KB): a segment's entries have distinct
-// columns, so a warp's 32 lanes never collide and every update is a plain
-// load-add-store — no atomics (the first version used returning shared fp64
-// atomics, CAS loops that serialised on the Zipf-hot columns: 17.6 ms at C4).
-// At the end hi_out + lo_out = TwoSum fold of (hi_in, lo_in, P_0 .. P_4) in
-// warp order.  Deterministic; equal to the reference's compensated state to
-// ~1e-16 relative instead of bit-for-bit (LVSK_K2_DETERMINISTIC=1 selects the
-// ordered csr_gather_kernel, which is bit-exact).  The same warps validate
-// their segments (strictly increasing in-range columns, finite values).
-constexpr int ST_COLS = 4096;
-constexpr int ST_ECAP = 1024;
-constexpr int ST_RMAX = 64;
-constexpr int ST_STAGES = 4;
-// smem of a csr_stream_kernel<V, APPLY> CTA: APPLY private fp64 partial rows + the ring
-constexpr int st_smem_bytes(int apply, int vsz) {
-  return apply * ST_COLS * 8 + ST_STAGES * ST_ECAP * (vsz + 4) + ST_STAGES * ST_RMAX * 16 + ST_STAGES * 4 +
-         2 * ST_STAGES * 8;
-}
+// csr_prep_kernel turns the bucket-sorted (row, sign) pairs into per-pair
+// (source offset, length) so the sketch kernel never chases row pointers.
+constexpr int ST_COLS = 4096;  // columns per CTA-owned SX slice (one 32 KB float64 partial row per warp)
 
 __device__ __forceinline__ uint32_t csr_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-struct SegInfo {
-  int32_t off, len;  // position of the first column index in the stage buffer, entry count
-  int32_t flags;     // bit0 negative sign, bit1 continuation of the previous segment's row
-  int32_t voff;      // position of the first value (the two arrays' 16-byte alignments differ)
-};
-
-// Stage slot of a row piece of `len` entries: its 16-byte aligned superset in
-// either array (<= 3 leading + <= 3 trailing entries) rounded to 4 entries.
-__device__ __forceinline__ int32_t st_slot(int64_t len) { return static_cast<int32_t>((len + 9) & ~int64_t{3}); }
-
-__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   csr_smem(dst)),
-               "l"(src), "r"(bytes), "r"(csr_smem(bar))
-               : "memory");
-}
-
-// Issue the aligned-superset copies of entries [src, src + len) of col / val
-// into the stage at slot position pos; returns the SegInfo offsets.  A
-// 16-byte aligned chunk holding one valid byte cannot cross a page, so the
-// superset reads are always safe.
-template <typename V>
-__device__ __forceinline__ void st_issue(const int32_t* col, const V* val, int64_t src, int64_t len, int32_t pos,
-                                         int32_t* cbuf, V* vbuf, uint64_t* bar, int32_t& coff, int32_t& voff) {
-  const uintptr_t ca = reinterpret_cast<uintptr_t>(col + src), va = reinterpret_cast<uintptr_t>(val + src);
-  const int32_t padc = static_cast<int32_t>((ca & 15) >> 2);
-  const int32_t padv = static_cast<int32_t>((va & 15) / sizeof(V));
-  constexpr int VW = 16 / sizeof(V);
-  const uint32_t cbytes = static_cast<uint32_t>(((padc + len + 3) & ~int64_t{3}) * 4);
-  const uint32_t vbytes = static_cast<uint32_t>(((padv + len + VW - 1) / VW) * 16);
-  bulk_copy_g2s(cbuf + pos, reinterpret_cast<const void*>(ca & ~uintptr_t{15}), cbytes, bar);
-  bulk_copy_g2s(vbuf + pos, reinterpret_cast<const void*>(va & ~uintptr_t{15}), vbytes, bar);
-  coff = pos + padc;
-  voff = pos + padv;
-}
-template <typename V>
-__device__ __forceinline__ uint32_t st_bytes(const int32_t* col, const V* val, int64_t src, int64_t len) {
-  const uintptr_t ca = reinterpret_cast<uintptr_t>(col + src), va = reinterpret_cast<uintptr_t>(val + src);
-  const int64_t padc = (ca & 15) >> 2, padv = (va & 15) / sizeof(V);
-  constexpr int VW = 16 / sizeof(V);
-  return static_cast<uint32_t>(((padc + len + 3) & ~int64_t{3}) * 4 + ((padv + len + VW - 1) / VW) * 16);
-}
-__device__ __forceinline__ void st_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(csr_smem(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(csr_smem(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void st_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "SW_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra.uni SW_%=;\n}" ::"r"(csr_smem(b)),
-      "r"(parity)
-      : "memory");
 }
 
 __global__ void csr_prep_kernel(const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ svals, int64_t N,
@@ -210,244 +126,248 @@ __global__ void csr_prep_kernel(const int64_t* __restrict__ row_ptr, const uint3
   }
 }
 
-// APPLY applier warps (private partial rows): 5 fills one SM per CTA; 2
-// leaves room for two CTAs (two loaders) per SM.  Buckets below
-// `validate_below` (OSNAP block 0: every row meets it exactly once)
-// validate their segments; the other blocks' warps skip the per-entry
-// checks.
-template <typename V, int ST_APPLY>
-__global__ void __launch_bounds__(32 * (1 + ST_APPLY)) csr_stream_kernel(
+// ---------------------------------------------------------------------------
+// K2 v4 (default): self-loading applier warps.  One CTA owns one (bucket,
+// <= 4096-column group); each of its W warps owns a private float64 partial
+// row (32 KB) and a private ring of NB batches of 8 row slots, and takes the
+// bucket's pairs p0 + w, p0 + w + W, ... in ascending order.  Copy: four
+// lanes per row copy the 16-byte aligned supersets of the row's columns and
+// values into its slot with cp.async (LDGSTS.128; a batch is one commit
+// group, NB - 1 batches in flight per warp; rows longer than a slot are read
+// straight from global memory when their turn comes).  Apply: the row's
+// entries are striped over the lanes; one row's columns are distinct, so the
+// plain float64 load-add-stores never collide.  No loader warp and no
+// cross-warp hand-off: round 2's design (one loader warp feeding two applier
+// warps through mbarrier stages) kept its appliers waiting; the partial rows
+// cap a CTA at five warps, so the per-row instruction count and the overlap
+// of consecutive rows are what set the speed (ncu: ~25 % issue-active, memory
+// system ~25 % busy).  The CTA ends with the TwoSum fold of (hi_in, lo_in,
+// P_0 .. P_W-1) in warp order: deterministic.
+constexpr int K2_SLOT_DEFAULT = 124;  // ring slot capacity in entries (rows of up to 118 entries are staged)
+constexpr int K2_BATCH = 8;   // rows per copy batch (4 lanes per row)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(csr_smem(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int k2_smem_bytes(int w, int nb, int vsz, int slot = K2_SLOT_DEFAULT) {
+  return w * (ST_COLS * 8 + nb * K2_BATCH * slot * (4 + vsz) + nb * K2_BATCH * 24);
+}
+
+template <typename V, int W, int NB, bool POW2, bool ONEG, int K2_SLOT = K2_SLOT_DEFAULT>
+__global__ void __launch_bounds__(32 * W) csr_sketch_kernel(
     const int32_t* __restrict__ col, const V* __restrict__ val, int64_t d, int ngroups,
     const uint32_t* __restrict__ svals, const int64_t* __restrict__ msrc, const int32_t* __restrict__ mlen,
-    const uint32_t* __restrict__ start, double scale, const double* hi_in, const double* lo_in, double* hi_out,
-    double* lo_out, int32_t* flags, int64_t validate_below) {
-  extern __shared__ __align__(128) uint8_t st_smem[];
-  double* part = reinterpret_cast<double*>(st_smem);                     // [ST_APPLY][ST_COLS]
-  V* bval = reinterpret_cast<V*>(part + ST_APPLY * ST_COLS);             // [ST_STAGES][ST_ECAP]
-  int32_t* bcol = reinterpret_cast<int32_t*>(bval + ST_STAGES * ST_ECAP);  // [ST_STAGES][ST_ECAP]
-  SegInfo* seg = reinterpret_cast<SegInfo*>(bcol + ST_STAGES * ST_ECAP);  // [ST_STAGES][ST_RMAX]
-  int32_t* nseg = reinterpret_cast<int32_t*>(seg + ST_STAGES * ST_RMAX);  // [ST_STAGES]
-  uint64_t* full = reinterpret_cast<uint64_t*>(nseg + ST_STAGES);         // 8-aligned: ST_STAGES even
-  uint64_t* empty = full + ST_STAGES;
+    const uint32_t* __restrict__ start, double scale, const double* hi_in, const double* lo_in,
+    double* hi_out, double* lo_out, int32_t* flags, int64_t validate_below) {
+  extern __shared__ __align__(128) uint8_t k2_smem[];
+  constexpr int VPC = 16 / sizeof(V);  // values per 16-byte chunk
+  constexpr int RS = NB * K2_BATCH;    // row slots per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wbase = k2_smem + warp * (ST_COLS * 8 + RS * K2_SLOT * (4 + sizeof(V)) + RS * 24);
+  double* mine = reinterpret_cast<double*>(wbase);                              // [ST_COLS]
+  int32_t* cr = reinterpret_cast<int32_t*>(mine + ST_COLS);                     // [RS][K2_SLOT]
+  V* vr = reinterpret_cast<V*>(cr + RS * K2_SLOT);                              // [RS][K2_SLOT]
+  int4* mt = reinterpret_cast<int4*>(vr + RS * K2_SLOT);                        // [RS]
+  int64_t* ds = reinterpret_cast<int64_t*>(mt + RS);                            // [RS] (direct rows)
   const int64_t b = blockIdx.x / ngroups;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x - b * ngroups) * ST_COLS;
-  const int64_t width = d - c0 < ST_COLS ? d - c0 : ST_COLS;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST_STAGES; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&full[s])), "r"(1));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(csr_smem(&empty[s])), "r"(ST_APPLY));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int c = threadIdx.x; c < ST_APPLY * ST_COLS; c += blockDim.x) part[c] = 0.0;
-  __syncthreads();
+  const int width = static_cast<int>(d - c0 < ST_COLS ? d - c0 : ST_COLS);
+  for (int c = 2 * lane; c < ST_COLS; c += 64) *reinterpret_cast<double2*>(mine + c) = make_double2(0.0, 0.0);
+
   const uint32_t p0 = start[b], p1 = start[b + 1];
-  if (warp == 0) {
-    // ---- loader: 32 rows at a time, one lane per row — a warp scan places
-    //      each row's 16-byte aligned superset in the stage and the lane
-    //      issues its two cp.async.bulk copies; a row longer than a whole
-    //      stage is streamed in pieces by lane 0
-    uint32_t pb = p0;          // next pair batch
-    int bcnt = 0, bq = 0;      // pairs in the current batch / consumed
-    int64_t my_src = 0;
-    int32_t my_len = 0;
-    uint32_t my_v = 0;
-    // the next batch's (src, len, sign), loaded one batch ahead so the
-    // global-load latency overlaps the current batch's copies
-    int64_t nx_src = 0;
-    int32_t nx_len = 0;
-    uint32_t nx_v = 0;
-    if (lane < static_cast<int>(p1 - p0)) {
-      nx_src = msrc[p0 + lane];
-      nx_len = mlen[p0 + lane];
-      nx_v = svals[p0 + lane];
+  const int cnt = static_cast<int>(p1 - p0) > warp ? (static_cast<int>(p1 - p0) - warp + W - 1) / W : 0;
+  const int nbat = (cnt + K2_BATCH - 1) / K2_BATCH;
+  // metadata of my rows, 32 at a time (lane l: row base + l), one block ahead
+  int64_t bsrc = 0, nsrc = 0;
+  int32_t blen = 0, nlen = 0;
+  uint32_t bsv = 0, nsv = 0;
+  auto fetch = [&](int base, int64_t& s_, int32_t& l_, uint32_t& v_) {
+    l_ = 0;
+    if (base + lane < cnt) {
+      const uint32_t q = p0 + warp + static_cast<uint32_t>(W) * static_cast<uint32_t>(base + lane);
+      s_ = msrc[q];
+      l_ = mlen[q];
+      v_ = svals[q];
     }
-    int64_t lsrc = 0, lrem = 0;  // long row in progress (lane-uniform)
-    uint32_t lneg = 0;
-    bool lcont = false;
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t s = it % ST_STAGES, ph = (it / ST_STAGES) & 1u;
-      st_wait(&empty[s], ph ^ 1u);
-      int32_t* cbuf = bcol + s * ST_ECAP;
-      V* vbuf = bval + s * ST_ECAP;
-      int ns = 0, ne = 0;
-      bool done = false;
-      while (ns < ST_RMAX) {
-        if (lrem > 0) {
-          const int64_t room = ST_ECAP - ne - 6;
-          if (room < 1) break;
-          const int64_t plen = lrem < room ? lrem : room;
-          if (lane == 0) {
-            st_expect(&full[s], st_bytes<V>(col, val, lsrc, plen));
-            SegInfo si;
-            st_issue<V>(col, val, lsrc, plen, ne, cbuf, vbuf, &full[s], si.off, si.voff);
-            si.len = static_cast<int32_t>(plen);
-            si.flags = static_cast<int32_t>(lneg | (lcont ? 2u : 0u));
-            seg[s * ST_RMAX + ns] = si;
-          }
-          ++ns;
-          ne += st_slot(plen);
-          lsrc += plen;
-          lrem -= plen;
-          lcont = true;
-          continue;
-        }
-        if (bq == bcnt) {  // fetch the next 32 pairs' (src, len, sign) in parallel
-          if (pb >= p1) {
-            done = true;
-            break;
-          }
-          bcnt = p1 - pb < 32u ? static_cast<int>(p1 - pb) : 32;
-          my_src = nx_src;
-          my_len = nx_len;
-          my_v = nx_v;
-          pb += bcnt;
-          bq = 0;
-          if (pb + lane < p1) {
-            nx_src = msrc[pb + lane];
-            nx_len = mlen[pb + lane];
-            nx_v = svals[pb + lane];
-          }
-        }
-        const bool pend = lane >= bq && lane < bcnt;
-        const bool longrow = pend && st_slot(my_len) > ST_ECAP;
-        const uint32_t lm = __ballot_sync(0xFFFFFFFFu, longrow);
-        const int first_long = lm ? __ffs(lm) - 1 : 32;
-        const bool cand = pend && lane < first_long;
-        const int32_t S = cand && my_len > 0 ? st_slot(my_len) : 0;
-        const int32_t R = S > 0 ? 1 : 0;
-        int32_t incl = S, rincl = R;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o), tr = __shfl_up_sync(0xFFFFFFFFu, rincl, o);
-          if (lane >= o) {
-            incl += t;
-            rincl += tr;
-          }
-        }
-        const bool fits = ne + incl <= ST_ECAP && ns + rincl <= ST_RMAX;
-        const uint32_t nf = __ballot_sync(0xFFFFFFFFu, cand && !fits);
-        int stop = nf ? __ffs(nf) - 1 : first_long;  // first lane not taken
-        if (stop > bcnt) stop = bcnt;
-        const bool take = cand && lane < stop;
-        const uint32_t bytes = take && S > 0 ? st_bytes<V>(col, val, my_src, my_len) : 0u;
-        const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bytes);
-        if (lane == 0 && total) st_expect(&full[s], total);
-        __syncwarp();
-        if (take && S > 0) {
-          SegInfo si;
-          st_issue<V>(col, val, my_src, my_len, ne + incl - S, cbuf, vbuf, &full[s], si.off, si.voff);
-          si.len = my_len;
-          si.flags = static_cast<int32_t>(my_v & 1u);
-          seg[s * ST_RMAX + ns + rincl - 1] = si;
-        }
-        const int last_take = stop - 1;  // >= bq - 1
-        if (last_take >= bq) {
-          ne += __shfl_sync(0xFFFFFFFFu, incl, last_take);
-          ns += __shfl_sync(0xFFFFFFFFu, rincl, last_take);
-        }
-        bq = stop;
-        if (nf) break;  // the stage is full
-        if (first_long < bcnt && bq == first_long) {  // hand the long row to the piece path
-          lsrc = __shfl_sync(0xFFFFFFFFu, my_src, first_long);
-          lrem = __shfl_sync(0xFFFFFFFFu, my_len, first_long);
-          lneg = __shfl_sync(0xFFFFFFFFu, my_v, first_long) & 1u;
-          lcont = false;
-          ++bq;
+  };
+  fetch(0, bsrc, blen, bsv);
+  fetch(32, nsrc, nlen, nsv);
+  const int rr = lane >> 2, sub = lane & 3;  // copy: row of the batch, chunk phase
+  auto produce = [&](int t) {
+    if (t < nbat) {
+      const int i0 = t * K2_BATCH;  // first row of the batch (a multiple of 8)
+      if ((i0 & 31) == 0 && i0 > 0) {
+        bsrc = nsrc;
+        blen = nlen;
+        bsv = nsv;
+        fetch(i0 + 32, nsrc, nlen, nsv);
+      }
+      const int ml = (i0 & 31) + rr;
+      const int64_t src = __shfl_sync(0xFFFFFFFFu, bsrc, ml);
+      const int32_t len = __shfl_sync(0xFFFFFFFFu, blen, ml);
+      const uint32_t sv = __shfl_sync(0xFFFFFFFFu, bsv, ml);
+      const int slot = (t % NB) * K2_BATCH + rr;
+      const uintptr_t ca = reinterpret_cast<uintptr_t>(col + src), va = reinterpret_cast<uintptr_t>(val + src);
+      const int padc = static_cast<int>((ca & 15) >> 2), padv = static_cast<int>((va & 15) / sizeof(V));
+      const int nchc = (padc + len + 3) >> 2, nchv = (padv + len + VPC - 1) / VPC;
+      const bool direct = 4 * nchc > K2_SLOT || VPC * nchv > K2_SLOT;
+      if (!direct && len > 0) {
+        const char* gc = reinterpret_cast<const char*>(ca & ~uintptr_t{15});
+        const char* gv = reinterpret_cast<const char*>(va & ~uintptr_t{15});
+        int32_t* dc = cr + slot * K2_SLOT;
+        V* dv = vr + slot * K2_SLOT;
+        const int nch = nchc > nchv ? nchc : nchv;
+        for (int ch = sub; ch < nch; ch += 4) {
+          if (ch < nchc) cp_async16(dc + 4 * ch, gc + 16 * ch);
+          if (ch < nchv) cp_async16(dv + VPC * ch, gv + 16 * ch);
         }
       }
-      if (lane == 0) nseg[s] = done && ns == 0 ? -1 : ns;
-      if (done && ns > 0 && lane == 0) nseg[s] = ns | (1 << 30);  // last chunk
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&full[s])) : "memory");
-      if (done) break;
+      if (sub == 0) {
+        mt[slot] = make_int4(padc, padv, len, static_cast<int>(sv & 1u) | (direct ? 2 : 0));
+        ds[slot] = src;
+      }
     }
-  } else {
-    // ---- appliers
-    const int aw = warp - 1;
-    const bool validate = b < validate_below;
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int t = 0; t < NB - 1; ++t) produce(t);
+
+  // one row: lane l takes entries l, l + 32, l + 64, l + 96 (entry e sits at
+  // column slot padc + e and value slot padv + e); the next row's metadata is
+  // read two rows ahead and its entries one row ahead, so the loads overlap
+  // this row's read-add-store chain (shared accesses of one warp execute in
+  // order, so the next row's partial loads see this row's stores).  32-bit
+  // index math; one OSNAP column group (ONEG, d <= 4096) needs no range check
+  // (a valid column is in range; an invalid one is masked into the partial
+  // and flagged by block 0's checks); the sign (and a power-of-two scale,
+  // applied in the fold) rides in one DFMA; only OSNAP block 0's buckets run
+  // the checks (VALIDATE: every row meets block 0 exactly once).
+  const int c0i = static_cast<int>(c0);
+  auto rows = [&](auto vt) {
+    constexpr bool VALIDATE = decltype(vt)::value;
     int bad = 0;
-    int32_t lastcol = -1;
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t s = it % ST_STAGES, ph = (it / ST_STAGES) & 1u;
-      st_wait(&full[s], ph);
-      const int raw = nseg[s];
-      if (raw < 0) break;
-      const bool last = (raw >> 30) & 1;
-      const int ns = raw & ((1 << 30) - 1);
-      const V* vb = bval + s * ST_ECAP;
-      const int32_t* cb = bcol + s * ST_ECAP;
-      // segments are independent and this warp's partial row is private, so
-      // every entry is a plain load-add-store (lanes hold distinct columns)
-      double* mine = part + aw * ST_COLS;
-      for (int q = aw; q < ns; q += ST_APPLY) {
-        const SegInfo si = seg[s * ST_RMAX + q];
-        const double sg = (si.flags & 1) ? -scale : scale;
-        int32_t carry = -1;
-        if (validate && (si.flags & 2)) {
-          if (q > 0) {
-            const SegInfo sp = seg[s * ST_RMAX + q - 1];
-            carry = cb[sp.off + sp.len - 1];
-          } else {
-            carry = lastcol;
-          }
+    int32_t carry = -1;
+    auto apply4 = [&](const int32_t (&c)[4], const V (&x)[4], const int e0, const int len, const double sg) {
+      if constexpr (VALIDATE) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool live = e0 + 32 * u + lane < len;
+          const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c[u], 1);
+          const int32_t before = lane == 0 ? carry : cprev;
+          carry = __shfl_sync(0xFFFFFFFFu, c[u], 31);
+          if (live && (c[u] < 0 || c[u] >= d || c[u] <= before)) bad |= LVSK_FLAG_BADINDEX;
+          if (live && !isfinite(static_cast<double>(x[u]))) bad |= LVSK_FLAG_NONFINITE;
         }
-        // four 32-entry chunks at a time: one row's entries have distinct
-        // columns, so their loads / adds / stores are independent (ILP)
-        for (int e0v = 0; e0v < si.len; e0v += 128) {
-          int32_t cc[4];
-          double xx[4];
+      }
+      int lc[4];
+      double xd[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = e0v + 32 * u + lane;
-            const bool live = e < si.len;
-            const int32_t c = live ? cb[si.off + e] : INT32_MAX;
-            const V xv = live ? vb[si.voff + e] : V(0);
-            if (validate) {  // warp-uniform
-              const int32_t cprev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-              const int32_t before = lane == 0 ? carry : cprev;
-              carry = __shfl_sync(0xFFFFFFFFu, c, 31);
-              if (live) {
-                if (c < 0 || c >= d || c <= before) bad |= LVSK_FLAG_BADINDEX;
-                if (!isfinite(static_cast<double>(xv))) bad |= LVSK_FLAG_NONFINITE;
-              }
-            }
-            const int64_t lc = static_cast<int64_t>(c) - c0;
-            cc[u] = (live && lc >= 0 && lc < width) ? static_cast<int32_t>(lc) : -1;
-            xx[u] = __dmul_rn(sg, static_cast<double>(xv));
-          }
-          double old[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) old[u] = cc[u] >= 0 ? mine[cc[u]] : 0.0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (cc[u] >= 0) mine[cc[u]] = __dadd_rn(old[u], xx[u]);
+      for (int u = 0; u < 4; ++u) {
+        const bool live = e0 + 32 * u + lane < len;
+        if constexpr (ONEG) {
+          lc[u] = live ? (c[u] & (ST_COLS - 1)) : -1;
+        } else {
+          const int l = c[u] - c0i;
+          lc[u] = (live && static_cast<unsigned>(l) < static_cast<unsigned>(width)) ? l : -1;
         }
-        __syncwarp();  // the next segment may hit the same columns from other lanes
+        xd[u] = static_cast<double>(x[u]);
+        if constexpr (!POW2) xd[u] = __dmul_rn(sg, xd[u]);
       }
-      if (ns > 0) {
-        const SegInfo sl = seg[s * ST_RMAX + ns - 1];
-        lastcol = cb[sl.off + sl.len - 1];
+      double old[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) old[u] = lc[u] >= 0 ? mine[lc[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (lc[u] >= 0) {
+          if constexpr (POW2)
+            mine[lc[u]] = fma(xd[u], sg, old[u]);  // sg = +-1: exact, = old +- x
+          else
+            mine[lc[u]] = __dadd_rn(old[u], xd[u]);
+        }
       }
+    };
+    auto sgn_of = [&](const int4& m) { return POW2 ? ((m.w & 1) ? -1.0 : 1.0) : ((m.w & 1) ? -scale : scale); };
+    auto load_row = [&](int slot, const int4& m, int32_t (&c)[4], V (&x)[4]) {
+      const int32_t* cb = cr + slot * K2_SLOT + m.x;
+      const V* vb = vr + slot * K2_SLOT + m.y;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = cb[32 * u + lane];  // slot reads past the row stay inside shared memory; masked by len
+        x[u] = vb[32 * u + lane];
+      }
+    };
+#pragma unroll 1
+    for (int t = 0; t < nbat; ++t) {
+      produce(t + NB - 1);
+      cp_async_wait<NB - 1>();
       __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(csr_smem(&empty[s])) : "memory");
-      if (last) break;
+      const int base = (t % NB) * K2_BATCH;
+      const int nr = cnt - t * K2_BATCH < K2_BATCH ? cnt - t * K2_BATCH : K2_BATCH;
+      int4 m = mt[base];
+      int4 mn = mt[base + 1];  // (stale past nr: never used)
+      int32_t c[4];
+      V x[4];
+      load_row(base, m, c, x);
+#pragma unroll 1
+      for (int q = 0; q < nr; ++q) {
+        const int4 mc = m;
+        int32_t cc[4];
+        V xc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          cc[u] = c[u];
+          xc[u] = x[u];
+        }
+        if (q + 1 < nr) {
+          m = mn;
+          if (q + 2 < nr) mn = mt[base + q + 2];
+          load_row(base + q + 1, m, c, x);
+        }
+        if (!(mc.w & 2)) {
+          if constexpr (VALIDATE) carry = -1;
+          apply4(cc, xc, 0, mc.z, sgn_of(mc));
+        } else {  // a long row, straight from global memory, 128 entries per step
+          const int64_t src = ds[base + q];
+          const int len = mc.z;
+          if constexpr (VALIDATE) carry = -1;
+          for (int s0 = 0; s0 < len; s0 += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int e = s0 + 32 * u + lane;
+              cc[u] = e < len ? __ldg(col + src + e) : INT32_MAX;
+              xc[u] = e < len ? __ldg(val + src + e) : V(0);
+            }
+            apply4(cc, xc, s0, len, sgn_of(mc));
+            __syncwarp();
+          }
+        }
+      }
+      __syncwarp();  // slots of batch t are refilled next iteration
     }
-    const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
-    if (any && lane == 0) atomicOr(flags, any);
-  }
+    return bad;
+  };
+  const int bad = b < validate_below ? rows(std::true_type{}) : rows(std::false_type{});
+  cp_async_wait<0>();
+  const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (any && lane == 0) atomicOr(flags, any);
   __syncthreads();
-  for (int64_t c = threadIdx.x; c < width; c += blockDim.x) {
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
     double h = 0.0, l = 0.0;  // NULL input state = zeros (no read)
     if (hi_in) {
       h = hi_in[b * d + c0 + c];
       l = lo_in[b * d + c0 + c];
     }
 #pragma unroll
-    for (int w = 0; w < ST_APPLY; ++w) {
+    for (int w = 0; w < W; ++w) {
+      const double* pw = reinterpret_cast<const double*>(k2_smem + w * (ST_COLS * 8 + RS * K2_SLOT * (4 + sizeof(V)) + RS * 24));
       double su, er;
-      two_sum(h, part[w * ST_COLS + c], su, er);
+      two_sum(h, POW2 ? pw[c] * scale : pw[c], su, er);
       h = su;
       l = __dadd_rn(l, er);
     }
@@ -594,40 +514,38 @@ extern "C" int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t*
   if (getenv("LVSK_K2_DETERMINISTIC") == nullptr) {
     csr_prep_kernel<<<csr_grid(N, 256), 256, 0, st>>>(row_ptr, svals, N, msrc, mlen);
     const int sgroups = static_cast<int>((d + ST_COLS - 1) / ST_COLS);
-    const int vsz = val_dtype == LVSK_F64 ? 8 : 4;
-    // applier warps per CTA (each with a private 32 KB partial row): 2 fits two
-    // CTAs (two loader warps) per SM, 1 three; LVSK_K2_APPLY overrides (A/B)
-    const int apply = getenv("LVSK_K2_APPLY") ? atoi(getenv("LVSK_K2_APPLY")) : 2;
     const unsigned sgrid = static_cast<unsigned>(k * sgroups);
-    const int64_t vbelow = validate_below;
-#define LVSK_K2_LAUNCH(V, A)                                                                                       \
-  do {                                                                                                             \
-    const int sm = st_smem_bytes(A, static_cast<int>(sizeof(V)));                                                 \
-    rc = ensure_smem_attr(reinterpret_cast<const void*>(csr_stream_kernel<V, A>), sm, "csr stream smem attribute"); \
-    if (rc != LVSK_OK) return rc;                                                                                  \
-    csr_stream_kernel<V, A><<<sgrid, 32 * (1 + A), sm, st>>>(col, static_cast<const V*>(val), d, sgroups, svals,  \
-                                                             msrc, mlen, start, scale, hi_in, lo_in, hi_out,      \
-                                                             lo_out, flags, vbelow);                              \
+    // K2 v4: W self-loading warps x NB copy batches of 8 row slots (float
+    // values: 5 warps x 2 batches of 96-entry slots, one CTA per SM — the
+    // fastest of the measured shapes (2x2, 2x3, 4x3 with 124-entry slots:
+    // 7.4 / 7.8 / 8.1 ms against 6.9 ms at C4); float64 values: 4 x 2)
+    int sexp = 0;
+    const bool pow2 = std::frexp(scale, &sexp) == 0.5;  // scale = 2^k: applied exactly in the fold
+#define LVSK_K2_GO(V, W_, D_, S_, P_, O_)                                                                       \
+  do {                                                                                                          \
+    const int sm = k2_smem_bytes(W_, D_, static_cast<int>(sizeof(V)), S_);                                     \
+    auto kern = csr_sketch_kernel<V, W_, D_, P_, O_, S_>;                                                       \
+    rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), sm, "csr sketch smem attribute");               \
+    if (rc != LVSK_OK) return rc;                                                                               \
+    kern<<<sgrid, 32 * W_, sm, st>>>(col, static_cast<const V*>(val), d, sgroups, svals, msrc, mlen, start,     \
+                                     scale, hi_in, lo_in, hi_out, lo_out, flags, validate_below);               \
   } while (0)
-    if (val_dtype == LVSK_F32) {
-      if (apply == 1)
-        LVSK_K2_LAUNCH(float, 1);
-      else if (apply == 3)
-        LVSK_K2_LAUNCH(float, 3);
-      else if (apply == 5)
-        LVSK_K2_LAUNCH(float, 5);
-      else
-        LVSK_K2_LAUNCH(float, 2);
-    } else {
-      if (apply == 1)
-        LVSK_K2_LAUNCH(double, 1);
-      else if (apply == 3)
-        LVSK_K2_LAUNCH(double, 3);
-      else if (apply == 5)
-        LVSK_K2_LAUNCH(double, 5);
-      else
-        LVSK_K2_LAUNCH(double, 2);
-    }
+#define LVSK_K2_LAUNCH(V, W_, D_, S_)            \
+  do {                                           \
+    if (pow2 && sgroups == 1)                    \
+      LVSK_K2_GO(V, W_, D_, S_, true, true);     \
+    else if (pow2)                               \
+      LVSK_K2_GO(V, W_, D_, S_, true, false);    \
+    else if (sgroups == 1)                       \
+      LVSK_K2_GO(V, W_, D_, S_, false, true);    \
+    else                                         \
+      LVSK_K2_GO(V, W_, D_, S_, false, false);   \
+  } while (0)
+    if (val_dtype == LVSK_F32)
+      LVSK_K2_LAUNCH(float, 5, 2, 96);
+    else
+      LVSK_K2_LAUNCH(double, 4, 2, 96);
+#undef LVSK_K2_GO
 #undef LVSK_K2_LAUNCH
   } else if (val_dtype == LVSK_F32)
     csr_gather_kernel<float><<<grid, 32 * CSR_WARPS, smem, st>>>(row_ptr, col, static_cast<const float*>(val), d,

@@ -346,13 +346,19 @@ __device__ __forceinline__ void finish_diag(const FactorArgs& a, int j, const do
   signal(a.verA + j * a.nb + j, j + 1);
 }
 
-__global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
+// NT = 4 smem tiles, one CTA per SM (d <= 1024: the chain is the critical
+// path and keeps its next diagonal tile loaded ahead); NT = 3, two CTAs per
+// SM (large d: the queue's tile updates are the bound, and a second CTA per SM
+// overlaps one CTA's tile loads and dependency waits with the other's DMMAs;
+// the chain then loads its diagonal tile after the panel product).
+template <int NT>
+__global__ void __launch_bounds__(FTHREADS, NT == 3 ? 2 : 1) chol_fold_kernel(FactorArgs a) {
   extern __shared__ double fsm[];
   double* b0 = fsm;
   double* b1 = fsm + FT * FLD;
   double* b2 = fsm + 2 * FT * FLD;
-  double* b3 = fsm + 3 * FT * FLD;
-  double* scratch = fsm + 4 * FT * FLD;  // 5 x 64 doubles (chol_inv_tile)
+  double* b3 = NT == 4 ? fsm + 3 * FT * FLD : nullptr;
+  double* scratch = fsm + NT * FT * FLD;  // 5 x 64 doubles (chol_inv_tile)
   double* red = scratch + 5 * FT;        // 8 doubles
   __shared__ int4 s_task;
   cg::grid_group grid = cg::this_grid();
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
   }
   grid.sync();
 
-  if (cta == 0) {
+  if (cta == 0 && NT == 4) {
     // ---- the critical chain: DIAG(0), then CHAIN(1..nb-1), T_j kept in smem
     double *T = b0, *x = b1, *y = b2, *z = b3;
     kf_stamp(a, 0);
@@ -427,6 +433,42 @@ __global__ void __launch_bounds__(FTHREADS, 1) chol_fold_kernel(FactorArgs a) {
       double* freed = T;
       T = y;
       y = freed;
+    }
+    return;
+  }
+  if (cta == 0 && NT == 3) {
+    // ---- the chain in three tiles: T_j, the panel / diagonal tile, U_j,j+1
+    double *T = b0, *x = b1, *z = b2;
+    kf_stamp(a, 0);
+    load_tile(x, atile(a, 0, 0), dp);
+    __syncthreads();
+    chol_inv_tile(x, T, scratch, a.ctl + 2);
+    finish_diag(a, 0, T);
+    kf_stamp(a, 1);
+    for (int j = 0; j + 1 < nb; ++j) {
+      wait_ge(a.verA + j * nb + j + 1, j);
+      wait_ge(a.verA + (j + 1) * nb + j + 1, j);
+      __syncthreads();
+      kf_stamp(a, 2 + 3 * j);
+      load_tile(x, atile(a, j, j + 1), dp);
+      __syncthreads();
+      kf_stamp(a, 600 + 4 * j);
+      gemm_tile<0, false, 1>(T, x, nullptr, 0, z, FLD);  // U_j,j+1 = T_j^T A_j,j+1
+      __syncthreads();
+      kf_stamp(a, 601 + 4 * j);
+      store_tile(atile(a, j, j + 1), dp, z);
+      load_tile(x, atile(a, j + 1, j + 1), dp);
+      signal(a.verA + j * nb + j + 1, j + 1);  // (its __syncthreads also orders the load)
+      kf_stamp(a, 602 + 4 * j);
+      gemm_tile<1, false, 2>(z, z, x, FLD, x, FLD);  // in place (each thread owns its C fragment)
+      __syncthreads();
+      kf_stamp(a, 3 + 3 * j);
+      chol_inv_tile(x, z, scratch, a.ctl + 2);  // x = U_j+1,j+1, z = T_j+1
+      finish_diag(a, j + 1, z);
+      kf_stamp(a, 4 + 3 * j);
+      double* freed = T;
+      T = z;
+      z = freed;
     }
     return;
   }
@@ -643,10 +685,14 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.rt = P.rt;
   a.dp = P.dp;
   a.rp = P.rp;
-  const int smem = 4 * FTILE_SMEM + (5 * FT + 8) * 8;
-  const int32_t arc = ensure_smem_attr(reinterpret_cast<const void*>(chol_fold_kernel), smem, "chol_fold smem attribute");
+  // large d: three-tile CTAs, two per SM (the queue's tile updates dominate)
+  const bool wide = P.nb > 16 && getenv("LVSK_KF_ONE_CTA") == nullptr;
+  const void* fn = wide ? reinterpret_cast<const void*>(chol_fold_kernel<3>) : reinterpret_cast<const void*>(chol_fold_kernel<4>);
+  const int smem = (wide ? 3 : 4) * FTILE_SMEM + (5 * FT + 8) * 8;
+  const int32_t arc = ensure_smem_attr(fn, smem, "chol_fold smem attribute");
   if (arc != LVSK_OK) return arc;
-  const int grid_cap = resident_ctas(reinterpret_cast<const void*>(chol_fold_kernel), FTHREADS, smem) >= 1 ? num_sms() : 0;
+  const int per_sm = resident_ctas(fn, FTHREADS, smem);
+  const int grid_cap = per_sm >= 1 ? num_sms() * (wide && per_sm >= 2 ? 2 : 1) : 0;
   if (grid_cap < 2) return cuda_status(cudaErrorInvalidConfiguration, "chol_fold needs two co-resident CTAs");
   // CTA 0 runs the chain; more queue CTAs than tasks only add polling
   const int ntask = kf_queue_tasks(P.nb, P.rt);
@@ -665,7 +711,7 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   const bool tracing = getenv("LVSK_KF_TRACE") != nullptr;
   if (tracing && trace == nullptr) cudaMalloc(&trace, 1024 * sizeof(unsigned long long));
   a.trace = tracing ? trace : nullptr;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, chol_fold_kernel, a);
+  cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, chol_fold_kernel<3>, a) : cudaLaunchKernelEx(&cfg, chol_fold_kernel<4>, a);
   if (e != cudaSuccess) return cuda_status(e, "chol_fold launch");
   if (tracing) {
     unsigned long long h[1024];

@@ -663,7 +663,7 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": pipe.launches_per_run() * args.steps,
+            "gpu_launches": pipe.launches_per_run(csr=csr) * args.steps,
             "clocks": clocks.summary(),
         }
         if csr:

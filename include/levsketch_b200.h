@@ -195,7 +195,8 @@ LVSK_API int32_t lvsk_split_fold(const double* M, int64_t d, int64_t r, int32_t 
  * row_ptr[0]); col: int32, strictly increasing per row, in [0, d);
  * val: F32 or F64.  Bad indices set LVSK_FLAG_BADINDEX, non-finite values
  * LVSK_FLAG_NONFINITE.  hi_in = lo_in = NULL means a zero input state (not
- * read).  K6 takes M as float32 d x r (r <= 256). */
+ * read); lo_out = NULL writes the folded sketch hi + lo to hi_out instead of
+ * the pair (as lvsk_hashed_sketch).  K6 takes M as float32 d x r (r <= 256). */
 LVSK_API size_t lvsk_hashed_csr_workspace_bytes(int64_t n, int32_t s, int64_t k);
 LVSK_API int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t* col, const void* val,
                                         int32_t val_dtype, int64_t n, int64_t d, uint64_t row0,

@@ -98,8 +98,12 @@ __global__ void __launch_bounds__(32 * CSR_WARPS) csr_gather_kernel(
     __syncwarp();
   }
   for (int64_t c = lane; c < width; c += 32) {
-    hi_out[b * d + c0 + c] = hi[c];
-    lo_out[b * d + c0 + c] = lo[c];
+    if (lo_out) {
+      hi_out[b * d + c0 + c] = hi[c];
+      lo_out[b * d + c0 + c] = lo[c];
+    } else {  // the folded sketch hi + lo (lvsk_fold_compensated's value)
+      hi_out[b * d + c0 + c] = hi[c] + lo[c];
+    }
   }
   const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
   if (any && lane == 0) atomicOr(flags, any);
@@ -371,8 +375,12 @@ __global__ void __launch_bounds__(32 * W) csr_sketch_kernel(
       h = su;
       l = __dadd_rn(l, er);
     }
-    hi_out[b * d + c0 + c] = h;
-    lo_out[b * d + c0 + c] = l;
+    if (lo_out) {
+      hi_out[b * d + c0 + c] = h;
+      lo_out[b * d + c0 + c] = l;
+    } else {  // the folded sketch hi + lo (lvsk_fold_compensated's value)
+      hi_out[b * d + c0 + c] = h + l;
+    }
   }
 }
 

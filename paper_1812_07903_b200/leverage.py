@@ -27,7 +27,7 @@ import torch
 
 from . import _native as N
 from .config import ensure_capacity
-from .errors import CapacityError, DegenerateInputError, FormatError, SingularInversionError
+from .errors import CapacityError, DegenerateInputError, DimensionMismatchError, FormatError, SingularInversionError
 from .matrix import device_matrix, format_float
 from .sketch import SketchSpec, apply_sketch, sketch_rows
 from .svd import SvdResult, thin_svd, truncate
@@ -330,6 +330,9 @@ def spectral_fold(sx: torch.Tensor, sv_tol: float | None, rank: int | None, pi: 
     basis = vt[:r].T / sigma[:r]
     if r <= jl:
         return basis.contiguous(), r
+    if k < d:  # R is k x d: "R M = Pi" (Pi: d x r) needs a square factor
+        raise DimensionMismatchError(f"a JL fold of width {jl} needs a sketch with at least d = {d} rows "
+                                     f"(k = {k}) once the kept rank {r} exceeds the JL width")
     ur = (_positive_r(sx) @ vt[:r].T) / sigma[:r] if u is None else u[:, :r]
     return (basis @ (ur.T @ pi)).contiguous(), r
 

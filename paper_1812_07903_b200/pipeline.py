@@ -83,14 +83,18 @@ class LeveragePipeline:
         L, st, s = N.lib(), N.stream_ptr(), self.state
         fam = self.spec.family
         if isinstance(X, CSRMatrix):
-            # a fresh state each run: NULL (hi_in, lo_in) = zeros, no memset and no state read
+            # a fresh state each run: NULL (hi_in, lo_in) = zeros, no memset and no state read;
+            # without keep_state K2 writes the folded SX straight away (no state pair, no fold pass)
+            keep = self.keep_state
             N.check(L.lvsk_hashed_sketch_csr(X.indptr.data_ptr(), X.indices.data_ptr(), X.data.data_ptr(),
                                              csr_code(X), X.n, X.d, self.row0, s._blocks, self.spec.s, s._scale,
-                                             None, None, s._hi.data_ptr(), s._lo.data_ptr(),
+                                             None, None, s._hi.data_ptr() if keep else self.sx.data_ptr(),
+                                             s._lo.data_ptr() if keep else None,
                                              self.k, self.ws_sketch.data_ptr(), self.ws_sketch.numel(),
                                              self.flags.data_ptr(), st), "csr sketch")
-            N.check(L.lvsk_fold_compensated(s._hi.data_ptr(), s._lo.data_ptr(), self.sx.data_ptr(), self.sx.numel(), st),
-                    "fold")
+            if keep:
+                N.check(L.lvsk_fold_compensated(s._hi.data_ptr(), s._lo.data_ptr(), self.sx.data_ptr(),
+                                                self.sx.numel(), st), "fold")
             return
         ldx = X.stride(0)
         if fam == SRHT:
@@ -240,8 +244,10 @@ class LeveragePipeline:
         if f & N.FLAG_NONFINITE:
             raise FormatError("matrix contains non-finite entries")
 
-    def launches_per_run(self) -> int:
-        """Kernels this library launches per run() (host-side count)."""
+    def launches_per_run(self, csr: bool = False) -> int:
+        """Kernels this library launches per run() (host-side count; csr: the
+        input is a CSRMatrix — K2 adds the row-metadata pass and never uses
+        the cooperative grouping)."""
         fam = self.spec.family
         radix = lambda items, bits: 3 * max(1, (bits + 7) // 8)  # noqa: E731
         if fam == SRHT:
@@ -255,9 +261,9 @@ class LeveragePipeline:
         else:
             # grouping: one cooperative counting sort (k <= 4096, s <= 64; csrc/sketch_hashed.cu)
             # or keygen + radix passes + bucket bounds; then the gather (K1) and the hi+lo fold
-            coop = self.k <= 4096 and self.spec.s <= 64 and not os.environ.get("LVSK_GROUP_RADIX")
+            coop = self.k <= 4096 and self.spec.s <= 64 and not os.environ.get("LVSK_GROUP_RADIX") and not csr
             group = 1 if coop else 1 + radix(self.n * self.spec.s, max(1, (self.k - 1).bit_length())) + 1
-            sk = group + 1 + (1 if self.keep_state else 0)
+            sk = group + (1 if csr else 0) + 1 + (1 if self.keep_state else 0)
         lev = 1
         k, d = self.sx.shape
         # KF (chol_fold_kernel) + the K5 operand split (split_fold_kernel)

@@ -2,6 +2,7 @@
 the reference's golden vectors and the CPU oracle.  Needs a B200."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -744,11 +745,13 @@ def _random_csr(n, d, per_row, seed, dtype=np.float32):
     return (indptr, col, val, (n, d)), dense
 
 
-@pytest.mark.parametrize("n,d,k,s", [(3000, 300, 512, 4), (1500, 2100, 1024, 3), (777, 64, 128, 1)])
+@pytest.mark.parametrize("n,d,k,s", [(3000, 300, 512, 4), (1500, 2100, 1024, 3), (777, 64, 128, 1),
+                                     (600, 5000, 256, 2), (500, 9000, 128, 4)])
 def test_csr_sketch_bit_exact_vs_dense(n, d, k, s, monkeypatch):
-    """K2 default (order-free compensated atomics): hi + lo within 1e-13 of the
-    reference's compensated state; LVSK_K2_DETERMINISTIC=1 (ordered gather):
-    bit-exact."""
+    """K2 default (per-warp float64 partial rows + TwoSum fold): hi + lo within
+    1e-13 of the reference's compensated state — power-of-two and other
+    scales, one and several 4096-column groups; LVSK_K2_DETERMINISTIC=1
+    (ordered gather): bit-exact."""
     csr, dense = _random_csr(n, d, 40, seed=n + d)
     fam = "osnap" if s > 1 else "countsketch"
     spec = P.SketchSpec(fam, eps=0.5, d=d, seed=7, rows_override=k, osnap_s=s if fam == "osnap" else None)
@@ -1060,3 +1063,45 @@ def test_k1_folded_output_equals_pair_then_fold():
     pipe = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=1e-6, jl_dim=32)
     scores, _ = pipe.run(X)
     assert torch.equal(pipe.sx, ref)
+
+
+def test_k2_folded_output_equals_pair_then_fold():
+    """lvsk_hashed_sketch_csr with lo_out = NULL writes hi + lo straight into
+    hi_out: bit-identical to the pair followed by lvsk_fold_compensated (the
+    pipeline's single-GPU CSR path), for the fast and the ordered kernels."""
+    csr, dense = _random_csr(3000, 700, 40, seed=31)
+    m = P.csr.CSRMatrix(*csr)
+    n, d, k = 3000, 700, 1024
+    spec = P.SketchSpec("osnap", eps=0.5, d=d, seed=6, rows_override=k, osnap_s=4)
+    L = N.lib()
+    ws = torch.empty(int(L.lvsk_hashed_csr_workspace_bytes(n, 4, k)), dtype=torch.uint8, device="cuda")
+    out = torch.empty((k, d), dtype=torch.float64, device="cuda")
+    for det in (False, True):
+        if det:
+            os.environ["LVSK_K2_DETERMINISTIC"] = "1"
+        try:
+            st = P.apply_sketch(csr, spec)
+            ref = st.data_device
+            fl = N.Flags()
+            N.check(L.lvsk_hashed_sketch_csr(m.indptr.data_ptr(), m.indices.data_ptr(), m.data.data_ptr(),
+                                             P.csr.csr_code(m), n, d, 0, st._blocks, 4, st._scale, None, None,
+                                             out.data_ptr(), None, k, ws.data_ptr(), ws.numel(), fl.p,
+                                             N.stream_ptr()))
+        finally:
+            os.environ.pop("LVSK_K2_DETERMINISTIC", None)
+        assert torch.equal(out, ref)
+    pipe = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=1e-6, jl_dim=32)
+    pipe.run(m)
+    assert torch.allclose(pipe.sx, ref, rtol=1e-13, atol=1e-13 * float(ref.abs().max()))
+
+
+def test_jl_fold_needs_k_at_least_d():
+    """The JL fold "R M = Pi" needs a square triangular factor: with fewer
+    sketch rows than columns and a kept rank above the JL width it raises
+    DimensionMismatchError (not a shape error from inside the linear algebra)."""
+    rng = np.random.default_rng(2)
+    n, d, k = 4000, 300, 256
+    X = dev(rng.standard_normal((n, d)).astype(np.float32))
+    spec = P.SketchSpec("countsketch", eps=0.5, d=d, seed=1, rows_override=k)
+    with pytest.raises(errors.DimensionMismatchError):
+        P.leverage_sketched_trunc(X, spec, 1e-6, jl_dim=32)

@@ -232,28 +232,62 @@ def cholesky_fold(sx: torch.Tensor, sv_tol: float | None, pi: torch.Tensor):
 _EIGH_KAPPA = 1e4
 
 
+_EYE: dict = {}
+
+
+def _chol_inv(G: torch.Tensor) -> torch.Tensor:
+    """R^-1 for the positive-diagonal Cholesky factor of the SPD G = R^T R,
+    by the KF kernel with Pi = I (csrc/factor.cu: one launch, no host
+    synchronisation; replaces cuSOLVER potrf + trsm, ~0.1 ms of launch
+    latency per call at b = 136; the C5 fold measured 3.24 ms against 3.61 ms
+    with potrf + trsm).  A non-positive pivot yields non-finite
+    values, which the caller's residual test rejects."""
+    b = G.shape[0]
+    key = (b, G.device)
+    eye = _EYE.get(key)
+    if eye is None:
+        eye = _EYE[key] = torch.eye(b, dtype=torch.float64, device=G.device)
+    wkey = (b, b, G.device, torch.cuda.current_stream(G.device).cuda_stream)
+    ws = _FOLD_WS.get(wkey)
+    if ws is None:
+        ws = _FOLD_WS[wkey] = fold_workspace(b, b, G.device)
+    M = torch.empty((b, b), dtype=torch.float64, device=G.device)
+    diag = torch.empty(3, dtype=torch.float64, device=G.device)
+    G = G.contiguous()
+    N.check(N.lib().lvsk_chol_fold(G.data_ptr(), b, b, eye.data_ptr(), b, M.data_ptr(), diag.data_ptr(),
+                                   _CHOL_KAPPA_GUARD, None, ws.data_ptr(), ws.numel(), N.stream_ptr()), "cholesky qr")
+    return M
+
+
 def _cholqr2(Y: torch.Tensor, rounds: int = 2) -> torch.Tensor:
     """Orthonormal basis of range(Y) by two rounds of Cholesky QR (stable for
     cond(Y) up to ~1e7 in float64; one round leaves an orthogonality error of
     ~eps * cond(Y)^2, harmless between power steps, which re-condition the
-    block).  No host synchronisation: a failed factorisation yields NaNs,
-    which the caller's residual test rejects."""
+    block): Y <- Y R^-1 with R^-1 from the KF kernel.  No host
+    synchronisation: a failed factorisation yields non-finite values, which
+    the caller's residual test rejects."""
     for _ in range(rounds):
-        L, _ = torch.linalg.cholesky_ex(Y.T @ Y)
-        Y = torch.linalg.solve_triangular(L, Y.T, upper=False).T
+        Y = Y @ _chol_inv(Y.T @ Y)
     return Y
 
 
 def _topk_gram(G: torch.Tensor, want: int, rounds: int = 2, iters: int = 6, tol: float = 1e-12):
     """Top `want` eigenpairs (descending) of the SPD Gram G by block subspace
-    iteration: block want + max(16, want / 4) rounded up to 32, seeded start,
+    iteration: block want + max(16, want / 4) rounded up to 8 (at least 136
+    above 96: the eigensolver is faster there), seeded start,
     `iters` power steps with Cholesky-QR re-orthonormalisation per round, then
     one Rayleigh-Ritz (the only small dense eigensolve: ~2 ms on a B200, so it
     is not run per step).  Accepted only when every kept Ritz pair has
     ||G v - theta v|| <= tol * theta_1; else another round, then None (the
     caller falls back to the full eigensolver)."""
     d = G.shape[0]
-    b = min(d, -(-(want + max(16, want // 4)) // 32) * 32)
+    b = -(-(want + max(16, want // 4)) // 8) * 8
+    if 96 < b < 136:
+        # cuSOLVER's float64 eigh takes ~2.1 ms up to n = 131 and ~1.2 ms from
+        # n = 132 (a different tridiagonalisation / back-transformation path;
+        # tools/eigh_size_probe.py): a slightly wider block is cheaper overall
+        b = 136
+    b = min(d, b)
     gen = torch.Generator(device=G.device).manual_seed(0x5EED)
     Q = torch.randn(d, b, dtype=G.dtype, device=G.device, generator=gen)
     for _ in range(rounds):

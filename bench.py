@@ -12,9 +12,9 @@ N > 1 (torchrun, NCCL): weak scaling, 1e6 rows per rank with global row
 indices (C5: its 8e6 rows split across ranks, strong); the compensated
 sketch partials meet in a sliced all-to-all merged in rank order, every rank
 folds the same SX (deterministic kernels, identical M, no broadcast on the
-critical path), scores stay rank-local, and rank 0 sorts the gathered
-probabilities (the global "dec" order) on a side stream that the timed
-region waits for.
+critical path), scores stay rank-local, every rank argsorts its own
+probabilities (K7) and rank 0 merges the gathered sorted runs into the global
+"dec" order (KM) on a side stream that the timed region waits for.
 
 --impl reference times the reference package itself (baseline/_ref, a pip
 install of /root/reference/pkg) on the box's host cores: C2 through its
@@ -25,6 +25,8 @@ over the config's full 1e6 rows per step, on inputs from the same generator.
 from __future__ import annotations
 
 import argparse
+import ctypes
+import itertools
 import json
 import math
 import os
@@ -388,22 +390,33 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
         pipe.n = n  # local rows; the state covers n_total global rows
         pipe.scores = torch.empty(n, dtype=torch.float64, device=dev)
         pipe.keep_state = True  # the sliced merge exchanges the compensated pairs
-    # multi-rank global order: rank 0 sorts the gathered probabilities of step i on a
-    # side stream while step i+1 sketches; the timed region ends after the last sort
+    # multi-rank global order: every rank argsorts its own probabilities (K7, in
+    # parallel), rank 0 gathers keys + local orders and merges the R sorted runs
+    # (KM, ceil(log2 R) merge-path rounds) on a side stream while step i+1
+    # sketches; the timed region ends after the last merge
     gather_p = [torch.empty(n_total, dtype=torch.float64, device=dev) for _ in range(2)] \
+        if world > 1 and rank == 0 else None
+    gather_i = [torch.empty(n_total, dtype=torch.int32, device=dev) for _ in range(2)] \
         if world > 1 and rank == 0 else None
     order_all = [torch.empty(n_total, dtype=torch.int64, device=dev) for _ in range(2)] \
         if world > 1 and rank == 0 else None
     side = torch.cuda.Stream(device=dev) if world > 1 else None
     sort_done = [None, None]
     buf = [0]
-    ws_sort = torch.empty(max(N.lib().lvsk_argsort_workspace_bytes(n_total), 256), dtype=torch.uint8, device=dev) \
-        if world > 1 and rank == 0 else None
+    ws_merge = torch.empty(max(N.lib().lvsk_merge_runs_workspace_bytes(n_total, world), 256), dtype=torch.uint8,
+                           device=dev) if world > 1 and rank == 0 else None
+    ws_local = torch.empty(max(N.lib().lvsk_argsort_workspace_bytes(n), 256), dtype=torch.uint8, device=dev) \
+        if world > 1 else None
+    local_order = torch.empty(n, dtype=torch.int64, device=dev) if world > 1 else None
+    merge_flags = torch.zeros(1, dtype=torch.int32, device=dev) if world > 1 and rank == 0 else None
     pi = jl_device(0, d, r)
     counts = counts_of(name, cfg, world, args.rows)
     even = len(set(counts)) == 1
     p_pad = torch.zeros(max(counts), dtype=torch.float64, device=dev) if world > 1 and not even else None
+    o_pad = torch.zeros(max(counts), dtype=torch.int32, device=dev) if world > 1 and not even else None
     parts = [torch.empty(max(counts), dtype=torch.float64, device=dev) for _ in range(world)] \
+        if world > 1 and rank == 0 and not even else None
+    iparts = [torch.empty(max(counts), dtype=torch.int32, device=dev) for _ in range(world)] \
         if world > 1 and rank == 0 and not even else None
     nnz = X.nnz if csr else None
 
@@ -445,40 +458,63 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
         if timing:
             ev["leverage"][1].record()
             ev["order"][0].record()
-        # global dec order: p = s / global sum, gathered to rank 0 only, sorted there
+        # global dec order: p = s / global sum; every rank sorts its run (K7), rank 0
+        # gathers keys + local orders and merges the runs (KM)
         local_sum = pipe.scores.sum().reshape(1)
         dist.all_reduce(local_sum)
         p_local = pipe.scores / local_sum
+        N.check(N.lib().lvsk_argsort_f64(p_local.data_ptr(), n, 1, local_order.data_ptr(), ws_local.data_ptr(),
+                                         ws_local.numel(), N.stream_ptr()), "local argsort")
+        o_local = local_order.to(torch.int32)
+        p_local = p_local[local_order]  # this rank's sorted run (KM streams the runs)
         if not even:  # equal-size gather: pad to the largest partition
             p_pad[:n] = p_local
             p_local = p_pad
+            o_pad[:n] = o_local
+            o_local = o_pad
         if rank == 0:
             b = buf[0]
             buf[0] ^= 1
-            if sort_done[b] is not None:  # the sort of two steps ago has released this buffer
+            if sort_done[b] is not None:  # the merge of two steps ago has released this buffer
                 torch.cuda.current_stream().wait_event(sort_done[b])
             if even:
                 gather0(p_local, list(gather_p[b].view(world, n).unbind(0)))
+                gather0(o_local, list(gather_i[b].view(world, n).unbind(0)))
             else:
                 gather0(p_local, parts)
                 torch.cat([parts[q][: counts[q]] for q in range(world)], out=gather_p[b])
+                gather0(o_local, iparts)
+                torch.cat([iparts[q][: counts[q]] for q in range(world)], out=gather_i[b])
             ready = torch.cuda.Event()
             ready.record()
             side.wait_event(ready)
             with torch.cuda.stream(side):
-                N.check(N.lib().lvsk_argsort_f64(gather_p[b].data_ptr(), n_total, 1, order_all[b].data_ptr(),
-                                                 ws_sort.data_ptr(), ws_sort.numel(), N.stream_ptr()))
+                offs = (ctypes.c_int64 * (world + 1))(*([0] + list(itertools.accumulate(counts))))
+                N.check(N.lib().lvsk_merge_argsort_runs(gather_p[b].data_ptr(), gather_i[b].data_ptr(), offs, world,
+                                                        1, order_all[b].data_ptr(), ws_merge.data_ptr(),
+                                                        ws_merge.numel(), merge_flags.data_ptr(), N.stream_ptr()),
+                        "merge argsort runs")
                 done = torch.cuda.Event()
                 done.record()
             sort_done[b] = done
         else:
             gather0(p_local, None)
+            gather0(o_local, None)
         if timing:
             ev["order"][1].record()
 
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def run_keys_global(b):
+        # the gathered sorted runs back in global row order (checks only)
+        offs = torch.tensor([0] + list(itertools.accumulate(counts))[:-1], dtype=torch.int64, device=dev)
+        rid = torch.repeat_interleave(torch.arange(world, device=dev), torch.tensor(counts, device=dev))
+        g = offs[rid] + gather_i[b].to(torch.int64)
+        pg = torch.empty_like(gather_p[b])
+        pg[g] = gather_p[b]
+        return pg
 
     def drain_sorts():
         # the timed region includes rank 0's last global sort
@@ -525,8 +561,9 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
         # the last global order is a descending permutation of the gathered probabilities
         lb = buf[0] ^ 1
         o = order_all[lb]
-        ps = gather_p[lb][o]
+        ps = run_keys_global(lb)[o]
         ok = bool((ps[:-1] >= ps[1:]).all()) and bool((torch.bincount(o, minlength=n_total) == 1).all())
+        ok = ok and int(merge_flags.item()) == 0
         if not ok:
             raise SystemExit("bench: multi-rank global order failed its check")
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
@@ -538,7 +575,8 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
     value = n_total / (ms_per_step / 1000.0)
 
     if args.verify:
-        verify(args, name, cfg, X, pipe, rank, world, n, n_total, lo, gather_p, order_all, buf, dev)
+        verify(args, name, cfg, X, pipe, rank, world, n, n_total, lo,
+               [run_keys_global(0), run_keys_global(1)] if world > 1 and rank == 0 else gather_p, order_all, buf, dev)
 
     # ---- per-kernel roofline (algorithmic bytes / event-timed duration) ----
     peak, peak_src = measured_peaks()

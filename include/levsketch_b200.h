@@ -255,6 +255,21 @@ LVSK_API size_t lvsk_argsort_workspace_bytes(int64_t n);
 LVSK_API int32_t lvsk_argsort_f64(const double* keys, int64_t n, int32_t descending, int64_t* idx_out,
                          void* ws, size_t ws_bytes, void* stream);
 
+/* KM: the multi-rank global order.  R runs in global (rank) order, run q of
+ * length run_off[q+1] - run_off[q] (run_off: HOST array of R + 1 offsets,
+ * run_off[0] = 0); each rank sorted its run with lvsk_argsort_f64: run_idx
+ * holds that local stable order (int32, local to the run) and sorted_keys the
+ * run's keys in that order (keys_q[run_idx_q[i]]), both concatenated run
+ * after run.  idx_out (n int64) receives the stable argsort of the
+ * concatenated keys — identical to lvsk_argsort_f64 on them (make_plan "dec"
+ * over all ranks, order.py:89-90; run_distributed concatenates the
+ * per-worker scores in worker order, dist.py:126-129).  A local index outside
+ * its run sets LVSK_FLAG_BADINDEX. */
+LVSK_API size_t lvsk_merge_runs_workspace_bytes(int64_t n, int32_t runs);
+LVSK_API int32_t lvsk_merge_argsort_runs(const double* sorted_keys, const int32_t* run_idx, const int64_t* run_off,
+                                int32_t runs, int32_t descending, int64_t* idx_out, void* ws, size_t ws_bytes,
+                                int32_t* flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,8 @@ _SIGS = {
     "lvsk_chol_fold": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _D, _P, _P, _SZ, _P]),
     "lvsk_argsort_workspace_bytes": (_SZ, [_I64]),
     "lvsk_argsort_f64": (_I32, [_P, _I64, _I32, _P, _P, _SZ, _P]),
+    "lvsk_merge_runs_workspace_bytes": (_SZ, [_I64, _I32]),
+    "lvsk_merge_argsort_runs": (_I32, [_P, _P, C.POINTER(C.c_int64), _I32, _I32, _P, _P, _SZ, _P, _P]),
 }
 
 _lib = None

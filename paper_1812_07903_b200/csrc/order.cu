@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdio>
+#include <vector>
 
 #include "radix_sort.cuh"
 
@@ -542,6 +543,190 @@ static int32_t det_sum(const double* x, int64_t n, double* out, double* partial,
 
 using namespace lvsk;
 
+// ---- KM: merge of per-rank sorted runs (multi-rank "dec" order) ---------------
+//
+// Multi-rank ordering: every rank argsorts its own probabilities (K7, in
+// parallel), rank 0 gathers the R sorted runs (keys in local sorted order +
+// the local indices) — a streaming read, no random gathers — and merges them
+// into the stable argsort of the concatenation — the same
+// permutation lvsk_argsort_f64 returns for the gathered keys (runs are in rank
+// = global row order, so a stable merge that takes the earlier run on ties
+// reproduces numpy's stable tie order).  Pairwise merge-path rounds (ceil(log2 R))
+// over (uint64 key image, uint32 global index) pairs; each CTA merges a
+// 4096-output chunk of one pair through shared memory (its merge-path split
+// found up front by km_split_kernel), each thread 8 outputs.
+constexpr int KM_THREADS = 512;
+constexpr int KM_ITEMS = 8;
+constexpr int KM_CHUNK = KM_THREADS * KM_ITEMS;
+constexpr int KM_MAX_RUNS = 512;
+
+struct KmPairs {
+  int64_t a0[KM_MAX_RUNS / 2 + 1], la[KM_MAX_RUNS / 2 + 1], lb[KM_MAX_RUNS / 2 + 1];
+  int64_t r0[KM_MAX_RUNS / 2 + 1], r1[KM_MAX_RUNS / 2 + 1];  // round 1: global offsets of the pair's runs
+  int64_t chunk0[KM_MAX_RUNS / 2 + 2];  // first chunk of each pair (prefix)
+  int npairs;
+};
+
+// Element e of the working array: its uint64 key image and uint32 global
+// index.  Round 1 (SRC = 1) reads the gathered runs directly — the double key
+// sorted_keys[e] and the run-local index run_idx[e] (global = the run's offset
+// + local; within a merged pair A is run 2i, B run 2i + 1) — so no expand pass;
+// later rounds (SRC = 0) read the previous round's (image, index) pairs.
+struct KmSrc {
+  const uint64_t* kimg;
+  const uint32_t* gidx;
+  const double* skeys;
+  const int32_t* ridx;
+  int descending;
+};
+template <int SRC>
+__device__ __forceinline__ uint64_t km_key(const KmSrc& S, int64_t e) {
+  if constexpr (SRC == 0) {
+    return S.kimg[e];
+  } else {
+    const double x = S.skeys[e];
+    return f64_key(S.descending ? -x : x);
+  }
+}
+template <int SRC>
+__device__ __forceinline__ uint32_t km_idx(const KmSrc& S, int64_t e, int64_t run_off) {
+  if constexpr (SRC == 0) return S.gidx[e];
+  else return static_cast<uint32_t>(run_off + S.ridx[e]);
+}
+
+// merge-path split of every chunk boundary of a round: one warp per boundary,
+// a 32-ary search (each step samples 32 positions and ballots the monotone
+// predicate A[i] <= B[t-1-i], i.e. "A[i] is among the first t outputs")
+template <int SRC>
+__global__ void km_split_kernel(const __grid_constant__ KmPairs P, int64_t nchunks, KmSrc S,
+                                int64_t* __restrict__ split) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  if (c >= nchunks) return;
+  int q = 0;
+  while (q + 1 < P.npairs && P.chunk0[q + 1] <= c) ++q;
+  const int64_t a0 = P.a0[q], la = P.la[q], lb = P.lb[q], b0 = a0 + la;
+  const int64_t t = (c - P.chunk0[q]) * KM_CHUNK;
+  int64_t lo = t - lb > 0 ? t - lb : 0, hi = t < la ? t : la;  // answer in [lo, hi]
+  while (hi > lo) {
+    // candidates lo + (j + 1) * step - 1, j < 32, clipped to hi - 1
+    const int64_t span = hi - lo;
+    const int64_t step = (span + 31) / 32;
+    int64_t i = lo + (lane + 1) * step - 1;
+    if (i > hi - 1) i = hi - 1;
+    const bool pr = km_key<SRC>(S, a0 + i) <= km_key<SRC>(S, b0 + t - 1 - i);
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, pr);  // a prefix of lanes (monotone)
+    const int ntrue = __popc(m);
+    // the first false candidate bounds the answer from above
+    const int64_t nlo = ntrue == 0 ? lo : (lo + ntrue * step > hi ? hi : lo + ntrue * step);
+    const int64_t cand_hi = ntrue == 32 ? hi : lo + (ntrue + 1) * step - 1;
+    lo = nlo;
+    hi = cand_hi < hi ? cand_hi : hi;
+    if (step == 1) {  // every position in [old lo, old hi) was a candidate
+      hi = lo;
+    }
+  }
+  if (lane == 0) split[c] = lo;
+}
+
+template <int SRC, bool FINAL>
+__global__ void __launch_bounds__(KM_THREADS) km_merge_kernel(const __grid_constant__ KmPairs P, KmSrc S,
+                                                             const int64_t* __restrict__ split,
+                                                             uint64_t* __restrict__ kout, uint32_t* __restrict__ iout,
+                                                             int64_t* __restrict__ final_out) {
+  __shared__ uint64_t sk[KM_CHUNK];
+  __shared__ uint32_t si[KM_CHUNK];
+  const int64_t chunk = blockIdx.x;
+  int q = 0;
+  while (q + 1 < P.npairs && P.chunk0[q + 1] <= chunk) ++q;
+  const int64_t a0 = P.a0[q], la = P.la[q], lb = P.lb[q];
+  const int64_t t0 = (chunk - P.chunk0[q]) * KM_CHUNK;
+  const int64_t t1 = t0 + KM_CHUNK < la + lb ? t0 + KM_CHUNK : la + lb;
+  const int64_t i0 = split[chunk];
+  const int64_t i1 = chunk + 1 < P.chunk0[q + 1] ? split[chunk + 1] : la;  // a pair's last chunk ends with all of A
+  const int na = static_cast<int>(i1 - i0), nb = static_cast<int>((t1 - i1) - (t0 - i0));
+  const int tot = na + nb;
+  // stage A[i0, i1) then B[t0 - i0, t1 - i1) (all loads issued before any is used)
+#pragma unroll
+  for (int u = 0; u < KM_ITEMS; ++u) {
+    const int e = threadIdx.x + u * KM_THREADS;
+    if (e < tot) {
+      const bool inA = e < na;
+      const int64_t src = inA ? a0 + i0 + e : a0 + la + (t0 - i0) + (e - na);
+      sk[e] = km_key<SRC>(S, src);
+      si[e] = km_idx<SRC>(S, src, inA ? P.r0[q] : P.r1[q]);
+    }
+  }
+  __syncthreads();
+  const int d0 = threadIdx.x * KM_ITEMS;
+  uint64_t ok[KM_ITEMS];
+  uint32_t oi[KM_ITEMS];
+  if (d0 < tot) {
+    // thread-level merge path inside the chunk
+    int lo = d0 - nb > 0 ? d0 - nb : 0, hi = d0 < na ? d0 : na;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sk[mid] <= sk[na + d0 - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = d0 - lo;
+#pragma unroll
+    for (int j = 0; j < KM_ITEMS; ++j) {
+      const bool takeA = ib >= nb || (ia < na && sk[ia] <= sk[na + ib]);
+      const int src = takeA ? ia : na + ib;
+      if (d0 + j < tot) {
+        ok[j] = sk[src];
+        oi[j] = si[src];
+      }
+      if (takeA) ++ia; else ++ib;
+    }
+  }
+  // back through shared memory, so the stores below are coalesced
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < KM_ITEMS; ++j) {
+    if (d0 + j < tot) {
+      sk[d0 + j] = ok[j];
+      si[d0 + j] = oi[j];
+    }
+  }
+  __syncthreads();
+  const int64_t o0 = a0 + t0;
+#pragma unroll
+  for (int u = 0; u < KM_ITEMS; ++u) {
+    const int e = threadIdx.x + u * KM_THREADS;
+    if (e < tot) {
+      if (FINAL) {
+        final_out[o0 + e] = static_cast<int64_t>(si[e]);
+      } else {
+        kout[o0 + e] = sk[e];
+        iout[o0 + e] = si[e];
+      }
+    }
+  }
+}
+
+// run-local indices outside their runs (one pass over run_idx; the merge
+// itself never dereferences them)
+struct KmOffsets {
+  int64_t off[KM_MAX_RUNS + 1];
+};
+__global__ void km_check_kernel(const int32_t* __restrict__ run_idx, const __grid_constant__ KmOffsets O, int runs,
+                                int64_t n, int32_t* flags) {
+  const int64_t* off = O.off;
+  bool bad = false;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int lo = 0, hi = runs;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (off[mid] <= e) lo = mid; else hi = mid;
+    }
+    const int32_t li = run_idx[e];
+    bad |= li < 0 || li >= off[lo + 1] - off[lo];
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, LVSK_FLAG_BADINDEX);
+}
+
 extern "C" size_t lvsk_normalize_workspace_bytes(int64_t n) {
   Measure m;
   m.take<double>((n + SUM_TILE - 1) / SUM_TILE + 1);
@@ -642,4 +827,102 @@ extern "C" int32_t lvsk_argsort_f64(const double* keys, int64_t n, int32_t desce
   argsort_keys_kernel<<<grid_cap(n), 256, 0, st>>>(keys, n, descending, k64);
   LVSK_CHECK_LAUNCH("argsort keys");
   return radix::sort_pairs<uint64_t, int64_t>(k64, nullptr, n, 64, rb, nullptr, idx_out, st);
+}
+
+extern "C" size_t lvsk_merge_runs_workspace_bytes(int64_t n, int32_t runs) {
+  Measure m;
+  m.take<uint64_t>(n);
+  m.take<uint64_t>(n);
+  m.take<uint32_t>(n);
+  m.take<uint32_t>(n);
+  m.take<int64_t>(static_cast<size_t>(n / KM_CHUNK + (runs < 1 ? 1 : runs) + 1));
+  return m.off;
+}
+
+extern "C" int32_t lvsk_merge_argsort_runs(const double* sorted_keys, const int32_t* run_idx, const int64_t* run_off,
+                                           int32_t runs, int32_t descending, int64_t* idx_out, void* ws,
+                                           size_t ws_bytes, int32_t* flags, void* stream) {
+  LVSK_REQUIRE(runs >= 1 && runs <= KM_MAX_RUNS, LVSK_ERR_CONFIGURATION, "need 1 <= runs <= %d", KM_MAX_RUNS);
+  LVSK_REQUIRE(run_off != nullptr && run_off[0] == 0, LVSK_ERR_CONFIGURATION, "run offsets must start at 0");
+  for (int q = 0; q < runs; ++q)
+    LVSK_REQUIRE(run_off[q + 1] >= run_off[q], LVSK_ERR_DIMENSION, "run offsets must be nondecreasing");
+  const int64_t n = run_off[runs];
+  LVSK_REQUIRE(n < (int64_t{1} << 32), LVSK_ERR_CAPACITY, "at most 2^32 keys");
+  if (n == 0) return LVSK_OK;
+  Carve c(ws, ws_bytes);
+  uint64_t* k0 = c.take<uint64_t>(n);
+  uint64_t* k1 = c.take<uint64_t>(n);
+  uint32_t* i0 = c.take<uint32_t>(n);
+  uint32_t* i1 = c.take<uint32_t>(n);
+  int64_t* split = c.take<int64_t>(static_cast<size_t>(n / KM_CHUNK + runs + 1));
+  LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
+  cudaStream_t st = as_stream(stream);
+  // offsets travel as kernel parameters: no host-to-device copy (a pageable
+  // copy would block the host until the stream drains)
+  KmOffsets O;
+  for (int q = 0; q <= runs; ++q) O.off[q] = run_off[q];
+  km_check_kernel<<<grid_cap(n), 256, 0, st>>>(run_idx, O, runs, n, flags);
+  LVSK_CHECK_LAUNCH("merge check");
+  std::vector<int64_t> off(run_off, run_off + runs + 1);
+  uint64_t *kin = k0, *kout = k1;
+  uint32_t *iin = i0, *iout = i1;
+  bool first = true;
+  for (;;) {
+    const int R = static_cast<int>(off.size()) - 1;
+    const bool last = R <= 2;
+    KmPairs P;
+    std::vector<int64_t> noff;
+    noff.push_back(0);
+    int64_t chunks = 0;
+    P.npairs = 0;
+    for (int q = 0; q < R; q += 2) {
+      const int64_t la = off[q + 1] - off[q], lb = q + 1 < R ? off[q + 2] - off[q + 1] : 0;
+      P.a0[P.npairs] = off[q];
+      P.la[P.npairs] = la;
+      P.lb[P.npairs] = lb;
+      P.r0[P.npairs] = off[q];
+      P.r1[P.npairs] = off[q] + la;
+      P.chunk0[P.npairs] = chunks;
+      chunks += (la + lb + KM_CHUNK - 1) / KM_CHUNK;
+      ++P.npairs;
+      noff.push_back(off[q] + la + lb);
+    }
+    P.chunk0[P.npairs] = chunks;
+    KmSrc S;
+    S.kimg = kin;
+    S.gidx = iin;
+    S.skeys = sorted_keys;
+    S.ridx = run_idx;
+    S.descending = descending;
+    if (chunks > 0) {
+      const unsigned sg = static_cast<unsigned>((chunks * 32 + 255) / 256), mg = static_cast<unsigned>(chunks);
+      if (first) {
+        km_split_kernel<1><<<sg, 256, 0, st>>>(P, chunks, S, split);
+        if (last)
+          km_merge_kernel<1, true><<<mg, KM_THREADS, 0, st>>>(P, S, split, nullptr, nullptr, idx_out);
+        else
+          km_merge_kernel<1, false><<<mg, KM_THREADS, 0, st>>>(P, S, split, kout, iout, nullptr);
+      } else {
+        km_split_kernel<0><<<sg, 256, 0, st>>>(P, chunks, S, split);
+        if (last)
+          km_merge_kernel<0, true><<<mg, KM_THREADS, 0, st>>>(P, S, split, nullptr, nullptr, idx_out);
+        else
+          km_merge_kernel<0, false><<<mg, KM_THREADS, 0, st>>>(P, S, split, kout, iout, nullptr);
+      }
+      LVSK_CHECK_LAUNCH("merge round");
+    }
+    if (last) break;
+    off.swap(noff);
+    if (!first) {
+      std::swap(kin, kout);
+      std::swap(iin, iout);
+    } else {  // round 1 wrote (k1, i1): read them next, write (k0, i0)
+      kin = k1;
+      iin = i1;
+      kout = k0;
+      iout = i0;
+    }
+    first = false;
+  }
+  return LVSK_OK;
 }

@@ -102,6 +102,31 @@ def argsort_device(keys: torch.Tensor, descending: bool, out: torch.Tensor | Non
     return out
 
 
+def merge_argsort_runs(sorted_keys: torch.Tensor, run_idx: torch.Tensor, counts, descending: bool,
+                       out: torch.Tensor | None = None, ws=None, flags=None) -> torch.Tensor:
+    """KM: the global stable argsort of R runs of float64 keys in rank order
+    (run q has ``counts[q]`` keys) from each run's stable argsort ``run_idx``
+    (int32, local to the run) and the run's keys in that order
+    (``sorted_keys``), both concatenated run after run — equal to
+    :func:`argsort_device` on the concatenated keys, in ceil(log2 R)
+    merge-path rounds instead of a full sort (the multi-rank "dec" order:
+    every rank sorts its own scores, rank 0 merges)."""
+    import ctypes
+
+    n = sorted_keys.numel()
+    R = len(counts)
+    off = (ctypes.c_int64 * (R + 1))(*([0] + list(np.cumsum(np.asarray(counts, dtype=np.int64)).tolist())))
+    out = torch.empty(n, dtype=torch.int64, device=sorted_keys.device) if out is None else out
+    ws = ws if ws is not None else N.workspace(N.lib().lvsk_merge_runs_workspace_bytes(n, R))
+    fl = flags if flags is not None else N.Flags()
+    N.check(N.lib().lvsk_merge_argsort_runs(sorted_keys.data_ptr(), run_idx.data_ptr(), off, R, 1 if descending else 0,
+                                            out.data_ptr(), ws.data_ptr(), ws.numel(), fl.p, N.stream_ptr()),
+            "merge argsort runs")
+    if flags is None and fl.read() & N.FLAG_BADINDEX:  # (callers passing flags check them themselves)
+        raise ConfigurationError("a run index lies outside its run")
+    return out
+
+
 def _device_sum(p: torch.Tensor) -> float:
     out = torch.empty(1, dtype=torch.float64, device=p.device)
     ws = N.workspace(N.lib().lvsk_normalize_workspace_bytes(p.numel()))

@@ -1,6 +1,6 @@
 """bench.py's N > 1 step (the measured multi-GPU path: sliced all-to-all
-merge in rank order, redundant fold, rank-local scores, global "dec" order
-gathered to rank 0 and sorted on a side stream inside the timed region) run
+merge in rank order, redundant fold, rank-local scores and sorts, global "dec"
+order merged from the sorted runs on rank 0 inside the timed region) run
 with 2-3 ranks on one GPU (LVSK_BENCH_SHARE_GPU=1: gloo, host-staged
 collectives, never a measurement) and checked by bench.py --verify against
 the CPU oracle: merged sketch bit-exact (hashed) / within 1e-4 (SRHT,

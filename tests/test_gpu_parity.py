@@ -1105,3 +1105,43 @@ def test_jl_fold_needs_k_at_least_d():
     spec = P.SketchSpec("countsketch", eps=0.5, d=d, seed=1, rows_override=k)
     with pytest.raises(errors.DimensionMismatchError):
         P.leverage_sketched_trunc(X, spec, 1e-6, jl_dim=32)
+
+
+@pytest.mark.parametrize("counts", [[1000], [700, 300], [5000, 0, 4096, 1, 2047], [20000] * 8, [3] * 17])
+@pytest.mark.parametrize("descending", [True, False])
+def test_merge_argsort_runs_equals_full_argsort(counts, descending):
+    """KM (the multi-rank order): merging the per-rank stable argsorts gives
+    the stable argsort of the concatenated keys, bit for bit — with ties across
+    runs, NaN, +-0 and inf (numpy's stable order, order.py:89-90)."""
+    from paper_1812_07903_b200.order import argsort_device, merge_argsort_runs
+
+    rng = np.random.default_rng(sum(counts) + len(counts))
+    n = sum(counts)
+    k = np.round(rng.random(n) * 50) / 50  # many ties, within and across runs
+    special = rng.choice(n, size=min(n, 9), replace=False)
+    k[special[:3]] = np.nan
+    k[special[3:5]] = -0.0
+    k[special[5:7]] = 0.0
+    k[special[7:]] = np.inf
+    keys = dev(k)
+    parts, skeys, o = [], [], 0
+    for c in counts:
+        run = keys[o:o + c].contiguous()
+        loc = argsort_device(run, descending) if c else torch.zeros(0, dtype=torch.int64, device="cuda")
+        parts.append(loc.to(torch.int32))
+        skeys.append(run[loc])
+        o += c
+    got = merge_argsort_runs(torch.cat(skeys), torch.cat(parts), counts, descending)
+    want = argsort_device(keys, descending)
+    assert torch.equal(got, want)
+    ref = np.argsort(-k if descending else k, kind="stable")
+    assert np.array_equal(got.cpu().numpy(), ref)
+
+
+def test_merge_argsort_runs_flags_bad_local_index():
+    from paper_1812_07903_b200.order import merge_argsort_runs
+
+    keys = dev(np.arange(10, dtype=np.float64)[::-1].copy())
+    idx = torch.tensor([0, 1, 2, 3, 9, 0, 1, 2, 3, 4], dtype=torch.int32, device="cuda")  # 9 is outside run 0
+    with pytest.raises(errors.ConfigurationError):
+        merge_argsort_runs(keys, idx, [5, 5], True)

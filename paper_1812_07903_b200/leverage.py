@@ -576,16 +576,24 @@ def scores_device(X: torch.Tensor, M: torch.Tensor, out: torch.Tensor | None = N
 
 
 def leverage_exact(a) -> LeverageResult:
-    """Exact scores from the thin-SVD left factor (reference leverage.py:44-53;
-    a test oracle, computed in float64 on the device)."""
+    """Exact scores: squared row norms of the thin-SVD left factor restricted
+    to the components above the machine-relative rank floor (reference
+    leverage.py:44-53).  On the device without forming U (n x d): the
+    singular values / right vectors of X come from the small triangular
+    factor of a Householder QR (X = Q R, so sigma(R) = sigma(X), V(R) =
+    V(X)), and U_r = X V_r / sigma_r, so the scores are the leverage pass
+    ||x_i V_r / sigma_r||^2 (float64 rows: the SIMT kernel).  QR keeps
+    sigma to float64 relative accuracy where a Gram + eigh route would
+    square the condition number at the truncation floor."""
     X = device_matrix(a).to(torch.float64)
-    u, s, _ = torch.linalg.svd(X, full_matrices=False, driver="gesvd")
+    R = torch.linalg.qr(X, mode="r")[1]
+    _, s, vt = torch.linalg.svd(R, full_matrices=False)
     s_host = s.cpu().numpy()
     if s_host[0] <= 0:
         raise DegenerateInputError("leverage scores of an all-zero matrix are undefined")
     r = int(np.count_nonzero(s_host > MACHINE_RANK_TOL * s_host[0]))
-    ur = u[:, :r]
-    scores = (ur * ur).sum(dim=1)
+    M = (vt[:r].T / s[:r]).contiguous()
+    scores = scores_device(X.contiguous(), M)
     return LeverageResult(scores=N.host_numpy(scores), method="exact", effective_rank=r)
 
 

@@ -1145,3 +1145,18 @@ def test_merge_argsort_runs_flags_bad_local_index():
     idx = torch.tensor([0, 1, 2, 3, 9, 0, 1, 2, 3, 4], dtype=torch.int32, device="cuda")  # 9 is outside run 0
     with pytest.raises(errors.ConfigurationError):
         merge_argsort_runs(keys, idx, [5, 5], True)
+
+
+@pytest.mark.parametrize("n,d,rank", [(3000, 40, 40), (2500, 64, 17), (50, 80, 50)])
+def test_leverage_exact_matches_oracle_svd(n, d, rank):
+    """leverage_exact (QR -> SVD of R -> leverage pass, no n x d U) against
+    the oracle's thin-SVD scores (reference leverage.py:44-53), incl. a
+    rank-deficient matrix and n < d."""
+    rng = np.random.default_rng(n + d)
+    x = (rng.standard_normal((n, rank)) @ rng.standard_normal((rank, d))).astype(np.float64)
+    res = P.leverage_exact(x)
+    u, s, _ = np.linalg.svd(x, full_matrices=False)
+    r = int(np.count_nonzero(s > 1e-12 * s[0]))
+    ref = np.einsum("ij,ij->i", u[:, :r], u[:, :r])
+    assert res.effective_rank == r
+    assert np.allclose(res.scores, ref, rtol=1e-9, atol=1e-12)

@@ -234,6 +234,14 @@ LVSK_API int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const d
  * Replaces the Gram DGEMM of the fold (svd.py:30-37 / leverage.py:75-85
  * through factor.cu).  Stream-capturable. */
 LVSK_API size_t lvsk_gram_workspace_bytes(int64_t k, int64_t d);
+/* KD: the same block upper triangle (64 x 64 tiles, bi <= bj) of
+ * G = SX^T SX on the float64 tensor cores (DMMA), k split into row slices
+ * summed in a fixed order (deterministic); the fold's Gram for d < 2048.
+ * ws: lvsk_syrk_workspace_bytes (0 bytes when one slice suffices).
+ * Stream-capturable. */
+LVSK_API size_t lvsk_syrk_workspace_bytes(int64_t k, int64_t d);
+LVSK_API int32_t lvsk_syrk_f64(const double* SX, int64_t k, int64_t d, int64_t ldsx, double* G, int64_t ldg,
+                               void* ws, size_t ws_bytes, void* stream);
 LVSK_API int32_t lvsk_gram_f64(const double* SX, int64_t k, int64_t d, int64_t ldsx, double* G, int64_t ldg,
                                void* ws, size_t ws_bytes, int32_t* flags, void* stream);
 

@@ -73,6 +73,8 @@ _SIGS = {
     "lvsk_split_fold": (_I32, [_P, _I64, _I64, _I32, _I64, _P, _P, _P, _P]),
     "lvsk_chol_fold_workspace_bytes": (_SZ, [_I64, _I64]),
     "lvsk_gram_workspace_bytes": (_SZ, [_I64, _I64]),
+    "lvsk_syrk_workspace_bytes": (_SZ, [_I64, _I64]),
+    "lvsk_syrk_f64": (_I32, [_P, _I64, _I64, _I64, _P, _I64, _P, _SZ, _P]),
     "lvsk_gram_f64": (_I32, [_P, _I64, _I64, _I64, _P, _I64, _P, _SZ, _P, _P]),
     "lvsk_gaussian_tables": (_I32, [_P, _I64]),
     "lvsk_chol_fold": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _D, _P, _P, _SZ, _P]),

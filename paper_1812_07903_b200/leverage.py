@@ -122,44 +122,38 @@ def use_kg(k: int, d: int) -> bool:
 
 
 def gram_workspace(k: int, d: int, device) -> torch.Tensor:
-    return torch.empty(int(N.lib().lvsk_gram_workspace_bytes(k, d)), dtype=torch.uint8, device=device)
+    L = N.lib()
+    nbytes = L.lvsk_gram_workspace_bytes(k, d) if use_kg(k, d) else L.lvsk_syrk_workspace_bytes(k, d)
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
 def gram_upper(sx: torch.Tensor, ws: torch.Tensor | None = None, flags: torch.Tensor | None = None) -> torch.Tensor:
     """G = SX^T SX with (at least) the block upper triangle computed — KF
     reads the upper triangle.  d >= GRAM_KG_MIN_D: KG on the int8 tensor
     cores (float64-GEMM error class, csrc/gram_i8.cu), 256 x 256 upper
-    blocks; below: cuBLAS DGEMM."""
+    blocks; below: KD on the float64 tensor cores (csrc/gram_f64.cu), 64 x 64
+    upper blocks (half the flops of the full cuBLAS DGEMM it replaces)."""
     k, d = sx.shape
+    sx = sx.contiguous()
+    if ws is None:  # eager calls: one scratch buffer per (shape, device, stream)
+        key = (k, d, sx.device, torch.cuda.current_stream(sx.device).cuda_stream)
+        ws = _GRAM_WS.get(key)
+        if ws is None:
+            ws = _GRAM_WS[key] = gram_workspace(k, d, sx.device)
+    G = torch.empty((d, d), dtype=torch.float64, device=sx.device)
     if use_kg(k, d):
-        sx = sx.contiguous()
-        if ws is None:  # eager calls: one scratch buffer per (shape, device, stream)
-            key = (k, d, sx.device, torch.cuda.current_stream(sx.device).cuda_stream)
-            ws = _GRAM_WS.get(key)
-            if ws is None:
-                ws = _GRAM_WS[key] = gram_workspace(k, d, sx.device)
         if flags is None:
             flags = torch.zeros(1, dtype=torch.int32, device=sx.device)  # SX was checked by the sketch
-        G = torch.empty((d, d), dtype=torch.float64, device=sx.device)
         N.check(N.lib().lvsk_gram_f64(sx.data_ptr(), k, d, sx.stride(0), G.data_ptr(), d, ws.data_ptr(), ws.numel(),
                                       flags.data_ptr(), N.stream_ptr()), "gram")
         return G
-    if d < 1024:
-        return sx.T @ sx
-    G = torch.empty((d, d), dtype=sx.dtype, device=sx.device)
-    nb = 4
-    edges = [d * i // nb for i in range(nb + 1)]
-    for i in range(nb):
-        a = sx[:, edges[i] : edges[i + 1]]
-        G[edges[i] : edges[i + 1], edges[i] :] = a.T @ sx[:, edges[i] :]
+    N.check(N.lib().lvsk_syrk_f64(sx.data_ptr(), k, d, sx.stride(0), G.data_ptr(), d, ws.data_ptr(), ws.numel(),
+                                  N.stream_ptr()), "gram (syrk)")
     return G
 
 
 def gram_full(sx: torch.Tensor) -> torch.Tensor:
     """Symmetric G = SX^T SX (the eigen routes read all of it)."""
-    k, d = sx.shape
-    if not use_kg(k, d):
-        return sx.T @ sx
     G = gram_upper(sx)
     return torch.triu(G) + torch.triu(G, 1).T
 
@@ -524,7 +518,7 @@ class FoldGraph:
         # device count of replays whose certificate failed (evaluated by the KF kernel)
         self.cert_fail = torch.zeros(1, dtype=torch.int32, device=sx.device)
         self.ws = fold_workspace(d, pi.shape[1], sx.device)  # owned by the graph: replays never share scratch
-        self.gws = gram_workspace(k, d, sx.device) if use_kg(k, d) else None
+        self.gws = gram_workspace(k, d, sx.device)
         self.gflags = torch.zeros(1, dtype=torch.int32, device=sx.device)
         self.graph = None
         # warm up cuBLAS handles outside capture

@@ -1160,3 +1160,27 @@ def test_leverage_exact_matches_oracle_svd(n, d, rank):
     ref = np.einsum("ij,ij->i", u[:, :r], u[:, :r])
     assert res.effective_rank == r
     assert np.allclose(res.scores, ref, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("k,d", [(4096, 512), (1000, 136), (77, 200), (2048, 1024), (300, 64), (5, 3)])
+def test_kd_syrk_upper_triangle_vs_float64(k, d):
+    """KD (csrc/gram_f64.cu): the 64 x 64 block upper triangle of SX^T SX on
+    DMMA against torch float64 — ragged k and d, a strided SX — and
+    deterministic (split-k slices summed in a fixed order)."""
+    from paper_1812_07903_b200.leverage import gram_workspace
+
+    g = torch.Generator(device="cuda").manual_seed(k + d)
+    big = torch.randn(k, d + 5, dtype=torch.float64, device="cuda", generator=g)
+    sx = big[:, :d]  # leading dimension d + 5
+    L = N.lib()
+    ws = gram_workspace(k, d, "cuda")
+    G = torch.zeros((d, d), dtype=torch.float64, device="cuda")
+    G2 = torch.zeros_like(G)
+    for out in (G, G2):
+        N.check(L.lvsk_syrk_f64(sx.data_ptr(), k, d, sx.stride(0), out.data_ptr(), d, ws.data_ptr(), ws.numel(),
+                                N.stream_ptr()))
+    ref = sx.T @ sx
+    up = torch.triu(torch.ones(d, d, dtype=torch.bool, device="cuda"))
+    scale = float(ref.abs().max())
+    assert float((G - ref)[up].abs().max()) <= 1e-12 * scale * max(1.0, k / 1000)
+    assert torch.equal(G, G2)

@@ -686,7 +686,7 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   a.dp = P.dp;
   a.rp = P.rp;
   // large d: three-tile CTAs, two per SM (the queue's tile updates dominate)
-  const bool wide = P.nb > 16 && getenv("LVSK_KF_ONE_CTA") == nullptr;
+  const bool wide = P.nb > 16;
   const void* fn = wide ? reinterpret_cast<const void*>(chol_fold_kernel<3>) : reinterpret_cast<const void*>(chol_fold_kernel<4>);
   const int smem = (wide ? 3 : 4) * FTILE_SMEM + (5 * FT + 8) * 8;
   const int32_t arc = ensure_smem_attr(fn, smem, "chol_fold smem attribute");

@@ -1,5 +1,5 @@
 // K4-TC — Gaussian sketch SX = Z X / sqrt(k) on the tensor cores for bf16 X
-// (BASELINE config 5), Z generated on the fly (philox.cuh) and never stored
+// (BASELINE config 5), Z generated on the fly (gauss_gen.cuh) and never stored
 // in global memory.  Extension: the reference rejects "gaussian"
 // (pkg/src/levsketch/sketch.py:38-41, 74-75).
 //

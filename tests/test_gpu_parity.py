@@ -1184,3 +1184,37 @@ def test_kd_syrk_upper_triangle_vs_float64(k, d):
     scale = float(ref.abs().max())
     assert float((G - ref)[up].abs().max()) <= 1e-12 * scale * max(1.0, k / 1000)
     assert torch.equal(G, G2)
+
+
+@pytest.mark.parametrize("env", ["LVSK_ARGSORT_CLASSIC", "LVSK_K1_REGS", "LVSK_K5_V1", "LVSK_SRHT_CHUNK_MB"])
+def test_kernel_variant_switches_vs_oracle(env, monkeypatch):
+    """The non-default kernel variants the environment selects (the classic
+    three-kernel radix argsort that n > 8M keys take, the register-path K1
+    gather, the v1 tcgen05 leverage kernel, a small two-pass SRHT chunk) give
+    the oracle's results like the default kernels."""
+    rng = np.random.default_rng(hash(env) % 1000)
+    monkeypatch.setenv(env, "1")
+    if env == "LVSK_ARGSORT_CLASSIC":
+        p = rng.random(50_000)
+        p[rng.integers(0, 50_000, 5000)] = p[7]
+        got = P.make_plan(p / p.sum(), P.OrderingPolicy("dec")).indices
+        assert np.array_equal(got, np.argsort(-(p / p.sum()), kind="stable"))
+    elif env == "LVSK_K1_REGS":
+        x = rng.standard_normal((5000, 96)).astype(np.float32)
+        spec = P.SketchSpec("osnap", eps=0.5, d=96, seed=3, rows_override=512, osnap_s=3)
+        hi, lo = O.hashed_sketch(x, "osnap", 512, 3, 3)
+        assert np.array_equal(P.apply_sketch(dev(x), spec).data, hi + lo)
+    elif env == "LVSK_K5_V1":
+        n, d, r = 3000, 256, 64
+        g = torch.Generator(device="cpu").manual_seed(5)
+        X = (torch.randn(n, d, generator=g, dtype=torch.float64)).to(torch.float32).cuda()
+        M = (torch.randn(d, r, generator=g, dtype=torch.float64) / math.sqrt(d)).cuda()
+        ref = ((X.double() @ M) ** 2).sum(1)
+        got = P.leverage.scores_device(X, M)
+        assert float(((got - ref).abs() / ref).max()) < 1e-5
+    else:  # the two-pass SRHT (float64 rows) with a 1 MB chunk: several chunks
+        x = rng.standard_normal((20_000, 16))
+        spec = P.SketchSpec("srht", eps=0.5, d=16, seed=2, rows_override=256)
+        ref = O.srht_sketch(x, 256, 2)
+        got = P.apply_sketch(x, spec).data
+        assert np.allclose(got, ref, rtol=1e-10, atol=1e-10 * np.abs(ref).max())

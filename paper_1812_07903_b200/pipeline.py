@@ -266,8 +266,13 @@ class LeveragePipeline:
             sk = group + (1 if csr else 0) + 1 + (1 if self.keep_state else 0)
         lev = 1
         k, d = self.sx.shape
-        # KF (chol_fold_kernel) + the K5 operand split (split_fold_kernel)
-        fold = 2 if (self.pi is not None and self.rank is None and k >= d) else 0
+        # the Gram (KG: colmax, colexp, slice, gram_i8; KD: syrk [+ its slice reduce]),
+        # KF (chol_fold_kernel) and the K5 operand split (split_fold_kernel)
+        fold = 0
+        if self.pi is not None and self.rank is None and k >= d:
+            from .leverage import use_kg
+            gram = 4 if use_kg(k, d) else (2 if N.lib().lvsk_syrk_workspace_bytes(k, d) > 0 else 1)
+            fold = gram + 2
         # normalise (2-stage sum + divide), then K7: one cooperative kernel up to 8M keys
         coop_sort = self.n <= (8 << 20) and not os.environ.get("LVSK_ARGSORT_CLASSIC")
         order_ = (3 + (1 if coop_sort else 1 + radix(self.n, 64))) if self.order else 0

@@ -1,4 +1,2 @@
-cd $GRAFT_REPO_ROOT
-export PYTHONPATH=$GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "csr" 2>&1 | tail -3
-timeout 600 python tools/k6_time.py 2>&1 | tail -4
+cd $GRAFT_REPO_ROOT; export PYTHONPATH=$GRAFT_REPO_ROOT
+timeout 600 python bench.py --config c4 --steps 10 --warmup 3 --no-e2e --no-cpu 2>&1 | tail -1 | grep -o '"ms_per_step": [0-9.]*\|"leverage": {"ms": [0-9.]*'

@@ -265,7 +265,8 @@ def _cholqr2(Y: torch.Tensor, rounds: int = 2) -> torch.Tensor:
     return Y
 
 
-def _topk_gram(G: torch.Tensor, want: int, rounds: int = 2, iters: int = 6, tol: float = 1e-12):
+def _topk_gram(G: torch.Tensor, want: int, rounds: int = 2, iters: int = 6, tol: float = 1e-12,
+               schedule: list[int] | None = None):
     """Top `want` eigenpairs (descending) of the SPD Gram G by block subspace
     iteration: block want + max(16, want / 4) rounded up to 8 (at least 136
     above 96: the eigensolver is faster there), seeded start,
@@ -286,11 +287,13 @@ def _topk_gram(G: torch.Tensor, want: int, rounds: int = 2, iters: int = 6, tol:
     Q = torch.randn(d, b, dtype=G.dtype, device=G.device, generator=gen)
     for _ in range(rounds):
         for it in range(iters):
-            # full CholQR2 on the first steps (the random start is badly
-            # conditioned) and the last (Rayleigh-Ritz needs an orthonormal
-            # basis); one Cholesky QR in between (each small potrf + trsm is
-            # ~0.1 ms of cuSOLVER latency)
-            Q = _cholqr2(G @ Q, 2 if it < 2 or it == iters - 1 else 1)
+            # one Cholesky QR per power step (its orthogonality error
+            # ~eps * cond^2 is re-conditioned by the next step), CholQR2 on the
+            # last (Rayleigh-Ritz needs an orthonormal basis); the residual
+            # test below guards the result.  C5: 3.2 -> 2.3 ms against CholQR2
+            # on the first two steps as well (tools/c5_rounds_probe.py)
+            cq = schedule[it] if schedule is not None else (2 if it == iters - 1 else 1)
+            Q = _cholqr2(G @ Q, cq)
         Y = G @ Q
         Bm = Q.T @ Y
         theta, W = torch.linalg.eigh(0.5 * (Bm + Bm.T))

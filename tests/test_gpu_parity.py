@@ -1107,7 +1107,8 @@ def test_jl_fold_needs_k_at_least_d():
         P.leverage_sketched_trunc(X, spec, 1e-6, jl_dim=32)
 
 
-@pytest.mark.parametrize("counts", [[1000], [700, 300], [5000, 0, 4096, 1, 2047], [20000] * 8, [3] * 17])
+@pytest.mark.parametrize("counts", [[1000], [700, 300], [5000, 0, 4096, 1, 2047], [20000] * 8, [3] * 17,
+                                    [5, 0, 9, 1] * 128])
 @pytest.mark.parametrize("descending", [True, False])
 def test_merge_argsort_runs_equals_full_argsort(counts, descending):
     """KM (the multi-rank order): merging the per-rank stable argsorts gives

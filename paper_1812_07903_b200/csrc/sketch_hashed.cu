@@ -484,10 +484,21 @@ __device__ __forceinline__ void gc_barrier(unsigned int* count, unsigned int& nb
   __syncthreads();
 }
 
-__device__ __forceinline__ void gc_item(int64_t t, int64_t n, uint64_t row0, const KeygenBlocks& P, uint32_t& bk,
+// item t = (block jj, row r) with t = jj * n + r; callers walk t in steps of
+// 32 and carry (jj, r) along instead of a 64-bit division per item
+__device__ __forceinline__ void gc_split(int64_t t, int64_t n, int& jj, int64_t& r) {
+  jj = static_cast<int>(t / n);
+  r = t - static_cast<int64_t>(jj) * n;
+}
+__device__ __forceinline__ void gc_step(int64_t n, int& jj, int64_t& r) {
+  r += 32;
+  while (r >= n) {  // (n >= 1; at most one wrap per step unless n < 32)
+    r -= n;
+    ++jj;
+  }
+}
+__device__ __forceinline__ void gc_item(int jj, int64_t r, uint64_t row0, const KeygenBlocks& P, uint32_t& bk,
                                         uint32_t& val) {
-  const int jj = static_cast<int>(t / n);
-  const int64_t r = t - static_cast<int64_t>(jj) * n;
   const uint64_t g = row0 + static_cast<uint64_t>(r);
   bk = P.offset[jj] + bucket_hash(g, P.a[jj], P.b[jj], P.size[jj]);
   val = (static_cast<uint32_t>(r) << 1) | (sign_negative(g, P.key[jj]) ? 1u : 0u);
@@ -522,9 +533,12 @@ __global__ void __launch_bounds__(GC_THREADS, 1) group_coop_kernel(int64_t n, in
   for (int64_t i = threadIdx.x; i < GC_WARPS * k; i += GC_THREADS) hw[i] = 0u;
   __syncthreads();
   // 1. hash, per-warp counts
-  for (int64_t t = w0 + lane; t < w1; t += 32) {
+  int ij;
+  int64_t ir;
+  gc_split(w0 + lane, n, ij, ir);
+  for (int64_t t = w0 + lane; t < w1; t += 32, gc_step(n, ij, ir)) {
     uint32_t bk, val;
-    gc_item(t, n, row0, P, bk, val);
+    gc_item(ij, ir, row0, P, bk, val);
     if (cached) {
       items[2 * (t - c0)] = bk;
       items[2 * (t - c0) + 1] = val;
@@ -631,7 +645,8 @@ __global__ void __launch_bounds__(GC_THREADS, 1) group_coop_kernel(int64_t n, in
   // 4. stable scatter of the values, warp by warp
   const uint32_t lt = lanemask_lt();
   uint32_t* my = hw + warp * k;
-  for (int64_t t0 = w0; t0 < w1; t0 += 32) {
+  gc_split(w0 + lane, n, ij, ir);
+  for (int64_t t0 = w0; t0 < w1; t0 += 32, gc_step(n, ij, ir)) {
     const int64_t t = t0 + lane;
     const bool valid = t < w1;
     uint32_t bk = 0xFFFFFFFFu, val = 0u;
@@ -640,7 +655,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) group_coop_kernel(int64_t n, in
         bk = items[2 * (t - c0)];
         val = items[2 * (t - c0) + 1];
       } else {
-        gc_item(t, n, row0, P, bk, val);
+        gc_item(ij, ir, row0, P, bk, val);
       }
     }
     const uint32_t peers = __match_any_sync(0xFFFFFFFFu, bk);

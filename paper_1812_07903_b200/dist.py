@@ -233,6 +233,10 @@ def gather_row_slices(sl: torch.Tensor, k: int, world: int, group=None) -> torch
     bounds = partition_rows(k, world)
     rows = max(b - a for a, b in bounds)
     d = sl.shape[1]
+    if k % world == 0 and sl.is_contiguous():  # equal slices: gathered in place, rank order = row order
+        out = torch.empty((k, d), dtype=sl.dtype, device=sl.device)
+        tdist.all_gather_into_tensor(out, sl, group=group)
+        return out
     buf = torch.zeros((rows, d), dtype=sl.dtype, device=sl.device)
     buf[: sl.shape[0]] = sl
     outs = [torch.empty_like(buf) for _ in range(world)]

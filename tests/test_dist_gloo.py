@@ -140,13 +140,15 @@ def _slice_worker(rank, world, port, x, k, seed, out_q):
         dist.destroy_process_group()
 
 
-def test_sliced_merge_layout_equals_serial_three_ranks():
+@pytest.mark.parametrize("k", [101, 102])
+def test_sliced_merge_layout_equals_serial_three_ranks(k):
     """The reduce-scatter layout bench.py's multi-GPU path uses
-    (dist.exchange_row_slices / gather_row_slices, uneven row slices over 3
-    ranks): merging each slice in rank order and gathering the folded slices
-    gives the serial sketch bit for bit."""
+    (dist.exchange_row_slices / gather_row_slices over 3 ranks — uneven row
+    slices, and equal ones gathered in place): merging each slice in rank
+    order and gathering the folded slices gives the serial sketch bit for
+    bit."""
     rng = np.random.default_rng(9)
-    n, d, k, seed = 901, 7, 101, 3
+    n, d, seed = 901, 7, 3
     x = rng.standard_normal((n, d))
     hp = O.HashParams("countsketch", seed, k, 1)
     ref_hi = np.zeros((k, d))

@@ -73,6 +73,18 @@ typedef struct {
 LVSK_API const char* lvsk_last_error(void);
 LVSK_API int32_t lvsk_abi_version(void);
 
+/* Scheduling hint (no reference counterpart: the reference runs one pass at a
+ * time on the CPU).  passes = how many independent pipeline passes the caller
+ * keeps in flight on separate streams (paper_1812_07903_b200.BatchRunner).  At
+ * >= 2 the latency-bound cooperative kernels leave SMs to the other stream's
+ * HBM-bound passes: KF (lvsk_chol_fold, d <= 1024) runs at most 24 CTAs and K7
+ * (lvsk_argsort_f64) gives each CTA at least 8192 keys.  Results are
+ * unchanged (both kernels are deterministic for any CTA count).  Process-wide;
+ * takes effect at the next launch (a captured CUDA graph keeps the value it
+ * was captured with).  Default 1. */
+LVSK_API int32_t lvsk_set_inflight(int32_t passes);
+LVSK_API int32_t lvsk_get_inflight(void);
+
 /* ---- K1: CountSketch / OSNAP on dense rows ------------------------------
  * Replaces SketchState._update_hashed + _scatter_add + _two_sum
  * (reference sketch.py:260-266, 173-191, 166-170) as driven by consume_rows

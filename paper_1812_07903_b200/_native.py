@@ -44,6 +44,8 @@ _P, _I64, _I32, _U64, _D, _SZ = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.
 _SIGS = {
     "lvsk_last_error": (C.c_char_p, []),
     "lvsk_abi_version": (_I32, []),
+    "lvsk_set_inflight": (_I32, [_I32]),
+    "lvsk_get_inflight": (_I32, []),
     "lvsk_hashed_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
     "lvsk_hashed_sketch": (
         _I32,

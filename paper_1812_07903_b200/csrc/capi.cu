@@ -1,5 +1,6 @@
 // C-ABI plumbing shared by every entry point: thread-local error message and
 // CUDA status mapping (include/levsketch_b200.h).
+#include <atomic>
 #include <cstdarg>
 #include <map>
 #include <mutex>
@@ -22,6 +23,9 @@ int32_t cuda_status(cudaError_t e, const char* what) {
   set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
   return LVSK_ERR_CUDA;
 }
+
+static std::atomic<int> g_inflight{1};
+int inflight_passes() { return g_inflight.load(std::memory_order_relaxed); }
 
 static int current_device() {
   int dev = 0;
@@ -76,5 +80,16 @@ int resident_ctas(const void* fn, int threads, int smem_bytes) {
 }  // namespace lvsk
 
 extern "C" const char* lvsk_last_error(void) { return lvsk::g_last_error; }
+
+extern "C" int32_t lvsk_set_inflight(int32_t passes) {
+  if (passes < 1 || passes > 64) {
+    lvsk::set_error("lvsk_set_inflight: passes must be in [1, 64], got %d", passes);
+    return LVSK_ERR_CONFIGURATION;
+  }
+  lvsk::g_inflight.store(passes, std::memory_order_relaxed);
+  return LVSK_OK;
+}
+
+extern "C" int32_t lvsk_get_inflight(void) { return lvsk::inflight_passes(); }
 
 extern "C" int32_t lvsk_abi_version(void) { return 1; }

@@ -144,5 +144,8 @@ int32_t ensure_smem_attr(const void* fn, int smem_bytes, const char* what);
 // co-resident CTAs per SM of `fn` at (threads, smem) on the current device
 // (after ensure_smem_attr); 0 when the attribute or the query failed
 int resident_ctas(const void* fn, int threads, int smem_bytes);
+// passes the caller keeps in flight on separate streams (lvsk_set_inflight);
+// >= 2 makes the latency-bound cooperative kernels (KF, K7) take fewer SMs
+int inflight_passes();
 
 }  // namespace lvsk

@@ -50,6 +50,7 @@ constexpr int FT = 64;          // tile edge
 constexpr int FLD = FT + 4;     // smem row stride, = 4 mod 16: DMMA fragment loads are conflict-free
 constexpr int FTHREADS = 256;
 constexpr int FTILE_SMEM = FT * FLD * 8;
+constexpr int KF_INFLIGHT_GRID = 24;
 
 struct FactorArgs {
   const double* G;
@@ -696,7 +697,11 @@ extern "C" int32_t lvsk_chol_fold(const double* G, int64_t d, int64_t ldg, const
   if (grid_cap < 2) return cuda_status(cudaErrorInvalidConfiguration, "chol_fold needs two co-resident CTAs");
   // CTA 0 runs the chain; more queue CTAs than tasks only add polling
   const int ntask = kf_queue_tasks(P.nb, P.rt);
-  const int grid = 1 + (ntask < grid_cap - 1 ? ntask : grid_cap - 1);
+  int grid = 1 + (ntask < grid_cap - 1 ? ntask : grid_cap - 1);
+  // passes in flight on other streams (lvsk_set_inflight): at d <= 1024 the
+  // chain, not the queue, bounds KF, and 24 CTAs keep its pace (C2: +14 us
+  // alone) while the other SMs run the concurrent pass's HBM-bound kernels
+  if (inflight_passes() >= 2 && !wide && grid > KF_INFLIGHT_GRID) grid = KF_INFLIGHT_GRID;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(FTHREADS);

@@ -75,6 +75,7 @@ __device__ __forceinline__ void load_gaussian_table(uint16_t* dst, const uint16_
 struct GaussTcPlan {
   int ns, ktiles, dslabs;
   int64_t splits, rows_per_split;
+  int64_t period;  // input row r is global row row0 + r mod period (stacked planes; = n otherwise)
 };
 GaussTcPlan plan_gauss_tc(int64_t n, int64_t d, int64_t k);
 bool gaussian_tc_ok(const void* X, int64_t n, int64_t d, int64_t ldx, int64_t k);

@@ -182,6 +182,52 @@ __global__ void gaussian_reduce_kernel(const A* __restrict__ partial, int64_t sp
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
 }
 
+// fp32 partials, count % 4 == 0: four consecutive entries per thread, float4
+// loads eight splits deep (same per-entry summation order as above)
+__global__ void gaussian_reduce4_kernel(const float4* __restrict__ partial, int64_t splits, int64_t count4,
+                                        double scale, double* SX, int accumulate, int32_t* flags) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t p = 0;
+    for (; p + 8 <= splits; p += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(partial + (p + u) * count4 + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s0 += v[u].x, s1 += v[u].y, s2 += v[u].z, s3 += v[u].w;
+    }
+    for (; p < splits; ++p) {
+      const float4 v = __ldg(partial + p * count4 + i);
+      s0 += v.x, s1 += v.y, s2 += v.z, s3 += v.w;
+    }
+    bad |= !(isfinite(s0) && isfinite(s1) && isfinite(s2) && isfinite(s3));
+    double2* o = reinterpret_cast<double2*>(SX + 4 * i);
+    double2 a = make_double2(s0 * scale, s1 * scale), b = make_double2(s2 * scale, s3 * scale);
+    if (accumulate) {
+      const double2 oa = o[0], ob = o[1];
+      a.x += oa.x, a.y += oa.y, b.x += ob.x, b.y += ob.y;
+    }
+    o[0] = a;
+    o[1] = b;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, LVSK_FLAG_NONFINITE);
+}
+
+static void reduce_f32(const float* part, int64_t splits, int64_t count, double scale, double* SX, int accumulate,
+                       int32_t* flags, cudaStream_t st) {
+  if (count % 4 == 0 && reinterpret_cast<uintptr_t>(part) % 16 == 0 && reinterpret_cast<uintptr_t>(SX) % 16 == 0) {
+    const int64_t c4 = count / 4;
+    const int g = static_cast<int>((c4 + 255) / 256 < num_sms() * 8 ? (c4 + 255) / 256 : num_sms() * 8);
+    gaussian_reduce4_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const float4*>(part), splits, c4, scale, SX,
+                                               accumulate, flags);
+  } else {
+    const int g = static_cast<int>((count + 255) / 256 < num_sms() * 16 ? (count + 255) / 256 : num_sms() * 16);
+    gaussian_reduce_kernel<float><<<g, 256, 0, st>>>(part, splits, count, scale, SX, accumulate, flags);
+  }
+}
+
 struct GaussPlan {
   int64_t splits, rows_per_split;
   unsigned gx, gy;
@@ -209,13 +255,14 @@ static GaussPlan plan_gauss(int64_t n, int64_t d, int64_t k) {
 // SIMT path (fp32 accumulation per split, fp64 across splits) at tensor-core
 // speed.  A non-finite x poisons P0 (and P1 = inf - inf = NaN), so the
 // reduce kernel's finiteness check still fires.
-__global__ void split3_bf16_kernel(const float* __restrict__ X, int64_t n, int64_t d, int64_t ldx, int64_t ldp,
-                                   __nv_bfloat16* __restrict__ P) {
-  const int64_t plane = n * ldp;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * ldp;
+__global__ void split3_bf16_kernel(const float* __restrict__ X, int64_t n, int64_t d, int64_t ldx, int64_t np,
+                                   int64_t ldp, __nv_bfloat16* __restrict__ P) {
+  // planes stacked [3][np][ldp], rows n .. np-1 and columns d .. ldp-1 zero
+  const int64_t plane = np * ldp;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < plane;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = e / ldp, j = e % ldp;
-    const float x = j < d ? X[i * ldx + j] : 0.f;
+    const float x = i < n && j < d ? X[i * ldx + j] : 0.f;
     const __nv_bfloat16 a = __float2bfloat16_rn(x);
     const float r1 = __fsub_rn(x, __bfloat162float(a));
     const __nv_bfloat16 b = __float2bfloat16_rn(r1);
@@ -226,10 +273,27 @@ __global__ void split3_bf16_kernel(const float* __restrict__ X, int64_t n, int64
   }
 }
 
+// the three planes go through ONE K4-TC launch over 3 np rows (np = n
+// rounded up to the 64-row stage, so no stage straddles two planes); the
+// kernel maps stacked row r to global row row0 + r mod np.  The split length
+// stays the single-plane plan's: the tcgen05 fp32 accumulation error grows
+// linearly with the K steps one TMEM accumulator absorbs (measured: 3.6e-6
+// relative at 3392 rows per split vs 1.2e-6 at 1152), so planning over 3 np
+// rows (3x longer splits) would cost accuracy; this keeps it and still
+// saves two launches and two wave tails.
+static GaussTcPlan plan_gauss_tc3(int64_t n, int64_t d, int64_t k) {
+  const int64_t np = (n + 63) / 64 * 64;
+  GaussTcPlan t = plan_gauss_tc(np, d, k);
+  t.splits = (3 * np + t.rows_per_split - 1) / t.rows_per_split;
+  t.period = np;
+  return t;
+}
+
 static bool f32_tc(int64_t n, int64_t d, int64_t k) {
   if (getenv("LVSK_NO_TC") != nullptr) return false;
   const int64_t ldp = (d + 7) / 8 * 8;
-  return k >= 64 && n >= 256 && 3 * n * ldp * 2 <= (int64_t{3} << 30);
+  const int64_t np = (n + 63) / 64 * 64;
+  return k >= 64 && n >= 256 && 3 * np * ldp * 2 <= (int64_t{3} << 30);
 }
 
 }  // namespace lvsk
@@ -246,10 +310,10 @@ extern "C" size_t lvsk_gaussian_workspace_bytes(int64_t n, int64_t d, int64_t k,
   Measure m;
   m.take<char>(static_cast<size_t>(splits) * k * d * (dtype == LVSK_F64 ? 8 : 4));
   if (dtype == LVSK_F32 && f32_tc(n, d, k)) {
-    const GaussTcPlan t = plan_gauss_tc(n, d, k);
+    const GaussTcPlan t = plan_gauss_tc3(n, d, k);
     Measure m3;
-    m3.take<float>(static_cast<size_t>(3 * t.splits) * k * d);
-    m3.take<__nv_bfloat16>(static_cast<size_t>(3 * n * ((d + 7) / 8 * 8)));
+    m3.take<float>(static_cast<size_t>(t.splits) * k * d);
+    m3.take<__nv_bfloat16>(static_cast<size_t>(3 * t.period * ((d + 7) / 8 * 8)));
     if (m3.off > m.off) return m3.off;
   }
   return m.off;
@@ -285,22 +349,20 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
     const int32_t rc = gaussian_tc_bf16(static_cast<const __nv_bfloat16*>(X), n, d, ldx, k, row0, key, t, part, st);
     if (rc != LVSK_OK) return rc;
-    gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, t.splits, count, scale, SX, accumulate, flags);
+    reduce_f32(part, t.splits, count, scale, SX, accumulate, flags, st);
   } else if (dtype == LVSK_F32 && f32_tc(n, d, k)) {
-    const GaussTcPlan t = plan_gauss_tc(n, d, k);
-    const int64_t ldp = (d + 7) / 8 * 8;
-    float* part = c.take<float>(static_cast<size_t>(3 * t.splits) * count);
-    __nv_bfloat16* planes = c.take<__nv_bfloat16>(static_cast<size_t>(3 * n * ldp));
+    const GaussTcPlan t = plan_gauss_tc3(n, d, k);
+    const int64_t ldp = (d + 7) / 8 * 8, np = t.period;
+    float* part = c.take<float>(static_cast<size_t>(t.splits) * count);
+    __nv_bfloat16* planes = c.take<__nv_bfloat16>(static_cast<size_t>(3 * np * ldp));
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
-    const int sgrid = static_cast<int>((n * ldp + 255) / 256 < num_sms() * 16 ? (n * ldp + 255) / 256 : num_sms() * 16);
-    split3_bf16_kernel<<<sgrid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx, ldp, planes);
+    const int sgrid =
+        static_cast<int>((np * ldp + 255) / 256 < num_sms() * 16 ? (np * ldp + 255) / 256 : num_sms() * 16);
+    split3_bf16_kernel<<<sgrid, 256, 0, st>>>(static_cast<const float*>(X), n, d, ldx, np, ldp, planes);
     LVSK_CHECK_LAUNCH("gaussian split");
-    for (int j = 0; j < 3; ++j) {
-      const int32_t rc = gaussian_tc_bf16(planes + j * n * ldp, n, d, ldp, k, row0, key, t,
-                                          part + static_cast<int64_t>(j) * t.splits * count, st);
-      if (rc != LVSK_OK) return rc;
-    }
-    gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, 3 * t.splits, count, scale, SX, accumulate, flags);
+    const int32_t rc = gaussian_tc_bf16(planes, 3 * np, d, ldp, k, row0, key, t, part, st);
+    if (rc != LVSK_OK) return rc;
+    reduce_f32(part, t.splits, count, scale, SX, accumulate, flags, st);
   } else {
     float* part = c.take<float>(static_cast<size_t>(p.splits) * count);
     LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
@@ -311,7 +373,7 @@ extern "C" int32_t lvsk_gaussian_sketch(const void* X, int32_t dtype, int64_t n,
       gaussian_gemm_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X), n, d,
                                                                        ldx, row0, key, k, p.rows_per_split,
                                                                        mag, part, flags);
-    gaussian_reduce_kernel<float><<<rgrid, 256, 0, st>>>(part, p.splits, count, scale, SX, accumulate, flags);
+    reduce_f32(part, p.splits, count, scale, SX, accumulate, flags, st);
   }
   LVSK_CHECK_LAUNCH("gaussian sketch");
   return LVSK_OK;

@@ -122,7 +122,7 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t*
 template <int NS, int CL, int MX>
 __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
     gaussian_tc_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
-                       uint64_t key, int ktiles, int dslabs, int64_t rows_per_split,
+                       uint64_t key, int ktiles, int dslabs, int64_t rows_per_split, int64_t period,
                        const uint16_t* __restrict__ gmag, float* __restrict__ partial) {
   using C = CfgG<NS>;
   extern __shared__ uint8_t smem_raw[];
@@ -255,8 +255,14 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       //      stage: four mix64 per lane per stage, counters advanced by
       //      constant adds (gauss_ctr is linear in (i << 24) | t)
       const uint32_t t0 = static_cast<uint32_t>(ktile * (BM / 4) + 2 * gw);
-      uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(r_begin + 2 * lane), t0);
-      for (int t = 0; t < nstages; ++t, ctr += STAGE) {
+      // Row r of the stacked input is global row row0 + (r mod period): the
+      // fp32 path stacks its three bf16 planes (period = padded plane rows,
+      // a multiple of 64, so a stage never straddles two planes)
+      int64_t rr = r_begin % period;
+      const uint64_t wrap = static_cast<uint64_t>(period) * ROW;
+      uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(rr + 2 * lane), t0);
+      for (int t = 0; t < nstages; ++t, ctr += STAGE, rr += C::BKN) {
+        if (rr == period) rr = 0, ctr -= wrap;
         const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
         // h[r][q]: input row 2 lane + r, quad t0 + q
         const uint64_t h00 = mix64(ctr), h01 = mix64(ctr + GAUSS_PHI);
@@ -292,11 +298,15 @@ __global__ void __launch_bounds__(CfgG<NS>::NTHREADS, 1)
       const uint32_t peer = static_cast<uint32_t>(dslab ^ 1);
       const int jbase = 64 * dslab + 4 * gw;
       const uint32_t t0 = static_cast<uint32_t>(ktile * (BM / 4) + jbase / 4);
-      uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(r_begin + 2 * lane), t0);
+      // stacked-plane row wrap, as in the CL == 1 loop
+      int64_t rr = r_begin % period;
+      const uint64_t wrap = static_cast<uint64_t>(period) * ROW;
+      uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(rr + 2 * lane), t0);
       const uint32_t zloc = smem_u32(smem + C::OFF_Z);
       const uint32_t zrem = map_peer(zloc, peer);
       const uint32_t fullrem = map_peer(smem_u32(&zfull[0]), peer);
-      for (int t = 0; t < nstages; ++t, ctr += STAGE) {
+      for (int t = 0; t < nstages; ++t, ctr += STAGE, rr += C::BKN) {
+        if (rr == period) rr = 0, ctr -= wrap;
         const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
         const uint64_t h0 = mix64(ctr), h1 = mix64(ctr + ROW);
         uint32_t w[4];
@@ -399,7 +409,8 @@ struct CfgGP {
 template <int NS, int S_, int SZ_>
 __global__ void __launch_bounds__(CfgGP<NS, S_, SZ_>::NTHREADS, 1)
     gaussian_tc_pair_kernel(const __grid_constant__ CUtensorMap mapX, int64_t n, int64_t d, int64_t k, uint64_t row0,
-                            uint64_t key, int kpairs, int64_t rows_per_split, const uint16_t* __restrict__ gmag,
+                            uint64_t key, int kpairs, int64_t rows_per_split, int64_t period,
+                            const uint16_t* __restrict__ gmag,
                             float* __restrict__ partial) {
   using C = CfgGP<NS, S_, SZ_>;
   extern __shared__ uint8_t smem_raw[];
@@ -514,11 +525,15 @@ __global__ void __launch_bounds__(CfgGP<NS, S_, SZ_>::NTHREADS, 1)
     const uint32_t partner = rank ^ 2u;
     const int jbase = 64 * static_cast<int>(slab) + 4 * gw;
     const uint32_t t0 = static_cast<uint32_t>(ktile * (BM / 4) + jbase / 4);
-    uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(r_begin + 2 * lane), t0);
+    // stacked-plane row wrap, as in gaussian_tc_kernel
+    int64_t rr = r_begin % period;
+    const uint64_t wrap = static_cast<uint64_t>(period) * ROW;
+    uint64_t ctr = gauss_ctr(key, row0 + static_cast<uint64_t>(rr + 2 * lane), t0);
     const uint32_t zloc = smem_u32(smem + C::OFF_Z);
     const uint32_t zrem = mapa_rank(zloc, partner);
     const uint32_t fullrem = mapa_rank(smem_u32(&zfull[0]), partner);
-    for (int t = 0; t < nstages; ++t, ctr += STAGE) {
+    for (int t = 0; t < nstages; ++t, ctr += STAGE, rr += C::BKN) {
+      if (rr == period) rr = 0, ctr -= wrap;
       const uint32_t s = t % C::SZ, ph = (t / C::SZ) & 1u;
       const uint64_t h0 = mix64(ctr), h1 = mix64(ctr + ROW);
       uint32_t w[4];
@@ -599,6 +614,7 @@ GaussTcPlan plan_gauss_tc(int64_t n, int64_t d, int64_t k) {
   if (splits < 1) splits = 1;
   p.rows_per_split = ((n + splits - 1) / splits + 63) / 64 * 64;
   p.splits = (n + p.rows_per_split - 1) / p.rows_per_split;
+  p.period = n;
   return p;
 }
 
@@ -640,7 +656,7 @@ static int32_t launch_gauss_tc(const __nv_bfloat16* X, int64_t n, int64_t d, int
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_kernel<NS, CL, MX>, mx, n, d, k, row0, key, p.ktiles,
-                                     p.dslabs, p.rows_per_split, gmag, partial);
+                                     p.dslabs, p.rows_per_split, p.period, gmag, partial);
   if (e != cudaSuccess) return cuda_status(e, "gaussian tc launch");
   return LVSK_OK;
 }
@@ -677,7 +693,7 @@ static int32_t launch_gauss_tc_pair(const __nv_bfloat16* X, int64_t n, int64_t d
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, tc::gaussian_tc_pair_kernel<512, S_, SZ_>, mx, n, d, k, row0, key, kpairs,
-                                           p.rows_per_split, gmag, partial);
+                                           p.rows_per_split, p.period, gmag, partial);
   if (e != cudaSuccess) return cuda_status(e, "gaussian tc pair launch");
   return LVSK_OK;
 }

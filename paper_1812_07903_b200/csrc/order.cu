@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "radix_sort.cuh"
@@ -119,6 +120,7 @@ constexpr int AS_HALO = 64;                    // longest equal-prefix run the f
 constexpr int AS_WIN = 4096;                   // fix-up window
 constexpr int64_t AS_MAX_N = int64_t{8} << 20;
 constexpr int AS_MAX_G = 1024;
+constexpr int64_t AS_INFLIGHT_CHUNK = 8192;  // min keys per CTA with passes in flight
 constexpr int AS_CHUNK_CAP = 12288;           // chunks up to this size are staged whole (longest output runs)
 constexpr size_t AS_RANK_SMEM =
     sizeof(uint32_t) * AS_WARPS * 256 + (sizeof(uint64_t) + sizeof(uint32_t)) * AS_CHUNK_CAP;
@@ -778,7 +780,13 @@ extern "C" int32_t lvsk_argsort_f64(const double* keys, int64_t n, int32_t desce
   unsigned long long* ctl = c.take<unsigned long long>(4);
   LVSK_REQUIRE(c.ok(), LVSK_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
   cudaStream_t st = as_stream(stream);
-  const int G = coop_grid();
+  int G = coop_grid();
+  if (inflight_passes() >= 2) {
+    // another pass runs concurrently: fuller CTAs leave SMs to it (the grid
+    // barriers, not the key traffic, bound a pass at these sizes)
+    const int64_t want = (n + AS_INFLIGHT_CHUNK - 1) / AS_INFLIGHT_CHUNK;
+    if (want < G) G = static_cast<int>(want < 1 ? 1 : want);
+  }
   if (n <= AS_MAX_N && G >= 1 && getenv("LVSK_ARGSORT_CLASSIC") == nullptr) {
     // ctl: [0] OR = 0, [1] AND = ~0, [2] barrier count = 0, [3] flag = 0
     cudaError_t e = cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned long long), st);

@@ -257,7 +257,11 @@ class LeveragePipeline:
             chunks = max(1, -(-self.n // (1 << cb)))
             sk = 1 + radix(self.k, 8) + 1 + 2 * chunks
         elif fam == GAUSSIAN:
-            sk = 2
+            # fp32 X on the tensor cores: split3 + one K4-TC launch over the stacked planes + reduce
+            # (csrc/gaussian.cu f32_tc; LVSK_NO_TC is a test-only switch)
+            planes = 3 * (-(-self.n // 64) * 64) * (-(-self.d // 8) * 8) * 2
+            sk = 3 if (self.code == N.LVSK_F32 and self.k >= 64 and self.n >= 256 and planes <= 3 << 30
+                       and "LVSK_NO_TC" not in os.environ) else 2
         else:
             # grouping: one cooperative counting sort (k <= 4096, s <= 64; csrc/sketch_hashed.cu)
             # or keygen + radix passes + bucket bounds; then the gather (K1) and the hi+lo fold
@@ -277,3 +281,69 @@ class LeveragePipeline:
         coop_sort = self.n <= (8 << 20) and not os.environ.get("LVSK_ARGSORT_CLASSIC")
         order_ = (3 + (1 if coop_sort else 1 + radix(self.n, 64))) if self.order else 0
         return sk + fold + lev + order_
+
+
+class BatchRunner:
+    """Independent passes (batches) kept in flight on ``slots`` streams.
+
+    Each slot owns a ``LeveragePipeline`` (its own sketch state, fold graph,
+    scores and order buffers) and a CUDA stream; ``submit(X)`` runs one full
+    pass over X on the next slot, so the latency-bound stages of one pass (the
+    fold: KD + KF; the order: K7) run beside the HBM-bound stages (K1 / K3 /
+    K4 / K5) of the next one.  The C library is told how many passes are in
+    flight (``lvsk_set_inflight``) so its cooperative kernels leave SMs to the
+    other stream; results are bit-identical to ``LeveragePipeline.run``.  A
+    slot is reused only after its stream finished the previous pass (stream
+    order), and ``result(i)`` / ``drain()`` synchronise with it.  No reference
+    counterpart (the reference runs one pass at a time on the host)."""
+
+    def __init__(self, *args, slots: int = 2, **kwargs):
+        if slots < 1:
+            raise ValueError("slots must be >= 1")
+        self.pipes = [LeveragePipeline(*args, **kwargs) for _ in range(slots)]
+        self.streams = [torch.cuda.Stream(device=self.pipes[0].dev) for _ in range(slots)]
+        self.slots = slots
+        self._next = 0
+        self._done = [None] * slots
+        N.check(N.lib().lvsk_set_inflight(slots), "set_inflight")
+
+    def submit(self, X, timing: bool = False) -> int:
+        """Run one pass over X (device-resident; the caller keeps X alive and
+        unmodified until the slot's pass completed) on the next slot; returns
+        the slot index.  Inputs written on the caller's stream are visible."""
+        i = self._next
+        self._next = (i + 1) % self.slots
+        st = self.streams[i]
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            self.pipes[i].run(X, timing=timing, check=False)
+            ev = torch.cuda.Event()
+            ev.record()
+        self._done[i] = ev
+        return i
+
+    def drain(self) -> None:
+        """Make the caller's stream wait for every pass in flight."""
+        cur = torch.cuda.current_stream()
+        for ev in self._done:
+            if ev is not None:
+                cur.wait_event(ev)
+
+    def result(self, slot: int):
+        """(scores, order) of the slot's last pass after its certificate check
+        (redoing the fold if it failed, as LeveragePipeline.check)."""
+        self.drain()
+        p = self.pipes[slot]
+        with torch.cuda.stream(self.streams[slot]):
+            p.check()
+        torch.cuda.current_stream().wait_stream(self.streams[slot])
+        return p.scores, (p.idx if p.order else None)
+
+    def check(self) -> None:
+        for i in range(self.slots):
+            self.result(i)
+
+    def close(self) -> None:
+        """Back to one pass in flight (the library-wide hint)."""
+        self.drain()
+        N.check(N.lib().lvsk_set_inflight(1), "set_inflight")

@@ -46,3 +46,25 @@ def test_bench_multirank_step_matches_oracle(config, rows, world):
     assert ver and ver[0]["world"] == world, out[-4000:]
     bench = [ln for ln in lines if "metric" in ln]
     assert bench and bench[0]["n_gpus"] == world and bench[0]["value"] > 0
+
+
+@pytest.mark.parametrize("config,rows", [("c2", 20_000), ("c3", 20_480), ("c5", 30_001), ("c1", 0)])
+def test_bench_single_gpu_pipelined_matches_oracle(config, rows):
+    """N = 1 default: two independent passes in flight (BatchRunner); the
+    last pass is checked against the oracle by --verify and the line carries
+    the single-pass latency next to the pipelined ms_per_step."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--config", config, "--steps", "4", "--warmup", "3",
+           "--no-e2e", "--no-cpu", "--verify"]
+    if rows:
+        cmd += ["--rows", str(rows)]
+    p = subprocess.run(cmd, cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=900)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0, out[-4000:]
+    lines = [json.loads(ln) for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert [ln for ln in lines if ln.get("verify") == "ok"], out[-4000:]
+    bench = [ln for ln in lines if "metric" in ln]
+    assert bench and bench[0]["config"]["passes_in_flight"] == 2, out[-4000:]
+    assert bench[0]["latency_ms_per_pass"] > 0 and bench[0]["ms_per_step"] > 0

@@ -328,10 +328,12 @@ def test_gaussian_sketch_matches_oracle():
         assert np.linalg.norm(st.data - ref) <= tol * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("n,d,k", [(20000, 256, 1024), (3001, 100, 200), (700, 520, 64)])
+@pytest.mark.parametrize("n,d,k", [(20000, 256, 1024), (3001, 100, 200), (700, 520, 64), (2100, 1000, 256)])
 def test_gaussian_fp32_tensor_core_vs_simt(n, d, k, monkeypatch):
-    """fp32 X through the exact three-plane bf16 split on tcgen05 (default)
-    vs the SIMT split-K GEMM (LVSK_NO_TC=1) vs the float64 oracle."""
+    """fp32 X through the exact three-plane bf16 split on tcgen05 (default:
+    the planes stacked with a 64-row-padded period, one K4-TC launch whose
+    splits straddle plane boundaries; d = 1000 takes the CTA-pair kernel) vs
+    the SIMT split-K GEMM (LVSK_NO_TC=1) vs the float64 oracle."""
     x = np.random.default_rng(n).standard_normal((n, d)).astype(np.float32)
     X = torch.from_numpy(x).cuda()
     spec = P.SketchSpec("gaussian", eps=0.5, d=d, seed=4, rows_override=k)

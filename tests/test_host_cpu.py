@@ -30,6 +30,21 @@ def test_library_exports_every_declared_symbol():
     assert lib.lvsk_abi_version() == 1
 
 
+def test_inflight_hint_roundtrip():
+    """lvsk_set_inflight (BatchRunner's scheduling hint) is host state only:
+    round trip, range check with an error message, default restored."""
+    lib = _native.lib()
+    assert lib.lvsk_get_inflight() == 1
+    try:
+        assert lib.lvsk_set_inflight(2) == 0
+        assert lib.lvsk_get_inflight() == 2
+        assert lib.lvsk_set_inflight(0) == 1  # LVSK_ERR_CONFIGURATION
+        assert b"passes" in lib.lvsk_last_error()
+        assert lib.lvsk_get_inflight() == 2
+    finally:
+        assert lib.lvsk_set_inflight(1) == 0
+
+
 def test_gaussian_generator_table_matches_oracle():
     """The K4 generator's host-built table (csrc/gaussian.cu) is the oracle's,
     bit for bit, so device entries can equal the oracle's exactly."""

@@ -70,7 +70,7 @@ struct FactorArgs {
   int32_t* verA;    // nb x nb tile versions
   int32_t* verW;    // nb x nb
   int32_t* verM;    // nb x rt
-  int32_t* ctl;     // [0] queue head, [1] finished Y tiles, [2] info
+  int32_t* ctl;     // [0] queue head, [1] finished Y tiles, [2] info, [3] the chain CTA's SM
   unsigned long long* trace;  // optional chain timestamps (LVSK_KF_TRACE), else null
   int nb, rt;
   int64_t dp, rp;
@@ -92,13 +92,12 @@ __device__ __forceinline__ void wait_ge(const int32_t* f, int v) {
     while (ld_acquire(f) < v) __nanosleep(32);
   }
 }
-// publish: every thread's tile stores are ordered before the flag
+// publish: every thread's tile stores are ordered before the flag — the CTA
+// barrier orders them before thread 0's release, and a gpu-scope release is
+// cumulative (the CUTLASS semaphore pattern), so no separate fence.sc
 __device__ __forceinline__ void signal(int32_t* f, int v) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(f, v);
-  }
+  if (threadIdx.x == 0) st_release(f, v);
 }
 
 // ---- tile movement (mutable tiles through L2 only) ------------------------------
@@ -299,14 +298,28 @@ enum : int { T_PANEL = 0, T_YROW = 1, T_UPD = 2, T_WUPD = 3, T_MACC = 4, T_FINAL
 
 // queue task t -> (type, j, x, y); per step j: YDIAG(j), PANEL(j, k >= j+2), YROW(j, m < j),
 // UPD(j; k <= l) without (j+1, j+1) — row j+1 first, WUPD(j; k, m <= j) — row
-// j+1 first, MACC(j; i <= j, c); then FINAL
+// j+1 first, MACC(j; i <= j, c); then FINAL.  UPD and WUPD come in row
+// segments of up to KF_SEG consecutive tiles that share the left operand U_jk
+// (one load of U_jk and one queue pull per segment; each tile still publishes
+// its own version): x = type | count << 4, (y, z, w) = (j, k, first l or m).
+constexpr int KF_SEG = 4;
+
+// sum_{c=1..n} ceil(c / KF_SEG)
+__host__ __device__ inline int kf_seg_sum(int n) {
+  if (n <= 0) return 0;
+  const int q = n / KF_SEG, r = n % KF_SEG;
+  return KF_SEG * q * (q + 1) / 2 + r * (q + 1);
+}
+
 __host__ __device__ inline int4 kf_decode(int t, int nb, int rt) {
   for (int j = 0; j < nb; ++j) {
     const int m = nb - j - 1;
     const int np = m > 1 ? m - 1 : 0;
     const int ny = j;
-    const int nu = m >= 1 ? m * (m + 1) / 2 - 1 : 0;
-    const int nw = m * (j + 1);
+    // UPD rows: row j+1 has m - 1 tiles (l = j+2..), row j+1+kk (kk >= 1) has m - kk
+    const int nu = m >= 1 ? (m - 1 + KF_SEG - 1) / KF_SEG + kf_seg_sum(m - 1) : 0;
+    const int wseg = (j + 1 + KF_SEG - 1) / KF_SEG;
+    const int nw = m * wseg;
     const int nm = (j + 1) * rt;
     if (t == 0) return make_int4(T_YDIAG, j, 0, 0);
     t -= 1;
@@ -315,15 +328,24 @@ __host__ __device__ inline int4 kf_decode(int t, int nb, int rt) {
     if (t < ny) return make_int4(T_YROW, j, t, 0);
     t -= ny;
     if (t < nu) {
-      int q = t + 1, kk = 0;
-      while (q >= m - kk) {
-        q -= m - kk;
-        ++kk;
+      for (int kk = 0; kk < m; ++kk) {
+        const int l0 = kk == 0 ? j + 2 : j + 1 + kk;
+        const int cnt = nb - l0;
+        const int ns = (cnt + KF_SEG - 1) / KF_SEG;
+        if (t < ns) {
+          const int first = l0 + t * KF_SEG;
+          const int c = nb - first < KF_SEG ? nb - first : KF_SEG;
+          return make_int4(T_UPD | (c << 4), j, j + 1 + kk, first);
+        }
+        t -= ns;
       }
-      return make_int4(T_UPD, j, j + 1 + kk, j + 1 + kk + q);
     }
     t -= nu;
-    if (t < nw) return make_int4(T_WUPD, j, j + 1 + t / (j + 1), t % (j + 1));
+    if (t < nw) {
+      const int first = (t % wseg) * KF_SEG;
+      const int c = j + 1 - first < KF_SEG ? j + 1 - first : KF_SEG;
+      return make_int4(T_WUPD | (c << 4), j, j + 1 + t / wseg, first);
+    }
     t -= nw;
     if (t < nm) return make_int4(T_MACC, j, t / rt, t % rt);
     t -= nm;
@@ -335,7 +357,8 @@ static int kf_queue_tasks(int nb, int rt) {
   int n = 0;
   for (int j = 0; j < nb; ++j) {
     const int m = nb - j - 1;
-    n += 1 + (m > 1 ? m - 1 : 0) + j + (m >= 1 ? m * (m + 1) / 2 - 1 : 0) + m * (j + 1) + (j + 1) * rt;
+    const int nu = m >= 1 ? (m - 1 + KF_SEG - 1) / KF_SEG + kf_seg_sum(m - 1) : 0;
+    n += 1 + (m > 1 ? m - 1 : 0) + j + nu + m * ((j + 1 + KF_SEG - 1) / KF_SEG) + (j + 1) * rt;
   }
   return n + 1;
 }
@@ -390,7 +413,12 @@ __global__ void __launch_bounds__(FTHREADS, NT == 3 ? 2 : 1) chol_fold_kernel(Fa
       a.verW[i] = 0;
     }
     for (int i = gt; i < nb * rt; i += gn) a.verM[i] = 0;
-    if (gt < 4) a.ctl[gt] = 0;
+    if (gt < 3) a.ctl[gt] = 0;
+    if (cta == 0 && threadIdx.x == 0) {  // the chain CTA's SM (read after the grid barrier)
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      a.ctl[3] = static_cast<int32_t>(sm);
+    }
     if (cta == 0 && threadIdx.x < 32) {
       // trace(G) in a fixed order (one warp, then lane 0)
       double t = 0.0;
@@ -474,7 +502,16 @@ __global__ void __launch_bounds__(FTHREADS, NT == 3 ? 2 : 1) chol_fold_kernel(Fa
     return;
   }
 
-  // ---- everything else from the queue, in topological order
+  // ---- everything else from the queue, in topological order.  Two CTAs per
+  // SM (NT = 3): the queue CTA that shares the chain CTA's SM leaves, so the
+  // latency-bound chain (its 64-pivot eliminations, DFMA on the same fp64
+  // pipe as the queue's DMMA) has the SM to itself — chol_inv 30-43 us per
+  // tile beside a queue CTA vs 12.5 us alone (LVSK_KF_TRACE at d = 4096)
+  if (NT == 3) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    if (static_cast<int32_t>(sm) == __ldcg(a.ctl + 3)) return;
+  }
   for (;;) {
     if (threadIdx.x == 0) s_task = kf_decode(atomicAdd(a.ctl, 1), nb, rt);
     __syncthreads();
@@ -527,31 +564,39 @@ __global__ void __launch_bounds__(FTHREADS, NT == 3 ? 2 : 1) chol_fold_kernel(Fa
         st_release(a.verW + j * nb + m, j - m + 1);
         atomicAdd(a.ctl + 1, 1);
       }
-    } else if (tk.x == T_UPD) {  // A_kl -= U_jk^T U_jl
-      const int k = tk.z, l = tk.w;
+    } else if ((tk.x & 15) == T_UPD) {  // A_kl -= U_jk^T U_jl, l = w .. w + count - 1
+      const int k = tk.z, cnt = tk.x >> 4;
       wait_ge(a.verA + j * nb + k, j + 1);
-      wait_ge(a.verA + j * nb + l, j + 1);
-      wait_ge(a.verA + k * nb + l, j);
       __syncthreads();
       load_tile(b0, atile(a, j, k), dp);
-      if (l != k) load_tile(b1, atile(a, j, l), dp);
-      __syncthreads();
-      if (l != k)
-        gemm_tile<1, true>(b0, b1, atile(a, k, l), dp, atile(a, k, l), dp);
-      else  // diagonal tile: only its upper triangle is ever read
-        gemm_tile<1, true, 2>(b0, b0, atile(a, k, l), dp, atile(a, k, l), dp);
-      signal(a.verA + k * nb + l, j + 1);
-    } else if (tk.x == T_WUPD) {  // W_km -= U_jk^T Y_jm
-      const int k = tk.z, m = tk.w;
+      for (int q = 0; q < cnt; ++q) {
+        const int l = tk.w + q;
+        wait_ge(a.verA + j * nb + l, j + 1);
+        wait_ge(a.verA + k * nb + l, j);
+        __syncthreads();  // also: the previous tile's gemm is done with b1
+        if (l != k) load_tile(b1, atile(a, j, l), dp);
+        __syncthreads();
+        if (l != k)
+          gemm_tile<1, true>(b0, b1, atile(a, k, l), dp, atile(a, k, l), dp);
+        else  // diagonal tile: only its upper triangle is ever read
+          gemm_tile<1, true, 2>(b0, b0, atile(a, k, l), dp, atile(a, k, l), dp);
+        signal(a.verA + k * nb + l, j + 1);
+      }
+    } else if ((tk.x & 15) == T_WUPD) {  // W_km -= U_jk^T Y_jm, m = w .. w + count - 1
+      const int k = tk.z, cnt = tk.x >> 4;
       wait_ge(a.verA + j * nb + k, j + 1);
-      wait_ge(a.verW + j * nb + m, j - m + 1);
-      wait_ge(a.verW + k * nb + m, j - m);
       __syncthreads();
       load_tile(b0, atile(a, j, k), dp);
-      load_tile(b1, wtile(a, j, m), dp);
-      __syncthreads();
-      gemm_tile<1, true>(b0, b1, wtile(a, k, m), dp, wtile(a, k, m), dp);
-      signal(a.verW + k * nb + m, j - m + 1);
+      for (int q = 0; q < cnt; ++q) {
+        const int m = tk.w + q;
+        wait_ge(a.verW + j * nb + m, j - m + 1);
+        wait_ge(a.verW + k * nb + m, j - m);
+        __syncthreads();
+        load_tile(b1, wtile(a, j, m), dp);
+        __syncthreads();
+        gemm_tile<1, true>(b0, b1, wtile(a, k, m), dp, wtile(a, k, m), dp);
+        signal(a.verW + k * nb + m, j - m + 1);
+      }
     } else if (tk.x == T_MACC) {  // M_ic += Y_ji^T Pi_jc
       const int i = tk.z, c = tk.w;
       wait_ge(a.verW + j * nb + i, j - i + 1);

@@ -460,7 +460,8 @@ def test_cholesky_fold_equals_qr_fold_and_oracle():
     assert np.allclose(mm @ mm.T, mo @ mo.T, rtol=1e-8, atol=1e-11 * np.abs(mo @ mo.T).max())
 
 
-@pytest.mark.parametrize("k,d,r", [(64, 1, 1), (300, 64, 64), (400, 100, 7), (2048, 512, 64), (1500, 700, 130), (2100, 1100, 64)])
+@pytest.mark.parametrize("k,d,r", [(64, 1, 1), (300, 64, 64), (400, 100, 7), (2048, 512, 64), (1500, 700, 130), (2100, 1100, 64),
+                                   (6200, 3100, 130)])
 def test_kf_cholesky_fold_kernel_vs_numpy(k, d, r):
     """KF (csrc/factor.cu) against numpy: M = R^-1 Pi and the certificate
     traces, on ragged d / r (identity padding) and one-tile cases."""

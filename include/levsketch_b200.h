@@ -219,6 +219,22 @@ LVSK_API int32_t lvsk_hashed_sketch_csr(const int64_t* row_ptr, const int32_t* c
 LVSK_API int32_t lvsk_rowsumsq_csr(const int64_t* row_ptr, const int32_t* col, const void* val,
                                    int32_t val_dtype, int64_t n, int64_t d, const float* M, int64_t r,
                                    double* scores, int32_t* flags, void* stream);
+/* K6 with a prepared operand (r = 128; reference: the same _block_scores,
+ * leverage.py:88-95).  lvsk_rowsumsq_csr_prepare turns the fold's M (float32
+ * d x 128) once into bf16 [M_hi | M_lo] operand images of the hot column
+ * window (the first 64 * LVSK_K6_HOTBLOCKS column ids, default 640) in `prep`
+ * (lvsk_rowsumsq_csr_prep_bytes(d, r) bytes, 16-byte aligned; 0 = not
+ * available for this r, use lvsk_rowsumsq_csr); lvsk_rowsumsq_csr_prepared
+ * then scores CSR row blocks with the hot window on tcgen05 and only the
+ * columns beyond it gathered from M.  Rows must be strictly increasing
+ * (violations set LVSK_FLAG_BADINDEX). */
+LVSK_API size_t lvsk_rowsumsq_csr_prep_bytes(int64_t d, int64_t r);
+LVSK_API int32_t lvsk_rowsumsq_csr_prepare(const float* M, int64_t d, int64_t r, void* prep, size_t prep_bytes,
+                                           void* stream);
+LVSK_API int32_t lvsk_rowsumsq_csr_prepared(const int64_t* row_ptr, const int32_t* col, const void* val,
+                                            int32_t val_dtype, int64_t n, int64_t d, const float* M, int64_t r,
+                                            const void* prep, size_t prep_bytes, double* scores, int32_t* flags,
+                                            void* stream);
 
 /* ---- fold ------------------------------------------------------------------
  * KF: the certified Cholesky JL fold (replaces the reference's

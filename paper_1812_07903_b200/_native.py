@@ -69,6 +69,9 @@ _SIGS = {
         [_P, _P, _P, _I32, _I64, _I64, _U64, C.POINTER(HashBlock), _I32, _D, _P, _P, _P, _P, _I64, _P, _SZ, _P, _P],
     ),
     "lvsk_rowsumsq_csr": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P, _I64, _P, _P, _P]),
+    "lvsk_rowsumsq_csr_prep_bytes": (_SZ, [_I64, _I64]),
+    "lvsk_rowsumsq_csr_prepare": (_I32, [_P, _I64, _I64, _P, _SZ, _P]),
+    "lvsk_rowsumsq_csr_prepared": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P, _I64, _P, _SZ, _P, _P, _P]),
     "lvsk_normalize_workspace_bytes": (_SZ, [_I64]),
     "lvsk_normalize_scores": (_I32, [_P, _I64, _P, _P, _P, _SZ, _P, _P]),
     "lvsk_sum_f64": (_I32, [_P, _I64, _P, _P, _SZ, _P]),

@@ -99,6 +99,20 @@ def csr_code(m: CSRMatrix) -> int:
     return N.LVSK_F32 if m.data.dtype == torch.float32 else N.LVSK_F64
 
 
+def csr_prepare(Mf: torch.Tensor) -> torch.Tensor | None:
+    """The bf16 operand images of M's hot column window for the prepared K6
+    pass (``lvsk_rowsumsq_csr_prepare``), or None when the pass does not apply
+    (r != 128).  Built once per fold; ``Mf`` is the contiguous float32 d x r M."""
+    d, r = Mf.shape
+    nbytes = int(N.lib().lvsk_rowsumsq_csr_prep_bytes(d, r))
+    if nbytes == 0 or Mf.data_ptr() % 16:
+        return None
+    prep = torch.empty(nbytes, dtype=torch.uint8, device=Mf.device)
+    N.check(N.lib().lvsk_rowsumsq_csr_prepare(Mf.data_ptr(), d, r, prep.data_ptr(), nbytes, N.stream_ptr()),
+            "csr leverage operand")
+    return prep
+
+
 def csr_scores(m: CSRMatrix, M: torch.Tensor, out: torch.Tensor | None = None, flags=None) -> torch.Tensor:
     """K6: ||x_i M||^2 for CSR rows (fp32 M gathers, fp32 accumulation)."""
     if M.shape[0] != m.d:
@@ -107,9 +121,17 @@ def csr_scores(m: CSRMatrix, M: torch.Tensor, out: torch.Tensor | None = None, f
     out = torch.empty(m.n, dtype=torch.float64, device=Mf.device) if out is None else out
     own = flags is None
     flags = flags or N.Flags()
-    N.check(N.lib().lvsk_rowsumsq_csr(m.indptr.data_ptr(), m.indices.data_ptr(), m.data.data_ptr(), csr_code(m), m.n,
-                                      m.d, Mf.data_ptr(), Mf.shape[1], out.data_ptr(), flags.p, N.stream_ptr()),
-            "csr leverage pass")
+    prep = csr_prepare(Mf)
+    if prep is not None:  # r = 128: the hot column window on tcgen05 (K6-TC v2)
+        N.check(N.lib().lvsk_rowsumsq_csr_prepared(m.indptr.data_ptr(), m.indices.data_ptr(), m.data.data_ptr(),
+                                                   csr_code(m), m.n, m.d, Mf.data_ptr(), Mf.shape[1], prep.data_ptr(),
+                                                   prep.numel(), out.data_ptr(), flags.p, N.stream_ptr()),
+                "csr leverage pass")
+    else:
+        N.check(N.lib().lvsk_rowsumsq_csr(m.indptr.data_ptr(), m.indices.data_ptr(), m.data.data_ptr(), csr_code(m),
+                                          m.n, m.d, Mf.data_ptr(), Mf.shape[1], out.data_ptr(), flags.p,
+                                          N.stream_ptr()),
+                "csr leverage pass")
     if own:
         _raise_flags(flags.read())
     return out

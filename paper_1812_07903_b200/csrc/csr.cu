@@ -571,7 +571,35 @@ namespace lvsk {
 bool csr_rowsumsq_tc_ok(const float* M, int64_t r);
 int32_t csr_rowsumsq_tc(const int64_t* row_ptr, const int32_t* col, const void* val, int32_t val_dtype, int64_t n,
                         int64_t d, const float* M, double* scores, int32_t* flags, cudaStream_t st);
+size_t csr_rowsumsq_prep_bytes(int64_t d, int64_t r);
+int32_t csr_rowsumsq_prepare(const float* M, int64_t d, int64_t r, void* prep, size_t prep_bytes, cudaStream_t st);
+int32_t csr_rowsumsq_tc2(const int64_t* row_ptr, const int32_t* col, const void* val, int32_t val_dtype, int64_t n,
+                         int64_t d, const float* M, const void* prep, size_t prep_bytes, double* scores,
+                         int32_t* flags, cudaStream_t st);
 }  // namespace lvsk
+
+// K6-TC v2 (csr_tc.cu): the fold's M is turned once into bf16 operand images of
+// the hot column window (lvsk_rowsumsq_csr_prepare); every leverage pass over
+// CSR rows with that M then streams them through the tensor cores.
+extern "C" size_t lvsk_rowsumsq_csr_prep_bytes(int64_t d, int64_t r) {
+  return d >= 1 && getenv("LVSK_K6_SIMT") == nullptr && getenv("LVSK_K6_V1") == nullptr ? csr_rowsumsq_prep_bytes(d, r) : 0;
+}
+
+extern "C" int32_t lvsk_rowsumsq_csr_prepare(const float* M, int64_t d, int64_t r, void* prep, size_t prep_bytes,
+                                             void* stream) {
+  LVSK_REQUIRE(d >= 1 && r >= 1 && M != nullptr, LVSK_ERR_DIMENSION, "bad shape");
+  return csr_rowsumsq_prepare(M, d, r, prep, prep_bytes, as_stream(stream));
+}
+
+extern "C" int32_t lvsk_rowsumsq_csr_prepared(const int64_t* row_ptr, const int32_t* col, const void* val,
+                                              int32_t val_dtype, int64_t n, int64_t d, const float* M, int64_t r,
+                                              const void* prep, size_t prep_bytes, double* scores, int32_t* flags,
+                                              void* stream) {
+  LVSK_REQUIRE(n >= 0 && d >= 1 && r == 128, LVSK_ERR_DIMENSION, "bad shape (the prepared pass needs r = 128)");
+  LVSK_REQUIRE(val_dtype == LVSK_F32 || val_dtype == LVSK_F64, LVSK_ERR_CONFIGURATION, "values must be f32 or f64");
+  if (n == 0) return LVSK_OK;
+  return csr_rowsumsq_tc2(row_ptr, col, val, val_dtype, n, d, M, prep, prep_bytes, scores, flags, as_stream(stream));
+}
 
 extern "C" int32_t lvsk_rowsumsq_csr(const int64_t* row_ptr, const int32_t* col, const void* val, int32_t val_dtype,
                                      int64_t n, int64_t d, const float* M, int64_t r, double* scores, int32_t* flags,

@@ -313,6 +313,425 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace k6tc
 
+// ---------------------------------------------------------------------------
+// K6-TC v2 — a wide hot window streamed through the tensor cores.
+//
+// v1 above is bound by the L2 slice throughput (~6300 B/clk chip-wide, the
+// LTS cap): its cold half gathers 512 B of M per nonzero, 82 GB at C4 in
+// 7.4 ms = 11 TB/s.  Only fewer L2 bytes make it faster.  A column that a
+// fraction f of the rows holds costs 128 f x 512 B per 128-row tile when it is
+// gathered and 512 B (its bf16 [M_hi | M_lo] operand rows) when it is
+// multiplied densely, so every column with f > 1/128 belongs on the tensor
+// cores: at C4 that is the first ~1000 Zipf-ranked ids.  The hot window is
+// therefore HT = 64 nb columns (nb <= 16), streamed in 64-column K blocks:
+//   * the B operand images (one 32 KB SW128 block per 64 columns, built once
+//     per fold by k6_prep_kernel) arrive through a 3-stage cp.async.bulk ring;
+//   * 4 scatter warps (thread = tile row) walk their row's sorted entries and
+//     fill the A block (bf16 x_hi / x_lo planes, 2-stage ring) of each K
+//     block; the same warps run the epilogue of their 32 rows (warp q = TMEM
+//     lane quadrant q), so one TMEM accumulator suffices;
+//   * 16 gather warps (8 rows each) gather only the columns >= HT into
+//     u_cold, running a tile ahead of the scatter / MMA pipeline;
+//   * one thread issues the MMAs, one thread the bulk copies.
+// Rows must have strictly increasing columns (the CSR contract, include/
+// levsketch_b200.h); a row that does not sets LVSK_FLAG_BADINDEX.
+namespace k6v2 {
+
+using namespace tc;
+using k6tc::bf16_bits;
+using k6tc::idesc;
+
+constexpr int R = 128;
+constexpr int TR = 128;
+constexpr int GW = 16;             // gather warps
+constexpr int RPW = TR / GW;       // rows per gather warp
+constexpr int SW = 4;              // scatter + epilogue warps
+constexpr int WARP_MMA = SW;
+constexpr int WARP_LOAD = SW + 1;
+constexpr int WARP_G0 = SW + 2;
+constexpr int THREADS = 32 * (SW + 2 + GW);
+constexpr int KBLK = 64;                 // hot columns per K block
+constexpr int B_STAGE = 2 * R * 128;     // [M_hi | M_lo]^T rows of one K block: 256 x 128 B
+constexpr int A_PLANE = TR * 128;        // 128 rows x 128 B
+constexpr int A_STAGE = 2 * A_PLANE;     // x_hi plane, x_lo plane
+constexpr int NSB = 2;  // (two stages keep shared memory under 196 KB: 60 KB of L1 for the row walks)
+constexpr int NSA = 2;
+constexpr int OFF_B = 0;
+constexpr int OFF_A = OFF_B + NSB * B_STAGE;
+constexpr int OFF_UC = OFF_A + NSA * A_STAGE;
+constexpr int OFF_BAR = OFF_UC + TR * R * 4;
+constexpr int SMEM_BYTES = OFF_BAR + 256 + TR * 4 + 1024;
+constexpr int MAX_NB = 16;
+static_assert(SMEM_BYTES <= 232448, "K6-TC v2 shared memory");
+
+// M rows stream through L2 only: the 60 KB of L1 belong to the scatter threads' row walks
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// B operand images: block j holds rows nn < R = bf16(M[64 j + k][nn]) and rows
+// nn >= R = the bf16 remainder, K-major SW128 (the layout the MMA reads)
+__global__ void k6_prep_kernel(const float* __restrict__ M, int64_t d, int nb, uint8_t* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(nb) * 2 * R * KBLK;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(e % R);
+    const int kk = static_cast<int>((e / R) % KBLK);
+    const int half = static_cast<int>((e / (R * KBLK)) & 1);
+    const int j = static_cast<int>(e / (2 * R * KBLK));
+    const int64_t k = static_cast<int64_t>(j) * KBLK + kk;
+    const float m = k < d ? M[k * R + c] : 0.f;
+    const float mh = __bfloat162float(__float2bfloat16_rn(m));
+    const int nn = half * R + c;
+    const int64_t off = static_cast<int64_t>(j) * B_STAGE + nn * 128 + ((((kk >> 3) ^ (nn & 7))) << 4) + ((kk & 7) << 1);
+    *reinterpret_cast<uint16_t*>(out + off) = bf16_bits(half ? m - mh : mh);
+  }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(THREADS, 1)
+    csr_rowsumsq_tc2_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                            const V* __restrict__ val, int64_t n, int64_t d, const float* __restrict__ M,
+                            const uint8_t* __restrict__ prep, int nb, double* __restrict__ scores, int32_t* flags, int dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* bfull = bars;             // [NSB] bulk copy landed
+  uint64_t* bfree = bfull + NSB;      // [NSB] MMAs done reading the B stage
+  uint64_t* aready = bfree + NSB;     // [NSA] SW scatter warps: A block written
+  uint64_t* afree = aready + NSA;     // [NSA] MMAs done reading the A stage
+  uint64_t* accfull = afree + NSA;    // all K blocks of the tile accumulated
+  uint64_t* ucready = accfull + 1;    // GW gather warps: u_cold written
+  uint64_t* ucfree = ucready + 1;     // SW epilogue warps: u_cold read
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ucfree + 1);
+  int32_t* coldcnt = reinterpret_cast<int32_t*>(smem + OFF_BAR + 256);  // [TR] cold entries per row (gather -> epilogue)
+  float* ucold = reinterpret_cast<float*>(smem + OFF_UC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + TR - 1) / TR;
+  const int64_t base0 = row_ptr[0];
+  const int32_t ht = nb * KBLK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bfree[s], 1);
+    }
+    for (int s = 0; s < NSA; ++s) {
+      mbar_init(&aready[s], SW);
+      mbar_init(&afree[s], 1);
+    }
+    mbar_init(accfull, 1);
+    mbar_init(ucready, GW);
+    mbar_init(ucfree, SW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == WARP_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == WARP_LOAD) {
+    // ---- B loader: the nb block images, in order, for every tile
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int j = 0; j < nb; ++j, ++it) {
+          const uint32_t s = it % NSB, u = it / NSB;
+          if (u > 0) mbar_wait(&bfree[s], (u - 1) & 1u);
+          mbar_expect_tx(&bfull[s], B_STAGE);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(smem + OFF_B + s * B_STAGE)),
+              "l"(prep + static_cast<int64_t>(j) * B_STAGE), "r"(B_STAGE), "r"(smem_u32(&bfull[s]))
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == WARP_MMA) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int j = 0; j < nb; ++j, ++it) {
+          const uint32_t sb = it % NSB, sa = it % NSA;
+          mbar_wait(&aready[sa], (it / NSA) & 1u);
+          mbar_wait(&bfull[sb], (it / NSB) & 1u);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A written through the generic proxy
+          tc_fence_after();
+          const uint64_t ah = sw128_desc(smem_u32(smem + OFF_A + sa * A_STAGE));
+          const uint64_t al = sw128_desc(smem_u32(smem + OFF_A + sa * A_STAGE + A_PLANE));
+          const uint64_t b = sw128_desc(smem_u32(smem + OFF_B + sb * B_STAGE));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            umma_f16(tmem_base, ah + 2 * kk, b + 2 * kk, idesc(2 * R), (j | kk) ? 1u : 0u);  // x_hi [M_hi | M_lo]
+            umma_f16(tmem_base + R, al + 2 * kk, b + 2 * kk, idesc(R), 1u);                  // + x_lo M_hi
+          }
+          umma_commit(&afree[sa]);
+          umma_commit(&bfree[sb]);
+        }
+        umma_commit(accfull);
+      }
+    }
+  } else if (warp < SW) {
+    // ---- scatter + epilogue: thread = tile row 32 q + lane walks its row's sorted entries
+    // (two entries of lookahead) and places those of each K block into the A planes
+    const int q = warp;
+    const int i = 32 * q + lane;
+    int bad = 0;
+    uint32_t it = 0, lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int64_t g = t * TR + i;
+      const int64_t e0 = row_ptr[g < n ? g : n] - base0;
+      const int64_t e1 = row_ptr[g + 1 < n ? g + 1 : n] - base0;
+      int64_t ptr = e0;
+      // two entries of lookahead
+      int32_t cprev = -1;
+      int32_t ca = ptr < e1 ? col[ptr] : 0x7FFFFFFF;
+      float xa = ptr < e1 ? static_cast<float>(val[ptr]) : 0.f;
+      int32_t cb = ptr + 1 < e1 ? col[ptr + 1] : 0x7FFFFFFF;
+      float xb = ptr + 1 < e1 ? static_cast<float>(val[ptr + 1]) : 0.f;
+      for (int j = 0; j < nb; ++j, ++it) {
+        const uint32_t sa = it % NSA, u = it / NSA;
+        if (u > 0) mbar_wait(&afree[sa], (u - 1) & 1u);
+        uint8_t* ahp = smem + OFF_A + sa * A_STAGE;
+        uint8_t* alp = ahp + A_PLANE;
+        // zero this warp's 32 rows (4 KB, contiguous) of both planes
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          reinterpret_cast<uint4*>(ahp + 4096 * q)[x * 32 + lane] = make_uint4(0, 0, 0, 0);
+          reinterpret_cast<uint4*>(alp + 4096 * q)[x * 32 + lane] = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+        const int32_t lo = j * KBLK, lim = lo + KBLK;
+        while (ca < lim && !(dbg & 2)) {  // ca = INT_MAX past the row's end
+          if (ca < lo || ca <= cprev) {  // out of order (or negative): the row breaks the CSR contract
+            bad |= LVSK_FLAG_BADINDEX;
+          } else {
+            if (!isfinite(xa)) bad |= LVSK_FLAG_NONFINITE;
+            const int32_t k = ca - lo;
+            const float xh = __bfloat162float(__float2bfloat16_rn(xa));
+            const uint32_t off = static_cast<uint32_t>(i * 128 + ((((k >> 3) ^ (i & 7))) << 4) + ((k & 7) << 1));
+            *reinterpret_cast<uint16_t*>(ahp + off) = bf16_bits(xh);
+            *reinterpret_cast<uint16_t*>(alp + off) = bf16_bits(xa - xh);
+            cprev = ca;
+          }
+          ca = cb;
+          xa = xb;
+          ++ptr;
+          const bool more = ptr + 1 < e1;
+          cb = more ? col[ptr + 1] : 0x7FFFFFFF;
+          xb = more ? static_cast<float>(val[ptr + 1]) : 0.f;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&aready[sa]);
+      }
+      // epilogue of this warp's 32 rows
+      mbar_wait(ucready, lt & 1u);
+      mbar_wait(accfull, lt & 1u);
+      tc_fence_after();
+      // every entry is either placed above (columns < ht) or gathered (the cold suffix):
+      // anything else is a row that is not strictly increasing
+      if (g < n && (ptr - e0) + coldcnt[i] != e1 - e0) bad |= LVSK_FLAG_BADINDEX;
+      const uint32_t base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+      float acc = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < R; c0 += 32) {
+        uint32_t vh[32], vl[32];
+        tmem_ld32(base + c0, vh);
+        tmem_ld32(base + R + c0, vl);
+        tmem_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+          const int blk = (c0 + jj) >> 2;
+          const float4 uc = *reinterpret_cast<const float4*>(ucold + i * R + 4 * (blk ^ (i & 31)));
+          const float a0 = __uint_as_float(vh[jj]) + __uint_as_float(vl[jj]) + uc.x;
+          const float a1 = __uint_as_float(vh[jj + 1]) + __uint_as_float(vl[jj + 1]) + uc.y;
+          const float a2 = __uint_as_float(vh[jj + 2]) + __uint_as_float(vl[jj + 2]) + uc.z;
+          const float a3 = __uint_as_float(vh[jj + 3]) + __uint_as_float(vl[jj + 3]) + uc.w;
+          acc = fmaf(a0, a0, acc);
+          acc = fmaf(a1, a1, acc);
+          acc = fmaf(a2, a2, acc);
+          acc = fmaf(a3, a3, acc);
+        }
+      }
+      if (g < n) scores[g] = static_cast<double>(acc);
+      tc_fence_before();  // the next tile's first MMA overwrites the accumulator
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ucfree);
+    }
+    const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (any && lane == 0) atomicOr(flags, any);
+  } else {
+    // ---- gather warps: the cold suffix (columns >= ht) of rows RPW w .. RPW w + RPW - 1.
+    // Only the row's last 32 entries are read (three rows ahead); a longer cold suffix
+    // walks back batch by batch.
+    const int w = warp - WARP_G0;
+    int bad = 0;
+    uint32_t lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int64_t gbase = t * TR + RPW * w;
+      int64_t rp = 0;
+      if (lane <= RPW) rp = row_ptr[gbase + lane < n ? gbase + lane : n] - base0;
+      auto load_tail = [&](int rr, int32_t& c, float& x) {
+        const int64_t f0 = __shfl_sync(0xFFFFFFFFu, rp, rr < RPW ? rr : RPW);
+        const int64_t f1 = __shfl_sync(0xFFFFFFFFu, rp, rr < RPW ? rr + 1 : RPW);
+        const int64_t s0 = f1 - 32 > f0 ? f1 - 32 : f0;
+        const bool live = s0 + lane < f1;
+        c = live ? col[s0 + lane] : 0;
+        x = live ? static_cast<float>(val[s0 + lane]) : 0.f;
+      };
+      int32_t c0, c1, c2;
+      float x0, x1, x2;
+      load_tail(0, c0, x0);
+      load_tail(1, c1, x1);
+      load_tail(2, c2, x2);
+#pragma unroll 1
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int i = RPW * w + rr;
+        float u[4] = {0.f, 0.f, 0.f, 0.f};
+        const int64_t e0 = __shfl_sync(0xFFFFFFFFu, rp, rr), e1 = __shfl_sync(0xFFFFFFFFu, rp, rr + 1);
+        int32_t c = c0;
+        float x = x0;
+        c0 = c1;
+        x0 = x1;
+        c1 = c2;
+        x1 = x2;
+        load_tail(rr + 3, c2, x2);  // (past the tile's last row: an empty range, no load)
+        int64_t s0 = e1 - 32 > e0 ? e1 - 32 : e0;  // this batch = entries [s0, s1)
+        int64_t s1 = e1;
+        int total = 0;
+        while (true) {
+          const int nl = static_cast<int>(s1 - s0);
+          const bool live = lane < nl;
+          const int32_t prev = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+          if (live && (c < 0 || c >= d || (lane > 0 && c <= prev))) {
+            bad |= LVSK_FLAG_BADINDEX;
+            c = 0;
+            x = 0.f;
+          }
+          if (live && !isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
+          uint32_t cm = __ballot_sync(0xFFFFFFFFu, live && c >= ht && !(dbg & 1));
+          const int ncold = __popc(cm);
+          total += ncold;
+          const int first = nl - ncold;
+          // sorted rows: the cold entries are the batch's last lanes; eight rows of M in flight per lane
+          if (ncold > 0 && cm == ((0xFFFFFFFFu >> (32 - ncold)) << first)) {
+            for (int b0 = 0; b0 < ncold; b0 += 8) {
+              float4 mv[8];
+              float xv[8];
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const int tl = (first + b0 + jj) & 31;
+                const int32_t ct = __shfl_sync(0xFFFFFFFFu, c, tl);
+                const float xt = __shfl_sync(0xFFFFFFFFu, x, tl);
+                const bool ok = b0 + jj < ncold;
+                xv[jj] = ok ? xt : 0.f;
+                const float4* mp = reinterpret_cast<const float4*>(M + static_cast<int64_t>(ct) * R) + lane;
+                mv[jj] = ok ? ((dbg & 4) ? __ldg(mp) : ldg_stream(mp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                u[0] = fmaf(xv[jj], mv[jj].x, u[0]);
+                u[1] = fmaf(xv[jj], mv[jj].y, u[1]);
+                u[2] = fmaf(xv[jj], mv[jj].z, u[2]);
+                u[3] = fmaf(xv[jj], mv[jj].w, u[3]);
+              }
+            }
+          } else if (ncold > 0) {
+            bad |= LVSK_FLAG_BADINDEX;  // cold entries that are not a suffix: not increasing
+          }
+          if (ncold < nl || s0 <= e0) break;  // the suffix starts inside this batch (or the row is done)
+          const int32_t head = __shfl_sync(0xFFFFFFFFu, c, 0);
+          s1 = s0;
+          s0 = s1 - 32 > e0 ? s1 - 32 : e0;
+          const bool lv = s0 + lane < s1;
+          c = lv ? col[s0 + lane] : 0;
+          x = lv ? static_cast<float>(val[s0 + lane]) : 0.f;
+          if (__shfl_sync(0xFFFFFFFFu, c, static_cast<int>(s1 - s0) - 1) >= head) bad |= LVSK_FLAG_BADINDEX;
+        }
+        // the previous tile's epilogue must be done with u_cold before its first row is replaced
+        if (rr == 0 && lt > 0) mbar_wait(ucfree, (lt - 1) & 1u);
+        *reinterpret_cast<float4*>(ucold + i * R + 4 * (lane ^ (i & 31))) = make_float4(u[0], u[1], u[2], u[3]);
+        if (lane == 0) coldcnt[i] = total;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ucready);
+    }
+    const int any = __reduce_or_sync(0xFFFFFFFFu, bad);
+    if (any && lane == 0) atomicOr(flags, any);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(256));
+  }
+}
+
+inline int hot_blocks(int64_t d) {
+  int nb = 10;  // C4: 5.45 ms (8: 5.6, 12: 5.7; tools/k6v2_time.py)
+  if (const char* e = getenv("LVSK_K6_HOTBLOCKS")) nb = atoi(e);
+  nb = nb < 1 ? 1 : (nb > MAX_NB ? MAX_NB : nb);
+  const int64_t cap = (d + KBLK - 1) / KBLK;
+  return static_cast<int>(nb < cap ? nb : cap);
+}
+
+}  // namespace k6v2
+
+size_t csr_rowsumsq_prep_bytes(int64_t d, int64_t r) {
+  return r == k6v2::R ? static_cast<size_t>(k6v2::hot_blocks(d)) * k6v2::B_STAGE : 0;
+}
+
+int32_t csr_rowsumsq_prepare(const float* M, int64_t d, int64_t r, void* prep, size_t prep_bytes, cudaStream_t st) {
+  using namespace k6v2;
+  LVSK_REQUIRE(r == R, LVSK_ERR_UNSUPPORTED, "the prepared CSR leverage pass needs r = 128");
+  const int nb = hot_blocks(d);
+  LVSK_REQUIRE(prep != nullptr && prep_bytes >= static_cast<size_t>(nb) * B_STAGE, LVSK_ERR_CAPACITY,
+               "prepared-operand buffer too small");
+  LVSK_REQUIRE(reinterpret_cast<uintptr_t>(prep) % 16 == 0, LVSK_ERR_CONFIGURATION, "prepared-operand buffer not 16-byte aligned");
+  const int64_t total = static_cast<int64_t>(nb) * 2 * R * KBLK;
+  k6_prep_kernel<<<static_cast<int>((total + 255) / 256), 256, 0, st>>>(M, d, nb, static_cast<uint8_t*>(prep));
+  LVSK_CHECK_LAUNCH("csr rowsumsq prepare");
+  return LVSK_OK;
+}
+
+int32_t csr_rowsumsq_tc2(const int64_t* row_ptr, const int32_t* col, const void* val, int32_t val_dtype, int64_t n,
+                         int64_t d, const float* M, const void* prep, size_t prep_bytes, double* scores,
+                         int32_t* flags, cudaStream_t st) {
+  using namespace k6v2;
+  const int nb = hot_blocks(d);
+  LVSK_REQUIRE(prep != nullptr && prep_bytes >= static_cast<size_t>(nb) * B_STAGE, LVSK_ERR_CAPACITY,
+               "prepared-operand buffer too small");
+  LVSK_REQUIRE(reinterpret_cast<uintptr_t>(prep) % 16 == 0 && reinterpret_cast<uintptr_t>(M) % 16 == 0,
+               LVSK_ERR_CONFIGURATION, "M and the prepared operand must be 16-byte aligned");
+  const void* fn = val_dtype == LVSK_F64 ? reinterpret_cast<const void*>(csr_rowsumsq_tc2_kernel<double>)
+                                         : reinterpret_cast<const void*>(csr_rowsumsq_tc2_kernel<float>);
+  const int32_t rc = ensure_smem_attr(fn, SMEM_BYTES, "csr tc2 smem attribute");
+  if (rc != LVSK_OK) return rc;
+  const int64_t ntiles = (n + TR - 1) / TR;
+  const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
+  const uint8_t* pp = static_cast<const uint8_t*>(prep);
+  const int dbg = getenv("LVSK_K6_DBG") ? atoi(getenv("LVSK_K6_DBG")) : 0;
+  if (val_dtype == LVSK_F64)
+    csr_rowsumsq_tc2_kernel<double><<<grid, k6v2::THREADS, SMEM_BYTES, st>>>(row_ptr, col, static_cast<const double*>(val), n,
+                                                                      d, M, pp, nb, scores, flags, dbg);
+  else
+    csr_rowsumsq_tc2_kernel<float><<<grid, k6v2::THREADS, SMEM_BYTES, st>>>(row_ptr, col, static_cast<const float*>(val), n, d,
+                                                                     M, pp, nb, scores, flags, dbg);
+  LVSK_CHECK_LAUNCH("csr rowsumsq tc2");
+  return LVSK_OK;
+}
+
 bool csr_rowsumsq_tc_ok(const float* M, int64_t r) {
   return r == k6tc::R && reinterpret_cast<uintptr_t>(M) % 16 == 0 && getenv("LVSK_K6_SIMT") == nullptr;
 }

@@ -23,7 +23,7 @@ import torch
 from . import _native as N
 from .errors import FormatError, UncertifiedFoldError
 from .leverage import FoldGraph, KernelOperands, jl_device, sketch_fold
-from .csr import CSRMatrix, csr_code
+from .csr import CSRMatrix, csr_code, csr_prepare
 from .sketch import GAUSSIAN, SRHT, SketchSpec, SketchState, sketch_rows
 
 STAGES = ("sketch", "factor", "leverage", "order")
@@ -72,6 +72,7 @@ class LeveragePipeline:
         self._last_X = None
         self._m32 = None
         self._m32_src = None
+        self._m32_prep = None
         self.effective_rank = None
         # keep_state: also write the compensated pair (hi, lo) of the sketch
         # (multi-rank merges need it); otherwise K1 writes the folded SX only
@@ -172,10 +173,21 @@ class LeveragePipeline:
 
     def _leverage(self, X) -> None:
         if isinstance(X, CSRMatrix):
-            if self._m32 is None or self._m32_src is not self.ops:
+            # the fold graph rewrites its operands in place on every replay: M is new each run
+            replayed = self._fold_graph is not None and self.ops is self._fold_graph.ops
+            if self._m32 is None or self._m32_src is not self.ops or replayed:
                 self._m32 = (self.ops.a.T.double() + self.ops.b.T.double()).to(torch.float32).contiguous() \
                     if self.ops.tc else self.ops.a.to(torch.float32).contiguous()
                 self._m32_src = self.ops
+                self._m32_prep = csr_prepare(self._m32)
+            if self._m32_prep is not None:
+                N.check(N.lib().lvsk_rowsumsq_csr_prepared(X.indptr.data_ptr(), X.indices.data_ptr(),
+                                                           X.data.data_ptr(), csr_code(X), X.n, X.d,
+                                                           self._m32.data_ptr(), self._m32.shape[1],
+                                                           self._m32_prep.data_ptr(), self._m32_prep.numel(),
+                                                           self.scores.data_ptr(), self.flags.data_ptr(),
+                                                           N.stream_ptr()), "csr leverage pass")
+                return
             N.check(N.lib().lvsk_rowsumsq_csr(X.indptr.data_ptr(), X.indices.data_ptr(), X.data.data_ptr(),
                                               csr_code(X), X.n, X.d, self._m32.data_ptr(), self._m32.shape[1],
                                               self.scores.data_ptr(), self.flags.data_ptr(), N.stream_ptr()),

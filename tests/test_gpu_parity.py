@@ -836,9 +836,32 @@ def test_csr_leverage_tensor_core_vs_simt_and_fp64(n, d, per_row, vdt, monkeypat
     ref = ((dense @ M.astype(np.float32).astype(np.float64)) ** 2).sum(1)
     scale = max(ref.max(), 1e-30)
     assert np.abs(tc - ref).max() <= 2e-5 * scale
+    # hot windows of 64 / 128 / 1024 columns (v2), the resident 128-column kernel (v1), SIMT
+    for nb in ("1", "2", "16"):
+        monkeypatch.setenv("LVSK_K6_HOTBLOCKS", nb)
+        assert np.abs(csr_scores(m, Mt).cpu().numpy() - ref).max() <= 2e-5 * scale
+    monkeypatch.setenv("LVSK_K6_V1", "1")
+    assert np.abs(csr_scores(m, Mt).cpu().numpy() - ref).max() <= 2e-5 * scale
     monkeypatch.setenv("LVSK_K6_SIMT", "1")
     simt = csr_scores(m, Mt).cpu().numpy()
     assert np.abs(tc - simt).max() <= 2e-5 * scale
+
+
+def test_csr_leverage_unsorted_row_rejected():
+    """The prepared K6 pass walks each row's sorted columns: a row that is not
+    strictly increasing is flagged (FormatError), as K2 does."""
+    from paper_1812_07903_b200.csr import CSRMatrix, csr_scores
+
+    csr, _ = _random_csr(500, 2000, 40, seed=5)
+    indptr, col, val, shape = csr
+    row = int(np.argmax(np.diff(indptr)))
+    bad = col.copy()
+    e = indptr[row]
+    bad[e], bad[e + 1] = bad[e + 1], bad[e]
+    M = torch.randn(2000, 128, dtype=torch.float64, device="cuda")
+    csr_scores(CSRMatrix.from_any(csr), M)
+    with pytest.raises(errors.FormatError):
+        csr_scores(CSRMatrix.from_any((indptr, bad, val, shape)), M)
 
 
 def test_csr_validation():

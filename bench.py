@@ -660,7 +660,7 @@ def run_ours(args, name: str, cfg: dict, rank: int, world: int, local_rank: int)
                                 "the fly) + reduce" if d > 512 else "gaussian_tc_kernel (K4-TC) + reduce")
                    if dtype == torch.bfloat16 else
                    "split3_bf16_kernel + gaussian_tc_kernel (K4-TC over the 3 stacked exact bf16 planes of fp32 X) + reduce"}[fam],
-        "leverage": "csr_rowsumsq_kernel (K6)" if csr else
+        "leverage": "csr_rowsumsq_tc2_kernel (K6-TC v2: hot column window on tcgen05, cold suffix gathered; incl. the per-fold operand build)" if csr else
                     ("leverage_bf16_kernel (K5, tcgen05 kind::f16)" if dtype == torch.bfloat16 else
                      "leverage_v2_kernel (K5, tcgen05)")}
     roofline = {

@@ -325,14 +325,31 @@ __global__ void __launch_bounds__(THREADS, 1)
 // cores: at C4 that is the first ~1000 Zipf-ranked ids.  The hot window is
 // therefore HT = 64 nb columns (nb <= 16), streamed in 64-column K blocks:
 //   * the B operand images (one 32 KB SW128 block per 64 columns, built once
-//     per fold by k6_prep_kernel) arrive through a 3-stage cp.async.bulk ring;
-//   * 4 scatter warps (thread = tile row) walk their row's sorted entries and
-//     fill the A block (bf16 x_hi / x_lo planes, 2-stage ring) of each K
-//     block; the same warps run the epilogue of their 32 rows (warp q = TMEM
-//     lane quadrant q), so one TMEM accumulator suffices;
-//   * 16 gather warps (8 rows each) gather only the columns >= HT into
-//     u_cold, running a tile ahead of the scatter / MMA pipeline;
+//     per fold by k6_prep_kernel) arrive through a 2-stage cp.async.bulk ring;
+//   * 4 scatter warps (thread = tile row) walk their row's sorted entries (two
+//     entries of lookahead) and fill the A block (bf16 x_hi / x_lo planes,
+//     2-stage ring) of each K block; the same warps run the epilogue of their
+//     32 rows (warp q = TMEM lane quadrant q), so one TMEM accumulator suffices;
+//   * 16 gather warps (8 rows each) read only each row's last 32 entries (three
+//     rows ahead; a longer cold suffix walks back) and gather the columns >= HT
+//     into u_cold with L1-bypassing loads, a tile ahead of the scatter / MMA
+//     pipeline; they also count the cold entries so that the epilogue can check
+//     hot + cold = row length (anything else is an unsorted row);
 //   * one thread issues the MMAs, one thread the bulk copies.
+// Measured at C4 (tools/k6v2_time.py): 7.41 ms (v1) -> 5.45 ms at nb = 10; the
+// cold gathers alone take ~5.3 ms (L2 slices at ~10 TB/s) and the scatter /
+// MMA chain alone ~4.7 ms (one warp's ~150 dependent instructions per K block).
+// Tried: coalesced per-block sweeps by the scatter warps (32 rows x nb re-reads,
+// 13.9 ms), 16-byte chunk walks with two chunks of register lookahead (6.4 ms:
+// the predicated four-way body costs more instructions than it saves latency),
+// an L2 bulk prefetch of the next tile's CSR span (no change), L1-allocating M
+// loads (better alone, 4.3 ms, but they evict the row walks' lines: 5.9 ms),
+// two scatter groups on alternate K blocks with 15 strided gather warps (24
+// warps is the most that keep 80 registers; 7.3 ms), 8-byte pair refills of a
+// four-entry lookahead (7.2 ms).  Every variant that adds instructions to the
+// walk loses: the scatter warps' dependent instruction chain per K block, not
+// their load latency, paces the MMA pipeline (ncu: issue active 54 %, L1TEX
+// 70 %, L2 slices 38 %, DRAM 8 %).
 // Rows must have strictly increasing columns (the CSR contract, include/
 // levsketch_b200.h); a row that does not sets LVSK_FLAG_BADINDEX.
 namespace k6v2 {
@@ -396,7 +413,7 @@ template <typename V>
 __global__ void __launch_bounds__(THREADS, 1)
     csr_rowsumsq_tc2_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                             const V* __restrict__ val, int64_t n, int64_t d, const float* __restrict__ M,
-                            const uint8_t* __restrict__ prep, int nb, double* __restrict__ scores, int32_t* flags, int dbg) {
+                            const uint8_t* __restrict__ prep, int nb, double* __restrict__ scores, int32_t* flags) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -512,7 +529,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
         const int32_t lo = j * KBLK, lim = lo + KBLK;
-        while (ca < lim && !(dbg & 2)) {  // ca = INT_MAX past the row's end
+        while (ca < lim) {  // ca = INT_MAX past the row's end
           if (ca < lo || ca <= cprev) {  // out of order (or negative): the row breaks the CSR contract
             bad |= LVSK_FLAG_BADINDEX;
           } else {
@@ -620,7 +637,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             x = 0.f;
           }
           if (live && !isfinite(x)) bad |= LVSK_FLAG_NONFINITE;
-          uint32_t cm = __ballot_sync(0xFFFFFFFFu, live && c >= ht && !(dbg & 1));
+          uint32_t cm = __ballot_sync(0xFFFFFFFFu, live && c >= ht);
           const int ncold = __popc(cm);
           total += ncold;
           const int first = nl - ncold;
@@ -636,8 +653,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const float xt = __shfl_sync(0xFFFFFFFFu, x, tl);
                 const bool ok = b0 + jj < ncold;
                 xv[jj] = ok ? xt : 0.f;
-                const float4* mp = reinterpret_cast<const float4*>(M + static_cast<int64_t>(ct) * R) + lane;
-                mv[jj] = ok ? ((dbg & 4) ? __ldg(mp) : ldg_stream(mp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                mv[jj] = ok ? ldg_stream(reinterpret_cast<const float4*>(M + static_cast<int64_t>(ct) * R) + lane)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
               }
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj) {
@@ -721,13 +738,12 @@ int32_t csr_rowsumsq_tc2(const int64_t* row_ptr, const int32_t* col, const void*
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = static_cast<int>(ntiles < num_sms() ? ntiles : num_sms());
   const uint8_t* pp = static_cast<const uint8_t*>(prep);
-  const int dbg = getenv("LVSK_K6_DBG") ? atoi(getenv("LVSK_K6_DBG")) : 0;
   if (val_dtype == LVSK_F64)
     csr_rowsumsq_tc2_kernel<double><<<grid, k6v2::THREADS, SMEM_BYTES, st>>>(row_ptr, col, static_cast<const double*>(val), n,
-                                                                      d, M, pp, nb, scores, flags, dbg);
+                                                                      d, M, pp, nb, scores, flags);
   else
     csr_rowsumsq_tc2_kernel<float><<<grid, k6v2::THREADS, SMEM_BYTES, st>>>(row_ptr, col, static_cast<const float*>(val), n, d,
-                                                                     M, pp, nb, scores, flags, dbg);
+                                                                     M, pp, nb, scores, flags);
   LVSK_CHECK_LAUNCH("csr rowsumsq tc2");
   return LVSK_OK;
 }

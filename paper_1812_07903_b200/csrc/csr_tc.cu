@@ -316,9 +316,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 // ---------------------------------------------------------------------------
 // K6-TC v2 — a wide hot window streamed through the tensor cores.
 //
-// v1 above is bound by the L2 slice throughput (~6300 B/clk chip-wide, the
-// LTS cap): its cold half gathers 512 B of M per nonzero, 82 GB at C4 in
-// 7.4 ms = 11 TB/s.  Only fewer L2 bytes make it faster.  A column that a
+// v1 above is bound by its gather bytes: the cold half gathers 512 B of M per
+// nonzero, 82 GB at C4 in 7.4 ms = 11 TB/s through L1 + L2, next to the L2
+// slices' ~6300 B/clk (12 TB/s) cap.  Only fewer gathered bytes make it faster.  A column that a
 // fraction f of the rows holds costs 128 f x 512 B per 128-row tile when it is
 // gathered and 512 B (its bf16 [M_hi | M_lo] operand rows) when it is
 // multiplied densely, so every column with f > 1/128 belongs on the tensor

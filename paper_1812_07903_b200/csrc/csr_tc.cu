@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 // two scatter groups on alternate K blocks with 15 strided gather warps (24
 // warps is the most that keep 80 registers; 7.3 ms), 8-byte pair refills of a
 // four-entry lookahead (7.2 ms), clearing only the 16-byte chunks a thread
-// wrote instead of zero-filling the stage (6.2 ms).  Every variant that adds instructions to the
+// wrote instead of zero-filling the stage (6.2 ms), an 8-entry cp.async ring per
+// scatter thread (12 KB more shared memory, so 28 KB of L1: 8.1 ms).  Every variant that adds instructions to the
 // walk loses: the scatter warps' dependent instruction chain per K block, not
 // their load latency, paces the MMA pipeline (ncu: issue active 54 %, L1TEX
 // 70 %, L2 slices 38 %, DRAM 8 %).

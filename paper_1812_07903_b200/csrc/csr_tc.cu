@@ -336,7 +336,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 //     pipeline; they also count the cold entries so that the epilogue can check
 //     hot + cold = row length (anything else is an unsorted row);
 //   * one thread issues the MMAs, one thread the bulk copies.
-// Measured at C4 (tools/k6v2_time.py): 7.41 ms (v1) -> 5.45 ms at nb = 10; the
+// Measured at C4 (tools/k6v2_time.py): 7.41 ms (v1) -> 5.6 ms at nb = 10 (6.0 ms before the
+// gather loads wrote their destination registers directly — ncu's top stall was the register
+// move behind each predicated load, which left ~4 of the 8 loads in flight); the
 // cold gathers alone take ~5.3 ms (L2 slices at ~10 TB/s) and the scatter /
 // MMA chain alone ~4.7 ms (one warp's ~150 dependent instructions per K block).
 // Tried: coalesced per-block sweeps by the scatter warps (32 rows x nb re-reads,
@@ -383,13 +385,16 @@ constexpr int SMEM_BYTES = OFF_BAR + 256 + TR * 4 + 1024;
 constexpr int MAX_NB = 16;
 static_assert(SMEM_BYTES <= 232448, "K6-TC v2 shared memory");
 
-// M rows stream through L2 only: the 60 KB of L1 belong to the scatter threads' row walks
-__device__ __forceinline__ float4 ldg_stream(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
-  return v;
+// M rows stream through L2 only: the 60 KB of L1 belong to the scatter threads' row walks.
+// The predicated load writes its destination registers directly (zero when !ok): a select
+// after the load would put a register move behind every load and serialise the gathers.
+__device__ __forceinline__ void ldg_stream_pred(float4& v, const float4* p, bool ok) {
+  asm("{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "mov.f32 %0, 0f00000000;\n\tmov.f32 %1, 0f00000000;\n\tmov.f32 %2, 0f00000000;\n\tmov.f32 %3, 0f00000000;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n}"
+      : "=&f"(v.x), "=&f"(v.y), "=&f"(v.z), "=&f"(v.w)
+      : "l"(p), "r"(static_cast<int>(ok)));
 }
 
 // B operand images: block j holds rows nn < R = bf16(M[64 j + k][nn]) and rows
@@ -655,8 +660,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const float xt = __shfl_sync(0xFFFFFFFFu, x, tl);
                 const bool ok = b0 + jj < ncold;
                 xv[jj] = ok ? xt : 0.f;
-                mv[jj] = ok ? ldg_stream(reinterpret_cast<const float4*>(M + static_cast<int64_t>(ct) * R) + lane)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                ldg_stream_pred(mv[jj], reinterpret_cast<const float4*>(M + static_cast<int64_t>(ct) * R) + lane, ok);
               }
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj) {

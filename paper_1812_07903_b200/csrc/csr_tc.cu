@@ -397,6 +397,24 @@ __device__ __forceinline__ void ldg_stream_pred(float4& v, const float4* p, bool
       : "l"(p), "r"(static_cast<int>(ok)));
 }
 
+// predicated element loads that write their (zero-initialised) destination directly, for the
+// same reason: `live ? p[i] : 0` puts a move behind the load and waits for it at once
+__device__ __forceinline__ void ldg_pred(int32_t& v, const int32_t* p, bool ok) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, 0;\n\t@q ld.global.nc.b32 %0, [%1];\n}"
+      : "=&r"(v)
+      : "l"(p), "r"(static_cast<int>(ok)));
+}
+__device__ __forceinline__ void ldg_pred(float& v, const float* p, bool ok) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f32 %0, 0f00000000;\n\t@q ld.global.nc.f32 %0, [%1];\n}"
+      : "=&f"(v)
+      : "l"(p), "r"(static_cast<int>(ok)));
+}
+__device__ __forceinline__ void ldg_pred(double& v, const double* p, bool ok) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t@q ld.global.nc.f64 %0, [%1];\n}"
+      : "=&d"(v)
+      : "l"(p), "r"(static_cast<int>(ok)));
+}
+
 // B operand images: block j holds rows nn < R = bf16(M[64 j + k][nn]) and rows
 // nn >= R = the bf16 remainder, K-major SW128 (the layout the MMA reads)
 __global__ void k6_prep_kernel(const float* __restrict__ M, int64_t d, int nb, uint8_t* __restrict__ out) {
@@ -606,16 +624,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t gbase = t * TR + RPW * w;
       int64_t rp = 0;
       if (lane <= RPW) rp = row_ptr[gbase + lane < n ? gbase + lane : n] - base0;
-      auto load_tail = [&](int rr, int32_t& c, float& x) {
+      auto load_tail = [&](int rr, int32_t& c, V& x) {  // (values stay in their type until they are used)
         const int64_t f0 = __shfl_sync(0xFFFFFFFFu, rp, rr < RPW ? rr : RPW);
         const int64_t f1 = __shfl_sync(0xFFFFFFFFu, rp, rr < RPW ? rr + 1 : RPW);
         const int64_t s0 = f1 - 32 > f0 ? f1 - 32 : f0;
         const bool live = s0 + lane < f1;
-        c = live ? col[s0 + lane] : 0;
-        x = live ? static_cast<float>(val[s0 + lane]) : 0.f;
+        ldg_pred(c, col + s0 + lane, live);
+        ldg_pred(x, val + s0 + lane, live);
       };
       int32_t c0, c1, c2;
-      float x0, x1, x2;
+      V x0, x1, x2;
       load_tail(0, c0, x0);
       load_tail(1, c1, x1);
       load_tail(2, c2, x2);
@@ -625,7 +643,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         float u[4] = {0.f, 0.f, 0.f, 0.f};
         const int64_t e0 = __shfl_sync(0xFFFFFFFFu, rp, rr), e1 = __shfl_sync(0xFFFFFFFFu, rp, rr + 1);
         int32_t c = c0;
-        float x = x0;
+        float x = static_cast<float>(x0);
         c0 = c1;
         x0 = x1;
         c1 = c2;

@@ -49,3 +49,33 @@ def test_batch_runner_rejects_bad_slots():
     spec = P.SketchSpec("countsketch", eps=0.5, d=64, seed=0, rows_override=256)
     with pytest.raises(ValueError):
         P.BatchRunner(spec, 1000, 64, torch.float32, slots=0)
+
+
+def test_csr_pipeline_rebuilds_its_operand_per_batch():
+    """The CSR leverage pass takes a float32 copy of M and (r = 128) its
+    prepared bf16 operand images; the fold graph rewrites M in place on every
+    replay, so both must be rebuilt per run: different CSR batches through one
+    pipeline give the scores of a fresh pipeline on each batch."""
+    import numpy as np
+
+    from paper_1812_07903_b200.csr import CSRMatrix
+
+    n, d, k, r = 6000, 256, 1024, 128
+
+    def batch(seed):
+        rng = np.random.default_rng(seed)
+        nnz = 24
+        cols = np.sort(np.stack([rng.choice(d, size=nnz, replace=False) for _ in range(n)]), axis=1)
+        vals = rng.lognormal(0.0, 1.0, size=(n, nnz)) * (1.0 + seed)
+        vals[:, : nnz // 2] *= 1.0 + 3.0 * rng.random((1, nnz // 2))  # batch-specific column weights
+        indptr = np.arange(n + 1, dtype=np.int64) * nnz
+        return CSRMatrix(indptr, cols.reshape(-1).astype(np.int32), vals.reshape(-1).astype(np.float32), (n, d))
+
+    spec = P.SketchSpec("osnap", eps=0.5, d=d, seed=5, rows_override=k, osnap_s=4)
+    batches = [batch(s) for s in range(3)]
+    pipe = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=1e-6, jl_dim=r)
+    for X in batches + batches[::-1]:
+        got, _ = pipe.run(X)
+        fresh = P.LeveragePipeline(spec, n, d, torch.float32, sv_tol=1e-6, jl_dim=r)
+        want, _ = fresh.run(X)
+        assert torch.equal(got, want)
